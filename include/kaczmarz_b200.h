@@ -1,0 +1,188 @@
+/*
+ * kaczmarz_b200.h — C ABI of the B200-native batched Kaczmarz precoding path.
+ *
+ * The reference (arXiv 2501.10689, `kaczprec`) is pure Python and has no FFI
+ * layer; its boundary is the Python API of `kaczprec.solvers` / `rzf` /
+ * `assembly` / `metrics`.  Each entry point below replaces one group of those
+ * calls for a whole batch of independent systems (realizations/subcarriers):
+ *
+ *   kz_solve     <- run_precoding   (pkg/src/kaczprec/solvers.py:556-623)
+ *                   solve / solve_all (solvers.py:460-537)
+ *                   InstanceRun.step + step primitives (solvers.py:143-423)
+ *   kz_rzf       <- rzf_precoder / auxiliary_matrix (pkg/src/kaczprec/rzf.py:38-83)
+ *   kz_epilogue  <- assemble_dense / assemble_vr (pkg/src/kaczprec/assembly.py:51-92),
+ *                   nmse / spectral_efficiency (pkg/src/kaczprec/metrics.py:44-78)
+ *
+ * Conventions
+ *  - Plain C types only; every device buffer is caller-owned (the library
+ *    never allocates device memory) and passed as a raw device pointer.
+ *  - Complex arrays are interleaved (re, im); element type is double for
+ *    KZ_C128 and float for KZ_C64.
+ *  - All calls are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  They return KZ_OK or a negative status;
+ *    kz_last_error() gives a thread-local message.  No exceptions cross the ABI.
+ *  - Non-convergence is a flag in the outputs, never an error (solvers.py:477,498-505).
+ */
+#ifndef KACZMARZ_B200_H
+#define KACZMARZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KZ_ABI_VERSION 1
+
+/* status codes */
+#define KZ_OK 0
+#define KZ_ERR_INVALID (-1)   /* bad argument; reference raises ValueError */
+#define KZ_ERR_CUDA (-2)      /* CUDA runtime error */
+#define KZ_ERR_NOT_PD (-3)    /* Gram not positive definite; reference raises LinAlgError (rzf.py:55-59) */
+#define KZ_ERR_WORKSPACE (-4) /* workspace too small */
+#define KZ_ERR_UNSUPPORTED (-5)
+
+/* schemes, in the order of SCHEMES (solvers.py:39) */
+enum kz_scheme { KZ_URK = 0, KZ_SWOR_ERK = 1, KZ_GK = 2, KZ_GRK = 3, KZ_VR_OGRK = 4, KZ_AHK = 5, KZ_VR_OAHK = 6 };
+enum kz_dtype { KZ_C128 = 0, KZ_C64 = 1 };
+
+/* stopping drivers */
+enum kz_stop_mode {
+  KZ_STOP_LOCKSTEP = 0, /* run_precoding: all K rhs advance per outer iteration; stop when
+                           NMSE(M/||M||, F_ref) < epsilon (epsilon = 0: fixed T) (solvers.py:587-603) */
+  KZ_STOP_RESIDUAL = 1, /* solve/solve_all mode="residual": ||r_true||_2 <= epsilon (solvers.py:494-497) */
+  KZ_STOP_ORACLE = 2    /* solve/solve_all mode="oracle": ||q - v_ref||/||v_ref|| < epsilon (solvers.py:488-493) */
+};
+
+/* where the random row draws come from */
+enum kz_rng_kind {
+  KZ_RNG_NONE = 0,           /* deterministic schemes (gk, ahk, vr-oahk) */
+  KZ_RNG_HOST_UNIFORM = 1,   /* u[b][rhs][s] fp64: one Generator.random() per greedy-weighted pick */
+  KZ_RNG_HOST_INDEX = 2,     /* idx[b][rhs][s] int32: host-evaluated uniform / energy-swor picks */
+  KZ_RNG_PHILOX = 3          /* on-device Philox4x32-10 keyed by (seed, b, rhs, draw) */
+};
+
+/*
+ * One batch of B independent systems sharing (K, Nt).  Row i of system b has
+ * support Gamma_bi given as a list of contiguous antenna segments and its
+ * restricted channel h_bi = H_b[Gamma_bi, i] packed contiguously
+ * (AugmentedSystem.supports / eff_rows, solvers.py:80-89).
+ */
+typedef struct kz_problem {
+  int32_t n_systems;   /* B */
+  int32_t n_users;     /* K (rows and right-hand sides) */
+  int32_t n_antennas;  /* Nt */
+  int32_t dtype;       /* kz_dtype of heff and of every complex output */
+  /* supports: row r = b*K + i owns segments [row_seg_ptr[r], row_seg_ptr[r+1]) */
+  const int32_t* row_seg_ptr;   /* [B*K+1] */
+  const int32_t* seg_start;     /* [n_seg] first antenna of the segment */
+  const int32_t* seg_len;       /* [n_seg] */
+  const int64_t* row_val_ptr;   /* [B*K+1] offset of h_bi in heff (complex elements) */
+  const void* heff;             /* packed complex values */
+  const double* row_energy;     /* [B*K] e_bi = ||h_bi||^2 + reg_b (solvers.py:90) */
+  const double* reg;            /* [B] ridge weight xi_b */
+  /* VR partition (vrgraph.py:84-114), only read by vr-ogrk / vr-oahk */
+  const int32_t* coupled_ptr;   /* [B*K+1] into coupled_idx; X_bi ascending */
+  const int32_t* coupled_idx;
+  const int32_t* orth_ptr;      /* [B+1] into orth_idx; O_b ascending */
+  const int32_t* orth_idx;
+  const int32_t* non_ptr;       /* [B+1] into non_idx; N_b ascending */
+  const int32_t* non_idx;
+  const int32_t* non_union_size;/* [B] |union of N_b supports| (flop charge of ahk_step) */
+} kz_problem;
+
+typedef struct kz_stop {
+  int32_t mode;         /* kz_stop_mode */
+  int32_t max_iters;    /* cap: outer iterations (LOCKSTEP) or per-rhs iterations (RESIDUAL/ORACLE) */
+  int32_t check_every;  /* StoppingRule.check_every (>= 1) */
+  int32_t _pad;
+  double epsilon;       /* LOCKSTEP: NMSE threshold (0 = fixed T); else StoppingRule.epsilon (> 0) */
+  const double* f_ref;  /* LOCKSTEP with epsilon > 0 or traces: [B][Nt][K] complex128 F_ref */
+  const double* v_ref;  /* ORACLE: [B][K][K] complex128, column c = reference for rhs c */
+  const uint8_t* rhs_mask; /* optional [B*K]; 0 = leave that rhs untouched (solve() on one column) */
+} kz_stop;
+
+typedef struct kz_rng {
+  int32_t kind;          /* kz_rng_kind */
+  int32_t stream_len;    /* draws per (b, rhs) available in this call (HOST_*) */
+  int64_t stream_base;   /* global draw index of element 0 (chunked resumption) */
+  const double* uniforms;/* HOST_UNIFORM: [B][K][stream_len] */
+  const int32_t* indices;/* HOST_INDEX:   [B][K][stream_len] */
+  uint64_t seed;         /* PHILOX key */
+} kz_rng;
+
+typedef struct kz_out {
+  void* v;                  /* [B][K][K] complex (dtype): v[b][i][c] = coef_i of rhs c (PrecodingRun.v) */
+  int32_t* iters;           /* [B*K] SolverState.iters per rhs */
+  uint8_t* converged;       /* [B*K] per-rhs convergence (solve) */
+  uint8_t* done;            /* [B*K] greedy/no-op termination flag (InstanceRun.done) */
+  int32_t* noop_steps;      /* [B*K] */
+  int64_t* flops;           /* [B*K] FlopCounter.total per rhs (metrics.py:25-41) */
+  int32_t* n_outer;         /* [B] LOCKSTEP outer iterations t (PrecodingRun.n_iters) */
+  uint8_t* sys_converged;   /* [B] LOCKSTEP convergence */
+  uint8_t* paused;          /* [B*K] optional: rhs ran out of host draws (resume with next chunk) */
+  int32_t* rows;            /* optional [B][K][rows_cap]: projected row per RK step */
+  int32_t rows_cap;
+  int32_t trace_cap;        /* length of the optional traces below */
+  /* LOCKSTEP: [B][trace_cap], one entry per outer iteration (PrecodingRun traces):
+       nmse of M/||M|| vs F_ref, ||I - H^H M - xi Q||_F, sum of per-rhs flop counters.
+     RESIDUAL/ORACLE: [B*K][trace_cap], one entry per check (RunTrace of solve):
+       ||q - v_ref||/||v_ref|| (oracle mode), fresh ||r||_2, the rhs's flop counter. */
+  double* nmse_trace;
+  double* resid_trace;
+  int64_t* flops_trace;
+  int32_t* n_checks;        /* optional [B*K] (RESIDUAL/ORACLE): entries written per rhs */
+} kz_out;
+
+/* Bytes of device workspace kz_solve needs for this problem (iterates M, residuals,
+   per-rhs scratch).  The workspace doubles as the resumable solver state. */
+size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop);
+
+/* Run scheme over every (system, rhs).  resume = 0 initialises the state
+   (SolverState.initial, solvers.py:129-136); resume = 1 continues from the
+   workspace (next host-stream chunk). */
+int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng,
+             kz_out* out, void* workspace, size_t workspace_bytes, int32_t resume, void* stream);
+
+/* Device pointer to the iterate block M (col = H coef) inside a solve workspace:
+   [B][K rhs][Nt] complex (dtype). */
+void* kz_workspace_iterates(const kz_problem* prob, void* workspace);
+
+/* Batched direct RZF (rzf.py:38-83): Gram H^H H + reg I from the packed rows,
+   Cholesky, V = Gram^{-1}, F = beta H V with ||F||_F = 1.  Always complex128.
+   v_out [B][K][K], f_out [B][Nt][K] (may be NULL), beta_out [B].
+   Returns KZ_ERR_NOT_PD if any Gram is not positive definite (status per
+   system in pd_ok [B], may be NULL). */
+size_t kz_rzf_workspace_bytes(const kz_problem* prob);
+int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_out,
+           uint8_t* pd_ok, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Precoder epilogue for a batch of auxiliary solutions V (assembly.py:51-92,
+   metrics.py:44-78):
+     beta = 1/||H V||_F, F = beta H V (blocked over the rows covering each antenna,
+     identical to the dense product because H is zero off-support);
+     nmse = ||F_ref - F||_F / ||F_ref||_F with F_ref = beta_ref H V_ref (never materialised);
+     rates_k = log2(1 + |h_k^H f_k|^2 / (sum_{i!=k} |h_k^H f_i|^2 + 1/snr_linear)), via
+     H^H F = beta (H^H H) V.
+   v [B][K][K] (prob->dtype); f_out [B][Nt][K] (prob->dtype, NULL = not stored);
+   v_ref [B][K][K] complex128 + beta_ref [B] (NULL = no NMSE); snr_linear [B]
+   (NULL = no rates); beta_out [B], nmse_out [B], rates_out [B][K], sum_rate_out [B]
+   each may be NULL. */
+size_t kz_epilogue_workspace_bytes(const kz_problem* prob);
+int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double* v_ref, const double* beta_ref,
+                const double* snr_linear, double* beta_out, double* nmse_out, double* rates_out,
+                double* sum_rate_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Number of kernels the last kz_* call on this thread launched (benchmark
+   bookkeeping for the gpu_launches count). */
+int32_t kz_last_launch_count(void);
+
+const char* kz_last_error(void);
+int32_t kz_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KACZMARZ_B200_H */

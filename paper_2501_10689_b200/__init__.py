@@ -1,0 +1,48 @@
+"""B200-native batched Kaczmarz RZF precoding (arXiv 2501.10689 hot path).
+
+Drop-in for the solver path of the reference package `kaczprec`
+(pkg/src/kaczprec/__init__.py:69-131): the same public names for the solver,
+RZF, assembly and metric entry points, backed by libkaczmarz_b200.so
+(hand-written sm_100a CUDA behind the C ABI in include/kaczmarz_b200.h).
+Batched entry points (`solve_batch`, `run_precoding_batched`, `rzf_batched`,
+`epilogue`) run thousands of systems per launch.  There is no CPU fallback.
+"""
+
+from .assembly import assemble_dense, assemble_vr, epilogue
+from .batch import DeviceBatch, HostBatch
+from .channel import CONFIGS, ContiguousChannels, NearFieldConfig, generate, solver_seed_sequence
+from .metrics import CADD, CMUL, nmse, spectral_efficiency
+from .rzf import Precoder, apply_auxiliary, auxiliary_matrix, mrc_precoder, rzf_batched, rzf_precoder
+from .solvers import (
+    SCHEMES,
+    STOCHASTIC_SCHEMES,
+    VR_SCHEMES,
+    AugmentedSystem,
+    BatchResult,
+    FlopCounter,
+    HostStreams,
+    PrecodingRun,
+    RunTrace,
+    SolverState,
+    StoppingRule,
+    canonical_scheme,
+    display_scheme,
+    run_precoding,
+    run_precoding_batched,
+    solve,
+    solve_all,
+    solve_batch,
+)
+from .vrgraph import UserPartition, build_partition
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AugmentedSystem", "BatchResult", "CADD", "CMUL", "CONFIGS", "ContiguousChannels", "DeviceBatch",
+    "FlopCounter", "HostBatch", "HostStreams", "NearFieldConfig", "Precoder", "PrecodingRun", "RunTrace",
+    "SCHEMES", "STOCHASTIC_SCHEMES", "SolverState", "StoppingRule", "UserPartition", "VR_SCHEMES",
+    "apply_auxiliary", "assemble_dense", "assemble_vr", "auxiliary_matrix", "build_partition",
+    "canonical_scheme", "display_scheme", "epilogue", "generate", "mrc_precoder", "nmse", "rzf_batched",
+    "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",
+    "solver_seed_sequence", "spectral_efficiency",
+]

@@ -1,0 +1,105 @@
+"""Precoder assembly / epilogue on the GPU (drop-in for pkg/src/kaczprec/assembly.py).
+
+`kz_epilogue` computes, per system, F = beta H V with beta = 1/||H V||_F over
+the rows covering each antenna (assemble_vr's blocked product with one-antenna
+blocks, equal to assemble_dense's H V because H is zero off-support), plus the
+NMSE against beta_ref H V_ref and the Eq. (7) rates — the per-system scalars
+gathered across GPUs.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .batch import DeviceBatch, HostBatch
+
+
+def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = False, snr_linear=None,
+             want_f: bool = False, stream=None) -> dict:
+    import torch
+    lb = _lib.lib()
+    b, k, nt = dev.n_systems, dev.n_users, dev.n_antennas
+    d = dev.device
+    v = v.to(dev.complex_dtype).contiguous()
+    f = torch.zeros((b, nt, k), dtype=dev.complex_dtype, device=d) if want_f else None
+    beta = torch.zeros(b, dtype=torch.float64, device=d)
+    nm = torch.full((b,), float("nan"), dtype=torch.float64, device=d) if v_ref is not None else None
+    keep = []
+    if v_ref is not None:
+        v_ref = torch.as_tensor(v_ref).to(device=d, dtype=torch.complex128).contiguous()
+        beta_ref = torch.as_tensor(beta_ref).to(device=d, dtype=torch.float64).contiguous()
+        keep += [v_ref, beta_ref]
+    snr = None
+    if rates:
+        snr = snr_linear if snr_linear is not None else dev.t.get("snr_linear")
+        if snr is None:
+            raise ValueError("rates need snr_linear (batch built without it)")
+        snr = torch.as_tensor(snr).to(device=d, dtype=torch.float64).contiguous()
+        keep.append(snr)
+    r = torch.zeros((b, k), dtype=torch.float64, device=d) if rates else None
+    sr = torch.zeros(b, dtype=torch.float64, device=d) if rates else None
+    need = lb.kz_epilogue_workspace_bytes(C.byref(dev.problem)) if rates else 0
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    P = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _lib.check(lb.kz_epilogue(C.byref(dev.problem), v.data_ptr(), P(f), P(v_ref), P(beta_ref), P(snr),
+                              beta.data_ptr(), P(nm), P(r), P(sr), ws.data_ptr(), ws.numel(),
+                              C.c_void_p(s.cuda_stream)))
+    return {"f": f, "beta": beta, "nmse": nm, "rates": r, "sum_rate": sr, "launches": lb.kz_last_launch_count()}
+
+
+class _VrSystem:
+    """Batch view of a ChannelMatrix (VR supports) for the epilogue."""
+
+    def __init__(self, chan):
+        from .vrgraph import UserPartition
+        h = np.asarray(chan.h)
+        self.n_antennas, self.n_users = h.shape
+        self.reg = 0.0
+        self.supports = tuple(np.asarray(vr.antenna_indices) for vr in chan.vrs)
+        self.eff_rows = tuple(np.ascontiguousarray(h[s, i]) for i, s in enumerate(self.supports))
+        self.row_energies = np.array([np.sum(np.abs(e) ** 2) for e in self.eff_rows])
+        k = self.n_users
+        self.partition = UserPartition(frozenset(), tuple(range(k)), tuple(frozenset({i}) for i in range(k)))
+
+
+def _assemble(chan, v, counter, scheme, blocked):
+    from .rzf import Precoder, _DenseSystem
+    h = np.asarray(chan.h if hasattr(chan, "h") else chan)
+    nt, k = h.shape
+    v = np.asarray(v)
+    if v.shape != (k, k):
+        raise ValueError(f"expected a ({k}, {k}) solution block, got {v.shape}")
+    sysv = _VrSystem(chan) if hasattr(chan, "vrs") else _DenseSystem(h, 0.0)
+    dev = HostBatch.from_systems([sysv]).to_device("c128")
+    import torch
+    ep = epilogue(dev, torch.as_tensor(v[None], dtype=torch.complex128, device="cuda"), want_f=True)
+    beta = float(ep["beta"][0])
+    if not np.isfinite(beta):
+        raise ValueError("degenerate precoder: H V vanished")
+    if counter is not None:
+        if blocked:
+            m = chan.cfg.subarray_size
+            for s in range(chan.cfg.n_subarrays):
+                q = sum(1 for vr in chan.vrs if s in vr.visible_subarrays)
+                if q:
+                    counter.total += 6 * m * q * k + 2 * m * (q - 1) * k
+        else:
+            counter.total += 6 * nt * k * k + 2 * nt * k * (k - 1)
+    return Precoder(f=ep["f"][0].cpu().numpy(), norm_factor=beta, scheme=scheme)
+
+
+def assemble_dense(chan, v, counter=None, scheme: str = ""):
+    """F = H V then unit-power normalisation (assembly.py:59-71)."""
+    return _assemble(chan, v, counter, scheme, blocked=False)
+
+
+def assemble_vr(chan, v, counter=None, scheme: str = ""):
+    """Subarray-blocked F = H V (assembly.py:74-92); takes the ChannelMatrix (the
+    reference's SubarrayChannel view is implicit in the VR supports)."""
+    if hasattr(chan, "blocks"):
+        raise TypeError("pass the ChannelMatrix; the VR blocking is derived on the device")
+    return _assemble(chan, v, counter, scheme, blocked=True)

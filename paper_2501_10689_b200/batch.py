@@ -1,0 +1,251 @@
+"""Packing B independent systems into the flat device layout of kz_problem.
+
+Host side (numpy) builds the CSR-style arrays once; `to_device` uploads them
+as torch tensors and fills the ctypes `KzProblem` with their device pointers.
+Layout in HBM:
+
+  heff         complex[n_val]   rows packed back to back, row r = b*K + i
+  row_val_ptr  int64[B*K+1]     offset of row r in heff
+  row_seg_ptr  int32[B*K+1]     row r's support segments (one per contiguous run)
+  seg_start    int32[n_seg]     first antenna of each segment
+  seg_len      int32[n_seg]
+  row_energy   float64[B*K]     ||h_r||^2 + reg_b
+  reg          float64[B]
+  coupled/orth/non CSR          the VR partition (vrgraph.py:84-114)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .vrgraph import greedy_mis, overlap_from_intervals, overlap_from_segments
+
+
+def _union_size_intervals(start, length):
+    if len(start) == 0:
+        return 0
+    order = np.argsort(start, kind="stable")
+    s = np.asarray(start)[order].astype(np.int64)
+    e = s + np.asarray(length)[order].astype(np.int64)
+    tot, cur_s, cur_e = 0, int(s[0]), int(e[0])
+    for a, b in zip(s[1:], e[1:]):
+        if a <= cur_e:
+            cur_e = max(cur_e, int(b))
+        else:
+            tot += cur_e - cur_s
+            cur_s, cur_e = int(a), int(b)
+    return tot + cur_e - cur_s
+
+
+@dataclass
+class HostBatch:
+    n_systems: int
+    n_users: int
+    n_antennas: int
+    row_seg_ptr: np.ndarray
+    seg_start: np.ndarray
+    seg_len: np.ndarray
+    row_val_ptr: np.ndarray
+    heff: np.ndarray
+    row_energy: np.ndarray
+    reg: np.ndarray
+    coupled_ptr: np.ndarray
+    coupled_idx: np.ndarray
+    orth_ptr: np.ndarray
+    orth_idx: np.ndarray
+    non_ptr: np.ndarray
+    non_idx: np.ndarray
+    non_union_size: np.ndarray
+    contiguous: bool
+    snr_linear: np.ndarray | None = None
+
+    # ------------------------------------------------------------ builders
+    @classmethod
+    def from_contiguous(cls, ch, partition: bool = True) -> "HostBatch":
+        """From `channel.ContiguousChannels` (one segment per user)."""
+        b, k = ch.start.shape
+        rows = b * k
+        lens = ch.length.reshape(-1).astype(np.int64)
+        if np.all(lens == lens[0]):
+            e = np.sum(np.abs(ch.heff.reshape(rows, int(lens[0]))) ** 2, axis=1)
+        else:
+            e = np.array([np.sum(np.abs(ch.heff[ch.row_val_ptr[r]:ch.row_val_ptr[r + 1]]) ** 2)
+                          for r in range(rows)])
+        energy = e + np.repeat(ch.reg, k)
+        cp, ci, op, oi, np_, ni, nu = [0], [], [0], [], [0], [], []
+        if partition:
+            for s in range(b):
+                adj = overlap_from_intervals(ch.start[s], ch.length[s])
+                orth = greedy_mis(adj)
+                in_o = np.zeros(k, dtype=bool)
+                in_o[orth] = True
+                non = np.flatnonzero(~in_o)
+                for i in range(k):
+                    x = np.flatnonzero(adj[i] | (np.arange(k) == i))
+                    ci.extend(x.tolist())
+                    cp.append(len(ci))
+                oi.extend(orth.tolist())
+                op.append(len(oi))
+                ni.extend(non.tolist())
+                np_.append(len(ni))
+                nu.append(_union_size_intervals(ch.start[s][non], ch.length[s][non]))
+        else:
+            cp = [0] * (rows + 1)
+            op = [0] * (b + 1)
+            np_ = [0] * (b + 1)
+            nu = [0] * b
+        i32 = lambda a: np.asarray(a, dtype=np.int32)  # noqa: E731
+        return cls(b, k, ch.n_antennas, np.arange(rows + 1, dtype=np.int32), i32(ch.start.reshape(-1)),
+                   i32(ch.length.reshape(-1)), ch.row_val_ptr.astype(np.int64), ch.heff.astype(np.complex128),
+                   energy, np.asarray(ch.reg, dtype=np.float64), i32(cp), i32(ci), i32(op), i32(oi), i32(np_),
+                   i32(ni), i32(nu), True, np.asarray(ch.snr_linear, dtype=np.float64))
+
+    @classmethod
+    def from_systems(cls, systems, snr_linear=None) -> "HostBatch":
+        """From AugmentedSystem-like objects (reference or this package): uses their
+        supports, eff_rows, row_energies, reg and partition as-is."""
+        b = len(systems)
+        k, nt = systems[0].n_users, systems[0].n_antennas
+        seg_ptr, seg_s, seg_l, val_ptr, vals = [0], [], [], [0], []
+        energy, reg = [], []
+        cp, ci, op, oi, np_, ni, nu = [0], [], [0], [], [0], [], []
+        contiguous = True
+        for s in systems:
+            if s.n_users != k or s.n_antennas != nt:
+                raise ValueError("all systems of a batch must share (K, Nt)")
+            for i in range(k):
+                idx = np.asarray(s.supports[i], dtype=np.int64)
+                brk = np.flatnonzero(np.diff(idx) != 1) + 1
+                starts = np.concatenate([[0], brk])
+                ends = np.concatenate([brk, [idx.size]])
+                for a, e in zip(starts, ends):
+                    seg_s.append(int(idx[a]))
+                    seg_l.append(int(e - a))
+                if len(starts) != 1:
+                    contiguous = False
+                seg_ptr.append(len(seg_s))
+                vals.append(np.asarray(s.eff_rows[i], dtype=np.complex128))
+                val_ptr.append(val_ptr[-1] + idx.size)
+            energy.extend(np.asarray(s.row_energies, dtype=np.float64).tolist())
+            reg.append(float(s.reg))
+            part = s.partition
+            for i in range(k):
+                ci.extend(sorted(part.coupled[i]))
+                cp.append(len(ci))
+            orth = sorted(part.orthogonal)
+            non = list(part.non_orthogonal)
+            oi.extend(orth)
+            op.append(len(oi))
+            ni.extend(non)
+            np_.append(len(ni))
+            if non:
+                nu.append(int(np.unique(np.concatenate([np.asarray(s.supports[i]) for i in non])).size))
+            else:
+                nu.append(0)
+        i32 = lambda a: np.asarray(a, dtype=np.int32)  # noqa: E731
+        return cls(b, k, nt, i32(seg_ptr), i32(seg_s), i32(seg_l), np.asarray(val_ptr, dtype=np.int64),
+                   np.concatenate(vals), np.asarray(energy), np.asarray(reg), i32(cp), i32(ci), i32(op), i32(oi),
+                   i32(np_), i32(ni), i32(nu), contiguous,
+                   None if snr_linear is None else np.asarray(snr_linear, dtype=np.float64))
+
+    @classmethod
+    def concat(cls, parts) -> "HostBatch":
+        """Stack batches sharing (K, Nt) (offsets rebased)."""
+        k, nt = parts[0].n_users, parts[0].n_antennas
+
+        def cat_ptr(name, base_name=None):
+            out, off = [np.zeros(1, dtype=getattr(parts[0], name).dtype)], 0
+            for p in parts:
+                a = getattr(p, name)
+                out.append(a[1:] + off)
+                off += a[-1]
+            return np.concatenate(out)
+
+        return cls(sum(p.n_systems for p in parts), k, nt, cat_ptr("row_seg_ptr"),
+                   np.concatenate([p.seg_start for p in parts]), np.concatenate([p.seg_len for p in parts]),
+                   cat_ptr("row_val_ptr"), np.concatenate([p.heff for p in parts]),
+                   np.concatenate([p.row_energy for p in parts]), np.concatenate([p.reg for p in parts]),
+                   cat_ptr("coupled_ptr"), np.concatenate([p.coupled_idx for p in parts]),
+                   cat_ptr("orth_ptr"), np.concatenate([p.orth_idx for p in parts]),
+                   cat_ptr("non_ptr"), np.concatenate([p.non_idx for p in parts]),
+                   np.concatenate([p.non_union_size for p in parts]), all(p.contiguous for p in parts),
+                   None if any(p.snr_linear is None for p in parts) else np.concatenate([p.snr_linear for p in parts]))
+
+    # ------------------------------------------------------------ accessors
+    def support_sizes(self) -> np.ndarray:
+        return np.diff(self.row_val_ptr).reshape(self.n_systems, self.n_users)
+
+    def to_device(self, dtype: str = "c128", device=None) -> "DeviceBatch":
+        return DeviceBatch(self, dtype, device)
+
+    @property
+    def nbytes(self) -> int:
+        return sum(getattr(self, f).nbytes for f in (
+            "row_seg_ptr", "seg_start", "seg_len", "row_val_ptr", "heff", "row_energy", "reg", "coupled_ptr",
+            "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"))
+
+
+class DeviceBatch:
+    """Device-resident copy of a HostBatch plus the KzProblem that points at it."""
+
+    def __init__(self, host: HostBatch, dtype: str = "c128", device=None, pinned: bool = False, stream=None):
+        import torch
+        if dtype not in ("c128", "c64"):
+            raise ValueError(f"dtype must be 'c128' or 'c64', got {dtype!r}")
+        self.host = host
+        self.dtype = dtype
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("the Kaczmarz path runs on CUDA devices only (no CPU fallback)")
+        cdt = torch.complex128 if dtype == "c128" else torch.complex64
+
+        def up(a, dt=None):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            if dt is not None:
+                t = t.to(dt)
+            if pinned:
+                t = t.pin_memory()
+            return t.to(self.device, non_blocking=pinned)
+
+        self.t = {
+            "row_seg_ptr": up(host.row_seg_ptr), "seg_start": up(host.seg_start), "seg_len": up(host.seg_len),
+            "row_val_ptr": up(host.row_val_ptr), "heff": up(host.heff, cdt), "row_energy": up(host.row_energy),
+            "reg": up(host.reg), "coupled_ptr": up(host.coupled_ptr), "coupled_idx": up(host.coupled_idx),
+            "orth_ptr": up(host.orth_ptr), "orth_idx": up(host.orth_idx), "non_ptr": up(host.non_ptr),
+            "non_idx": up(host.non_idx), "non_union_size": up(host.non_union_size),
+        }
+        if host.snr_linear is not None:
+            self.t["snr_linear"] = up(host.snr_linear)
+        self.problem = self._make_problem(self.t)
+
+    def _make_problem(self, t):
+        p = _lib.KzProblem()
+        p.n_systems = self.host.n_systems
+        p.n_users = self.host.n_users
+        p.n_antennas = self.host.n_antennas
+        p.dtype = _lib.KZ_C128 if self.dtype == "c128" else _lib.KZ_C64
+        for name in ("row_seg_ptr", "seg_start", "seg_len", "row_val_ptr", "heff", "row_energy", "reg",
+                     "coupled_ptr", "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"):
+            ten = t[name]
+            setattr(p, name, ten.data_ptr() if ten.numel() else None)
+        return p
+
+    @property
+    def n_systems(self):
+        return self.host.n_systems
+
+    @property
+    def n_users(self):
+        return self.host.n_users
+
+    @property
+    def n_antennas(self):
+        return self.host.n_antennas
+
+    @property
+    def complex_dtype(self):
+        import torch
+        return torch.complex128 if self.dtype == "c128" else torch.complex64

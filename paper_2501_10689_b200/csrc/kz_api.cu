@@ -1,0 +1,192 @@
+// C-ABI entry points of libkaczmarz_b200.so (see include/kaczmarz_b200.h).
+//
+// Validation mirrors the reference's ValueError conditions where they apply
+// to a packed batch (solvers.py:48-52, 76-92, 351-352, 444-450; rzf.py:51-59).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "kz_common.cuh"
+#include "kz_dense.cuh"
+#include "kz_solve_generic.cuh"
+#include "kz_solve_lockstep.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+__attribute__((format(printf, 2, 3))) int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return KZ_ERR_CUDA;
+  }
+  return KZ_OK;
+}
+
+int check_problem(const kz_problem* p) {
+  if (!p) return fail(KZ_ERR_INVALID, "null problem");
+  if (p->n_systems < 0) return fail(KZ_ERR_INVALID, "n_systems must be >= 0 (got %d)", (int)p->n_systems);
+  if (p->n_users < 1) return fail(KZ_ERR_INVALID, "need at least one user (got %d)", (int)p->n_users);
+  if (p->n_antennas < 1) return fail(KZ_ERR_INVALID, "need at least one antenna (got %d)", (int)p->n_antennas);
+  if (p->dtype != KZ_C128 && p->dtype != KZ_C64) return fail(KZ_ERR_INVALID, "unknown dtype %d", (int)p->dtype);
+  if (p->n_systems == 0) return KZ_OK;
+  if (!p->row_seg_ptr || !p->seg_start || !p->seg_len || !p->row_val_ptr || !p->heff || !p->row_energy || !p->reg)
+    return fail(KZ_ERR_INVALID, "problem arrays must be non-null");
+  return KZ_OK;
+}
+
+}  // namespace
+
+using namespace kz;
+
+extern "C" {
+
+int32_t kz_abi_version(void) { return KZ_ABI_VERSION; }
+const char* kz_last_error(void) { return g_err.c_str(); }
+int32_t kz_last_launch_count(void) { return g_launches; }
+
+size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop) {
+  (void)stop;
+  if (!prob) return 0;
+  size_t gen = gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).total;
+  return gen;
+}
+
+void* kz_workspace_iterates(const kz_problem* prob, void* workspace) {
+  if (!prob || !workspace) return nullptr;
+  return (char*)workspace + gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).M;
+}
+
+int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng, kz_out* out,
+             void* workspace, size_t workspace_bytes, int32_t resume, void* stream) {
+  g_launches = 0;
+  int st = check_problem(prob);
+  if (st) return st;
+  if (scheme < KZ_URK || scheme > KZ_VR_OAHK) return fail(KZ_ERR_INVALID, "unknown scheme %d", (int)scheme);
+  if (!stop || !rng || !out) return fail(KZ_ERR_INVALID, "null stop/rng/out");
+  if (stop->mode < KZ_STOP_LOCKSTEP || stop->mode > KZ_STOP_ORACLE)
+    return fail(KZ_ERR_INVALID, "unknown stopping mode %d", (int)stop->mode);
+  if (stop->max_iters < 1) return fail(KZ_ERR_INVALID, "max_iters must be >= 1 (got %d)", (int)stop->max_iters);
+  if (stop->check_every < 1) return fail(KZ_ERR_INVALID, "check_every must be >= 1");
+  if (stop->mode == KZ_STOP_LOCKSTEP) {
+    if (stop->epsilon < 0.0) return fail(KZ_ERR_INVALID, "epsilon must be >= 0 in lockstep mode");
+    if ((stop->epsilon > 0.0 || out->nmse_trace) && !stop->f_ref)
+      return fail(KZ_ERR_INVALID, "lockstep NMSE stopping needs f_ref");
+  } else {
+    if (!(stop->epsilon > 0.0)) return fail(KZ_ERR_INVALID, "epsilon must be positive");
+    if (stop->mode == KZ_STOP_ORACLE && !stop->v_ref)
+      return fail(KZ_ERR_INVALID, "oracle stopping needs the direct-solver reference");
+  }
+  const bool stochastic = scheme == KZ_URK || scheme == KZ_SWOR_ERK || scheme == KZ_GRK || scheme == KZ_VR_OGRK;
+  if (stochastic) {
+    bool idx_scheme = scheme == KZ_URK || scheme == KZ_SWOR_ERK;
+    if (rng->kind == KZ_RNG_NONE) return fail(KZ_ERR_INVALID, "scheme draws rows at random; pass an rng");
+    if (rng->kind == KZ_RNG_HOST_UNIFORM && (idx_scheme || !rng->uniforms))
+      return fail(KZ_ERR_INVALID, "host uniform streams are for grk / vr-ogrk");
+    if (rng->kind == KZ_RNG_HOST_INDEX && (!idx_scheme || !rng->indices))
+      return fail(KZ_ERR_INVALID, "host index streams are for urk / swor-erk");
+    if ((rng->kind == KZ_RNG_HOST_UNIFORM || rng->kind == KZ_RNG_HOST_INDEX) && rng->stream_len < 0)
+      return fail(KZ_ERR_INVALID, "negative stream_len");
+  }
+  if ((scheme == KZ_VR_OGRK) && (!prob->coupled_ptr || !prob->coupled_idx))
+    return fail(KZ_ERR_INVALID, "vr-ogrk needs the coupled sets");
+  if ((scheme == KZ_VR_OAHK) && (!prob->orth_ptr || !prob->non_ptr || !prob->non_union_size))
+    return fail(KZ_ERR_INVALID, "vr-oahk needs the orthogonal / non-orthogonal partition");
+  if (!out->v) return fail(KZ_ERR_INVALID, "out->v must be non-null");
+  if (prob->n_systems == 0) return KZ_OK;
+  size_t need = kz_solve_workspace_bytes(prob, stop);
+  if (!workspace || workspace_bytes < need)
+    return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+
+  cudaStream_t s = (cudaStream_t)stream;
+  const int K = prob->n_users;
+  // fast path: fixed-T lockstep over contiguous supports (kz_solve_lockstep.cuh)
+  int fast = lockstep_try_launch(*prob, scheme, *stop, *rng, *out, s, &g_launches);
+  if (fast == 1) return cuda_check("kz_solve(lockstep)");
+  if (fast < 0) return fail(KZ_ERR_CUDA, "lockstep launch failed");
+
+  const int nw = GEN_WARPS;
+  size_t cs = prob->dtype == KZ_C128 ? 16 : 8;
+  size_t smem = (size_t)nw * 2 * K * sizeof(double) + (size_t)nw * K * cs;
+  GenLayout L = gen_layout(prob->n_systems, K, prob->n_antennas, prob->dtype);
+  if (prob->dtype == KZ_C128) {
+    Gen<double2> g{*prob, *stop, *rng, *out, scheme, (char*)workspace, L};
+    cudaFuncSetAttribute(kz_generic_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kz_generic_kernel<double2><<<prob->n_systems, nw * 32, smem, s>>>(g, resume);
+  } else {
+    Gen<float2> g{*prob, *stop, *rng, *out, scheme, (char*)workspace, L};
+    cudaFuncSetAttribute(kz_generic_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kz_generic_kernel<float2><<<prob->n_systems, nw * 32, smem, s>>>(g, resume);
+  }
+  g_launches = 1;
+  return cuda_check("kz_solve(generic)");
+}
+
+size_t kz_rzf_workspace_bytes(const kz_problem* prob) {
+  if (!prob) return 0;
+  return kz_align((size_t)prob->n_systems * 2 * prob->n_users * prob->n_users * sizeof(double2));
+}
+
+int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_out, uint8_t* pd_ok, void* workspace,
+           size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int st = check_problem(prob);
+  if (st) return st;
+  if (!v_out) return fail(KZ_ERR_INVALID, "v_out must be non-null");
+  if (prob->n_systems == 0) return KZ_OK;
+  size_t need = kz_rzf_workspace_bytes(prob);
+  if (!workspace || workspace_bytes < need)
+    return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prob->dtype == KZ_C128)
+    kz_rzf_kernel<double2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(*prob, v_out, f_out, beta_out, pd_ok, (double2*)workspace);
+  else
+    kz_rzf_kernel<float2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(*prob, v_out, f_out, beta_out, pd_ok, (double2*)workspace);
+  g_launches = 1;
+  return cuda_check("kz_rzf");
+}
+
+size_t kz_epilogue_workspace_bytes(const kz_problem* prob) {
+  if (!prob) return 0;
+  return kz_align((size_t)prob->n_systems * prob->n_users * prob->n_users * sizeof(double2));
+}
+
+int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double* v_ref, const double* beta_ref,
+                const double* snr_linear, double* beta_out, double* nmse_out, double* rates_out, double* sum_rate_out,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  int st = check_problem(prob);
+  if (st) return st;
+  if (!v) return fail(KZ_ERR_INVALID, "v must be non-null");
+  if (v_ref && !beta_ref) return fail(KZ_ERR_INVALID, "v_ref needs beta_ref");
+  if (prob->n_systems == 0) return KZ_OK;
+  size_t need = snr_linear ? kz_epilogue_workspace_bytes(prob) : 0;
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prob->dtype == KZ_C128)
+    kz_epilogue_kernel<double2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(
+        *prob, (const double2*)v, (double2*)f_out, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out,
+        sum_rate_out, (double2*)workspace);
+  else
+    kz_epilogue_kernel<float2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(
+        *prob, (const float2*)v, (float2*)f_out, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out,
+        sum_rate_out, (double2*)workspace);
+  g_launches = 1;
+  return cuda_check("kz_epilogue");
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// Common device helpers for the batched Kaczmarz kernels (sm_100a).
+//
+// Complex values are interleaved (re, im) pairs: float2 for complex64 and
+// double2 for complex128.  Arithmetic follows the reference's numpy semantics
+// where it matters for row selection:
+//   * |z| as numpy's SIMD cabs: sqrt(fma(lo/hi, lo/hi, 1)) * hi
+//   * float64 sums of greedy weights as numpy's 8-accumulator pairwise sum
+//   * Generator.choice as searchsorted(cumsum(p)/cumsum(p)[-1], u, 'right')
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/kaczmarz_b200.h"
+
+namespace kz {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <class T> struct Cx;
+template <> struct Cx<float2> {
+  using real = float;
+  static __host__ __device__ __forceinline__ float2 make(float r, float i) { return make_float2(r, i); }
+};
+template <> struct Cx<double2> {
+  using real = double;
+  static __host__ __device__ __forceinline__ double2 make(double r, double i) { return make_double2(r, i); }
+};
+
+template <class T> __device__ __forceinline__ T cadd(T a, T b) { return Cx<T>::make(a.x + b.x, a.y + b.y); }
+template <class T> __device__ __forceinline__ T csub(T a, T b) { return Cx<T>::make(a.x - b.x, a.y - b.y); }
+// a * b
+template <class T> __device__ __forceinline__ T cmul(T a, T b) {
+  return Cx<T>::make(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
+}
+// acc += conj(a) * b
+template <class T> __device__ __forceinline__ T cfma_conj(T a, T b, T acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+// acc += a * b
+template <class T> __device__ __forceinline__ T cfma(T a, T b, T acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+template <class T> __device__ __forceinline__ T cscale(T a, typename Cx<T>::real s) { return Cx<T>::make(a.x * s, a.y * s); }
+template <class T> __device__ __forceinline__ T cdivr(T a, double e) {
+  using R = typename Cx<T>::real;
+  return Cx<T>::make(a.x / (R)e, a.y / (R)e);
+}
+template <class T> __device__ __forceinline__ double2 to_d2(T a) { return make_double2((double)a.x, (double)a.y); }
+template <class T> __device__ __forceinline__ T from_d2(double2 a) {
+  using R = typename Cx<T>::real;
+  return Cx<T>::make((R)a.x, (R)a.y);
+}
+template <class T> __device__ __forceinline__ T czero() { return Cx<T>::make(0, 0); }
+
+// numpy SIMD complex abs (verified bit-exact against np.abs on AVX-512 hosts).
+__device__ __forceinline__ double np_cabs(double re, double im) {
+  double a = fabs(re), b = fabs(im);
+  double hi = a > b ? a : b, lo = a > b ? b : a;
+  if (hi == 0.0) return 0.0;
+  double r = lo / hi;
+  return sqrt(fma(r, r, 1.0)) * hi;
+}
+__device__ __forceinline__ double np_abs2(double re, double im) {
+  double a = np_cabs(re, im);
+  return a * a;
+}
+
+template <class R> __device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+template <class T> __device__ __forceinline__ T warp_csum(T v) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  return v;
+}
+
+// numpy pairwise summation (umath loops, PW_BLOCKSIZE 128, 8-way unroll),
+// evaluated by one thread.  Blocks above 128 split at n/2 rounded down to a
+// multiple of 8, exactly as numpy does.
+__device__ inline double np_pairwise_block(const double* a, int m) {
+  if (m < 8) {
+    double res = 0.0;
+    for (int i = 0; i < m; ++i) res += a[i];
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int full = m - (m % 8);
+  for (int i = 8; i < full; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (int i = full; i < m; ++i) res += a[i];
+  return res;
+}
+__device__ inline double np_pairwise_sum(const double* a, int n) {
+  if (n <= 128) return np_pairwise_block(a, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+// ---------------------------------------------------------------- Philox4x32-10
+struct U4 { uint32_t x, y, z, w; };
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += W0;
+    k1 += W1;
+  }
+  return c;
+}
+// uniform double in [0, 1) with 53 random bits, keyed by (seed, system, rhs, draw)
+__device__ __forceinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t rhs, uint64_t draw) {
+  U4 c{(uint32_t)draw, (uint32_t)(draw >> 32), rhs, b};
+  U4 o = philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint64_t bits = ((uint64_t)o.x << 32 | o.y) >> 11;
+  return (double)bits * (1.0 / 9007199254740992.0);
+}
+
+}  // namespace kz

@@ -1,0 +1,542 @@
+"""GPU drop-in for the reference solver API (pkg/src/kaczprec/solvers.py).
+
+Public functions keep the reference names, arguments and return types:
+
+  run_precoding(scheme, sys, reference, epsilon=1e-6, max_iters=None, rng=None)   solvers.py:556
+  solve(scheme, sys, rhs, stop, rng=None) -> (state, trace)                       solvers.py:460
+  solve_all(scheme, sys, stop, rng=None) -> V                                     solvers.py:510
+
+and add batched entry points that take many systems at once:
+
+  solve_batch(dev_batch, scheme, ...)            one kz_solve call over B systems
+  run_precoding_batched(scheme, batch, ...)      solve + epilogue (F, NMSE, sum-rate)
+
+Every call runs `kz_solve` from libkaczmarz_b200.so; there is no CPU path.
+Random row choices consume the caller's numpy Generator exactly as the
+reference does (one `rng.spawn(K)` child per rhs; one `random()` per
+greedy-weighted pick, one `integers(K)` per uniform pick, the energy-swor pool
+draws) — the draws are evaluated on the host in chunks and streamed to the
+device, so row sequences match the reference's.  `rng=("philox", seed)`
+instead draws on the device (throughput mode; no reference counterpart).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .batch import DeviceBatch, HostBatch
+from .vrgraph import UserPartition, build_partition
+
+SCHEMES = ("urk", "swor-erk", "gk", "grk", "vr-ogrk", "ahk", "vr-oahk")
+STOCHASTIC_SCHEMES = frozenset({"urk", "swor-erk", "grk", "vr-ogrk"})
+VR_SCHEMES = frozenset({"vr-ogrk", "vr-oahk"})
+_UNIFORM_SCHEMES = frozenset({"grk", "vr-ogrk"})
+
+
+def canonical_scheme(name: str) -> str:
+    """solvers.py:48-52."""
+    low = name.strip().lower()
+    if low not in SCHEMES:
+        raise ValueError(f"unknown scheme {name!r}; expected one of {SCHEMES}")
+    return low
+
+
+def display_scheme(name: str) -> str:
+    return canonical_scheme(name).upper()
+
+
+# ---------------------------------------------------------------------------
+# problem description (solvers.py:59-109)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class AugmentedSystem:
+    channel: object
+    reg: float
+    row_energies: np.ndarray
+    supports: tuple
+    eff_rows: tuple
+    h_adj: np.ndarray
+    partition: UserPartition
+
+    @classmethod
+    def from_channel(cls, chan, reg: float) -> "AugmentedSystem":
+        if reg < 0.0:
+            raise ValueError("regularisation must be non-negative")
+        if chan.n_users < 1:
+            raise ValueError("need at least one user")
+        supports, eff = [], []
+        for k, vr in enumerate(chan.vrs):
+            idx = vr.antenna_indices
+            outside = np.delete(chan.h[:, k], idx)
+            if outside.size and np.any(outside != 0.0):
+                raise ValueError(f"column {k} is nonzero outside its visibility region")
+            supports.append(idx)
+            eff.append(np.ascontiguousarray(chan.h[idx, k]))
+        energies = np.array([np.sum(np.abs(e) ** 2) for e in eff]) + reg
+        if np.any(energies == 0.0):
+            raise ValueError("zero-energy row: empty channel with reg = 0")
+        return cls(channel=chan, reg=float(reg), row_energies=energies, supports=tuple(supports),
+                   eff_rows=tuple(eff), h_adj=np.ascontiguousarray(chan.h.conj().T),
+                   partition=build_partition(chan.vrs))
+
+    @property
+    def n_users(self) -> int:
+        return self.channel.h.shape[1]
+
+    @property
+    def n_antennas(self) -> int:
+        return self.channel.h.shape[0]
+
+
+@dataclass
+class StoppingRule:
+    """solvers.py:426-450."""
+
+    mode: str = "oracle"
+    epsilon: float = 1e-6
+    reference: np.ndarray | None = None
+    max_iters: int | None = None
+    check_every: int = 1
+
+    def __post_init__(self):
+        if self.mode not in ("oracle", "residual"):
+            raise ValueError(f"unknown stopping mode {self.mode!r}")
+        if self.epsilon <= 0.0:
+            raise ValueError("epsilon must be positive")
+        if self.check_every < 1:
+            raise ValueError("check_every must be >= 1")
+
+
+class FlopCounter:
+    """metrics.py:25-41 (totals come back from the device)."""
+
+    __slots__ = ("total",)
+
+    def __init__(self, total: int = 0):
+        self.total = int(total)
+
+
+@dataclass
+class SolverState:
+    rhs: int
+    col: np.ndarray
+    coef: np.ndarray
+    resid: np.ndarray
+    counter: FlopCounter = field(default_factory=FlopCounter)
+    iters: int = 0
+    noop_steps: int = 0
+
+
+@dataclass
+class RunTrace:
+    scheme: str
+    seed: int | None = None
+    nmse: list = field(default_factory=list)
+    resid: list = field(default_factory=list)
+    flops: list = field(default_factory=list)
+    n_iters: int = 0
+    converged: bool = True
+    flops_analytic: float | None = None
+    flops_measured: int | None = None
+    sum_rate: float | None = None
+
+
+@dataclass
+class PrecodingRun:
+    """solvers.py:540-553."""
+
+    scheme: str
+    v: np.ndarray
+    precoder: object
+    n_iters: int
+    converged: bool
+    nmse_trace: list
+    resid_trace: list
+    flops_trace: list
+    flops_measured: int
+    noop_steps: int
+
+
+# ---------------------------------------------------------------------------
+# host-evaluated row streams
+# ---------------------------------------------------------------------------
+
+class HostStreams:
+    """Draw the reference's random row decisions chunk by chunk.
+
+    gens[b][c] is the Generator the reference's InstanceRun for (system b, rhs c)
+    would hold.  Per chunk, each rhs yields `n` draws:
+      grk / vr-ogrk : Generator.random()           (solvers.py:237, via choice)
+      urk           : Generator.integers(K)         (solvers.py:219)
+      swor-erk      : pool pick index                (solvers.py:224-230)
+    """
+
+    def __init__(self, scheme: str, gens, energies: np.ndarray):
+        self.scheme = scheme
+        self.gens = gens
+        self.energies = energies  # (B, K)
+        b, k = energies.shape
+        self.pools = [[[] for _ in range(k)] for _ in range(b)]
+
+    @property
+    def kind(self):
+        return _lib.RNG_HOST_UNIFORM if self.scheme in _UNIFORM_SCHEMES else _lib.RNG_HOST_INDEX
+
+    def chunk(self, n: int, active=None) -> np.ndarray:
+        b, k = self.energies.shape
+        if self.kind == _lib.RNG_HOST_UNIFORM:
+            out = np.zeros((b, k, n), dtype=np.float64)
+        else:
+            out = np.zeros((b, k, n), dtype=np.int32)
+        for s in range(b):
+            for c in range(k):
+                g = self.gens[s][c]
+                if g is None or (active is not None and not active[s, c]):
+                    continue
+                if self.scheme in _UNIFORM_SCHEMES:
+                    out[s, c] = g.random(n)
+                elif self.scheme == "urk":
+                    out[s, c] = g.integers(k, size=n)
+                else:
+                    pool = self.pools[s][c]
+                    e = self.energies[s]
+                    for t in range(n):
+                        if not pool:
+                            pool.extend(range(k))
+                        w = e[pool]
+                        out[s, c, t] = pool.pop(int(g.choice(len(pool), p=w / w.sum())))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# batched solve (one kz_solve call, chunked only for host streams)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class BatchResult:
+    scheme: str
+    dev: DeviceBatch
+    v: object                 # torch (B, K, K) complex on device: v[b, i, c]
+    iters: object             # torch (B, K) int32
+    converged: object         # (B, K) uint8
+    done: object
+    noop_steps: object
+    flops: object             # (B, K) int64
+    n_outer: object           # (B,) int32
+    sys_converged: object     # (B,) uint8
+    rows: object = None       # (B, K, rows_cap) int32
+    nmse_trace: object = None
+    resid_trace: object = None
+    flops_trace: object = None
+    n_checks: object = None
+    workspace: object = None
+    launches: int = 0
+
+    def iterates(self):
+        """Device view of the iterate block M as (B, K rhs, Nt) complex."""
+        import torch
+        ptr = _lib.lib().kz_workspace_iterates(C.byref(self.dev.problem), self.workspace.data_ptr())
+        off = ptr - self.workspace.data_ptr()
+        b, k, nt = self.dev.n_systems, self.dev.n_users, self.dev.n_antennas
+        isz = 16 if self.dev.dtype == "c128" else 8
+        raw = self.workspace[off:off + b * k * nt * isz]
+        return raw.view(self.dev.complex_dtype).view(b, k, nt)
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_iters: int, epsilon: float = 0.0,
+                check_every: int = 1, f_ref=None, v_ref=None, rng=None, rows_cap: int = 0, trace_cap: int = 0,
+                rhs_mask=None, chunk: int | None = None, stream=None, workspace=None) -> BatchResult:
+    """Run `scheme` on every (system, rhs) of `dev` with one kz_solve launch.
+
+    mode: "lockstep" (run_precoding), "residual" / "oracle" (solve / solve_all).
+    rng : None, ("philox", seed), or a HostStreams.
+    """
+    import torch
+    scheme = canonical_scheme(scheme)
+    lb = _lib.lib()
+    b, k = dev.n_systems, dev.n_users
+    d = dev.device
+    cdt = dev.complex_dtype
+    mode_id = {"lockstep": _lib.STOP_LOCKSTEP, "residual": _lib.STOP_RESIDUAL, "oracle": _lib.STOP_ORACLE}[mode]
+    if scheme in STOCHASTIC_SCHEMES and rng is None:
+        raise ValueError(f"scheme {scheme!r} draws rows at random; pass an rng")
+
+    z = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=d)  # noqa: E731
+    res = BatchResult(scheme=scheme, dev=dev, v=z(b, k, k, dt=cdt), iters=z(b, k, dt=torch.int32),
+                      converged=z(b, k, dt=torch.uint8), done=z(b, k, dt=torch.uint8),
+                      noop_steps=z(b, k, dt=torch.int32), flops=z(b, k, dt=torch.int64),
+                      n_outer=z(b, dt=torch.int32), sys_converged=z(b, dt=torch.uint8))
+    paused = z(b, k, dt=torch.uint8)
+    if rows_cap:
+        res.rows = torch.full((b, k, rows_cap), -1, dtype=torch.int32, device=d)
+    if trace_cap:
+        n = b if mode == "lockstep" else b * k
+        res.nmse_trace = z(n, trace_cap, dt=torch.float64)
+        res.resid_trace = z(n, trace_cap, dt=torch.float64)
+        res.flops_trace = z(n, trace_cap, dt=torch.int64)
+        res.n_checks = z(b, k, dt=torch.int32)
+
+    stop = _lib.KzStop()
+    stop.mode = mode_id
+    stop.max_iters = int(max_iters)
+    stop.check_every = int(check_every)
+    stop.epsilon = float(epsilon)
+    keep = []
+    if f_ref is not None:
+        f_ref = torch.as_tensor(f_ref).to(device=d, dtype=torch.complex128).contiguous()
+        keep.append(f_ref)
+        stop.f_ref = f_ref.data_ptr()
+    if v_ref is not None:
+        v_ref = torch.as_tensor(v_ref).to(device=d, dtype=torch.complex128).contiguous()
+        keep.append(v_ref)
+        stop.v_ref = v_ref.data_ptr()
+    if rhs_mask is not None:
+        m = torch.as_tensor(np.asarray(rhs_mask, dtype=np.uint8)).to(d)
+        keep.append(m)
+        stop.rhs_mask = m.data_ptr()
+
+    out = _lib.KzOut()
+    out.v = res.v.data_ptr()
+    out.iters = res.iters.data_ptr()
+    out.converged = res.converged.data_ptr()
+    out.done = res.done.data_ptr()
+    out.noop_steps = res.noop_steps.data_ptr()
+    out.flops = res.flops.data_ptr()
+    out.n_outer = res.n_outer.data_ptr()
+    out.sys_converged = res.sys_converged.data_ptr()
+    out.paused = paused.data_ptr()
+    if rows_cap:
+        out.rows = res.rows.data_ptr()
+        out.rows_cap = rows_cap
+    if trace_cap:
+        out.trace_cap = trace_cap
+        out.nmse_trace = res.nmse_trace.data_ptr()
+        out.resid_trace = res.resid_trace.data_ptr()
+        out.flops_trace = res.flops_trace.data_ptr()
+        out.n_checks = res.n_checks.data_ptr()
+
+    need = lb.kz_solve_workspace_bytes(C.byref(dev.problem), C.byref(stop))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
+    res.workspace = workspace
+
+    rg = _lib.KzRng()
+    host = isinstance(rng, HostStreams)
+    if rng is None:
+        rg.kind = _lib.RNG_NONE
+    elif host:
+        rg.kind = rng.kind
+    else:
+        kind, seed = rng
+        if kind != "philox":
+            raise ValueError(f"unknown rng spec {rng!r}")
+        rg.kind = _lib.RNG_PHILOX
+        rg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    if host and scheme not in STOCHASTIC_SCHEMES:
+        host = False
+        rg.kind = _lib.RNG_NONE
+    sp = _stream_ptr(stream)
+    resume = 0
+    base = 0
+    if chunk is None:
+        chunk = int(max_iters) if mode == "lockstep" else min(int(max_iters), 1024)
+    launches = 0
+    active = np.ones((b, k), dtype=bool) if rhs_mask is None else np.asarray(rhs_mask, dtype=bool).reshape(b, k)
+    while True:
+        if host:
+            arr = torch.from_numpy(rng.chunk(chunk, active)).to(d)
+            keep.append(arr)
+            rg.stream_len = chunk
+            rg.stream_base = base
+            if rg.kind == _lib.RNG_HOST_UNIFORM:
+                rg.uniforms = arr.data_ptr()
+            else:
+                rg.indices = arr.data_ptr()
+        _lib.check(lb.kz_solve(C.byref(dev.problem), _lib.SCHEME_IDS[scheme], C.byref(stop), C.byref(rg),
+                               C.byref(out), workspace.data_ptr(), workspace.numel(), resume, sp))
+        launches += lb.kz_last_launch_count()
+        if not host:
+            break
+        pz = paused.cpu().numpy().astype(bool)
+        if not pz.any():
+            break
+        active = pz
+        paused.zero_()
+        base += chunk
+        resume = 1
+    res.launches = launches
+    res._keep = keep
+    return res
+
+
+# ---------------------------------------------------------------------------
+# flop bookkeeping that happens outside the kernels (run_precoding :579, :604-611)
+# ---------------------------------------------------------------------------
+
+def _assembly_flops_vr(sys) -> int:
+    """assemble_vr counter charges for the channel's subarray grid (assembly.py:74-92)."""
+    chan = sys.channel
+    k = sys.n_users
+    m = chan.cfg.subarray_size
+    tot = 0
+    for s in range(chan.cfg.n_subarrays):
+        q = sum(1 for vr in chan.vrs if s in vr.visible_subarrays)
+        if q:
+            tot += 6 * m * q * k + 2 * m * (q - 1) * k
+    return tot
+
+
+def _assembly_flops_dense(nt: int, k: int) -> int:
+    return 6 * nt * k * k + 2 * nt * k * (k - 1)
+
+
+def _gens_for(rng, k):
+    return rng.spawn(k) if rng is not None else [None] * k
+
+
+def _f_ref_of(reference):
+    return reference.f if hasattr(reference, "f") else np.asarray(reference)
+
+
+# ---------------------------------------------------------------------------
+# reference-signature entry points
+# ---------------------------------------------------------------------------
+
+def run_precoding(scheme: str, sys, reference, epsilon: float = 1e-6, max_iters: int | None = None,
+                  rng: np.random.Generator | None = None) -> PrecodingRun:
+    """Lockstep K-rhs run with NMSE stopping (solvers.py:556-623), on the GPU."""
+    import torch
+    from .assembly import epilogue
+    from .rzf import Precoder
+    scheme = canonical_scheme(scheme)
+    k, nt = sys.n_users, sys.n_antennas
+    cap = max_iters if max_iters is not None else 10_000 * k
+    host = HostBatch.from_systems([sys])
+    dev = host.to_device("c128")
+    f_ref = np.asarray(_f_ref_of(reference), dtype=np.complex128)[None]
+    streams = None
+    if scheme in STOCHASTIC_SCHEMES:
+        if rng is None:
+            raise ValueError(f"scheme {scheme!r} draws rows at random; pass an rng")
+        streams = HostStreams(scheme, [_gens_for(rng, k)], host.row_energy.reshape(1, k))
+    res = solve_batch(dev, scheme, mode="lockstep", max_iters=cap, epsilon=epsilon, f_ref=f_ref, rng=streams,
+                      trace_cap=cap)
+    t = int(res.n_outer[0])
+    setup = 4 * nt * k
+    v = res.v[0].cpu().numpy()
+    ep = epilogue(dev, res.v, want_f=True)
+    f = ep["f"][0].cpu().numpy()
+    asm = _assembly_flops_vr(sys) if scheme in VR_SCHEMES else _assembly_flops_dense(nt, k)
+    flops_rhs = int(res.flops[0].sum())
+    return PrecodingRun(
+        scheme=display_scheme(scheme), v=v,
+        precoder=Precoder(f=f, norm_factor=float(ep["beta"][0]), scheme=display_scheme(scheme)),
+        n_iters=t, converged=bool(res.sys_converged[0]),
+        nmse_trace=res.nmse_trace[0, :t].cpu().tolist(), resid_trace=res.resid_trace[0, :t].cpu().tolist(),
+        flops_trace=[setup + int(x) for x in res.flops_trace[0, :t].cpu().tolist()],
+        flops_measured=setup + flops_rhs + asm, noop_steps=int(res.noop_steps[0].sum()))
+
+
+def _state_from(res: BatchResult, c: int) -> SolverState:
+    m = res.iterates()[0, c].cpu().numpy()
+    return SolverState(rhs=c, col=m, coef=res.v[0, :, c].cpu().numpy(), resid=np.zeros(res.dev.n_users, complex),
+                       counter=FlopCounter(int(res.flops[0, c])), iters=int(res.iters[0, c]),
+                       noop_steps=int(res.noop_steps[0, c]))
+
+
+def solve(scheme: str, sys, rhs: int, stop: StoppingRule, rng: np.random.Generator | None = None):
+    """Single-rhs run with oracle / residual stopping (solvers.py:460-507), on the GPU."""
+    scheme = canonical_scheme(scheme)
+    k = sys.n_users
+    if not 0 <= rhs < k:
+        raise ValueError(f"rhs index {rhs} out of range")
+    v_ref = None
+    if stop.mode == "oracle":
+        if stop.reference is None:
+            raise ValueError("oracle stopping needs the direct-solver reference column")
+        ref = np.asarray(stop.reference)
+        if float(np.linalg.norm(ref)) == 0.0:
+            raise ValueError("oracle reference column is zero")
+        v_ref = np.zeros((1, k, k), dtype=np.complex128)
+        v_ref[0, :, rhs] = ref
+    if scheme in STOCHASTIC_SCHEMES and rng is None:
+        raise ValueError(f"scheme {scheme!r} draws rows at random; pass an rng")
+    cap = stop.max_iters if stop.max_iters is not None else 10_000 * k
+    host = HostBatch.from_systems([sys])
+    dev = host.to_device("c128")
+    streams = None
+    if scheme in STOCHASTIC_SCHEMES:
+        gens = [[rng if c == rhs else None for c in range(k)]]
+        streams = HostStreams(scheme, gens, host.row_energy.reshape(1, k))
+    mask = np.zeros(k, dtype=np.uint8)
+    mask[rhs] = 1
+    cap_trace = max(1, cap // stop.check_every + 1)
+    res = solve_batch(dev, scheme, mode=stop.mode, max_iters=cap, epsilon=stop.epsilon,
+                      check_every=stop.check_every, v_ref=v_ref, rng=streams, rhs_mask=mask,
+                      trace_cap=min(cap_trace, 1 << 20))
+    st = _state_from(res, rhs)
+    n = int(res.n_checks[0, rhs])
+    tr = RunTrace(scheme=display_scheme(scheme))
+    tr.resid = res.resid_trace[rhs, :n].cpu().tolist()
+    tr.flops = [int(x) for x in res.flops_trace[rhs, :n].cpu().tolist()]
+    if stop.mode == "oracle":
+        tr.nmse = res.nmse_trace[rhs, :n].cpu().tolist()
+    tr.n_iters = st.iters
+    tr.converged = bool(res.converged[0, rhs])
+    tr.flops_measured = st.counter.total
+    return st, tr
+
+
+def solve_all(scheme: str, sys, stop: StoppingRule, rng: np.random.Generator | None = None) -> np.ndarray:
+    """Per-column solves, rng.spawn(K) children (solvers.py:510-537), on the GPU."""
+    scheme = canonical_scheme(scheme)
+    k = sys.n_users
+    v_ref = None
+    if stop.mode == "oracle":
+        ref = np.asarray(stop.reference)
+        if ref.shape != (k, k):
+            raise ValueError(f"oracle reference must be (K, K), got {ref.shape}")
+        if np.any(np.linalg.norm(ref, axis=0) == 0.0):
+            raise ValueError("oracle reference column is zero")
+        v_ref = ref[None]
+    if scheme in STOCHASTIC_SCHEMES and rng is None:
+        raise ValueError(f"scheme {scheme!r} draws rows at random; pass an rng")
+    cap = stop.max_iters if stop.max_iters is not None else 10_000 * k
+    host = HostBatch.from_systems([sys])
+    dev = host.to_device("c128")
+    streams = None
+    if scheme in STOCHASTIC_SCHEMES:
+        streams = HostStreams(scheme, [_gens_for(rng, k)], host.row_energy.reshape(1, k))
+    res = solve_batch(dev, scheme, mode=stop.mode, max_iters=cap, epsilon=stop.epsilon,
+                      check_every=stop.check_every, v_ref=v_ref, rng=streams)
+    return res.v[0].cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# batched precoding (the throughput entry point)
+# ---------------------------------------------------------------------------
+
+def run_precoding_batched(scheme: str, dev: DeviceBatch, *, max_iters: int, rng=None, epsilon: float = 0.0,
+                          f_ref=None, v_ref=None, beta_ref=None, rates: bool = True, want_f: bool = False,
+                          rows_cap: int = 0, stream=None, workspace=None) -> dict:
+    """Fixed-T (epsilon = 0) or NMSE-stopped lockstep precoding of every system in `dev`,
+    followed by the fused epilogue (F = beta H V, NMSE vs beta_ref H V_ref, Eq. (7) rates)."""
+    from .assembly import epilogue
+    res = solve_batch(dev, scheme, mode="lockstep", max_iters=max_iters, epsilon=epsilon, f_ref=f_ref, rng=rng,
+                      rows_cap=rows_cap, stream=stream, workspace=workspace)
+    ep = epilogue(dev, res.v, v_ref=v_ref, beta_ref=beta_ref, rates=rates, want_f=want_f, stream=stream)
+    out = {"solve": res, **ep}
+    out["launches"] = res.launches + ep["launches"]
+    return out

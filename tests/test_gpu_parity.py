@@ -1,0 +1,377 @@
+"""GPU parity: libkaczmarz_b200.so against the CPU oracle and the committed
+reference fixtures.
+
+Tolerances (BASELINE.json north_star):
+  complex128 oracle mode  - selected row sequences identical; iterates within
+                            1e-10 relative (Frobenius) of the reference.
+  complex64 throughput    - final NMSE against RZF and sum-rate within 1e-3
+                            relative, NMSE compared only above the fp32 floor
+                            (NMSE_128 >= 1e-5; below it NMSE_64 <= 1e-6), per
+                            SURVEY.md §9.7, with the same host streams.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import contiguous_from_fixture, load, oracle_channel_contiguous, oracle_channel_from_mask
+
+pytestmark = pytest.mark.gpu
+
+REL_C128 = 1e-10
+REL_C64 = 1e-3
+
+
+def _kz():
+    import paper_2501_10689_b200 as kz
+    return kz
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (n if n > 0 else 1.0)
+
+
+def run_rows(sys_list, scheme, T, rngs, dtype="c128", epsilon=0.0, f_ref=None, spawn=True):
+    """Lockstep run of a list of systems; returns (BatchResult, DeviceBatch)."""
+    kz = _kz()
+    host = kz.HostBatch.from_systems(sys_list)
+    dev = host.to_device(dtype)
+    k = host.n_users
+    streams = None
+    if scheme in kz.STOCHASTIC_SCHEMES:
+        gens = [r.spawn(k) if spawn else r for r in rngs]
+        streams = kz.HostStreams(scheme, gens, host.row_energy.reshape(host.n_systems, k))
+    res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, epsilon=epsilon, f_ref=f_ref,
+                         rng=streams, rows_cap=T)
+    return res, dev
+
+
+def assert_rows(res_rows, want_rows, b):
+    got = res_rows[b].cpu().numpy()
+    for c in range(got.shape[0]):
+        g = got[c][got[c] >= 0]
+        w = np.asarray(want_rows[c])
+        w = w[w >= 0]
+        np.testing.assert_array_equal(g, w, err_msg=f"rhs {c}")
+
+
+# --------------------------------------------------------------------------- c128 parity
+
+@pytest.mark.parametrize("scheme", O.SCHEMES)
+def test_lockstep_nmse_stop_matches_reference(scheme):
+    """run_precoding(eps=1e-6, rng=42) on the reference test drop: iteration count, V,
+    flops, noop steps, traces and row sequences (tests/test_solvers.py:505-523)."""
+    kz = _kz()
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    reg = float(z["reg"])
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    ref = O.rzf_precoder(chan, reg)
+    run = kz.run_precoding(scheme, sys_, ref, epsilon=1e-6, rng=np.random.default_rng(42))
+    assert run.n_iters == int(z[f"{scheme}/n_iters"])
+    assert run.converged
+    assert rel(run.v, z[f"{scheme}/v"]) <= REL_C128
+    assert run.flops_measured == int(z[f"{scheme}/flops_measured"])
+    assert run.noop_steps == int(z[f"{scheme}/noop_steps"])
+    np.testing.assert_array_equal(run.flops_trace, z[f"{scheme}/flops_trace"])
+    np.testing.assert_allclose(run.nmse_trace, z[f"{scheme}/nmse_trace"], rtol=1e-7, atol=1e-14)
+    np.testing.assert_allclose(run.resid_trace, z[f"{scheme}/resid_trace"], rtol=1e-7, atol=1e-13)
+    assert rel(run.precoder.f, z[f"{scheme}/f"]) <= REL_C128
+    res, _ = run_rows([sys_], scheme, int(z[f"{scheme}/n_iters"]), [np.random.default_rng(42)])
+    assert_rows(res.rows, z[f"{scheme}/rows"], 0)
+
+
+def test_fixed_t_batch_matches_reference():
+    """Four conftest-scale drops batched in one launch per scheme, T = 15."""
+    kz = _kz()
+    z = load("ref_fixed_t.npz")
+    systems, chans = [], []
+    for seed in range(4):
+        chan = oracle_channel_from_mask(z[f"{seed}/h"], z[f"{seed}/vr_mask"], 4)
+        chans.append(chan)
+        systems.append(O.AugmentedSystem.from_channel(chan, float(z[f"{seed}/reg"])))
+    for sc in O.SCHEMES:
+        rngs = [np.random.default_rng(100 + s) for s in range(4)]
+        res, dev = run_rows(systems, sc, 15, rngs)
+        ep = kz.epilogue(dev, res.v, want_f=True, rates=True,
+                         snr_linear=np.array([1.0 / float(z[f"{s}/reg"]) for s in range(4)]))
+        for s in range(4):
+            assert rel(res.v[s].cpu().numpy(), z[f"{s}/{sc}/v"]) <= REL_C128, (sc, s)
+            assert_rows(res.rows, z[f"{s}/{sc}/rows"], s)
+            assert rel(ep["f"][s].cpu().numpy(), z[f"{s}/{sc}/f"]) <= REL_C128
+            assert float(ep["sum_rate"][s]) == pytest.approx(float(z[f"{s}/{sc}/sum_rate"]), rel=1e-10)
+
+
+@pytest.mark.parametrize("mode,eps", [("residual", 1e-8), ("oracle", 1e-6)])
+def test_solve_all_modes_match_reference(mode, eps):
+    kz = _kz()
+    z = load("ref_solve.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], 8)
+    sys_ = O.AugmentedSystem.from_channel(chan, float(z["reg"]))
+    vref = z["v_ref"]
+    for sc in O.SCHEMES:
+        key = f"{mode}/{sc}"
+        stop = kz.StoppingRule(mode=mode, epsilon=eps, reference=vref if mode == "oracle" else None,
+                               check_every=2)
+        v = kz.solve_all(sc, sys_, stop, rng=np.random.default_rng(7))
+        assert rel(v, z[f"{key}/v"]) <= REL_C128, sc
+        host = kz.HostBatch.from_systems([sys_])
+        dev = host.to_device("c128")
+        streams = None
+        if sc in kz.STOCHASTIC_SCHEMES:
+            streams = kz.HostStreams(sc, [np.random.default_rng(7).spawn(8)], host.row_energy.reshape(1, 8))
+        res = kz.solve_batch(dev, sc, mode=mode, max_iters=80_000, epsilon=eps, check_every=2,
+                             v_ref=vref[None] if mode == "oracle" else None, rng=streams, rows_cap=4096,
+                             trace_cap=4096, chunk=64)
+        np.testing.assert_array_equal(res.iters[0].cpu().numpy(), z[f"{key}/iters"])
+        np.testing.assert_array_equal(res.converged[0].cpu().numpy().astype(bool), z[f"{key}/converged"])
+        np.testing.assert_array_equal(res.n_checks[0].cpu().numpy(), z[f"{key}/n_checks"])
+        assert_rows(res.rows, z[f"{key}/rows"], 0)
+
+
+def test_single_rhs_solve_frozen_counts():
+    """tests/test_solvers.py:435-446 through the GPU `solve`: gk 32, urk 93."""
+    kz = _kz()
+    cfg = O.ArrayConfig(64, 100e9, 8)
+    chan, reg = O.power_control(O.random_channel(cfg, 8, 5, 0.5, np.random.default_rng(0)), 0.0)
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    vref = O.auxiliary_matrix(chan, reg)
+    st, tr = kz.solve("gk", sys_, 0, kz.StoppingRule(epsilon=1e-6, reference=vref[:, 0]))
+    assert tr.n_iters == 32 and tr.converged
+    st, tr = kz.solve("urk", sys_, 0, kz.StoppingRule(epsilon=1e-6, reference=vref[:, 0]),
+                      rng=np.random.default_rng(7))
+    assert tr.n_iters == 93
+    ost, otr = O.solve("urk", sys_, 0, O.StoppingRule(epsilon=1e-6, reference=vref[:, 0]),
+                       rng=np.random.default_rng(7))
+    assert rel(st.coef, ost.coef) <= REL_C128
+    assert rel(st.col, ost.col) <= REL_C128
+    assert st.counter.total == ost.counter.total
+    np.testing.assert_allclose(tr.resid, otr.resid, rtol=1e-7, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", ["ref_cfg1.npz", "ref_cfg2.npz"])
+def test_config_parity_c128(name):
+    """BASELINE cfg1 (GRK, T=50) and cfg2 (5 schemes, T=200) shapes in complex128."""
+    kz = _kz()
+    z = load(name)
+    ch = contiguous_from_fixture(z)
+    T = int(z["n_iters"])
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device("c128")
+    b, k = host.n_systems, host.n_users
+    schemes = sorted({key.split("/")[1] for key in z.files if key.count("/") == 2})
+    for b_i in range(b):
+        assert np.array_equal(host.orth_idx[host.orth_ptr[b_i]:host.orth_ptr[b_i + 1]], z[f"{b_i}/orthogonal"])
+    v_ref = np.stack([z[f"{i}/v_ref"] for i in range(b)])
+    beta_ref = np.array([float(z[f"{i}/beta_ref"]) for i in range(b)])
+    rz = kz.rzf_batched(dev)
+    assert rel(rz["v"].cpu().numpy(), v_ref) <= REL_C128
+    np.testing.assert_allclose(rz["beta"].cpu().numpy(), beta_ref, rtol=1e-12)
+    for sc in schemes:
+        streams = None
+        if sc in kz.STOCHASTIC_SCHEMES:
+            gens = [np.random.default_rng(kz.solver_seed_sequence(int(s))).spawn(k) for s in z["seeds"]]
+            streams = kz.HostStreams(sc, gens, host.row_energy.reshape(b, k))
+        res = kz.solve_batch(dev, sc, mode="lockstep", max_iters=T, rng=streams, rows_cap=T)
+        ep = kz.epilogue(dev, res.v, v_ref=v_ref, beta_ref=beta_ref, rates=True)
+        for b_i in range(b):
+            assert rel(res.v[b_i].cpu().numpy(), z[f"{b_i}/{sc}/v"]) <= REL_C128, (sc, b_i)
+            assert_rows(res.rows, z[f"{b_i}/{sc}/rows"], b_i)
+            assert float(ep["nmse"][b_i]) == pytest.approx(float(z[f"{b_i}/{sc}/nmse"]), rel=1e-6, abs=1e-13)
+            assert float(ep["sum_rate"][b_i]) == pytest.approx(float(z[f"{b_i}/{sc}/sum_rate"]), rel=1e-10)
+
+
+# --------------------------------------------------------------------------- c64 throughput mode
+
+def _c64_ok(n64, n128, s64, s128):
+    assert s64 == pytest.approx(s128, rel=REL_C64)
+    if n128 >= 1e-5:
+        assert n64 == pytest.approx(n128, rel=REL_C64)
+    else:
+        assert n64 <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["ref_cfg1.npz", "ref_cfg2.npz"])
+def test_config_parity_c64(name):
+    kz = _kz()
+    z = load(name)
+    ch = contiguous_from_fixture(z)
+    T = int(z["n_iters"])
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device("c64")
+    b, k = host.n_systems, host.n_users
+    v_ref = np.stack([z[f"{i}/v_ref"] for i in range(b)])
+    beta_ref = np.array([float(z[f"{i}/beta_ref"]) for i in range(b)])
+    schemes = sorted({key.split("/")[1] for key in z.files if key.count("/") == 2})
+    for sc in schemes:
+        streams = None
+        if sc in kz.STOCHASTIC_SCHEMES:
+            gens = [np.random.default_rng(kz.solver_seed_sequence(int(s))).spawn(k) for s in z["seeds"]]
+            streams = kz.HostStreams(sc, gens, host.row_energy.reshape(b, k))
+        out = kz.run_precoding_batched(sc, dev, max_iters=T, rng=streams, v_ref=v_ref, beta_ref=beta_ref)
+        for b_i in range(b):
+            _c64_ok(float(out["nmse"][b_i]), float(z[f"{b_i}/{sc}/nmse"]),
+                    float(out["sum_rate"][b_i]), float(z[f"{b_i}/{sc}/sum_rate"]))
+
+
+# --------------------------------------------------------------------------- RZF / epilogue
+
+def test_rzf_frozen_entries_gpu():
+    kz = _kz()
+    rng = np.random.default_rng(1234)
+    h = (rng.standard_normal((8, 3)) + 1j * rng.standard_normal((8, 3))) / np.sqrt(2)
+    v = kz.auxiliary_matrix(h, 0.4)
+    assert v[0, 0] == pytest.approx(0.08743823337750342 + 0j, abs=1e-10)
+    assert v[1, 2] == pytest.approx(-0.00047276679288917284 - 0.0117275702144454j, abs=1e-10)
+    prec = kz.rzf_precoder(h, 0.4)
+    assert prec.norm_factor == pytest.approx(1.8189422748831143, rel=1e-10)
+    assert prec.f[0, 0] == pytest.approx(-0.16744310691337447 + 0.09294283936181302j, abs=1e-10)
+    assert np.linalg.norm(prec.f) == pytest.approx(1.0, abs=1e-12)
+    np.testing.assert_allclose(v, O.auxiliary_matrix(h, 0.4), rtol=0, atol=1e-13)
+
+
+def test_rzf_not_pd_raises():
+    kz = _kz()
+    with pytest.raises(Exception):
+        kz.rzf_precoder(np.zeros((6, 2), dtype=complex), 0.0)
+
+
+def test_rzf_on_vr_drops_matches_oracle():
+    kz = _kz()
+    for seed in range(5):
+        chan, reg = O.power_control(O.random_channel(O.ArrayConfig(32, 100e9, 4), 4, 3, 0.6,
+                                                     np.random.default_rng(seed)), 0.0)
+        p = kz.rzf_precoder(chan, reg)
+        q = O.rzf_precoder(chan, reg)
+        assert rel(p.f, q.f) <= 1e-12
+        assert p.norm_factor == pytest.approx(q.norm_factor, rel=1e-12)
+
+
+def test_assembly_and_metrics_match_oracle():
+    kz = _kz()
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    v = z["gk/v"]
+    a = kz.assemble_vr(chan, v, scheme="GK")
+    b = O.assemble_vr(chan, v)
+    c = kz.assemble_dense(chan, v)
+    assert rel(a.f, b.f) <= 1e-13 and rel(c.f, b.f) <= 1e-13
+    assert a.norm_factor == pytest.approx(b.norm_factor, rel=1e-13)
+    assert kz.nmse(a.f, z["f_ref"]) == pytest.approx(O.nmse(b.f, z["f_ref"]), rel=1e-9)
+    r1, s1 = kz.spectral_efficiency(chan.h, a.f, 1.0)
+    r2, s2 = O.spectral_efficiency(chan.h, b.f, 1.0)
+    np.testing.assert_allclose(r1, r2, rtol=1e-12)
+
+
+# --------------------------------------------------------------------------- edge cases
+
+def test_single_user_one_iteration_all_schemes():
+    """tests/test_solvers.py:396-406: K = 1 converges in one iteration for every scheme."""
+    kz = _kz()
+    cfg = O.ArrayConfig(8, 1e9, 2)
+    chan, reg = O.power_control(O.random_channel(cfg, 1, 2, 1.0, np.random.default_rng(0)), 0.0)
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    expect = 1.0 / (np.linalg.norm(chan.h[:, 0]) ** 2 + reg)
+    for sc in O.SCHEMES:
+        st, tr = kz.solve(sc, sys_, 0, kz.StoppingRule(epsilon=1e-9, reference=np.array([expect])),
+                          rng=np.random.default_rng(5))
+        assert tr.n_iters == 1, sc
+        assert st.coef[0] == pytest.approx(expect, rel=1e-12)
+
+
+def test_disjoint_vrs_vr_oahk_one_iteration():
+    """tests/test_solvers.py:449-469: all users orthogonal -> the block step solves outright (N empty)."""
+    kz = _kz()
+    nt, k = 16, 4
+    rng = np.random.default_rng(4)
+    h = np.zeros((nt, k), dtype=complex)
+    for i in range(k):
+        h[4 * i:4 * i + 4, i] = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    h /= np.linalg.norm(h, axis=0)
+    cfg = O.ArrayConfig(nt, 1e9, 4)
+    vrs = tuple(O.VisibilityRegion(frozenset({i}), 4, 4) for i in range(k))
+    chan = O.ChannelMatrix(h=h, vrs=vrs, cfg=cfg)
+    sys_ = O.AugmentedSystem.from_channel(chan, 1.0)
+    vref = O.auxiliary_matrix(chan, 1.0)
+    _, tr = kz.solve("vr-oahk", sys_, 0, kz.StoppingRule(epsilon=1e-9, reference=vref[:, 0]))
+    assert tr.n_iters == 1
+    run = kz.run_precoding("vr-oahk", sys_, O.rzf_precoder(chan, 1.0), epsilon=1e-9)
+    assert run.n_iters == 1 and run.converged
+
+
+def test_ragged_vr_lengths_cfg3_shape():
+    """cfg3-style ragged VR lengths (U[128,512]) at reduced B: VR-OAHK c128 vs oracle."""
+    kz = _kz()
+    ch = kz.generate("cfg3", [0, 1])
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device("c128")
+    res = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20)
+    for b in range(2):
+        chan = oracle_channel_contiguous(ch, b)
+        sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+        run = O.run_precoding("vr-oahk", sys_, O.rzf_precoder(chan, float(ch.reg[b])), epsilon=0.0,
+                              max_iters=20, traces=False)
+        assert rel(res.v[b].cpu().numpy(), run.v) <= REL_C128
+        assert int(res.noop_steps[b].sum()) == run.noop_steps
+
+
+def test_rhs_mask_leaves_other_columns_untouched():
+    kz = _kz()
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    sys_ = O.AugmentedSystem.from_channel(chan, float(z["reg"]))
+    dev = kz.HostBatch.from_systems([sys_]).to_device("c128")
+    mask = np.zeros(8, dtype=np.uint8)
+    mask[3] = 1
+    res = kz.solve_batch(dev, "gk", mode="residual", max_iters=1000, epsilon=1e-8, rhs_mask=mask)
+    v = res.v[0].cpu().numpy()
+    assert np.all(v[:, [0, 1, 2, 4, 5, 6, 7]] == 0)
+    assert int(res.iters[0, 3]) > 0 and bool(res.converged[0, 3])
+
+
+def test_invalid_arguments_raise():
+    kz = _kz()
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    sys_ = O.AugmentedSystem.from_channel(chan, float(z["reg"]))
+    ref = O.rzf_precoder(chan, float(z["reg"]))
+    with pytest.raises(ValueError):
+        kz.run_precoding("bogus", sys_, ref)
+    with pytest.raises(ValueError):
+        kz.run_precoding("grk", sys_, ref, rng=None)
+    with pytest.raises(ValueError):
+        kz.solve("gk", sys_, 0, kz.StoppingRule(mode="oracle", reference=None))
+    dev = kz.HostBatch.from_systems([sys_]).to_device("c128")
+    from paper_2501_10689_b200._lib import KzError
+    with pytest.raises(KzError):
+        kz.solve_batch(dev, "gk", mode="residual", max_iters=10, epsilon=0.0)
+
+
+# --------------------------------------------------------------------------- throughput-mode properties
+
+@pytest.mark.parametrize("scheme", ["urk", "grk", "vr-ogrk", "ahk", "vr-oahk", "gk", "swor-erk"])
+def test_philox_full_cfg2_properties(scheme):
+    """Full cfg2 shape (Nt=512, K=64) at B=148 in c64 with on-device draws:
+    col = H coef invariant, power-normalised F, finite rates, error contraction."""
+    import torch
+    kz = _kz()
+    ch = kz.generate("cfg2", range(148))
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device("c64")
+    rz = kz.rzf_batched(dev)
+    errs = []
+    for T in (25, 200):
+        res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rng=("philox", 1234))
+        ep = kz.epilogue(dev, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, want_f=True)
+        errs.append(ep["nmse"].cpu().numpy())
+        assert torch.isfinite(ep["sum_rate"]).all()
+        fn = torch.linalg.norm(ep["f"].reshape(dev.n_systems, -1), dim=1)
+        np.testing.assert_allclose(fn.cpu().numpy(), 1.0, rtol=1e-5)
+        # col = H coef: the workspace iterate equals H v
+        m = res.iterates()[:4].to(torch.complex128)
+        hv = kz.epilogue(dev, res.v, want_f=True)  # beta H V for every system
+        hv_f = hv["f"][:4].to(torch.complex128) / hv["beta"][:4, None, None]
+        assert rel(m.transpose(1, 2).cpu().numpy(), hv_f.cpu().numpy()) <= 1e-4
+    assert np.median(errs[1]) < np.median(errs[0])

@@ -1,0 +1,161 @@
+"""Pin the CPU oracle to the reference: committed fixtures from the real
+reference (tests/golden/make_golden.py) plus the reference tests' own frozen
+known answers.  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import contiguous_from_fixture, load, oracle_channel_contiguous, oracle_channel_from_mask
+
+SCHEMES = O.SCHEMES
+
+
+def test_frozen_lockstep_iteration_counts():
+    """tests/test_solvers.py:505-523 of the reference: urk 127 ... vr-oahk 8."""
+    cfg = O.ArrayConfig(64, 100e9, 8)
+    chan, reg = O.power_control(O.random_channel(cfg, 8, 5, 0.5, np.random.default_rng(0)), 0.0)
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    ref = O.rzf_precoder(chan, reg)
+    expected = {"urk": 127, "swor-erk": 56, "gk": 33, "grk": 37, "vr-ogrk": 37, "ahk": 10, "vr-oahk": 8}
+    flops = {}
+    for sc, t in expected.items():
+        run = O.run_precoding(sc, sys_, ref, epsilon=1e-6, rng=np.random.default_rng(42))
+        assert run.converged and run.n_iters == t, sc
+        flops[sc] = run.flops_measured
+    assert flops["vr-ogrk"] < 0.5 * flops["grk"]
+
+
+def test_frozen_single_rhs_counts():
+    """tests/test_solvers.py:435-446: gk 32, urk 93 (rng 7)."""
+    cfg = O.ArrayConfig(64, 100e9, 8)
+    chan, reg = O.power_control(O.random_channel(cfg, 8, 5, 0.5, np.random.default_rng(0)), 0.0)
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    vref = O.auxiliary_matrix(chan, reg)
+    _, tr = O.solve("gk", sys_, 0, O.StoppingRule(epsilon=1e-6, reference=vref[:, 0]))
+    assert tr.n_iters == 32
+    _, tr = O.solve("urk", sys_, 0, O.StoppingRule(epsilon=1e-6, reference=vref[:, 0]),
+                    rng=np.random.default_rng(7))
+    assert tr.n_iters == 93
+
+
+def test_rzf_frozen_entries():
+    """tests/test_rzf.py:33-51: seed-1234 8x3, xi = 0.4."""
+    rng = np.random.default_rng(1234)
+    h = (rng.standard_normal((8, 3)) + 1j * rng.standard_normal((8, 3))) / math.sqrt(2)
+    v = O.auxiliary_matrix(h, 0.4)
+    assert v[0, 0] == pytest.approx(0.08743823337750342 + 0j, abs=1e-10)
+    assert v[1, 2] == pytest.approx(-0.00047276679288917284 - 0.0117275702144454j, abs=1e-10)
+    prec = O.rzf_precoder(h, 0.4)
+    assert prec.norm_factor == pytest.approx(1.8189422748831143, rel=1e-10)
+    assert prec.f[0, 0] == pytest.approx(-0.16744310691337447 + 0.09294283936181302j, abs=1e-10)
+
+
+def test_sum_rate_hand_case():
+    """tests/test_metrics.py:63-70: every rate exactly 1."""
+    h = np.zeros((4, 2), dtype=complex)
+    h[0, 0] = h[1, 1] = 1.0
+    rates, total = O.spectral_efficiency(h, h / math.sqrt(2), 2.0)
+    np.testing.assert_allclose(rates, [1.0, 1.0], rtol=1e-14)
+    assert total == pytest.approx(2.0)
+
+
+def test_lockstep_fixture_bitwise():
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    reg = float(z["reg"])
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    ref = O.rzf_precoder(chan, reg)
+    np.testing.assert_allclose(ref.f, z["f_ref"], rtol=0, atol=1e-14)
+    for sc in SCHEMES:
+        run = O.run_precoding(sc, sys_, ref, epsilon=1e-6, rng=np.random.default_rng(42))
+        assert run.n_iters == int(z[f"{sc}/n_iters"]), sc
+        assert run.flops_measured == int(z[f"{sc}/flops_measured"]), sc
+        assert run.noop_steps == int(z[f"{sc}/noop_steps"]), sc
+        np.testing.assert_array_equal(run.v, z[f"{sc}/v"])
+        np.testing.assert_array_equal(np.asarray(run.flops_trace), z[f"{sc}/flops_trace"])
+        np.testing.assert_allclose(run.nmse_trace, z[f"{sc}/nmse_trace"], rtol=1e-12, atol=0)
+        rows = z[f"{sc}/rows"]
+        for c in range(8):
+            got = run.rows[c]
+            np.testing.assert_array_equal(got, rows[c, :len(got)])
+            assert np.all(rows[c, len(got):] == -1)
+
+
+def test_fixed_t_fixture():
+    z = load("ref_fixed_t.npz")
+    for seed in range(4):
+        chan = oracle_channel_from_mask(z[f"{seed}/h"], z[f"{seed}/vr_mask"], 4)
+        reg = float(z[f"{seed}/reg"])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        for sc in SCHEMES:
+            run = O.run_precoding(sc, sys_, ref, epsilon=0.0, max_iters=15,
+                                  rng=np.random.default_rng(100 + seed))
+            np.testing.assert_array_equal(run.v, z[f"{seed}/{sc}/v"])
+            assert run.flops_measured == int(z[f"{seed}/{sc}/flops_measured"])
+            _, sr = O.spectral_efficiency(chan.h, run.precoder.f, 1.0 / reg)
+            assert sr == pytest.approx(float(z[f"{seed}/{sc}/sum_rate"]), rel=1e-13)
+
+
+def test_solve_fixture():
+    z = load("ref_solve.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], 8)
+    reg = float(z["reg"])
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    vref = z["v_ref"]
+    for mode, eps in (("residual", 1e-8), ("oracle", 1e-6)):
+        for sc in SCHEMES:
+            traces = []
+            v = O.solve_all(sc, sys_, O.StoppingRule(mode=mode, epsilon=eps,
+                                                     reference=vref if mode == "oracle" else None,
+                                                     check_every=2),
+                            rng=np.random.default_rng(7), traces=traces)
+            key = f"{mode}/{sc}"
+            np.testing.assert_array_equal(v, z[f"{key}/v"])
+            np.testing.assert_array_equal([t.n_iters for t in traces], z[f"{key}/iters"])
+            np.testing.assert_array_equal([t.converged for t in traces], z[f"{key}/converged"])
+            np.testing.assert_array_equal([len(t.resid) for t in traces], z[f"{key}/n_checks"])
+
+
+@pytest.mark.parametrize("name", ["ref_cfg1.npz", "ref_cfg2.npz"])
+def test_config_fixtures(name):
+    z = load(name)
+    ch = contiguous_from_fixture(z)
+    iters = int(z["n_iters"])
+    schemes = sorted({k.split("/")[1] for k in z.files if k.count("/") == 2})
+    for b, seed in enumerate(z["seeds"]):
+        chan = oracle_channel_contiguous(ch, b)
+        reg = float(ch.reg[b])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        assert np.array_equal(np.asarray(sys_.partition.orthogonal_sorted), z[f"{b}/orthogonal"])
+        ref = O.rzf_precoder(chan, reg)
+        np.testing.assert_allclose(O.auxiliary_matrix(chan, reg), z[f"{b}/v_ref"], rtol=0, atol=1e-13)
+        for sc in schemes:
+            rng = np.random.default_rng(np.random.SeedSequence(entropy=int(seed), spawn_key=(1,)))
+            run = O.run_precoding(sc, sys_, ref, epsilon=0.0, max_iters=iters, rng=rng, traces=False)
+            np.testing.assert_array_equal(run.v, z[f"{b}/{sc}/v"])
+            rows = z[f"{b}/{sc}/rows"]
+            for c in range(ch.n_users):
+                np.testing.assert_array_equal(run.rows[c], rows[c, :len(run.rows[c])])
+
+
+def test_kaczplot_golden_csv():
+    """The reference's own cross-machine golden (pkg/kaczplot/tests/data/convergence.csv)."""
+    z = load("kaczplot_convergence.npz")
+    cfg = O.ArrayConfig(32, 100e9, 4)
+    for seed in (0, 1):
+        chan, reg = O.power_control(O.random_channel(cfg, 4, 5, 0.6, np.random.default_rng(seed)), 0.0)
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        for sc in SCHEMES:
+            rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(1,)))
+            run = O.run_precoding(sc, sys_, ref, epsilon=1e-6, max_iters=20_000, rng=rng)
+            want_n = z[f"{sc}/{seed}/nmse"]
+            assert run.n_iters == want_n.size, (sc, seed)
+            np.testing.assert_array_equal(run.flops_trace, z[f"{sc}/{seed}/flops"])
+            big = want_n > 1e-9
+            np.testing.assert_allclose(np.asarray(run.nmse_trace)[big], want_n[big], rtol=1e-9)
+            np.testing.assert_allclose(run.resid_trace, z[f"{sc}/{seed}/resid"], rtol=1e-8, atol=1e-14)
