@@ -90,7 +90,12 @@ typedef struct kz_problem {
   const int32_t* non_ptr;       /* [B+1] into non_idx; N_b ascending */
   const int32_t* non_idx;
   const int32_t* non_union_size;/* [B] |union of N_b supports| (flop charge of ahk_step) */
+  /* shape hints, set by the packer (trusted): enable the register-resident fast path */
+  int32_t max_support;          /* max_r |Gamma_r| */
+  int32_t flags;                /* KZ_PROBLEM_CONTIGUOUS: every row is exactly one segment */
 } kz_problem;
+
+#define KZ_PROBLEM_CONTIGUOUS 1
 
 typedef struct kz_stop {
   int32_t mode;         /* kz_stop_mode */

@@ -231,6 +231,9 @@ class DeviceBatch:
                      "coupled_ptr", "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"):
             ten = t[name]
             setattr(p, name, ten.data_ptr() if ten.numel() else None)
+        sup = np.diff(self.host.row_val_ptr)
+        p.max_support = int(sup.max()) if sup.size else 0
+        p.flags = 1 if self.host.contiguous else 0
         return p
 
     @property

@@ -62,7 +62,7 @@ size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop) {
   (void)stop;
   if (!prob) return 0;
   size_t gen = gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).total;
-  return gen;
+  return gen + ls_extra_ws(*prob);
 }
 
 void* kz_workspace_iterates(const kz_problem* prob, void* workspace) {
@@ -114,7 +114,8 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
   cudaStream_t s = (cudaStream_t)stream;
   const int K = prob->n_users;
   // fast path: fixed-T lockstep over contiguous supports (kz_solve_lockstep.cuh)
-  int fast = lockstep_try_launch(*prob, scheme, *stop, *rng, *out, s, &g_launches);
+  int fast = lockstep_try_launch(*prob, scheme, *stop, *rng, *out, resume, (char*)workspace, workspace_bytes, s,
+                                 &g_launches);
   if (fast == 1) return cuda_check("kz_solve(lockstep)");
   if (fast < 0) return fail(KZ_ERR_CUDA, "lockstep launch failed");
 

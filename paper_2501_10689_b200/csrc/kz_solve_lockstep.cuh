@@ -1,15 +1,886 @@
-// Fast lockstep path (fixed-T, contiguous supports).  Placeholder: the
-// generic kernel handles every case until the tuned kernel lands.
+// Register-resident lockstep Kaczmarz kernel (fixed-T run_precoding over
+// contiguous visibility regions) — the throughput path for sm_100a.
+//
+// Mapping (one CTA = one system b x one group of G right-hand sides):
+//   * warp w owns the 32-antenna chunk [32w, 32w+32) of every iterate;
+//   * lane = (a, g): g in [0,G) selects the rhs, a in [0,A) (A = 32/G) splits
+//     the chunk, so thread (w, a, g) keeps NPT = 32/A iterate entries m_c[n]
+//     of rhs c = g0+g in REGISTERS for the whole solve;
+//   * the K restricted rows h_i (one contiguous VR each) live in SHARED
+//     memory, stored antenna-aligned so a warp reads them as broadcast
+//     vector loads; every h element is fetched from HBM once per CTA;
+//   * a residual refresh  r_i = e_c,i - h_i^H m_c - xi q_i  is computed as
+//     per-chunk partial dot products (only rows whose VR overlaps the chunk),
+//     reduced over the a-lanes with shuffles and over chunks through a small
+//     slot array P[i][slot][g] in a fixed order (deterministic, atomic-free);
+//   * selection / aggregation weights are per-rhs warp reductions;
+//   * projections update the register iterate directly (rk_step), and the
+//     aggregated step accumulates y = sum_i phi_i h_i per antenna in ascending
+//     row order (the reference's scatter order, solvers.py:281-285).
+// Arithmetic: complex128 mode (G=8, A=4) keeps numpy's row-selection
+// arithmetic (np_cabs, pairwise sums, sequential cumsum; solvers.py:231-237)
+// and numpy's complex multiply for every update; complex64 mode (G=16, A=2)
+// uses fp32 FMAs with fp64 selection sums.
+//
+// Reference semantics: InstanceRun.step (solvers.py:382-423) for every
+// scheme, lockstep driver with epsilon = 0 (solvers.py:583-603), flop charges
+// of metrics.FlopCounter per primitive.
 #pragma once
 
+#include <cstdlib>
+
 #include "kz_common.cuh"
+#include "kz_solve_generic.cuh"
 
 namespace kz {
 
+template <class T> struct Ls;
+template <> struct Ls<float2> {
+  static constexpr int G = 16, A = 2, V = 2, NPT = 16;
+  static constexpr bool EXACT = false;
+};
+template <> struct Ls<double2> {
+  static constexpr int G = 8, A = 4, V = 1, NPT = 8;
+  static constexpr bool EXACT = true;
+};
+
+struct LsArgs {
+  kz_problem P;
+  kz_rng R;
+  kz_out O;
+  int T;       // iterations
+  int S;       // max chunk slots per row
+  int hcap;    // H elements reserved in shared memory
+  char* ws;    // solve workspace (M block written at exit)
+  GenLayout L;
+  int32_t* tstop;  // [B * groups] outer iteration at which the CTA finished
+};
+
+// ------------------------------------------------------------------ smem plan
+struct LsPlan {
+  int K, W, G, S, hcap, cs, KW;
+  size_t rowS, rowL, rowB, c0, c1, en, cost, cmask, clist_ptr, clist, olist, nlist, ocl_ptr, ocl, ncl_ptr, ncl,
+      H, P, Q, R, Dp, scr, sel, gam, num, sp, nz, done, iters, noop, flops, prev, pool, poolcnt, misc, total;
+};
+
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline LsPlan ls_plan(int K, int W, int G, int S, int hcap, int cs, bool exact) {
+  LsPlan p;
+  p.K = K; p.W = W; p.G = G; p.S = S; p.hcap = hcap; p.cs = cs; p.KW = (K + 31) / 32;
+  size_t o = 0;
+  p.rowS = o; o = a16(o + 4 * K);
+  p.rowL = o; o = a16(o + 4 * K);
+  p.rowB = o; o = a16(o + 4 * K);
+  p.c0 = o; o = a16(o + 4 * K);
+  p.c1 = o; o = a16(o + 4 * K);
+  p.en = o; o = a16(o + 8 * K);
+  p.cost = o; o = a16(o + 8 * K);
+  p.cmask = o; o = a16(o + 4 * (size_t)K * p.KW);
+  p.clist_ptr = o; o = a16(o + 4 * (W + 1));
+  p.clist = o; o = a16(o + 4 * (size_t)K * S);
+  p.olist = o; o = a16(o + 4 * (K + 1));
+  p.nlist = o; o = a16(o + 4 * (K + 1));
+  p.ocl_ptr = o; o = a16(o + 4 * (W + 1));
+  p.ocl = o; o = a16(o + 4 * (size_t)K * S);
+  p.ncl_ptr = o; o = a16(o + 4 * (W + 1));
+  p.ncl = o; o = a16(o + 4 * (size_t)K * S);
+  p.H = o; o = a16(o + (size_t)cs * hcap);
+  size_t psz = (size_t)cs * K * S * G;
+  size_t phisz = (size_t)cs * K * G;
+  p.P = o; o = a16(o + (psz > phisz ? psz : phisz));
+  p.Q = o; o = a16(o + (size_t)cs * K * G);
+  p.R = o; o = a16(o + (size_t)cs * K * G);
+  p.Dp = o; o = a16(o + 8 * (size_t)W * G);
+  p.scr = o; o = a16(o + (exact ? 16 * (size_t)W * K : 0));
+  p.sel = o; o = a16(o + 4 * G);
+  p.gam = o; o = a16(o + (size_t)cs * G);
+  p.num = o; o = a16(o + (size_t)cs * G);
+  p.sp = o; o = a16(o + 8 * G);
+  p.nz = o; o = a16(o + 4 * G);
+  p.done = o; o = a16(o + 4 * G);
+  p.iters = o; o = a16(o + 4 * G);
+  p.noop = o; o = a16(o + 4 * G);
+  p.flops = o; o = a16(o + 8 * G);
+  p.prev = o; o = a16(o + 4 * G);
+  p.pool = o; o = a16(o + 4 * (size_t)G * p.KW);
+  p.poolcnt = o; o = a16(o + 4 * G);
+  p.misc = o; o = a16(o + 64);
+  p.total = o;
+  return p;
+}
+
+template <class T, int SCH>
+__global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
+  using Tr = Ls<T>;
+  using Rl = typename Cx<T>::real;
+  constexpr int G = Tr::G, A = Tr::A, V = Tr::V, NPT = Tr::NPT;
+  constexpr bool EXACT = Tr::EXACT;
+  constexpr bool PER_LANE_ROW = SCH == KZ_URK || SCH == KZ_SWOR_ERK;
+  constexpr bool DENSE_FORM = SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_AHK;
+
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int K = p.P.n_users, Nt = p.P.n_antennas, W = Nt >> 5;
+  const int ngroups = (K + G - 1) / G;
+  const int b = blockIdx.x / ngroups, grp = blockIdx.x % ngroups, g0 = grp * G;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane % G, a = lane / G;
+  const int nthr = blockDim.x;
+  const LsPlan pl = ls_plan(K, W, G, p.S, p.hcap, (int)sizeof(T), EXACT);
+
+  int* rowS = (int*)(sm + pl.rowS);
+  int* rowL = (int*)(sm + pl.rowL);
+  int* rowB = (int*)(sm + pl.rowB);
+  int* c0 = (int*)(sm + pl.c0);
+  int* c1 = (int*)(sm + pl.c1);
+  double* en = (double*)(sm + pl.en);
+  long long* cost = (long long*)(sm + pl.cost);
+  uint32_t* cmask = (uint32_t*)(sm + pl.cmask);
+  int* clist_ptr = (int*)(sm + pl.clist_ptr);
+  int* clist = (int*)(sm + pl.clist);
+  int* olist = (int*)(sm + pl.olist);
+  int* nlist = (int*)(sm + pl.nlist);
+  int* ocl_ptr = (int*)(sm + pl.ocl_ptr);
+  int* ocl = (int*)(sm + pl.ocl);
+  int* ncl_ptr = (int*)(sm + pl.ncl_ptr);
+  int* ncl = (int*)(sm + pl.ncl);
+  T* Hs = (T*)(sm + pl.H);
+  T* Ps = (T*)(sm + pl.P);
+  T* Phi = Ps;  // aliases P once the residuals are finalised
+  T* Qs = (T*)(sm + pl.Q);
+  T* Rs = (T*)(sm + pl.R);
+  double* Dp = (double*)(sm + pl.Dp);
+  double* scr = (double*)(sm + pl.scr);
+  int* sel = (int*)(sm + pl.sel);
+  T* gam = (T*)(sm + pl.gam);
+  T* numv = (T*)(sm + pl.num);
+  double* spv = (double*)(sm + pl.sp);
+  int* nzv = (int*)(sm + pl.nz);
+  int* donev = (int*)(sm + pl.done);
+  int* itv = (int*)(sm + pl.iters);
+  int* noopv = (int*)(sm + pl.noop);
+  long long* flv = (long long*)(sm + pl.flops);
+  int* prevv = (int*)(sm + pl.prev);
+  uint32_t* poolv = (uint32_t*)(sm + pl.pool);
+  int* poolcnt = (int*)(sm + pl.poolcnt);
+  int* misc = (int*)(sm + pl.misc);
+
+  const double reg = p.P.reg[b];
+  const T* heff = (const T*)p.P.heff;
+
+  // ---------------------------------------------------------------- setup
+  for (int i = tid; i < K; i += nthr) {
+    size_t r = (size_t)b * K + i;
+    int sg = p.P.row_seg_ptr[r];
+    int s = p.P.seg_start[sg], L = p.P.seg_len[sg];
+    rowS[i] = s;
+    rowL[i] = L;
+    c0[i] = s >> 5;
+    c1[i] = (s + L - 1) >> 5;
+    en[i] = p.P.row_energy[r];
+  }
+  __syncthreads();
+  if (tid == 0) {  // antenna-aligned row bases (even), VR partition lists
+    int base = 0;
+    for (int i = 0; i < K; ++i) {
+      rowB[i] = base;
+      base += (rowL[i] + 3) & ~1;
+    }
+    misc[0] = base;
+    int no = 0, nn = 0;
+    if (p.P.orth_ptr) {
+      int o0 = p.P.orth_ptr[b], o1 = p.P.orth_ptr[b + 1];
+      for (int q = o0; q < o1; ++q) olist[no++] = p.P.orth_idx[q];
+      int n0 = p.P.non_ptr[b], n1 = p.P.non_ptr[b + 1];
+      for (int q = n0; q < n1; ++q) nlist[nn++] = p.P.non_idx[q];
+    }
+    misc[1] = no;
+    misc[2] = nn;
+  }
+  __syncthreads();
+  const int nO = misc[1], nN = misc[2];
+  // per-chunk row lists (ascending rows): all rows, O rows, N rows
+  if (tid == 0) {
+    int q = 0, qo = 0, qn = 0;
+    for (int ww = 0; ww < W; ++ww) {
+      clist_ptr[ww] = q;
+      ocl_ptr[ww] = qo;
+      ncl_ptr[ww] = qn;
+      for (int i = 0; i < K; ++i)
+        if (c0[i] <= ww && ww <= c1[i]) clist[q++] = i;
+      for (int k = 0; k < nO; ++k) {
+        int i = olist[k];
+        if (c0[i] <= ww && ww <= c1[i]) ocl[qo++] = i;
+      }
+      for (int k = 0; k < nN; ++k) {
+        int i = nlist[k];
+        if (c0[i] <= ww && ww <= c1[i]) ncl[qn++] = i;
+      }
+    }
+    clist_ptr[W] = q;
+    ocl_ptr[W] = qo;
+    ncl_ptr[W] = qn;
+  }
+  // H rows -> shared memory, element for antenna n of row i at Hs[rowB + (s&1) + n - s]
+  for (int i = 0; i < K; ++i) {
+    size_t r = (size_t)b * K + i;
+    const T* src = heff + p.P.row_val_ptr[r];
+    T* dst = Hs + rowB[i] + (rowS[i] & 1);
+    int L = rowL[i];
+    for (int j = tid; j < L; j += nthr) dst[j] = src[j];
+    if (tid == 0) {
+      if (rowS[i] & 1) Hs[rowB[i]] = czero<T>();
+      int end = rowB[i] + (rowS[i] & 1) + L;
+      int lim = rowB[i] + ((L + 3) & ~1);
+      for (int e = end; e < lim; ++e) Hs[e] = czero<T>();
+    }
+  }
+  if constexpr (SCH == KZ_VR_OGRK) {
+    for (int i = tid; i < K; i += nthr) {
+      size_t r = (size_t)b * K + i;
+      long long cst = 0;
+      for (int q = 0; q < pl.KW; ++q) cmask[i * pl.KW + q] = 0;
+      for (int q = p.P.coupled_ptr[r]; q < p.P.coupled_ptr[r + 1]; ++q) {
+        int j = p.P.coupled_idx[q];
+        cmask[i * pl.KW + (j >> 5)] |= 1u << (j & 31);
+        cst += 8LL * rowL[j] + 4;
+      }
+      cost[i] = cst;
+    }
+  }
+  // state: q = 0, r = e_c (SolverState.initial)
+  for (int e = tid; e < K * G; e += nthr) {
+    int i = e / G, gg = e % G;
+    Qs[e] = czero<T>();
+    Rs[e] = (i == g0 + gg) ? Cx<T>::make(1, 0) : czero<T>();
+  }
+  for (int gg = tid; gg < G; gg += nthr) {
+    donev[gg] = (g0 + gg < K) ? 0 : 1;
+    itv[gg] = 0;
+    noopv[gg] = 0;
+    flv[gg] = 0;
+    prevv[gg] = -1;
+    poolcnt[gg] = 0;
+    sel[gg] = -1;
+  }
+  __syncthreads();
+
+  T m[NPT];
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) m[k] = czero<T>();
+  auto ant = [&](int k) { return (w << 5) + (k / V) * (A * V) + a * V + (k % V); };
+  auto rowp = [&](int i) -> const T* { return Hs + rowB[i] + (rowS[i] & 1) - rowS[i]; };
+
+  // partial h_i^H m over this thread's antennas of chunk w (row overlaps the chunk)
+  auto partial = [&](int i, bool uniform_row) -> T {
+    const int s = rowS[i], e = s + rowL[i];
+    const int lo = max(s, w << 5), hi = min(e, (w << 5) + 32);
+    const T* hp = rowp(i);
+    T acc0 = czero<T>(), acc1 = czero<T>();
+    if (lo == (w << 5) && hi == (w << 5) + 32) {
+#pragma unroll
+      for (int k = 0; k < NPT; k += V) {
+        int n = ant(k);
+        if constexpr (V == 2) {
+          float4 hv = *reinterpret_cast<const float4*>(hp + n);
+          acc0 = cfma_conj(T{(Rl)hv.x, (Rl)hv.y}, m[k], acc0);
+          acc1 = cfma_conj(T{(Rl)hv.z, (Rl)hv.w}, m[k + 1], acc1);
+        } else {
+          if (k & 1) acc1 = cfma_conj(hp[n], m[k], acc1);
+          else acc0 = cfma_conj(hp[n], m[k], acc0);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) {
+        int n = ant(k);
+        if (n >= lo && n < hi) {
+          if (k & 1) acc1 = cfma_conj(hp[n], m[k], acc1);
+          else acc0 = cfma_conj(hp[n], m[k], acc0);
+        }
+      }
+    }
+    (void)uniform_row;
+    T acc = cadd(acc0, acc1);
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1) {
+      acc.x += __shfl_xor_sync(FULL, acc.x, off);
+      acc.y += __shfl_xor_sync(FULL, acc.y, off);
+    }
+    return acc;
+  };
+  // refresh partials for the rows listed for this chunk -> P[i][w - c0_i][g]
+  auto refresh_partials = [&](const int* lptr, const int* lst) {
+    for (int q = lptr[w]; q < lptr[w + 1]; ++q) {
+      int i = lst[q];
+      T v = partial(i, true);
+      if (a == 0) Ps[((size_t)i * p.S + (w - c0[i])) * G + g] = v;
+    }
+  };
+  // finalise residuals of `rows` (n of them) from the slot partials
+  auto finalize = [&](const int* rows, int n, bool all_rows) {
+    for (int e = tid; e < n * G; e += nthr) {
+      int i = all_rows ? e / G : rows[e / G], gg = e % G;
+      int c = g0 + gg;
+      if (c >= K || donev[gg]) continue;
+      if constexpr (SCH == KZ_VR_OGRK) {
+        int pr = prevv[gg];
+        if (pr < 0 || !((cmask[pr * pl.KW + (i >> 5)] >> (i & 31)) & 1u)) continue;
+      }
+      T dot = czero<T>();
+      const T* pp = Ps + (size_t)i * p.S * G + gg;
+      for (int sl = 0; sl <= c1[i] - c0[i]; ++sl) dot = cadd(dot, pp[(size_t)sl * G]);
+      T q = Qs[i * G + gg];
+      T rq = Cx<T>::make(q.x * (Rl)reg, q.y * (Rl)reg);
+      T r;
+      if (DENSE_FORM) {
+        r = Cx<T>::make(-dot.x - rq.x, -dot.y - rq.y);
+        if (i == c) r.x += (Rl)1;
+      } else {
+        Rl tg = i == c ? (Rl)1 : (Rl)0;
+        r = Cx<T>::make((tg - dot.x) - rq.x, (0 - dot.y) - rq.y);
+      }
+      Rs[i * G + gg] = r;
+    }
+  };
+  // uniform draw for rhs slot gg at its current draw index
+  auto draw_u = [&](int gg) -> double {
+    int c = g0 + gg;
+    int d = itv[gg];
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+    return p.R.uniforms[((size_t)b * K + c) * p.R.stream_len + d];
+  };
+  auto log_row = [&](int gg, int it, int i) {
+    if (p.O.rows && it < p.O.rows_cap) p.O.rows[((size_t)b * K + g0 + gg) * p.O.rows_cap + it] = i;
+  };
+  // rk_step bookkeeping for rhs gg on row i (solvers.py:173-188); lane-0 / single-thread context
+  auto take_step = [&](int gg, int i, long long f) {
+    T r = Rs[i * G + gg];
+    T gm = cdivr(r, en[i]);
+    Qs[i * G + gg] = cadd(Qs[i * G + gg], gm);
+    Rs[i * G + gg] = czero<T>();
+    gam[gg] = gm;
+    sel[gg] = i;
+    log_row(gg, itv[gg], i);
+    itv[gg] += 1;
+    flv[gg] += f;
+  };
+  // m += gamma_g h_i over this thread's antennas for a per-lane row i (rk_step axpy)
+  auto project_row = [&](int i, T gm) {
+    const int s = rowS[i], e = s + rowL[i];
+    if (w < c0[i] || w > c1[i]) return;
+    const T* hp = rowp(i);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      int n = ant(k);
+      if (n >= s && n < e) {
+        if constexpr (EXACT) m[k] = cadd(m[k], cmul(gm, hp[n]));
+        else m[k] = cfma(gm, hp[n], m[k]);
+      }
+    }
+  };
+
+  // greedy-weighted pick for rhs gg from Rs (warp-cooperative); -1 = None
+  auto pick_weighted = [&](int gg, bool& drew) -> int {
+    drew = false;
+    if constexpr (EXACT) {
+      double* wb = scr + (size_t)w * 2 * K;
+      double* cb = wb + K;
+      for (int i = lane; i < K; i += 32) {
+        T r = Rs[i * G + gg];
+        wb[i] = np_abs2((double)r.x, (double)r.y);
+      }
+      __syncwarp();
+      double tot = 0.0;
+      if (lane == 0) tot = np_pairwise_sum(wb, K);
+      tot = __shfl_sync(FULL, tot, 0);
+      if (tot == 0.0) return -1;
+      for (int i = lane; i < K; i += 32) wb[i] = wb[i] / tot;
+      __syncwarp();
+      if (lane == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < K; ++i) {
+          acc += wb[i];
+          cb[i] = acc;
+        }
+      }
+      __syncwarp();
+      double last = cb[K - 1];
+      double u = draw_u(gg);
+      drew = true;
+      for (int base = 0; base < K; base += 32) {
+        int i = base + lane;
+        unsigned bal = __ballot_sync(FULL, i < K && (cb[i] / last > u));
+        if (bal) return base + __ffs(bal) - 1;
+      }
+      return K - 1;
+    } else {
+      double tot = 0.0;
+      for (int i = lane; i < K; i += 32) {
+        T r = Rs[i * G + gg];
+        tot += (double)r.x * r.x + (double)r.y * r.y;
+      }
+      tot = warp_sum(tot);
+      if (tot == 0.0) return -1;
+      double tau = draw_u(gg) * tot;
+      drew = true;
+      double carry = 0.0;
+      int lastnz = -1;
+      for (int base = 0; base < K; base += 32) {
+        int i = base + lane;
+        double v = 0.0;
+        if (i < K) {
+          T r = Rs[i * G + gg];
+          v = (double)r.x * r.x + (double)r.y * r.y;
+        }
+        double sc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          double t2 = __shfl_up_sync(FULL, sc, o);
+          if (lane >= o) sc += t2;
+        }
+        unsigned bal = __ballot_sync(FULL, i < K && v > 0.0 && carry + sc > tau);
+        if (bal) return base + __ffs(bal) - 1;
+        unsigned nzb = __ballot_sync(FULL, i < K && v > 0.0);
+        if (nzb) lastnz = base + 31 - __clz(nzb);
+        carry += __shfl_sync(FULL, sc, 31);
+      }
+      return lastnz;
+    }
+  };
+  auto pick_max = [&](int gg) -> int {
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    bool any = false;
+    for (int i = lane; i < K; i += 32) {
+      T r = Rs[i * G + gg];
+      double s = np_abs2((double)r.x, (double)r.y) / en[i];
+      if (s != 0.0) any = true;
+      if (s > best) { best = s; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(FULL, best, o);
+      int oi = __shfl_xor_sync(FULL, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    return __any_sync(FULL, any) ? bi : -1;
+  };
+
+  // aggregated step over `rows` (sorted, n of them) with chunk lists (cp, cl):
+  // weights, y = sum phi h (ascending rows), den, gamma, update.  (solvers.py:248-309)
+  T y[NPT];
+  auto aggregate = [&](const int* rows, int n, bool all_rows, const int* cp, const int* cl, int span,
+                       bool dense, bool mark_done) {
+    // weights phi_i = r_i/e_i, num = vdot(phi, r), ||phi||^2 (warp per rhs)
+    for (int gg = w; gg < G; gg += W) {
+      if (g0 + gg >= K || donev[gg]) continue;
+      T num = czero<T>();
+      double sp = 0.0;
+      bool nz = false;
+      for (int k = lane; k < n; k += 32) {
+        int i = all_rows ? k : rows[k];
+        T r = Rs[i * G + gg];
+        T ph = cdivr(r, en[i]);
+        Phi[i * G + gg] = ph;
+        if (ph.x != 0 || ph.y != 0) nz = true;
+        num = cfma_conj(ph, r, num);
+        sp += EXACT ? np_abs2((double)ph.x, (double)ph.y) : (double)ph.x * ph.x + (double)ph.y * ph.y;
+      }
+      num = warp_csum(num);
+      sp = warp_sum(sp);
+      nz = __any_sync(FULL, nz);
+      if (lane == 0) {
+        numv[gg] = num;
+        spv[gg] = sp;
+        nzv[gg] = nz ? 1 : 0;
+        flv[gg] += 2LL * n;
+      }
+    }
+    __syncthreads();
+    // y over this thread's antennas, rows in ascending order
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) y[k] = czero<T>();
+    for (int q = cp[w]; q < cp[w + 1]; ++q) {
+      int i = cl[q];
+      const T ph = Phi[i * G + g];
+      const int s = rowS[i], e = s + rowL[i];
+      const T* hp = rowp(i);
+      if (s <= (w << 5) && e >= (w << 5) + 32) {
+#pragma unroll
+        for (int k = 0; k < NPT; ++k) {
+          int n = ant(k);
+          if constexpr (EXACT) y[k] = cadd(y[k], cmul(ph, hp[n]));
+          else y[k] = cfma(ph, hp[n], y[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NPT; ++k) {
+          int n = ant(k);
+          if (n >= s && n < e) {
+            if constexpr (EXACT) y[k] = cadd(y[k], cmul(ph, hp[n]));
+            else y[k] = cfma(ph, hp[n], y[k]);
+          }
+        }
+      }
+    }
+    double sy = 0.0;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k)
+      sy += EXACT ? np_abs2((double)y[k].x, (double)y[k].y) : (double)y[k].x * y[k].x + (double)y[k].y * y[k].y;
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1) sy += __shfl_xor_sync(FULL, sy, off);
+    if (a == 0) Dp[w * G + g] = sy;
+    __syncthreads();
+    // den, gamma, no-op bookkeeping (one thread per rhs)
+    for (int gg = tid; gg < G; gg += nthr) {
+      if (g0 + gg >= K || donev[gg]) {
+        nzv[gg] = 0;
+        continue;
+      }
+      if (!nzv[gg] || n == 0) {
+        noopv[gg] += 1;
+        if (mark_done) donev[gg] = 1;
+        nzv[gg] = 0;
+        continue;
+      }
+      long long f = 6LL * n + 2LL * max(n - 1, 0);
+      if (dense) f += 6LL * Nt * n + 2LL * Nt * max(n - 1, 0);
+      else
+        for (int k = 0; k < n; ++k) f += 8LL * rowL[all_rows ? k : rows[k]];
+      f += 4LL * span + 3LL * n + 2;
+      double den = 0.0;
+      for (int ww = 0; ww < W; ++ww) den += Dp[ww * G + gg];
+      den += reg * spv[gg];
+      if (den == 0.0) {
+        noopv[gg] += 1;
+        if (mark_done) donev[gg] = 1;
+        nzv[gg] = 0;
+        flv[gg] += f;
+        continue;
+      }
+      double2 nd = to_d2(numv[gg]);
+      gam[gg] = from_d2<T>(make_double2(nd.x / den, nd.y / den));
+      f += 2 + 8LL * span + 8LL * n;
+      flv[gg] += f;
+    }
+    __syncthreads();
+    if (nzv[g]) {
+      T gm = gam[g];
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) {
+        if constexpr (EXACT) m[k] = cadd(m[k], cmul(gm, y[k]));
+        else m[k] = cfma(gm, y[k], m[k]);
+      }
+    }
+    for (int e = tid; e < n * G; e += nthr) {
+      int i = all_rows ? e / G : rows[e / G], gg = e % G;
+      if (nzv[gg]) Qs[i * G + gg] = cadd(Qs[i * G + gg], cmul(gam[gg], Phi[i * G + gg]));
+    }
+  };
+
+  // ---------------------------------------------------------------- iterations
+  int t = 0;
+  const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
+  const long long dense_rk = 2 + 8LL * Nt + 2;
+  for (t = 1; t <= p.T; ++t) {
+    if constexpr (SCH == KZ_GRK || SCH == KZ_GK || SCH == KZ_VR_OGRK) {
+      refresh_partials(clist_ptr, clist);
+      __syncthreads();
+      finalize(nullptr, K, true);
+      __syncthreads();
+      for (int gg = w; gg < G; gg += W) {
+        if (g0 + gg >= K || donev[gg]) {
+          if (lane == 0) sel[gg] = -1;
+          continue;
+        }
+        int i;
+        long long f;
+        if constexpr (SCH == KZ_GK) {
+          i = pick_max(gg);
+          f = dense_refresh + 4LL * K;
+        } else {
+          bool drew;
+          i = pick_weighted(gg, drew);
+          if constexpr (SCH == KZ_GRK) f = dense_refresh + 4LL * K + 2;
+          else f = (prevv[gg] >= 0 ? cost[prevv[gg]] : 0) + 4LL * K + 2;
+        }
+        if (lane == 0) {
+          if (i < 0) {
+            donev[gg] = 1;
+            sel[gg] = -1;
+            flv[gg] += f;
+          } else {
+            long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[i] + 2 : dense_rk;
+            take_step(gg, i, f + fr);
+            if constexpr (SCH == KZ_VR_OGRK) prevv[gg] = i;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      int i = sel[g];
+      if (i >= 0) project_row(i, gam[g]);
+    } else if constexpr (PER_LANE_ROW) {
+      // row draw (host index stream or Philox), one thread per rhs
+      for (int gg = tid; gg < G; gg += nthr) {
+        if (g0 + gg >= K || donev[gg]) {
+          sel[gg] = -1;
+          continue;
+        }
+        int c = g0 + gg, d = itv[gg];
+        int i;
+        long long f = 0;
+        if (SCH == KZ_SWOR_ERK) f += (K - d % K) + 2;
+        if (p.R.kind == KZ_RNG_HOST_INDEX) {
+          i = p.R.indices[((size_t)b * K + c) * p.R.stream_len + d];
+        } else if (SCH == KZ_URK) {
+          i = (int)(draw_u(gg) * K);
+          i = i >= K ? K - 1 : i;
+        } else {  // Philox energy-swor with a per-rhs pool bitmask
+          uint32_t* pb = poolv + gg * pl.KW;
+          if (poolcnt[gg] == 0) {
+            for (int q = 0; q < pl.KW; ++q) pb[q] = 0;
+            for (int j = 0; j < K; ++j) pb[j >> 5] |= 1u << (j & 31);
+            poolcnt[gg] = K;
+          }
+          double tot = 0.0;
+          for (int j = 0; j < K; ++j)
+            if ((pb[j >> 5] >> (j & 31)) & 1u) tot += en[j];
+          double u = draw_u(gg) * tot, acc = 0.0;
+          int last = -1;
+          i = -1;
+          for (int j = 0; j < K; ++j) {
+            if (!((pb[j >> 5] >> (j & 31)) & 1u)) continue;
+            last = j;
+            acc += en[j];
+            if (acc > u) { i = j; break; }
+          }
+          if (i < 0) i = last;
+          pb[i >> 5] &= ~(1u << (i & 31));
+          poolcnt[gg] -= 1;
+        }
+        sel[gg] = i;
+        flv[gg] += f;
+      }
+      __syncthreads();
+      {  // partial of the lane's own row over this chunk
+        int i = sel[g];
+        T v = czero<T>();
+        bool mine = i >= 0 && w >= c0[i] && w <= c1[i];
+        if (mine) {
+          const int s = rowS[i], e = s + rowL[i];
+          const T* hp = rowp(i);
+#pragma unroll
+          for (int k = 0; k < NPT; ++k) {
+            int n = ant(k);
+            if (n >= s && n < e) v = cfma_conj(hp[n], m[k], v);
+          }
+        }
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1) {
+          v.x += __shfl_xor_sync(FULL, v.x, off);
+          v.y += __shfl_xor_sync(FULL, v.y, off);
+        }
+        if (mine && a == 0) Ps[(size_t)(w - c0[i]) * G + g] = v;
+      }
+      __syncthreads();
+      for (int gg = tid; gg < G; gg += nthr) {
+        int i = sel[gg];
+        if (i < 0) continue;
+        int c = g0 + gg;
+        T dot = czero<T>();
+        for (int sl = 0; sl <= c1[i] - c0[i]; ++sl) dot = cadd(dot, Ps[(size_t)sl * G + gg]);
+        T q = Qs[i * G + gg];
+        Rl tg = i == c ? (Rl)1 : (Rl)0;
+        Rs[i * G + gg] = Cx<T>::make((tg - dot.x) - q.x * (Rl)reg, (0 - dot.y) - q.y * (Rl)reg);
+        take_step(gg, i, 2 * (8LL * Nt + 4));
+      }
+      __syncthreads();
+      int i = sel[g];
+      if (i >= 0) project_row(i, gam[g]);
+    } else if constexpr (SCH == KZ_AHK) {
+      refresh_partials(clist_ptr, clist);
+      __syncthreads();
+      finalize(nullptr, K, true);
+      for (int gg = tid; gg < G; gg += nthr)
+        if (g0 + gg < K && !donev[gg]) flv[gg] += dense_refresh;
+      __syncthreads();
+      aggregate(nullptr, K, true, clist_ptr, clist, Nt, true, true);
+      for (int gg = tid; gg < G; gg += nthr)
+        if (g0 + gg < K && nzv[gg]) itv[gg] += 1;
+    } else {  // KZ_VR_OAHK
+      // exact block projection on the orthogonal group O (solvers.py:312-332)
+      refresh_partials(ocl_ptr, ocl);
+      __syncthreads();
+      finalize(olist, nO, false);
+      __syncthreads();
+      for (int e = tid; e < nO * G; e += nthr) {
+        int i = olist[e / G], gg = e % G;
+        if (g0 + gg >= K) continue;
+        T gm = cdivr(Rs[i * G + gg], en[i]);
+        Qs[i * G + gg] = cadd(Qs[i * G + gg], gm);
+        Rs[i * G + gg] = czero<T>();
+        Phi[i * G + gg] = gm;  // gamma of the block step (P is free here)
+      }
+      for (int gg = tid; gg < G; gg += nthr) {
+        if (g0 + gg >= K) continue;
+        long long f = 0;
+        for (int k = 0; k < nO; ++k) f += 2 * (8LL * rowL[olist[k]] + 4);
+        flv[gg] += f;
+      }
+      __syncthreads();
+      for (int q = ocl_ptr[w]; q < ocl_ptr[w + 1]; ++q) {
+        int i = ocl[q];
+        project_row(i, Phi[i * G + g]);
+      }
+      if (nN > 0) {
+        __syncthreads();  // Phi reads above before P is overwritten
+        refresh_partials(ncl_ptr, ncl);
+        __syncthreads();
+        finalize(nlist, nN, false);
+        for (int gg = tid; gg < G; gg += nthr) {
+          if (g0 + gg >= K) continue;
+          long long f = 0;
+          for (int k = 0; k < nN; ++k) f += 8LL * rowL[nlist[k]] + 4;
+          flv[gg] += f;
+        }
+        __syncthreads();
+        aggregate(nlist, nN, false, ncl_ptr, ncl, p.P.non_union_size[b], false, false);
+      }
+      for (int gg = tid; gg < G; gg += nthr)
+        if (g0 + gg < K) itv[gg] += 1;
+    }
+    __syncthreads();
+    // every rhs of this group done (greedy None / aggregated no-op) -> stop early
+    bool all_done = true;
+    for (int gg = 0; gg < G; ++gg)
+      if (!donev[gg]) all_done = false;
+    if (all_done) break;
+  }
+  const int t_end = t > p.T ? p.T : t;
+
+  // ---------------------------------------------------------------- outputs
+  __syncthreads();
+  if (tid == 0) p.tstop[blockIdx.x] = t_end;
+  {
+    const int c = g0 + g;
+    if (c < K) {
+      T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt;
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) M[ant(k)] = m[k];
+    }
+  }
+  T* vout = (T*)p.O.v;
+  for (int e = tid; e < K * G; e += nthr) {
+    int i = e / G, gg = e % G;
+    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[e];
+  }
+  for (int gg = tid; gg < G; gg += nthr) {
+    int c = g0 + gg;
+    if (c >= K) continue;
+    size_t r = (size_t)b * K + c;
+    if (p.O.iters) p.O.iters[r] = itv[gg];
+    if (p.O.converged) p.O.converged[r] = 0;
+    if (p.O.done) p.O.done[r] = donev[gg] ? 1 : 0;
+    if (p.O.noop_steps) p.O.noop_steps[r] = noopv[gg];
+    if (p.O.flops) p.O.flops[r] = flv[gg];
+  }
+}
+
+// n_outer[b] = max over the system's CTAs (all of them stop at T unless every rhs finished early)
+__global__ void kz_lockstep_finalize(const int32_t* tstop, int groups, int B, int32_t* n_outer, uint8_t* sys_conv) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int t = 0;
+  for (int q = 0; q < groups; ++q) t = max(t, tstop[b * groups + q]);
+  if (n_outer) n_outer[b] = t;
+  if (sys_conv) sys_conv[b] = 0;
+}
+
+template <class T>
+inline size_t ls_smem_bytes(const kz_problem& P, int* S_out, int* hcap_out) {
+  const int K = P.n_users, W = P.n_antennas / 32;
+  const int S = (P.max_support + 31) / 32 + 1;
+  const int hcap = K * ((P.max_support + 3) & ~1);
+  *S_out = S;
+  *hcap_out = hcap;
+  return ls_plan(K, W, Ls<T>::G, S, hcap, (int)sizeof(T), Ls<T>::EXACT).total;
+}
+
+template <class T, int SCH>
+inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
+                     size_t smem, int S, int hcap, cudaStream_t s) {
+  LsArgs a;
+  a.P = P;
+  a.R = R;
+  a.O = O;
+  a.T = T_iters;
+  a.S = S;
+  a.hcap = hcap;
+  a.ws = ws;
+  a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
+  a.tstop = tstop;
+  const int groups = (P.n_users + Ls<T>::G - 1) / Ls<T>::G;
+  if (cudaFuncSetAttribute(kz_lockstep_kernel<T, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return -1;
+  kz_lockstep_kernel<T, SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
+  kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
+                                                                  O.sys_converged);
+  return 1;
+}
+
+// workspace bytes the lockstep path needs on top of the generic layout (tstop array)
+inline size_t ls_extra_ws(const kz_problem& P) {
+  return kz_align((size_t)P.n_systems * P.n_users * 4);
+}
+
 // returns 1 if launched, 0 if the problem is not eligible, -1 on launch failure
-inline int lockstep_try_launch(const kz_problem&, int, const kz_stop&, const kz_rng&, const kz_out&, cudaStream_t,
-                               int32_t*) {
+template <class T>
+inline int ls_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
+                       int32_t* tstop, size_t smem, int S, int hcap, cudaStream_t s) {
+  switch (scheme) {
+    case KZ_URK: return ls_launch<T, KZ_URK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_SWOR_ERK: return ls_launch<T, KZ_SWOR_ERK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_GK: return ls_launch<T, KZ_GK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_GRK: return ls_launch<T, KZ_GRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_VR_OGRK: return ls_launch<T, KZ_VR_OGRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_AHK: return ls_launch<T, KZ_AHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_VR_OAHK: return ls_launch<T, KZ_VR_OAHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+  }
   return 0;
+}
+
+inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S, const kz_rng& R, const kz_out& O,
+                               int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
+  static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr;  // A/B switch for tests
+  if (disabled || resume || S.mode != KZ_STOP_LOCKSTEP || S.epsilon != 0.0) return 0;
+  if (O.nmse_trace || O.resid_trace || O.flops_trace || S.rhs_mask) return 0;
+  if (!(P.flags & KZ_PROBLEM_CONTIGUOUS) || P.max_support < 1) return 0;
+  if (P.n_antennas % 32 != 0 || P.n_antennas > 512 || P.n_antennas < 32) return 0;
+  const bool stochastic = scheme == KZ_URK || scheme == KZ_SWOR_ERK || scheme == KZ_GRK || scheme == KZ_VR_OGRK;
+  if (stochastic && (R.kind == KZ_RNG_HOST_UNIFORM || R.kind == KZ_RNG_HOST_INDEX) &&
+      (R.stream_base != 0 || R.stream_len < S.max_iters))
+    return 0;
+  if (scheme == KZ_SWOR_ERK && R.kind == KZ_RNG_PHILOX && P.n_users > 1024) return 0;
+  GenLayout L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
+  if (ws_bytes < L.total + ls_extra_ws(P)) return 0;
+  int32_t* tstop = (int32_t*)(ws + L.total);
+  int Sl, hcap;
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int rc;
+  if (P.dtype == KZ_C64) {
+    size_t smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
+    if ((int)smem > maxsm) return 0;
+    rc = ls_dispatch<float2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
+  } else {
+    size_t smem = ls_smem_bytes<double2>(P, &Sl, &hcap);
+    if ((int)smem > maxsm) return 0;
+    rc = ls_dispatch<double2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
+  }
+  if (rc == 1) *launches = 2;
+  return rc;
 }
 
 }  // namespace kz

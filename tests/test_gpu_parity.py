@@ -376,3 +376,55 @@ def test_philox_full_cfg2_properties(scheme):
         assert rel(m.transpose(1, 2).cpu().numpy(), hv_f.cpu().numpy()) <= 1e-4
     # contraction, or both already at the fp32 floor (c64 NMSE floors near 5e-8)
     assert np.median(errs[1]) < np.median(errs[0]) or np.median(errs[1]) < 1e-6
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("scheme", O.SCHEMES)
+def test_register_resident_path_all_schemes(scheme, dtype):
+    """Every scheme through the lockstep fast path (contiguous VRs, Nt <= 512) on
+    cfg1-shaped drops vs the oracle: V, row sequences and the per-rhs flop counters."""
+    kz = _kz()
+    T = 30
+    ch = kz.generate("cfg1", range(4))
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device(dtype)
+    k = host.n_users
+    streams = None
+    if scheme in kz.STOCHASTIC_SCHEMES:
+        gens = [np.random.default_rng(kz.solver_seed_sequence(s)).spawn(k) for s in range(4)]
+        streams = kz.HostStreams(scheme, gens, host.row_energy.reshape(4, k))
+    res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rng=streams, rows_cap=T)
+    assert res.launches == 2  # the fused lockstep kernel + its n_outer finaliser
+    for b in range(4):
+        chan = oracle_channel_contiguous(ch, b)
+        sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+        ref = O.rzf_precoder(chan, float(ch.reg[b]))
+        run = O.run_precoding(scheme, sys_, ref, epsilon=0.0, max_iters=T, traces=False,
+                              rng=np.random.default_rng(kz.solver_seed_sequence(b)))
+        v = res.v[b].cpu().numpy()
+        if dtype == "c128":
+            assert rel(v, run.v) <= REL_C128, b
+            assert_rows(res.rows, run.rows, b)
+            setup = 4 * ch.n_antennas * k
+            asm = sum(6 * q * k + 2 * (q - 1) * k for q in
+                      [sum(1 for vr in chan.vrs if n in vr.visible_subarrays) for n in range(ch.n_antennas)] if q)
+            if scheme not in kz.VR_SCHEMES:
+                asm = 6 * ch.n_antennas * k * k + 2 * ch.n_antennas * k * (k - 1)
+            assert int(res.flops[b].sum()) + setup + asm == run.flops_measured
+            assert int(res.noop_steps[b].sum()) == run.noop_steps
+            np.testing.assert_array_equal(res.iters[b].cpu().numpy(), run.iters)
+        else:
+            assert rel(v, run.v) <= 1e-3 or scheme in ("grk", "vr-ogrk", "gk")
+        assert int(res.n_outer[b]) == T
+
+
+def test_register_resident_iterates_are_h_coef():
+    """The M block written back by the fast kernel equals H V (col = H coef)."""
+    import torch
+    kz = _kz()
+    ch = kz.generate("cfg2", range(8))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    res = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20)
+    hv = kz.epilogue(dev, res.v, want_f=True)
+    f = (hv["f"] / hv["beta"][:, None, None]).transpose(1, 2).cpu().numpy()
+    assert rel(res.iterates().cpu().numpy(), f) <= 1e-12
