@@ -1,0 +1,33 @@
+"""Run one lockstep solve of a cfg workload (for ncu / timing).
+
+    python tools/prof_solve.py --scheme grk --dtype c64 --batch 1024 --iters 200 [--reps 3]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2501_10689_b200 as kz  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--scheme", default="grk")
+ap.add_argument("--dtype", default="c64")
+ap.add_argument("--batch", type=int, default=1024)
+ap.add_argument("--iters", type=int, default=200)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+ch = kz.generate(a.config, range(a.batch))
+dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
+rng = ("philox", 7) if a.scheme in kz.STOCHASTIC_SCHEMES else None
+for r in range(a.reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{a.scheme} {a.dtype} B={a.batch} T={a.iters}: {e0.elapsed_time(e1):.3f} ms (launches {res.launches})")
