@@ -850,6 +850,12 @@ inline int ls_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const k
   return 0;
 }
 
+}  // namespace kz
+
+#include "kz_solve_balanced.cuh"
+
+namespace kz {
+
 inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S, const kz_rng& R, const kz_out& O,
                                int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
   static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr;  // A/B switch for tests
@@ -870,10 +876,16 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   int rc;
+  static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: pre-balancing kernel
   if (P.dtype == KZ_C64) {
-    size_t smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
-    if ((int)smem > maxsm) return 0;
-    rc = ls_dispatch<float2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
+    size_t smem = bal_smem_bytes(P, &Sl, &hcap);
+    if (!chunked && (int)smem <= maxsm && P.n_antennas % bal::PS == 0) {
+      rc = bal_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
+    } else {
+      smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
+      if ((int)smem > maxsm) return 0;
+      rc = ls_dispatch<float2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
+    }
   } else {
     size_t smem = ls_smem_bytes<double2>(P, &Sl, &hcap);
     if ((int)smem > maxsm) return 0;
