@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .build import LIB_PATH
+from .build import lib_path
 
 KZ_OK = 0
 KZ_ERR_INVALID = -1
@@ -76,6 +76,7 @@ def lib():
     global _LIB
     if _LIB is not None:
         return _LIB
+    LIB_PATH = lib_path(os.environ.get("KZ_LIB_VARIANT", ""))
     if not os.path.exists(LIB_PATH):
         raise ExtensionMissingError(
             f"{LIB_PATH} not found; build it with `python -m paper_2501_10689_b200.build` "

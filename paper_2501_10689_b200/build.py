@@ -16,6 +16,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libkaczmarz_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
+# variant "timing": per-phase clock64 accounting in the lockstep kernels (-DKZ_TIMING)
+VARIANTS = {"": [], "timing": ["-DKZ_TIMING"]}
+
+
+def lib_path(variant: str = "") -> str:
+    return LIB_PATH if not variant else os.path.join(HERE, f"libkaczmarz_b200_{variant}.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,18 +48,20 @@ def _inputs():
     return files
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB_PATH):
+def up_to_date(variant: str = "") -> bool:
+    path = lib_path(variant)
+    if not os.path.exists(path):
         return False
-    t = os.path.getmtime(LIB_PATH)
+    t = os.path.getmtime(path)
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    path = lib_path(variant)
+    if not force and up_to_date(variant):
+        return path
+    tmp = path + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, *VARIANTS[variant], "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
@@ -64,9 +72,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (exit {res.returncode}); see {log}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, path)
+    return path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    var = "timing" if "--timing" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose=True, variant=var))

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
 
   const double reg = p.P.reg[b];
   const T* heff = (const T*)p.P.heff;
+  KZ_TSTART
 
   // ---------------------------------------------------------------- setup
   for (int i = tid; i < K; i += nthr) {
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     c1[i] = (s + L - 1) >> 5;
     en[i] = p.P.row_energy[r];
   }
-  __syncthreads();
+  __syncthreads(); KZ_PHASE();
   if (tid == 0) {  // antenna-aligned row bases (even), VR partition lists
     int base = 0;
     for (int i = 0; i < K; ++i) {
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     misc[1] = no;
     misc[2] = nn;
   }
-  __syncthreads();
+  __syncthreads(); KZ_PHASE();
   const int nO = misc[1], nN = misc[2];
   // per-chunk row lists (ascending rows): all rows, O rows, N rows
   if (tid == 0) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     poolcnt[gg] = 0;
     sel[gg] = -1;
   }
-  __syncthreads();
+  __syncthreads(); KZ_PHASE();
 
   T m[NPT];
 #pragma unroll
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         flv[gg] += 2LL * n;
       }
     }
-    __syncthreads();
+    __syncthreads(); KZ_PHASE();
     // y over this thread's antennas, rows in ascending order
 #pragma unroll
     for (int k = 0; k < NPT; ++k) y[k] = czero<T>();
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
 #pragma unroll
     for (int off = G; off < 32; off <<= 1) sy += __shfl_xor_sync(FULL, sy, off);
     if (a == 0) Dp[w * G + g] = sy;
-    __syncthreads();
+    __syncthreads(); KZ_PHASE();
     // den, gamma, no-op bookkeeping (one thread per rhs)
     for (int gg = tid; gg < G; gg += nthr) {
       if (g0 + gg >= K || donev[gg]) {
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       f += 2 + 8LL * span + 8LL * n;
       flv[gg] += f;
     }
-    __syncthreads();
+    __syncthreads(); KZ_PHASE();
     if (nzv[g]) {
       T gm = gam[g];
 #pragma unroll
@@ -582,11 +583,12 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
   const long long dense_rk = 2 + 8LL * Nt + 2;
   for (t = 1; t <= p.T; ++t) {
+    KZ_ITER();
     if constexpr (SCH == KZ_GRK || SCH == KZ_GK || SCH == KZ_VR_OGRK) {
       refresh_partials(clist_ptr, clist);
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       finalize(nullptr, K, true);
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       for (int gg = w; gg < G; gg += W) {
         if (g0 + gg >= K || donev[gg]) {
           if (lane == 0) sel[gg] = -1;
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         }
         __syncwarp();
       }
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       int i = sel[g];
       if (i >= 0) project_row(i, gam[g]);
     } else if constexpr (PER_LANE_ROW) {
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         sel[gg] = i;
         flv[gg] += f;
       }
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       {  // partial of the lane's own row over this chunk
         int i = sel[g];
         T v = czero<T>();
@@ -682,7 +684,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         }
         if (mine && a == 0) Ps[(size_t)(w - c0[i]) * G + g] = v;
       }
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       for (int gg = tid; gg < G; gg += nthr) {
         int i = sel[gg];
         if (i < 0) continue;
@@ -694,25 +696,25 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         Rs[i * G + gg] = Cx<T>::make((tg - dot.x) - q.x * (Rl)reg, (0 - dot.y) - q.y * (Rl)reg);
         take_step(gg, i, 2 * (8LL * Nt + 4));
       }
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       int i = sel[g];
       if (i >= 0) project_row(i, gam[g]);
     } else if constexpr (SCH == KZ_AHK) {
       refresh_partials(clist_ptr, clist);
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       finalize(nullptr, K, true);
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K && !donev[gg]) flv[gg] += dense_refresh;
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       aggregate(nullptr, K, true, clist_ptr, clist, Nt, true, true);
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K && nzv[gg]) itv[gg] += 1;
     } else {  // KZ_VR_OAHK
       // exact block projection on the orthogonal group O (solvers.py:312-332)
       refresh_partials(ocl_ptr, ocl);
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       finalize(olist, nO, false);
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       for (int e = tid; e < nO * G; e += nthr) {
         int i = olist[e / G], gg = e % G;
         if (g0 + gg >= K) continue;
@@ -727,15 +729,15 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         for (int k = 0; k < nO; ++k) f += 2 * (8LL * rowL[olist[k]] + 4);
         flv[gg] += f;
       }
-      __syncthreads();
+      __syncthreads(); KZ_PHASE();
       for (int q = ocl_ptr[w]; q < ocl_ptr[w + 1]; ++q) {
         int i = ocl[q];
         project_row(i, Phi[i * G + g]);
       }
       if (nN > 0) {
-        __syncthreads();  // Phi reads above before P is overwritten
+        __syncthreads(); KZ_PHASE();  // Phi reads above before P is overwritten
         refresh_partials(ncl_ptr, ncl);
-        __syncthreads();
+        __syncthreads(); KZ_PHASE();
         finalize(nlist, nN, false);
         for (int gg = tid; gg < G; gg += nthr) {
           if (g0 + gg >= K) continue;
@@ -743,13 +745,13 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
           for (int k = 0; k < nN; ++k) f += 8LL * rowL[nlist[k]] + 4;
           flv[gg] += f;
         }
-        __syncthreads();
+        __syncthreads(); KZ_PHASE();
         aggregate(nlist, nN, false, ncl_ptr, ncl, p.P.non_union_size[b], false, false);
       }
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K) itv[gg] += 1;
     }
-    __syncthreads();
+    __syncthreads(); KZ_PHASE();
     // every rhs of this group done (greedy None / aggregated no-op) -> stop early
     bool all_done = true;
     for (int gg = 0; gg < G; ++gg)
@@ -759,8 +761,9 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   const int t_end = t > p.T ? p.T : t;
 
   // ---------------------------------------------------------------- outputs
-  __syncthreads();
+  __syncthreads(); KZ_PHASE();
   if (tid == 0) p.tstop[blockIdx.x] = t_end;
+  KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   {
     const int c = g0 + g;
     if (c < K) {
@@ -831,7 +834,11 @@ inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int 
 
 // workspace bytes the lockstep path needs on top of the generic layout (tstop array)
 inline size_t ls_extra_ws(const kz_problem& P) {
+#ifdef KZ_TIMING
+  return kz_align((size_t)P.n_systems * P.n_users * 4 + 8) + (size_t)P.n_systems * P.n_users * 12 * 8;
+#else
   return kz_align((size_t)P.n_systems * P.n_users * 4);
+#endif
 }
 
 // returns 1 if launched, 0 if the problem is not eligible, -1 on launch failure
@@ -852,7 +859,7 @@ inline int ls_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const k
 
 }  // namespace kz
 
-#include "kz_solve_balanced.cuh"
+#include "kz_solve_wide.cuh"
 
 namespace kz {
 
@@ -876,13 +883,11 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   int rc;
-  static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: pre-balancing kernel
+  static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: 16-rhs chunked kernel only
   if (P.dtype == KZ_C64) {
-    size_t smem = bal_smem_bytes(P, &Sl, &hcap);
-    if (!chunked && (int)smem <= maxsm && P.n_antennas % bal::PS == 0) {
-      rc = bal_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
-    } else {
-      smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
+    rc = chunked ? 0 : wide_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
+    if (rc == 0) {
+      size_t smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
       if ((int)smem > maxsm) return 0;
       rc = ls_dispatch<float2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
     }

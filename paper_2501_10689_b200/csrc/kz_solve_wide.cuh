@@ -1,0 +1,547 @@
+// Wide register-resident lockstep kernel for the single-row (RK) family in
+// complex64: urk, swor-erk, gk, grk, vr-ogrk (fixed T, contiguous VRs).
+//
+// One CTA = one system x 32 right-hand sides, one rhs per LANE (no lane
+// split): thread (w, lane) keeps m_c[32w .. 32w+31] of rhs c = g0 + lane in
+// 64 registers.  Rows live in shared memory zero-padded to whole 32-antenna
+// chunks, so a (row, chunk) product is 16 broadcast LDS.128 feeding 128 FMAs
+// with no predicates and no cross-lane reduction; partials go to the slot
+// array P[i][slot][lane] (slot = chunk - first chunk of the row) and are summed
+// in a fixed order by the warp that selects for that rhs (deterministic).
+// Per-iteration phase timing of the 16-rhs chunked kernel (tools/phase_times.py)
+// showed its refresh latency-bound at ~750 cycles per (row, chunk) with 4
+// warps per scheduler; doubling the FMA work per row and removing the
+// shuffle/predicate overhead attacks exactly that.
+// Semantics: InstanceRun.step for urk / swor-erk / gk / grk / vr-ogrk
+// (solvers.py:382-406) with the FlopCounter charges of each primitive.
+#pragma once
+
+#include "kz_common.cuh"
+#include "kz_solve_generic.cuh"
+
+namespace kz {
+
+namespace wide {
+
+constexpr int G = 32;
+constexpr int CH = 32;  // chunk = antennas per warp
+
+struct Plan {
+  int K, W, SL, hcap;
+  size_t rowS, rowL, c0, c1, hoff, en, cost, cmask, lptr, lst, H, P, Q, R, sel, gam, done, iters, flops, prev, pool,
+      poolcnt, total;
+};
+
+__host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
+  Plan p;
+  p.K = K;
+  p.W = Nt / CH;
+  p.SL = SL;
+  p.hcap = hcap;
+  const int KW = (K + 31) / 32;
+  size_t o = 0;
+  p.rowS = o; o = al(o + 4 * K);
+  p.rowL = o; o = al(o + 4 * K);
+  p.c0 = o; o = al(o + 4 * K);
+  p.c1 = o; o = al(o + 4 * K);
+  p.hoff = o; o = al(o + 4 * K);
+  p.en = o; o = al(o + 4 * K);
+  p.cost = o; o = al(o + 8 * K);
+  p.cmask = o; o = al(o + 4 * (size_t)K * KW);
+  p.lptr = o; o = al(o + 4 * (p.W + 1));
+  p.lst = o; o = al(o + 8 * (size_t)K * SL);
+  p.H = o; o = al(o + 8 * (size_t)hcap);
+  p.P = o; o = al(o + 8 * (size_t)K * SL * G);
+  p.Q = o; o = al(o + 8 * (size_t)K * G);
+  p.R = o; o = al(o + 8 * (size_t)K * G);
+  p.sel = o; o = al(o + 4 * G);
+  p.gam = o; o = al(o + 8 * G);
+  p.done = o; o = al(o + 4 * G);
+  p.iters = o; o = al(o + 4 * G);
+  p.flops = o; o = al(o + 8 * G);
+  p.prev = o; o = al(o + 4 * G);
+  p.pool = o; o = al(o + 4 * (size_t)G * KW);
+  p.poolcnt = o; o = al(o + 4 * G);
+  p.total = o;
+  return p;
+}
+
+}  // namespace wide
+
+template <int SCH>
+__global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
+  using namespace wide;
+  using T = float2;
+  constexpr bool PER_LANE_ROW = SCH == KZ_URK || SCH == KZ_SWOR_ERK;
+  static_assert(SCH == KZ_URK || SCH == KZ_SWOR_ERK || SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK,
+                "wide kernel serves the single-row schemes");
+
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int K = p.P.n_users, Nt = p.P.n_antennas;
+  const int ngroups = (K + G - 1) / G;
+  const int b = blockIdx.x / ngroups, grp = blockIdx.x % ngroups, g0 = grp * G;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int nthr = blockDim.x;
+  const Plan pl = plan(K, Nt, p.S, p.hcap);
+  const int W = pl.W, SL = pl.SL, KW = (K + 31) / 32;
+
+  int* rowS = (int*)(sm + pl.rowS);
+  int* rowL = (int*)(sm + pl.rowL);
+  int* c0 = (int*)(sm + pl.c0);
+  int* c1 = (int*)(sm + pl.c1);
+  int* hoff = (int*)(sm + pl.hoff);  // element index of antenna CH*c0 of row i
+  float* en = (float*)(sm + pl.en);
+  long long* cost = (long long*)(sm + pl.cost);
+  uint32_t* cmask = (uint32_t*)(sm + pl.cmask);
+  int* lptr = (int*)(sm + pl.lptr);
+  int2* lst = (int2*)(sm + pl.lst);  // (h element offset of this chunk, P offset of this (row, slot))
+  T* Hs = (T*)(sm + pl.H);
+  T* Ps = (T*)(sm + pl.P);
+  T* Qs = (T*)(sm + pl.Q);
+  T* Rs = (T*)(sm + pl.R);
+  int* sel = (int*)(sm + pl.sel);
+  T* gam = (T*)(sm + pl.gam);
+  int* donev = (int*)(sm + pl.done);
+  int* itv = (int*)(sm + pl.iters);
+  long long* flv = (long long*)(sm + pl.flops);
+  int* prevv = (int*)(sm + pl.prev);
+  uint32_t* poolv = (uint32_t*)(sm + pl.pool);
+  int* poolcnt = (int*)(sm + pl.poolcnt);
+
+  const float regf = (float)p.P.reg[b];
+  const T* heff = (const T*)p.P.heff;
+  KZ_TSTART
+
+  // ------------------------------------------------------------------ setup
+  for (int i = tid; i < K; i += nthr) {
+    size_t r = (size_t)b * K + i;
+    int sg = p.P.row_seg_ptr[r];
+    int s = p.P.seg_start[sg], L = p.P.seg_len[sg];
+    rowS[i] = s;
+    rowL[i] = L;
+    c0[i] = s / CH;
+    c1[i] = (s + L - 1) / CH;
+    en[i] = (float)p.P.row_energy[r];
+  }
+  __syncthreads();
+  // padded row offsets (prefix over rows) by warp 0
+  if (w == 0) {
+    int carry = 0;
+    for (int base = 0; base < K; base += 32) {
+      int i = base + lane;
+      int v = i < K ? (c1[i] - c0[i] + 1) * CH : 0;
+      int sc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t2 = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += t2;
+      }
+      if (i < K) hoff[i] = carry + sc - v;
+      carry += __shfl_sync(FULL, sc, 31);
+    }
+  }
+  // per-chunk row lists: warp w scans the rows with a ballot compaction
+  {
+    int n = 0;
+    for (int base = 0; base < K; base += 32) {
+      int i = base + lane;
+      bool ov = i < K && c0[i] <= w && w <= c1[i];
+      unsigned bal = __ballot_sync(FULL, ov);
+      n += __popc(bal);
+    }
+    if (lane == 0) lptr[w + 1] = n;  // counts first; prefix below
+  }
+  __syncthreads();
+  if (tid == 0) {
+    lptr[0] = 0;
+    for (int ww = 0; ww < W; ++ww) lptr[ww + 1] += lptr[ww];
+  }
+  __syncthreads();
+  {
+    int n = lptr[w];
+    for (int base = 0; base < K; base += 32) {
+      int i = base + lane;
+      bool ov = i < K && c0[i] <= w && w <= c1[i];
+      unsigned bal = __ballot_sync(FULL, ov);
+      if (ov) {
+        int slot = w - c0[i];
+        lst[n + __popc(bal & ((1u << lane) - 1))] = make_int2(hoff[i] + slot * CH, (i * SL + slot) * G);
+      }
+      n += __popc(bal);
+    }
+  }
+  // rows -> shared memory, zero padded to whole chunks (flat parallel copy)
+  {
+    const int total = hoff[K - 1] + (c1[K - 1] - c0[K - 1] + 1) * CH;
+    for (int e = tid; e < total; e += nthr) {
+      // row of element e: last i with hoff[i] <= e (binary search)
+      int lo = 0, hi = K - 1;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (hoff[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      int i = lo;
+      int n = c0[i] * CH + (e - hoff[i]);
+      int s = rowS[i];
+      Hs[e] = (n >= s && n < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (n - s)] : make_float2(0.f, 0.f);
+    }
+  }
+  if constexpr (SCH == KZ_VR_OGRK) {
+    for (int i = tid; i < K; i += nthr) {
+      size_t r = (size_t)b * K + i;
+      long long cst = 0;
+      for (int q = 0; q < KW; ++q) cmask[i * KW + q] = 0;
+      for (int q = p.P.coupled_ptr[r]; q < p.P.coupled_ptr[r + 1]; ++q) {
+        int j = p.P.coupled_idx[q];
+        cmask[i * KW + (j >> 5)] |= 1u << (j & 31);
+        cst += 8LL * rowL[j] + 4;
+      }
+      cost[i] = cst;
+    }
+  }
+  for (int e = tid; e < K * G; e += nthr) {
+    int i = e / G, gg = e % G;
+    Qs[e] = make_float2(0.f, 0.f);
+    Rs[e] = make_float2(i == g0 + gg ? 1.f : 0.f, 0.f);
+  }
+  for (int gg = tid; gg < G; gg += nthr) {
+    donev[gg] = (g0 + gg < K) ? 0 : 1;
+    itv[gg] = 0;
+    flv[gg] = 0;
+    prevv[gg] = -1;
+    poolcnt[gg] = 0;
+    sel[gg] = -1;
+  }
+  __syncthreads();
+  KZ_PHASE();
+
+  T m[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) m[k] = make_float2(0.f, 0.f);
+  const int l0 = lptr[w], l1 = lptr[w + 1];
+  const float4* H4 = reinterpret_cast<const float4*>(Hs);
+
+  // conj(h) . m over the chunk, 4 accumulator pairs for ILP
+  auto dot_chunk = [&](int h0) -> T {
+    const float4* hp = H4 + (h0 >> 1);
+    float ax0 = 0.f, ay0 = 0.f, ax1 = 0.f, ay1 = 0.f, ax2 = 0.f, ay2 = 0.f, ax3 = 0.f, ay3 = 0.f;
+#pragma unroll
+    for (int k = 0; k < CH; k += 4) {
+      float4 h01 = hp[k >> 1], h23 = hp[(k >> 1) + 1];
+      ax0 = fmaf(h01.x, m[k].x, ax0); ax0 = fmaf(h01.y, m[k].y, ax0);
+      ay0 = fmaf(h01.x, m[k].y, ay0); ay0 = fmaf(-h01.y, m[k].x, ay0);
+      ax1 = fmaf(h01.z, m[k + 1].x, ax1); ax1 = fmaf(h01.w, m[k + 1].y, ax1);
+      ay1 = fmaf(h01.z, m[k + 1].y, ay1); ay1 = fmaf(-h01.w, m[k + 1].x, ay1);
+      ax2 = fmaf(h23.x, m[k + 2].x, ax2); ax2 = fmaf(h23.y, m[k + 2].y, ax2);
+      ay2 = fmaf(h23.x, m[k + 2].y, ay2); ay2 = fmaf(-h23.y, m[k + 2].x, ay2);
+      ax3 = fmaf(h23.z, m[k + 3].x, ax3); ax3 = fmaf(h23.w, m[k + 3].y, ax3);
+      ay3 = fmaf(h23.z, m[k + 3].y, ay3); ay3 = fmaf(-h23.w, m[k + 3].x, ay3);
+    }
+    return make_float2((ax0 + ax1) + (ax2 + ax3), (ay0 + ay1) + (ay2 + ay3));
+  };
+  auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
+    const T* pp = Ps + (size_t)i * SL * G + gg;
+    float dx = 0.f, dy = 0.f;
+    const int ns = c1[i] - c0[i];
+    for (int s = 0; s <= ns; ++s) {
+      T v = pp[(size_t)s * G];
+      dx += v.x;
+      dy += v.y;
+    }
+    T q = Qs[i * G + gg];
+    const int c = g0 + gg;
+    if (SCH == KZ_GK || SCH == KZ_GRK) {  // dense form (solvers.py:149-153)
+      T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
+      if (i == c) r.x += 1.f;
+      return r;
+    }
+    float tg = i == c ? 1.f : 0.f;  // VR form (solvers.py:166)
+    return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
+  };
+  auto draw_u = [&](int gg) -> double {
+    int c = g0 + gg, d = itv[gg];
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+    return p.R.uniforms[((size_t)b * K + c) * p.R.stream_len + d];
+  };
+  auto take_step = [&](int gg, int i, T r, long long f) {
+    const float e = en[i];
+    T gm = make_float2(r.x / e, r.y / e);
+    T q = Qs[i * G + gg];
+    Qs[i * G + gg] = make_float2(q.x + gm.x, q.y + gm.y);
+    Rs[i * G + gg] = make_float2(0.f, 0.f);
+    gam[gg] = gm;
+    sel[gg] = i;
+    const int it = itv[gg];
+    if (p.O.rows && it < p.O.rows_cap) p.O.rows[((size_t)b * K + g0 + gg) * p.O.rows_cap + it] = i;
+    itv[gg] = it + 1;
+    flv[gg] += f;
+  };
+  // lane's own row i on this chunk: m += gm h_i (rows zero padded => whole chunk)
+  auto project = [&](int i, T gm) {
+    if (i < 0 || w < c0[i] || w > c1[i]) return;
+    const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH) >> 1);
+#pragma unroll
+    for (int k = 0; k < CH; k += 2) {
+      float4 h = hp[k >> 1];
+      m[k].x = fmaf(gm.x, h.x, m[k].x); m[k].x = fmaf(-gm.y, h.y, m[k].x);
+      m[k].y = fmaf(gm.x, h.y, m[k].y); m[k].y = fmaf(gm.y, h.x, m[k].y);
+      m[k + 1].x = fmaf(gm.x, h.z, m[k + 1].x); m[k + 1].x = fmaf(-gm.y, h.w, m[k + 1].x);
+      m[k + 1].y = fmaf(gm.x, h.w, m[k + 1].y); m[k + 1].y = fmaf(gm.y, h.z, m[k + 1].y);
+    }
+  };
+
+  const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
+  const long long dense_rk = 2 + 8LL * Nt + 2;
+  int t;
+  for (t = 1; t <= p.T; ++t) {
+    KZ_ITER();
+    if constexpr (!PER_LANE_ROW) {
+      // refresh every row overlapping this chunk, two rows in flight
+      int q = l0;
+      for (; q + 1 < l1; q += 2) {
+        int2 e0 = lst[q], e1 = lst[q + 1];
+        T v0 = dot_chunk(e0.x);
+        T v1 = dot_chunk(e1.x);
+        Ps[e0.y + lane] = v0;
+        Ps[e1.y + lane] = v1;
+      }
+      if (q < l1) {
+        int2 e0 = lst[q];
+        Ps[e0.y + lane] = dot_chunk(e0.x);
+      }
+      __syncthreads();
+      KZ_PHASE();
+      // finalise + select, one warp per rhs (lanes over rows)
+      for (int gg = w; gg < G; gg += W) {
+        if (g0 + gg >= K || donev[gg]) {
+          if (lane == 0) sel[gg] = -1;
+          continue;
+        }
+        float wsum = 0.f;
+        for (int i = lane; i < K; i += 32) {
+          bool upd = true;
+          if constexpr (SCH == KZ_VR_OGRK) {
+            int pr = prevv[gg];
+            upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
+          }
+          T r = upd ? resid(i, gg) : Rs[i * G + gg];
+          if (upd) Rs[i * G + gg] = r;
+          wsum += r.x * r.x + r.y * r.y;
+        }
+        __syncwarp();
+        int isel;
+        long long f;
+        if constexpr (SCH == KZ_GK) {
+          float best = -1.f;
+          int bi = 0x7fffffff;
+          bool any = false;
+          for (int i = lane; i < K; i += 32) {
+            T r = Rs[i * G + gg];
+            float s = (r.x * r.x + r.y * r.y) / en[i];
+            if (s != 0.f) any = true;
+            if (s > best) { best = s; bi = i; }
+          }
+          for (int o = 16; o > 0; o >>= 1) {
+            float ob = __shfl_xor_sync(FULL, best, o);
+            int oi = __shfl_xor_sync(FULL, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          }
+          isel = __any_sync(FULL, any) ? bi : -1;
+          f = dense_refresh + 4LL * K;
+        } else {
+          float tot = warp_sum(wsum);
+          f = (SCH == KZ_GRK ? dense_refresh : (prevv[gg] >= 0 ? cost[prevv[gg]] : 0)) + 4LL * K + 2;
+          if (tot == 0.f) {
+            isel = -1;
+          } else {
+            const float tau = (float)draw_u(gg) * tot;
+            float carry = 0.f;
+            int lastnz = -1;
+            isel = -1;
+            for (int base = 0; base < K && isel < 0; base += 32) {
+              int i = base + lane;
+              float v = 0.f;
+              if (i < K) {
+                T r = Rs[i * G + gg];
+                v = r.x * r.x + r.y * r.y;
+              }
+              float sc = v;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                float t2 = __shfl_up_sync(FULL, sc, o);
+                if (lane >= o) sc += t2;
+              }
+              unsigned bal = __ballot_sync(FULL, i < K && v > 0.f && carry + sc > tau);
+              if (bal) isel = base + __ffs(bal) - 1;
+              unsigned nzb = __ballot_sync(FULL, i < K && v > 0.f);
+              if (nzb) lastnz = base + 31 - __clz(nzb);
+              carry += __shfl_sync(FULL, sc, 31);
+            }
+            if (isel < 0) isel = lastnz;
+          }
+        }
+        if (lane == 0) {
+          if (isel < 0) {
+            donev[gg] = 1;
+            sel[gg] = -1;
+            flv[gg] += f;
+          } else {
+            long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[isel] + 2 : dense_rk;
+            take_step(gg, isel, Rs[isel * G + gg], f + fr);
+            if constexpr (SCH == KZ_VR_OGRK) prevv[gg] = isel;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      KZ_PHASE();
+      project(sel[lane], gam[lane]);
+    } else {
+      // row draw per rhs (host index stream / Philox), one thread per rhs
+      if (tid < G) {
+        const int gg = tid;
+        int i = -1;
+        if (g0 + gg < K && !donev[gg]) {
+          const int c = g0 + gg, d = itv[gg];
+          long long f = SCH == KZ_SWOR_ERK ? (K - d % K) + 2 : 0;
+          if (p.R.kind == KZ_RNG_HOST_INDEX) {
+            i = p.R.indices[((size_t)b * K + c) * p.R.stream_len + d];
+          } else if (SCH == KZ_URK) {
+            i = (int)(draw_u(gg) * K);
+            i = i >= K ? K - 1 : i;
+          } else {
+            uint32_t* pbm = poolv + gg * KW;
+            if (poolcnt[gg] == 0) {
+              for (int q = 0; q < KW; ++q) pbm[q] = 0;
+              for (int j = 0; j < K; ++j) pbm[j >> 5] |= 1u << (j & 31);
+              poolcnt[gg] = K;
+            }
+            double tot = 0.0;
+            for (int j = 0; j < K; ++j)
+              if ((pbm[j >> 5] >> (j & 31)) & 1u) tot += p.P.row_energy[(size_t)b * K + j];
+            double u = draw_u(gg) * tot, acc = 0.0;
+            int last = -1;
+            for (int j = 0; j < K; ++j) {
+              if (!((pbm[j >> 5] >> (j & 31)) & 1u)) continue;
+              last = j;
+              acc += p.P.row_energy[(size_t)b * K + j];
+              if (acc > u) { i = j; break; }
+            }
+            if (i < 0) i = last;
+            pbm[i >> 5] &= ~(1u << (i & 31));
+            poolcnt[gg] -= 1;
+          }
+          flv[gg] += f;
+        }
+        sel[gg] = i;
+      }
+      __syncthreads();
+      KZ_PHASE();
+      {  // partial of the lane's own row on this chunk (gathered loads)
+        const int i = sel[lane];
+        if (i >= 0 && w >= c0[i] && w <= c1[i]) {
+          const int slot = w - c0[i];
+          Ps[(size_t)(i * SL + slot) * G + lane] = dot_chunk(hoff[i] + slot * CH);
+        }
+      }
+      __syncthreads();
+      KZ_PHASE();
+      if (tid < G) {
+        const int i = sel[tid];
+        if (i >= 0) take_step(tid, i, resid(i, tid), 2 * (8LL * Nt + 4));
+      }
+      __syncthreads();
+      KZ_PHASE();
+      project(sel[lane], gam[lane]);
+      __syncthreads();  // sel/gam are rewritten by the next draw
+    }
+    bool all_done = true;
+    for (int gg = 0; gg < G; ++gg)
+      if (!donev[gg]) all_done = false;
+    if (all_done) break;
+    // next iteration's writers of sel/gam run after the refresh barrier: no extra barrier needed
+  }
+  const int t_end = t > p.T ? p.T : t;
+  __syncthreads();
+  KZ_PHASE();
+
+  // ------------------------------------------------------------------ outputs
+  if (tid == 0) p.tstop[blockIdx.x] = t_end;
+  KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
+  {
+    const int c = g0 + lane;
+    if (c < K) {
+      T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt + w * CH;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) M[k] = m[k];
+    }
+  }
+  T* vout = (T*)p.O.v;
+  for (int e = tid; e < K * G; e += nthr) {
+    int i = e / G, gg = e % G;
+    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[e];
+  }
+  for (int gg = tid; gg < G; gg += nthr) {
+    int c = g0 + gg;
+    if (c >= K) continue;
+    size_t r = (size_t)b * K + c;
+    if (p.O.iters) p.O.iters[r] = itv[gg];
+    if (p.O.converged) p.O.converged[r] = 0;
+    if (p.O.done) p.O.done[r] = donev[gg] ? 1 : 0;
+    if (p.O.noop_steps) p.O.noop_steps[r] = 0;
+    if (p.O.flops) p.O.flops[r] = flv[gg];
+  }
+}
+
+inline size_t wide_smem_bytes(const kz_problem& P, int* S_out, int* hcap_out) {
+  const int K = P.n_users;
+  const int S = (P.max_support + wide::CH - 2) / wide::CH + 1;  // chunks a row can touch
+  const int hcap = K * S * wide::CH;
+  *S_out = S;
+  *hcap_out = hcap;
+  return wide::plan(K, P.n_antennas, S, hcap).total;
+}
+
+template <int SCH>
+inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
+                       size_t smem, int S, int hcap, cudaStream_t s) {
+  LsArgs a;
+  a.P = P;
+  a.R = R;
+  a.O = O;
+  a.T = T_iters;
+  a.S = S;
+  a.hcap = hcap;
+  a.ws = ws;
+  a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
+  a.tstop = tstop;
+  const int groups = (P.n_users + wide::G - 1) / wide::G;
+  if (cudaFuncSetAttribute(kz_wide_kernel<SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return -1;
+  kz_wide_kernel<SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
+  kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
+                                                                  O.sys_converged);
+  return 1;
+}
+
+// 1 launched, 0 not eligible / not a single-row scheme, -1 failure
+inline int wide_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
+                         int32_t* tstop, int maxsm, cudaStream_t s) {
+  if (P.dtype != KZ_C64 || P.n_antennas % wide::CH != 0 || P.n_users < 17) return 0;
+  int S, hcap;
+  size_t smem = wide_smem_bytes(P, &S, &hcap);
+  if ((int)smem > maxsm) return 0;
+  switch (scheme) {
+    case KZ_URK: return wide_launch<KZ_URK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_SWOR_ERK: return wide_launch<KZ_SWOR_ERK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_GK: return wide_launch<KZ_GK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_GRK: return wide_launch<KZ_GRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_VR_OGRK: return wide_launch<KZ_VR_OGRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+  }
+  return 0;
+}
+
+}  // namespace kz

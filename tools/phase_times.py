@@ -1,0 +1,54 @@
+"""Per-phase cycle breakdown of the lockstep kernels (timing build).
+
+    python -m paper_2501_10689_b200.build --timing
+    KZ_LIB_VARIANT=timing python tools/phase_times.py --scheme grk [--chunked]
+Phases: 0 = setup; then one slot per CTA barrier inside an iteration, in order.
+"""
+import argparse
+import os
+import sys
+
+os.environ.setdefault("KZ_LIB_VARIANT", "timing")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2501_10689_b200 as kz  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--scheme", default="grk")
+ap.add_argument("--dtype", default="c64")
+ap.add_argument("--batch", type=int, default=296)
+ap.add_argument("--iters", type=int, default=100)
+a = ap.parse_args()
+ch = kz.generate("cfg2", range(a.batch))
+dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
+rng = ("philox", 3) if a.scheme in kz.STOCHASTIC_SCHEMES else None
+res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng, workspace=res.workspace)
+e1.record()
+torch.cuda.synchronize()
+B, K = dev.n_systems, dev.n_users
+import ctypes  # noqa: E402
+from paper_2501_10689_b200 import _lib  # noqa: E402
+lb = _lib.lib()
+ws = res.workspace
+m_off = lb.kz_workspace_iterates(ctypes.byref(dev.problem), ws.data_ptr()) - ws.data_ptr()
+cs = 16 if a.dtype == "c128" else 8
+# generic layout total = offset of tstop; recompute from the end: tstop region starts at ws.numel() - extra
+extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 12 * 8
+base = ws.numel() - extra
+off = base + (B * K * 4 + 7) // 8 * 8
+G = 16 if a.dtype == "c64" else 8
+ncta = B * ((K + G - 1) // G)
+ph = ws[off:off + ncta * 12 * 8].view(torch.int64).view(ncta, 12).cpu().numpy().astype(np.float64)
+tot = ph.sum(axis=1)
+print(f"{a.scheme} {a.dtype} B={B} T={a.iters} kernel {e0.elapsed_time(e1):.2f} ms; cycles/CTA mean {tot.mean():.3e}")
+per_it = ph[:, 1:].mean(axis=0) / a.iters
+print(f"  setup {ph[:, 0].mean():.0f} cyc ({ph[:, 0].mean() / tot.mean() * 100:.1f}%)")
+for q, v in enumerate(per_it, start=1):
+    if v > 0:
+        print(f"  phase {q}: {v:8.0f} cyc/iter ({v * a.iters / tot.mean() * 100:5.1f}%)")
