@@ -16,10 +16,13 @@
 // Optional per-phase cycle accounting (build variant `timing`, -DKZ_TIMING):
 // thread 0 of each CTA accumulates clock64() deltas between CTA barriers.
 #ifdef KZ_TIMING
-#define KZ_TSTART long long kz_t_last = clock64(); long long kz_ph[12] = {0}; int kz_pi = 0;
-#define KZ_PHASE() do { if (threadIdx.x == 0) { long long n_ = clock64(); kz_ph[kz_pi < 11 ? kz_pi : 11] += n_ - kz_t_last; kz_t_last = n_; } ++kz_pi; } while (0)
+#define KZ_TSTART long long kz_t_last = clock64(); long long kz_ph[12] = {0}; int kz_pi = 0; \
+  unsigned long long kz_g0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(kz_g0));
+#define KZ_PHASE() do { if (threadIdx.x == 0) { long long n_ = clock64(); kz_ph[kz_pi < 9 ? kz_pi : 9] += n_ - kz_t_last; kz_t_last = n_; } ++kz_pi; } while (0)
 #define KZ_ITER() (kz_pi = 1)
-#define KZ_TDUMP(ptr) do { if (threadIdx.x == 0 && (ptr)) for (int q_ = 0; q_ < 12; ++q_) (ptr)[(size_t)blockIdx.x * 12 + q_] = kz_ph[q_]; } while (0)
+#define KZ_TDUMP(ptr) do { if (threadIdx.x == 0 && (ptr)) { unsigned long long g1_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1_)); \
+  kz_ph[10] = (long long)(g1_ - kz_g0); unsigned smid_; asm("mov.u32 %0, %%smid;" : "=r"(smid_)); kz_ph[11] = smid_; \
+  for (int q_ = 0; q_ < 12; ++q_) (ptr)[(size_t)blockIdx.x * 12 + q_] = kz_ph[q_]; } } while (0)
 #else
 #define KZ_TSTART
 #define KZ_PHASE() do {} while (0)

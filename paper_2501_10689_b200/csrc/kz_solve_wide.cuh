@@ -1,17 +1,20 @@
 // Wide register-resident lockstep kernel for the single-row (RK) family in
 // complex64: urk, swor-erk, gk, grk, vr-ogrk (fixed T, contiguous VRs).
 //
-// One CTA = one system x 32 right-hand sides, one rhs per LANE (no lane
-// split): thread (w, lane) keeps m_c[32w .. 32w+31] of rhs c = g0 + lane in
-// 64 registers.  Rows live in shared memory zero-padded to whole 32-antenna
-// chunks, so a (row, chunk) product is 16 broadcast LDS.128 feeding 128 FMAs
-// with no predicates and no cross-lane reduction; partials go to the slot
-// array P[i][slot][lane] (slot = chunk - first chunk of the row) and are summed
-// in a fixed order by the warp that selects for that rhs (deterministic).
-// Per-iteration phase timing of the 16-rhs chunked kernel (tools/phase_times.py)
-// showed its refresh latency-bound at ~750 cycles per (row, chunk) with 4
-// warps per scheduler; doubling the FMA work per row and removing the
-// shuffle/predicate overhead attacks exactly that.
+// One CTA = one system x 32 right-hand sides.  Lane (a, g), a = lane >> 4,
+// g = lane & 15, owns the two rhs c = g0 + g and c + 16 (register blocking)
+// on the 16 antennas 32w + 4j + 2a + e (j < 8, e < 2) of warp w's chunk, so
+// thread (w, lane) keeps 2 x 16 iterate entries in 64 registers.  Rows live
+// in shared memory zero-padded to whole 32-antenna chunks; a (row, chunk)
+// product is 8 LDS.128 per thread feeding 128 FMAs (each h element reused for
+// both rhs) with no predicates.  The two a-lanes exchange one partial each
+// (one shuffle pair), then every lane stores its own rhs partial into the slot
+// array P[i][slot][rhs] (slot = chunk - first chunk of the row), summed in a
+// fixed order by the warp that selects for that rhs (deterministic).
+// Why: shared memory delivers 128 B/clk/SM on B200 (tools/microbench.cu, a
+// broadcast LDS.128 costs as much as a distinct one) and FFMA issues 128
+// lanes/clk/SM, so one rhs per h element (8 B -> 4 FMA) caps the refresh at
+// 50% of the FMA roofline; two rhs per element balance the two pipes.
 // Semantics: InstanceRun.step for urk / swor-erk / gk / grk / vr-ogrk
 // (solvers.py:382-406) with the FlopCounter charges of each primitive.
 #pragma once
@@ -217,29 +220,38 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   __syncthreads();
   KZ_PHASE();
 
-  T m[CH];
+  constexpr int E = 16;  // antennas per thread per chunk
+  const int a = lane >> 4, g = lane & 15;
+  T m0[E], m1[E];  // rhs g and g + 16
 #pragma unroll
-  for (int k = 0; k < CH; ++k) m[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
   const int l0 = lptr[w], l1 = lptr[w + 1];
   const float4* H4 = reinterpret_cast<const float4*>(Hs);
+  // antenna of element k of this thread within the chunk: 4*(k/2) + 2a + (k&1)
 
-  // conj(h) . m over the chunk, 4 accumulator pairs for ILP
+  // conj(h) . m for both rhs over the chunk; returns this lane's rhs partial after
+  // the a-lane exchange (lane a keeps rhs g + 16a)
   auto dot_chunk = [&](int h0) -> T {
-    const float4* hp = H4 + (h0 >> 1);
-    float ax0 = 0.f, ay0 = 0.f, ax1 = 0.f, ay1 = 0.f, ax2 = 0.f, ay2 = 0.f, ax3 = 0.f, ay3 = 0.f;
+    const float4* hp = H4 + ((h0 + 2 * a) >> 1);
+    float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < CH; k += 4) {
-      float4 h01 = hp[k >> 1], h23 = hp[(k >> 1) + 1];
-      ax0 = fmaf(h01.x, m[k].x, ax0); ax0 = fmaf(h01.y, m[k].y, ax0);
-      ay0 = fmaf(h01.x, m[k].y, ay0); ay0 = fmaf(-h01.y, m[k].x, ay0);
-      ax1 = fmaf(h01.z, m[k + 1].x, ax1); ax1 = fmaf(h01.w, m[k + 1].y, ax1);
-      ay1 = fmaf(h01.z, m[k + 1].y, ay1); ay1 = fmaf(-h01.w, m[k + 1].x, ay1);
-      ax2 = fmaf(h23.x, m[k + 2].x, ax2); ax2 = fmaf(h23.y, m[k + 2].y, ax2);
-      ay2 = fmaf(h23.x, m[k + 2].y, ay2); ay2 = fmaf(-h23.y, m[k + 2].x, ay2);
-      ax3 = fmaf(h23.z, m[k + 3].x, ax3); ax3 = fmaf(h23.w, m[k + 3].y, ax3);
-      ay3 = fmaf(h23.z, m[k + 3].y, ay3); ay3 = fmaf(-h23.w, m[k + 3].x, ay3);
+    for (int j = 0; j < E / 2; ++j) {
+      float4 h = hp[2 * j];
+      const int k = 2 * j;
+      x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
+      y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
+      x1 = fmaf(h.z, m0[k + 1].x, x1); x1 = fmaf(h.w, m0[k + 1].y, x1);
+      y1 = fmaf(h.z, m0[k + 1].y, y1); y1 = fmaf(-h.w, m0[k + 1].x, y1);
+      u0 = fmaf(h.x, m1[k].x, u0); u0 = fmaf(h.y, m1[k].y, u0);
+      v0 = fmaf(h.x, m1[k].y, v0); v0 = fmaf(-h.y, m1[k].x, v0);
+      u1 = fmaf(h.z, m1[k + 1].x, u1); u1 = fmaf(h.w, m1[k + 1].y, u1);
+      v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
     }
-    return make_float2((ax0 + ax1) + (ax2 + ax3), (ay0 + ay1) + (ay2 + ay3));
+    const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
+    // lane a keeps rhs a: send the other rhs' partial to the partner lane
+    const float sx = a ? px : qx, sy = a ? py : qy;
+    const float rx = __shfl_xor_sync(FULL, sx, 16), ry = __shfl_xor_sync(FULL, sy, 16);
+    return a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
   };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
     const T* pp = Ps + (size_t)i * SL * G + gg;
@@ -278,17 +290,18 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     itv[gg] = it + 1;
     flv[gg] += f;
   };
-  // lane's own row i on this chunk: m += gm h_i (rows zero padded => whole chunk)
-  auto project = [&](int i, T gm) {
+  // m_r += gm h_i on this thread's antennas of the chunk (rows zero padded => whole chunk)
+  auto project = [&](T (&mr)[E], int i, T gm) {
     if (i < 0 || w < c0[i] || w > c1[i]) return;
-    const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH) >> 1);
+    const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
 #pragma unroll
-    for (int k = 0; k < CH; k += 2) {
-      float4 h = hp[k >> 1];
-      m[k].x = fmaf(gm.x, h.x, m[k].x); m[k].x = fmaf(-gm.y, h.y, m[k].x);
-      m[k].y = fmaf(gm.x, h.y, m[k].y); m[k].y = fmaf(gm.y, h.x, m[k].y);
-      m[k + 1].x = fmaf(gm.x, h.z, m[k + 1].x); m[k + 1].x = fmaf(-gm.y, h.w, m[k + 1].x);
-      m[k + 1].y = fmaf(gm.x, h.w, m[k + 1].y); m[k + 1].y = fmaf(gm.y, h.z, m[k + 1].y);
+    for (int j = 0; j < E / 2; ++j) {
+      float4 h = hp[2 * j];
+      const int k = 2 * j;
+      mr[k].x = fmaf(gm.x, h.x, mr[k].x); mr[k].x = fmaf(-gm.y, h.y, mr[k].x);
+      mr[k].y = fmaf(gm.x, h.y, mr[k].y); mr[k].y = fmaf(gm.y, h.x, mr[k].y);
+      mr[k + 1].x = fmaf(gm.x, h.z, mr[k + 1].x); mr[k + 1].x = fmaf(-gm.y, h.w, mr[k + 1].x);
+      mr[k + 1].y = fmaf(gm.x, h.w, mr[k + 1].y); mr[k + 1].y = fmaf(gm.y, h.z, mr[k + 1].y);
     }
   };
 
@@ -304,12 +317,12 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         int2 e0 = lst[q], e1 = lst[q + 1];
         T v0 = dot_chunk(e0.x);
         T v1 = dot_chunk(e1.x);
-        Ps[e0.y + lane] = v0;
-        Ps[e1.y + lane] = v1;
+        Ps[e0.y + g + 16 * a] = v0;
+        Ps[e1.y + g + 16 * a] = v1;
       }
       if (q < l1) {
         int2 e0 = lst[q];
-        Ps[e0.y + lane] = dot_chunk(e0.x);
+        Ps[e0.y + g + 16 * a] = dot_chunk(e0.x);
       }
       __syncthreads();
       KZ_PHASE();
@@ -397,7 +410,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-      project(sel[lane], gam[lane]);
+      project(m0, sel[g], gam[g]);
+      project(m1, sel[g + 16], gam[g + 16]);
     } else {
       // row draw per rhs (host index stream / Philox), one thread per rhs
       if (tid < G) {
@@ -439,12 +453,29 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-      {  // partial of the lane's own row on this chunk (gathered loads)
-        const int i = sel[lane];
-        if (i >= 0 && w >= c0[i] && w <= c1[i]) {
-          const int slot = w - c0[i];
-          Ps[(size_t)(i * SL + slot) * G + lane] = dot_chunk(hoff[i] + slot * CH);
-        }
+      {  // partials of the lanes' own rows on this chunk (gathered loads), rhs g then g + 16
+        auto own_row = [&](const T (&mr)[E], int r) {
+          const int i = sel[g + 16 * r];
+          const bool ov = i >= 0 && w >= c0[i] && w <= c1[i];
+          float px = 0.f, py = 0.f;
+          if (ov) {
+            const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+              float4 h = hp[2 * j];
+              const int k = 2 * j;
+              px = fmaf(h.x, mr[k].x, px); px = fmaf(h.y, mr[k].y, px);
+              py = fmaf(h.x, mr[k].y, py); py = fmaf(-h.y, mr[k].x, py);
+              px = fmaf(h.z, mr[k + 1].x, px); px = fmaf(h.w, mr[k + 1].y, px);
+              py = fmaf(h.z, mr[k + 1].y, py); py = fmaf(-h.w, mr[k + 1].x, py);
+            }
+          }
+          px += __shfl_xor_sync(FULL, px, 16);
+          py += __shfl_xor_sync(FULL, py, 16);
+          if (ov && a == r) Ps[(size_t)(i * SL + (w - c0[i])) * G + g + 16 * r] = make_float2(px, py);
+        };
+        own_row(m0, 0);
+        own_row(m1, 1);
       }
       __syncthreads();
       KZ_PHASE();
@@ -454,7 +485,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-      project(sel[lane], gam[lane]);
+      project(m0, sel[g], gam[g]);
+      project(m1, sel[g + 16], gam[g + 16]);
       __syncthreads();  // sel/gam are rewritten by the next draw
     }
     bool all_done = true;
@@ -470,14 +502,15 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   // ------------------------------------------------------------------ outputs
   if (tid == 0) p.tstop[blockIdx.x] = t_end;
   KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
-  {
-    const int c = g0 + lane;
-    if (c < K) {
-      T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt + w * CH;
+  auto store_m = [&](const T (&mr)[E], int r) {
+    const int c = g0 + g + 16 * r;
+    if (c >= K) return;
+    T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt + w * CH;
 #pragma unroll
-      for (int k = 0; k < CH; ++k) M[k] = m[k];
-    }
-  }
+    for (int k = 0; k < E; ++k) M[4 * (k >> 1) + 2 * a + (k & 1)] = mr[k];
+  };
+  store_m(m0, 0);
+  store_m(m1, 1);
   T* vout = (T*)p.O.v;
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;

@@ -42,10 +42,16 @@ cs = 16 if a.dtype == "c128" else 8
 extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 12 * 8
 base = ws.numel() - extra
 off = base + (B * K * 4 + 7) // 8 * 8
-G = 16 if a.dtype == "c64" else 8
+rk = a.scheme in ("urk", "swor-erk", "gk", "grk", "vr-ogrk")
+G = (32 if rk and K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype == "c64" else 8
 ncta = B * ((K + G - 1) // G)
 ph = ws[off:off + ncta * 12 * 8].view(torch.int64).view(ncta, 12).cpu().numpy().astype(np.float64)
+ns = ph[:, 10].copy()
+smid = ph[:, 11].astype(int)
+ph[:, 10:] = 0
 tot = ph.sum(axis=1)
+print(f"  CTA wall {ns.mean() / 1e3:.1f} us mean, cycles/ns {np.mean(tot / ns):.3f} GHz; SMs used {len(set(smid))}; "
+      f"CTAs per SM max {np.bincount(smid).max()}")
 print(f"{a.scheme} {a.dtype} B={B} T={a.iters} kernel {e0.elapsed_time(e1):.2f} ms; cycles/CTA mean {tot.mean():.3e}")
 per_it = ph[:, 1:].mean(axis=0) / a.iters
 print(f"  setup {ph[:, 0].mean():.0f} cyc ({ph[:, 0].mean() / tot.mean() * 100:.1f}%)")
