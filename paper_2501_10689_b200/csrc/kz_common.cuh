@@ -16,17 +16,26 @@
 // Optional per-phase cycle accounting (build variant `timing`, -DKZ_TIMING):
 // thread 0 of each CTA accumulates clock64() deltas between CTA barriers.
 #ifdef KZ_TIMING
-#define KZ_TSTART long long kz_t_last = clock64(); long long kz_ph[12] = {0}; int kz_pi = 0; \
+// per CTA dump: [0..9] phase cycles (0 = setup, k = segment ending at the k-th CTA barrier of an
+// iteration), [10] wall ns, [11] smid, [12..43] per-warp cycles from iteration start to the end of
+// the warp's refresh (KZ_WSTAMP), summed over iterations.
+#define KZ_TSTART __shared__ volatile int kz_dummy; long long kz_t_last = clock64(); long long kz_ph[12] = {0}; \
+  int kz_pi = 0; long long kz_w0 = 0, kz_wacc = 0; \
   unsigned long long kz_g0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(kz_g0));
-#define KZ_PHASE() do { if (threadIdx.x == 0) { long long n_ = clock64(); kz_ph[kz_pi < 9 ? kz_pi : 9] += n_ - kz_t_last; kz_t_last = n_; } ++kz_pi; } while (0)
-#define KZ_ITER() (kz_pi = 1)
-#define KZ_TDUMP(ptr) do { if (threadIdx.x == 0 && (ptr)) { unsigned long long g1_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1_)); \
+#define KZ_PHASE() do { (void)kz_dummy; if (threadIdx.x == 0) { long long n_ = clock64(); \
+  kz_ph[kz_pi < 9 ? kz_pi : 9] += n_ - kz_t_last; kz_t_last = n_; } ++kz_pi; } while (0)
+#define KZ_ITER() (kz_pi = 1, kz_w0 = clock64())
+#define KZ_WSTAMP() (kz_wacc += clock64() - kz_w0)
+#define KZ_TDUMP(ptr) do { if ((ptr)) { long long* o_ = (ptr) + (size_t)blockIdx.x * 44; \
+  if ((threadIdx.x & 31) == 0) o_[12 + (threadIdx.x >> 5)] = kz_wacc; \
+  if (threadIdx.x == 0) { unsigned long long g1_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1_)); \
   kz_ph[10] = (long long)(g1_ - kz_g0); unsigned smid_; asm("mov.u32 %0, %%smid;" : "=r"(smid_)); kz_ph[11] = smid_; \
-  for (int q_ = 0; q_ < 12; ++q_) (ptr)[(size_t)blockIdx.x * 12 + q_] = kz_ph[q_]; } } while (0)
+  for (int q_ = 0; q_ < 12; ++q_) o_[q_] = kz_ph[q_]; } } } while (0)
 #else
 #define KZ_TSTART
 #define KZ_PHASE() do {} while (0)
 #define KZ_ITER() ((void)0)
+#define KZ_WSTAMP() ((void)0)
 #define KZ_TDUMP(ptr) do {} while (0)
 #endif
 

@@ -166,6 +166,8 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
 
   const double reg = p.P.reg[b];
   const T* heff = (const T*)p.P.heff;
+  // [row][rhs] arrays are XOR-swizzled on rhs so lanes-over-rows accesses are conflict free
+  auto xs = [&](int i, int r) { return i * G + (r ^ (i & (G - 1))); };
   KZ_TSTART
 
   // ---------------------------------------------------------------- setup
@@ -251,8 +253,8 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   // state: q = 0, r = e_c (SolverState.initial)
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;
-    Qs[e] = czero<T>();
-    Rs[e] = (i == g0 + gg) ? Cx<T>::make(1, 0) : czero<T>();
+    Qs[xs(i, gg)] = czero<T>();
+    Rs[xs(i, gg)] = (i == g0 + gg) ? Cx<T>::make(1, 0) : czero<T>();
   }
   for (int gg = tid; gg < G; gg += nthr) {
     donev[gg] = (g0 + gg < K) ? 0 : 1;
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       T dot = czero<T>();
       const T* pp = Ps + (size_t)i * p.S * G + gg;
       for (int sl = 0; sl <= c1[i] - c0[i]; ++sl) dot = cadd(dot, pp[(size_t)sl * G]);
-      T q = Qs[i * G + gg];
+      T q = Qs[xs(i, gg)];
       T rq = Cx<T>::make(q.x * (Rl)reg, q.y * (Rl)reg);
       T r;
       if (DENSE_FORM) {
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         Rl tg = i == c ? (Rl)1 : (Rl)0;
         r = Cx<T>::make((tg - dot.x) - rq.x, (0 - dot.y) - rq.y);
       }
-      Rs[i * G + gg] = r;
+      Rs[xs(i, gg)] = r;
     }
   };
   // uniform draw for rhs slot gg at its current draw index
@@ -355,10 +357,10 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   };
   // rk_step bookkeeping for rhs gg on row i (solvers.py:173-188); lane-0 / single-thread context
   auto take_step = [&](int gg, int i, long long f) {
-    T r = Rs[i * G + gg];
+    T r = Rs[xs(i, gg)];
     T gm = cdivr(r, en[i]);
-    Qs[i * G + gg] = cadd(Qs[i * G + gg], gm);
-    Rs[i * G + gg] = czero<T>();
+    Qs[xs(i, gg)] = cadd(Qs[xs(i, gg)], gm);
+    Rs[xs(i, gg)] = czero<T>();
     gam[gg] = gm;
     sel[gg] = i;
     log_row(gg, itv[gg], i);
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       double* wb = scr + (size_t)w * 2 * K;
       double* cb = wb + K;
       for (int i = lane; i < K; i += 32) {
-        T r = Rs[i * G + gg];
+        T r = Rs[xs(i, gg)];
         wb[i] = np_abs2((double)r.x, (double)r.y);
       }
       __syncwarp();
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     } else {
       double tot = 0.0;
       for (int i = lane; i < K; i += 32) {
-        T r = Rs[i * G + gg];
+        T r = Rs[xs(i, gg)];
         tot += (double)r.x * r.x + (double)r.y * r.y;
       }
       tot = warp_sum(tot);
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         int i = base + lane;
         double v = 0.0;
         if (i < K) {
-          T r = Rs[i * G + gg];
+          T r = Rs[xs(i, gg)];
           v = (double)r.x * r.x + (double)r.y * r.y;
         }
         double sc = v;
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     int bi = 0x7fffffff;
     bool any = false;
     for (int i = lane; i < K; i += 32) {
-      T r = Rs[i * G + gg];
+      T r = Rs[xs(i, gg)];
       double s = np_abs2((double)r.x, (double)r.y) / en[i];
       if (s != 0.0) any = true;
       if (s > best) { best = s; bi = i; }
@@ -479,9 +481,9 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       bool nz = false;
       for (int k = lane; k < n; k += 32) {
         int i = all_rows ? k : rows[k];
-        T r = Rs[i * G + gg];
+        T r = Rs[xs(i, gg)];
         T ph = cdivr(r, en[i]);
-        Phi[i * G + gg] = ph;
+        Phi[xs(i, gg)] = ph;
         if (ph.x != 0 || ph.y != 0) nz = true;
         num = cfma_conj(ph, r, num);
         sp += EXACT ? np_abs2((double)ph.x, (double)ph.y) : (double)ph.x * ph.x + (double)ph.y * ph.y;
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     for (int k = 0; k < NPT; ++k) y[k] = czero<T>();
     for (int q = cp[w]; q < cp[w + 1]; ++q) {
       int i = cl[q];
-      const T ph = Phi[i * G + g];
+      const T ph = Phi[xs(i, g)];
       const int s = rowS[i], e = s + rowL[i];
       const T* hp = rowp(i);
       if (s <= (w << 5) && e >= (w << 5) + 32) {
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     }
     for (int e = tid; e < n * G; e += nthr) {
       int i = all_rows ? e / G : rows[e / G], gg = e % G;
-      if (nzv[gg]) Qs[i * G + gg] = cadd(Qs[i * G + gg], cmul(gam[gg], Phi[i * G + gg]));
+      if (nzv[gg]) Qs[xs(i, gg)] = cadd(Qs[xs(i, gg)], cmul(gam[gg], Phi[xs(i, gg)]));
     }
   };
 
@@ -691,9 +693,9 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         int c = g0 + gg;
         T dot = czero<T>();
         for (int sl = 0; sl <= c1[i] - c0[i]; ++sl) dot = cadd(dot, Ps[(size_t)sl * G + gg]);
-        T q = Qs[i * G + gg];
+        T q = Qs[xs(i, gg)];
         Rl tg = i == c ? (Rl)1 : (Rl)0;
-        Rs[i * G + gg] = Cx<T>::make((tg - dot.x) - q.x * (Rl)reg, (0 - dot.y) - q.y * (Rl)reg);
+        Rs[xs(i, gg)] = Cx<T>::make((tg - dot.x) - q.x * (Rl)reg, (0 - dot.y) - q.y * (Rl)reg);
         take_step(gg, i, 2 * (8LL * Nt + 4));
       }
       __syncthreads(); KZ_PHASE();
@@ -718,10 +720,10 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       for (int e = tid; e < nO * G; e += nthr) {
         int i = olist[e / G], gg = e % G;
         if (g0 + gg >= K) continue;
-        T gm = cdivr(Rs[i * G + gg], en[i]);
-        Qs[i * G + gg] = cadd(Qs[i * G + gg], gm);
-        Rs[i * G + gg] = czero<T>();
-        Phi[i * G + gg] = gm;  // gamma of the block step (P is free here)
+        T gm = cdivr(Rs[xs(i, gg)], en[i]);
+        Qs[xs(i, gg)] = cadd(Qs[xs(i, gg)], gm);
+        Rs[xs(i, gg)] = czero<T>();
+        Phi[xs(i, gg)] = gm;  // gamma of the block step (P is free here)
       }
       for (int gg = tid; gg < G; gg += nthr) {
         if (g0 + gg >= K) continue;
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       __syncthreads(); KZ_PHASE();
       for (int q = ocl_ptr[w]; q < ocl_ptr[w + 1]; ++q) {
         int i = ocl[q];
-        project_row(i, Phi[i * G + g]);
+        project_row(i, Phi[xs(i, g)]);
       }
       if (nN > 0) {
         __syncthreads(); KZ_PHASE();  // Phi reads above before P is overwritten
@@ -775,7 +777,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   T* vout = (T*)p.O.v;
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;
-    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[e];
+    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[xs(i, gg)];
   }
   for (int gg = tid; gg < G; gg += nthr) {
     int c = g0 + gg;
@@ -835,7 +837,7 @@ inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int 
 // workspace bytes the lockstep path needs on top of the generic layout (tstop array)
 inline size_t ls_extra_ws(const kz_problem& P) {
 #ifdef KZ_TIMING
-  return kz_align((size_t)P.n_systems * P.n_users * 4 + 8) + (size_t)P.n_systems * P.n_users * 12 * 8;
+  return kz_align((size_t)P.n_systems * P.n_users * 4 + 8) + (size_t)P.n_systems * P.n_users * 44 * 8;
 #else
   return kz_align((size_t)P.n_systems * P.n_users * 4);
 #endif

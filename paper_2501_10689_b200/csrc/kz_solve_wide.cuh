@@ -28,6 +28,10 @@ namespace wide {
 
 constexpr int G = 32;
 constexpr int CH = 32;  // chunk = antennas per warp
+// [row][rhs] arrays (P slots, Q, R) are XOR-swizzled on the rhs index so that
+// both access directions (lanes over rhs: refresh / projection; lanes over
+// rows: finalise / selection) are bank-conflict free.
+__device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 15)); }
 
 struct Plan {
   int K, W, SL, hcap;
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       unsigned bal = __ballot_sync(FULL, ov);
       if (ov) {
         int slot = w - c0[i];
-        lst[n + __popc(bal & ((1u << lane) - 1))] = make_int2(hoff[i] + slot * CH, (i * SL + slot) * G);
+        lst[n + __popc(bal & ((1u << lane) - 1))] = make_int2(hoff[i] + slot * CH, (i * SL + slot) * G | (i & 15));
       }
       n += __popc(bal);
     }
@@ -206,8 +210,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   }
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;
-    Qs[e] = make_float2(0.f, 0.f);
-    Rs[e] = make_float2(i == g0 + gg ? 1.f : 0.f, 0.f);
+    Qs[xs(i, gg)] = make_float2(0.f, 0.f);
+    Rs[xs(i, gg)] = make_float2(i == g0 + gg ? 1.f : 0.f, 0.f);
   }
   for (int gg = tid; gg < G; gg += nthr) {
     donev[gg] = (g0 + gg < K) ? 0 : 1;
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     return a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
   };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
-    const T* pp = Ps + (size_t)i * SL * G + gg;
+    const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
     const int ns = c1[i] - c0[i];
     for (int s = 0; s <= ns; ++s) {
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       dx += v.x;
       dy += v.y;
     }
-    T q = Qs[i * G + gg];
+    T q = Qs[xs(i, gg)];
     const int c = g0 + gg;
     if (SCH == KZ_GK || SCH == KZ_GRK) {  // dense form (solvers.py:149-153)
       T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
@@ -280,9 +284,9 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   auto take_step = [&](int gg, int i, T r, long long f) {
     const float e = en[i];
     T gm = make_float2(r.x / e, r.y / e);
-    T q = Qs[i * G + gg];
-    Qs[i * G + gg] = make_float2(q.x + gm.x, q.y + gm.y);
-    Rs[i * G + gg] = make_float2(0.f, 0.f);
+    T q = Qs[xs(i, gg)];
+    Qs[xs(i, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
+    Rs[xs(i, gg)] = make_float2(0.f, 0.f);
     gam[gg] = gm;
     sel[gg] = i;
     const int it = itv[gg];
@@ -317,13 +321,14 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         int2 e0 = lst[q], e1 = lst[q + 1];
         T v0 = dot_chunk(e0.x);
         T v1 = dot_chunk(e1.x);
-        Ps[e0.y + g + 16 * a] = v0;
-        Ps[e1.y + g + 16 * a] = v1;
+        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = v0;
+        Ps[(e1.y & ~31) + ((g + 16 * a) ^ (e1.y & 15))] = v1;
       }
       if (q < l1) {
         int2 e0 = lst[q];
-        Ps[e0.y + g + 16 * a] = dot_chunk(e0.x);
+        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x);
       }
+      KZ_WSTAMP();
       __syncthreads();
       KZ_PHASE();
       // finalise + select, one warp per rhs (lanes over rows)
@@ -339,8 +344,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             int pr = prevv[gg];
             upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
           }
-          T r = upd ? resid(i, gg) : Rs[i * G + gg];
-          if (upd) Rs[i * G + gg] = r;
+          T r = upd ? resid(i, gg) : Rs[xs(i, gg)];
+          if (upd) Rs[xs(i, gg)] = r;
           wsum += r.x * r.x + r.y * r.y;
         }
         __syncwarp();
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           int bi = 0x7fffffff;
           bool any = false;
           for (int i = lane; i < K; i += 32) {
-            T r = Rs[i * G + gg];
+            T r = Rs[xs(i, gg)];
             float s = (r.x * r.x + r.y * r.y) / en[i];
             if (s != 0.f) any = true;
             if (s > best) { best = s; bi = i; }
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
               int i = base + lane;
               float v = 0.f;
               if (i < K) {
-                T r = Rs[i * G + gg];
+                T r = Rs[xs(i, gg)];
                 v = r.x * r.x + r.y * r.y;
               }
               float sc = v;
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             flv[gg] += f;
           } else {
             long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[isel] + 2 : dense_rk;
-            take_step(gg, isel, Rs[isel * G + gg], f + fr);
+            take_step(gg, isel, Rs[xs(isel, gg)], f + fr);
             if constexpr (SCH == KZ_VR_OGRK) prevv[gg] = isel;
           }
         }
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           }
           px += __shfl_xor_sync(FULL, px, 16);
           py += __shfl_xor_sync(FULL, py, 16);
-          if (ov && a == r) Ps[(size_t)(i * SL + (w - c0[i])) * G + g + 16 * r] = make_float2(px, py);
+          if (ov && a == r) Ps[(size_t)(i * SL + (w - c0[i])) * G + ((g + 16 * r) ^ (i & 15))] = make_float2(px, py);
         };
         own_row(m0, 0);
         own_row(m1, 1);
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   T* vout = (T*)p.O.v;
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;
-    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[e];
+    if (g0 + gg < K) vout[((size_t)b * K + i) * K + g0 + gg] = Qs[xs(i, gg)];
   }
   for (int gg = tid; gg < G; gg += nthr) {
     int c = g0 + gg;

@@ -31,7 +31,7 @@ e0.record()
 res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng, workspace=res.workspace)
 e1.record()
 torch.cuda.synchronize()
-B, K = dev.n_systems, dev.n_users
+B, K, Nt = dev.n_systems, dev.n_users, dev.n_antennas
 import ctypes  # noqa: E402
 from paper_2501_10689_b200 import _lib  # noqa: E402
 lb = _lib.lib()
@@ -39,13 +39,16 @@ ws = res.workspace
 m_off = lb.kz_workspace_iterates(ctypes.byref(dev.problem), ws.data_ptr()) - ws.data_ptr()
 cs = 16 if a.dtype == "c128" else 8
 # generic layout total = offset of tstop; recompute from the end: tstop region starts at ws.numel() - extra
-extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 12 * 8
+extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 44 * 8
 base = ws.numel() - extra
 off = base + (B * K * 4 + 7) // 8 * 8
 rk = a.scheme in ("urk", "swor-erk", "gk", "grk", "vr-ogrk")
 G = (32 if rk and K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype == "c64" else 8
 ncta = B * ((K + G - 1) // G)
-ph = ws[off:off + ncta * 12 * 8].view(torch.int64).view(ncta, 12).cpu().numpy().astype(np.float64)
+raw = ws[off:off + ncta * 44 * 8].view(torch.int64).view(ncta, 44).cpu().numpy().astype(np.float64)
+ph = raw[:, :12].copy()
+wst = raw[:, 12:12 + Nt // 32] / a.iters  # per-warp refresh-end cycles per iteration
+Nt_ = Nt
 ns = ph[:, 10].copy()
 smid = ph[:, 11].astype(int)
 ph[:, 10:] = 0
@@ -54,6 +57,9 @@ print(f"  CTA wall {ns.mean() / 1e3:.1f} us mean, cycles/ns {np.mean(tot / ns):.
       f"CTAs per SM max {np.bincount(smid).max()}")
 print(f"{a.scheme} {a.dtype} B={B} T={a.iters} kernel {e0.elapsed_time(e1):.2f} ms; cycles/CTA mean {tot.mean():.3e}")
 per_it = ph[:, 1:].mean(axis=0) / a.iters
+if wst.max() > 0:
+    print("  per-warp refresh end (cyc/iter, mean over CTAs):", " ".join(f"{x:.0f}" for x in wst.mean(axis=0)))
+    print(f"  slowest warp per CTA: mean {wst.max(axis=1).mean():.0f}  fastest: {wst.min(axis=1).mean():.0f}")
 print(f"  setup {ph[:, 0].mean():.0f} cyc ({ph[:, 0].mean() / tot.mean() * 100:.1f}%)")
 for q, v in enumerate(per_it, start=1):
     if v > 0:
