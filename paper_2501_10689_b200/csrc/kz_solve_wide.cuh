@@ -21,6 +21,7 @@
 
 #include "kz_common.cuh"
 #include "kz_solve_generic.cuh"
+#include "kz_tmem.cuh"
 
 namespace kz {
 
@@ -35,8 +36,8 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 
 struct Plan {
   int K, W, SL, hcap;
-  size_t rowS, rowL, c0, c1, hoff, en, cost, cmask, lptr, lst, H, P, Q, R, sel, gam, done, iters, flops, prev, pool,
-      poolcnt, total;
+  size_t rowS, rowL, c0, c1, hoff, en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
+      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -57,20 +58,32 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.en = o; o = al(o + 4 * K);
   p.cost = o; o = al(o + 8 * K);
   p.cmask = o; o = al(o + 4 * (size_t)K * KW);
+  p.inset = o; o = al(o + K);
   p.lptr = o; o = al(o + 4 * (p.W + 1));
   p.lst = o; o = al(o + 8 * (size_t)K * SL);
+  p.optr = o; o = al(o + 4 * (p.W + 1));
+  p.olst = o; o = al(o + 8 * (size_t)K * SL);
+  p.nptr = o; o = al(o + 4 * (p.W + 1));
+  p.nlst = o; o = al(o + 8 * (size_t)K * SL);
   p.H = o; o = al(o + 8 * (size_t)hcap);
   p.P = o; o = al(o + 8 * (size_t)K * SL * G);
   p.Q = o; o = al(o + 8 * (size_t)K * G);
   p.R = o; o = al(o + 8 * (size_t)K * G);
+  p.Phi = o; o = al(o + 8 * (size_t)K * G);
+  p.Dp = o; o = al(o + 4 * (size_t)p.W * G);
   p.sel = o; o = al(o + 4 * G);
   p.gam = o; o = al(o + 8 * G);
+  p.num = o; o = al(o + 8 * G);
+  p.sp = o; o = al(o + 4 * G);
+  p.nz = o; o = al(o + 4 * G);
+  p.noop = o; o = al(o + 4 * G);
   p.done = o; o = al(o + 4 * G);
   p.iters = o; o = al(o + 4 * G);
   p.flops = o; o = al(o + 8 * G);
   p.prev = o; o = al(o + 4 * G);
   p.pool = o; o = al(o + 4 * (size_t)G * KW);
   p.poolcnt = o; o = al(o + 4 * G);
+  p.misc = o; o = al(o + 32);
   p.total = o;
   return p;
 }
@@ -82,8 +95,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   using namespace wide;
   using T = float2;
   constexpr bool PER_LANE_ROW = SCH == KZ_URK || SCH == KZ_SWOR_ERK;
-  static_assert(SCH == KZ_URK || SCH == KZ_SWOR_ERK || SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK,
-                "wide kernel serves the single-row schemes");
+  constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
 
   extern __shared__ __align__(16) unsigned char sm[];
   const int K = p.P.n_users, Nt = p.P.n_antennas;
@@ -116,6 +128,18 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   int* prevv = (int*)(sm + pl.prev);
   uint32_t* poolv = (uint32_t*)(sm + pl.pool);
   int* poolcnt = (int*)(sm + pl.poolcnt);
+  uint8_t* inset = (uint8_t*)(sm + pl.inset);
+  int* optr = (int*)(sm + pl.optr);
+  int2* olst = (int2*)(sm + pl.olst);
+  int* nptr = (int*)(sm + pl.nptr);
+  int2* nlst = (int2*)(sm + pl.nlst);
+  T* Phi = (T*)(sm + pl.Phi);
+  float* Dp = (float*)(sm + pl.Dp);
+  T* numv = (T*)(sm + pl.num);
+  float* spv = (float*)(sm + pl.sp);
+  int* nzv = (int*)(sm + pl.nz);
+  int* noopv = (int*)(sm + pl.noop);
+  uint32_t* misc = (uint32_t*)(sm + pl.misc);
 
   const float regf = (float)p.P.reg[b];
   const T* heff = (const T*)p.P.heff;
@@ -149,35 +173,52 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       carry += __shfl_sync(FULL, sc, 31);
     }
   }
-  // per-chunk row lists: warp w scans the rows with a ballot compaction
-  {
+  // partition flags: 1 = orthogonal group O, 2 = non-orthogonal N (vrgraph.py:84-114)
+  for (int i = tid; i < K; i += nthr) inset[i] = 0;
+  __syncthreads();
+  if (AGG && p.P.orth_ptr) {
+    for (int q = p.P.orth_ptr[b] + tid; q < p.P.orth_ptr[b + 1]; q += nthr) inset[p.P.orth_idx[q]] = 1;
+    for (int q = p.P.non_ptr[b] + tid; q < p.P.non_ptr[b + 1]; q += nthr) inset[p.P.non_idx[q]] = 2;
+  }
+  __syncthreads();
+  // per-chunk row lists (all rows / O / N), ascending rows: warp w compacts with ballots.
+  // entry = (h element offset of this chunk | row << 20, P offset of (row, slot) | (row & 15))
+  auto build_list = [&](int* ptr, int2* out, int which) {
     int n = 0;
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
-      bool ov = i < K && c0[i] <= w && w <= c1[i];
-      unsigned bal = __ballot_sync(FULL, ov);
-      n += __popc(bal);
+      bool ov = i < K && c0[i] <= w && w <= c1[i] && (which == 0 || inset[i] == which);
+      n += __popc(__ballot_sync(FULL, ov));
     }
-    if (lane == 0) lptr[w + 1] = n;  // counts first; prefix below
-  }
-  __syncthreads();
-  if (tid == 0) {
-    lptr[0] = 0;
-    for (int ww = 0; ww < W; ++ww) lptr[ww + 1] += lptr[ww];
-  }
-  __syncthreads();
-  {
-    int n = lptr[w];
+    if (lane == 0) ptr[w + 1] = n;
+    __syncthreads();
+    if (tid == 0) {
+      ptr[0] = 0;
+      for (int ww = 0; ww < W; ++ww) ptr[ww + 1] += ptr[ww];
+    }
+    __syncthreads();
+    n = ptr[w];
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
-      bool ov = i < K && c0[i] <= w && w <= c1[i];
+      bool ov = i < K && c0[i] <= w && w <= c1[i] && (which == 0 || inset[i] == which);
       unsigned bal = __ballot_sync(FULL, ov);
       if (ov) {
         int slot = w - c0[i];
-        lst[n + __popc(bal & ((1u << lane) - 1))] = make_int2(hoff[i] + slot * CH, (i * SL + slot) * G | (i & 15));
+        out[n + __popc(bal & ((1u << lane) - 1))] = make_int2((hoff[i] + slot * CH) | (i << 20), (i * SL + slot) * G | (i & 15));
       }
       n += __popc(bal);
     }
+  };
+  __syncthreads();  // hoff ready
+  if (SCH != KZ_VR_OAHK) build_list(lptr, lst, 0);
+  if (SCH == KZ_VR_OAHK) {
+    build_list(optr, olst, 1);
+    build_list(nptr, nlst, 2);
+  }
+  // TMEM: 4 warps per 32-lane subpartition x 64 columns (2 rhs x 16 complex antennas) each
+  if constexpr (AGG) {
+    if (w == 0) tmem::alloc(misc, 256);
+    tmem::fence_before();
   }
   // rows -> shared memory, zero padded to whole chunks (flat parallel copy)
   {
@@ -220,9 +261,23 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     prevv[gg] = -1;
     poolcnt[gg] = 0;
     sel[gg] = -1;
+    noopv[gg] = 0;
+    nzv[gg] = 0;
   }
   __syncthreads();
   KZ_PHASE();
+  uint32_t my_tmem = 0;
+  if constexpr (AGG) {
+    tmem::fence_after();
+    my_tmem = misc[0] + ((uint32_t)(32 * (w & 3)) << 16) + 64u * (uint32_t)(w >> 2);
+  }
+  long long costO = 0, costN = 0;
+  int nN = 0;
+  for (int i = 0; i < K; ++i) {
+    if (inset[i] == 1) costO += 8LL * rowL[i] + 4;
+    if (inset[i] == 2) { costN += 8LL * rowL[i]; ++nN; }
+  }
+  const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
 
   constexpr int E = 16;  // antennas per thread per chunk
   const int a = lane >> 4, g = lane & 15;
@@ -268,7 +323,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     }
     T q = Qs[xs(i, gg)];
     const int c = g0 + gg;
-    if (SCH == KZ_GK || SCH == KZ_GRK) {  // dense form (solvers.py:149-153)
+    if (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_AHK) {  // dense form (solvers.py:149-153)
       T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
       if (i == c) r.x += 1.f;
       return r;
@@ -314,19 +369,19 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   int t;
   for (t = 1; t <= p.T; ++t) {
     KZ_ITER();
-    if constexpr (!PER_LANE_ROW) {
+    if constexpr (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK) {
       // refresh every row overlapping this chunk, two rows in flight
       int q = l0;
       for (; q + 1 < l1; q += 2) {
         int2 e0 = lst[q], e1 = lst[q + 1];
-        T v0 = dot_chunk(e0.x);
-        T v1 = dot_chunk(e1.x);
+        T v0 = dot_chunk(e0.x & 0xFFFFF);
+        T v1 = dot_chunk(e1.x & 0xFFFFF);
         Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = v0;
         Ps[(e1.y & ~31) + ((g + 16 * a) ^ (e1.y & 15))] = v1;
       }
       if (q < l1) {
         int2 e0 = lst[q];
-        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x);
+        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x & 0xFFFFF);
       }
       KZ_WSTAMP();
       __syncthreads();
@@ -417,7 +472,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       KZ_PHASE();
       project(m0, sel[g], gam[g]);
       project(m1, sel[g + 16], gam[g + 16]);
-    } else {
+    } else if constexpr (PER_LANE_ROW) {
       // row draw per rhs (host index stream / Philox), one thread per rhs
       if (tid < G) {
         const int gg = tid;
@@ -493,6 +548,216 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       project(m0, sel[g], gam[g]);
       project(m1, sel[g + 16], gam[g + 16]);
       __syncthreads();  // sel/gam are rewritten by the next draw
+    } else {  // AHK / VR-OAHK (solvers.py:407-421)
+      // refresh partials of the rows in list (ptr, L) -> P
+      auto refresh_list = [&](const int* ptr, const int2* L) {
+        int q = ptr[w];
+        const int q1 = ptr[w + 1];
+        for (; q + 1 < q1; q += 2) {
+          int2 e0 = L[q], e1 = L[q + 1];
+          T v0 = dot_chunk(e0.x & 0xFFFFF);
+          T v1 = dot_chunk(e1.x & 0xFFFFF);
+          Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = v0;
+          Ps[(e1.y & ~31) + ((g + 16 * a) ^ (e1.y & 15))] = v1;
+        }
+        if (q < q1) {
+          int2 e0 = L[q];
+          Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x & 0xFFFFF);
+        }
+      };
+      // residuals -> weights phi = r/e, num = vdot(phi, r), ||phi||^2 (warp per rhs; solvers.py:248-254, 274)
+      auto weights = [&](int which, int nrows) {
+        for (int gg = w; gg < G; gg += W) {
+          if (g0 + gg >= K || donev[gg]) {
+            if (lane == 0) nzv[gg] = 0;
+            continue;
+          }
+          float nx = 0.f, ny = 0.f, sp = 0.f;
+          bool nz = false;
+          for (int i = lane; i < K; i += 32) {
+            if (which && inset[i] != which) continue;
+            T r = resid(i, gg);
+            T ph = make_float2(r.x / en[i], r.y / en[i]);
+            Phi[xs(i, gg)] = ph;
+            nz |= (ph.x != 0.f || ph.y != 0.f);
+            nx = fmaf(ph.x, r.x, nx); nx = fmaf(ph.y, r.y, nx);
+            ny = fmaf(ph.x, r.y, ny); ny = fmaf(-ph.y, r.x, ny);
+            sp = fmaf(ph.x, ph.x, sp); sp = fmaf(ph.y, ph.y, sp);
+          }
+          nx = warp_sum(nx);
+          ny = warp_sum(ny);
+          sp = warp_sum(sp);
+          nz = __any_sync(FULL, nz);
+          if (lane == 0) {
+            numv[gg] = make_float2(nx, ny);
+            spv[gg] = sp;
+            nzv[gg] = (nz && nrows > 0) ? 1 : 0;
+            flv[gg] += 2LL * nrows;
+          }
+        }
+      };
+      // aggregated projection (solvers.py:257-309): m parked in TMEM while y = sum phi h
+      // (ascending rows) occupies the registers
+      auto aggregate = [&](const int* ptr, const int2* L, int nrows, int span, bool dense, bool mark_done,
+                           long long ycost) {
+        {
+          float f0[16], f1[16];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            f0[2 * k] = m0[k].x; f0[2 * k + 1] = m0[k].y;
+            f1[2 * k] = m0[k + 8].x; f1[2 * k + 1] = m0[k + 8].y;
+          }
+          tmem::st16(my_tmem, f0);
+          tmem::st16(my_tmem + 16, f1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            f0[2 * k] = m1[k].x; f0[2 * k + 1] = m1[k].y;
+            f1[2 * k] = m1[k + 8].x; f1[2 * k + 1] = m1[k + 8].y;
+          }
+          tmem::st16(my_tmem + 32, f0);
+          tmem::st16(my_tmem + 48, f1);
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);  // registers now hold y
+        for (int q = ptr[w]; q < ptr[w + 1]; ++q) {
+          const int2 e = L[q];
+          const int i = e.x >> 20;
+          const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
+          const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
+#pragma unroll
+          for (int j = 0; j < E / 2; ++j) {
+            float4 h = hp[2 * j];
+            const int k = 2 * j;
+            m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
+            m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
+            m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
+            m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
+          }
+        }
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          s0 = fmaf(m0[k].x, m0[k].x, fmaf(m0[k].y, m0[k].y, s0));
+          s1 = fmaf(m1[k].x, m1[k].x, fmaf(m1[k].y, m1[k].y, s1));
+        }
+        {
+          const float sd = a ? s0 : s1;
+          const float rv = __shfl_xor_sync(FULL, sd, 16);
+          Dp[w * G + g + 16 * a] = (a ? s1 : s0) + rv;
+        }
+        __syncthreads();
+        KZ_PHASE();
+        // step lengths of this thread's two rhs (fixed-order sums => identical in every thread)
+        auto gamma_of = [&](int rr, bool& step) -> T {
+          step = false;
+          if (!nzv[rr]) return make_float2(0.f, 0.f);
+          float den = 0.f;
+          for (int ww = 0; ww < W; ++ww) den += Dp[ww * G + rr];
+          den = fmaf(regf, spv[rr], den);
+          if (den == 0.f) return make_float2(0.f, 0.f);
+          step = true;
+          T nm = numv[rr];
+          return make_float2(nm.x / den, nm.y / den);
+        };
+        bool st0, st1;
+        const T gm0 = gamma_of(g, st0), gm1 = gamma_of(g + 16, st1);
+        tmem::wait_st();
+        {
+          float f0[16], f1[16];
+          tmem::ld16(my_tmem, f0);
+          tmem::ld16(my_tmem + 16, f1);
+          tmem::wait_ld();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            T o0 = make_float2(f0[2 * k], f0[2 * k + 1]), o1 = make_float2(f1[2 * k], f1[2 * k + 1]);
+            m0[k] = st0 ? cfma(gm0, m0[k], o0) : o0;
+            m0[k + 8] = st0 ? cfma(gm0, m0[k + 8], o1) : o1;
+          }
+          tmem::ld16(my_tmem + 32, f0);
+          tmem::ld16(my_tmem + 48, f1);
+          tmem::wait_ld();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            T o0 = make_float2(f0[2 * k], f0[2 * k + 1]), o1 = make_float2(f1[2 * k], f1[2 * k + 1]);
+            m1[k] = st1 ? cfma(gm1, m1[k], o0) : o0;
+            m1[k + 8] = st1 ? cfma(gm1, m1[k + 8], o1) : o1;
+          }
+        }
+        // q += gamma phi over the aggregated rows (threads over (row, rhs))
+        for (int e = tid; e < K * G; e += nthr) {
+          const int i = e / G, rr = e % G;
+          if ((SCH == KZ_VR_OAHK && inset[i] != 2) || g0 + rr >= K) continue;
+          bool st;
+          const T gm = gamma_of(rr, st);
+          if (st) Qs[xs(i, rr)] = cfma(gm, Phi[xs(i, rr)], Qs[xs(i, rr)]);
+        }
+        // bookkeeping once per rhs (warp 0: lane = rhs slot)
+        if (w == 0 && g0 + lane < K && !donev[lane]) {
+          bool st;
+          (void)gamma_of(lane, st);
+          const int n = nrows;
+          if (!nzv[lane]) {
+            noopv[lane] += 1;
+            if (mark_done) donev[lane] = 1;
+          } else {
+            long long f = 6LL * n + 2LL * max(n - 1, 0) + ycost + 4LL * span + 3LL * n + 2;
+            if (!st) {
+              noopv[lane] += 1;
+              if (mark_done) donev[lane] = 1;
+            } else {
+              f += 2 + 8LL * span + 8LL * n;
+              if (SCH == KZ_AHK) itv[lane] += 1;
+            }
+            flv[lane] += f;
+          }
+        }
+        (void)dense;
+      };
+
+      if constexpr (SCH == KZ_AHK) {
+        refresh_list(lptr, lst);
+        if (tid < G && g0 + tid < K && !donev[tid]) flv[tid] += dense_refresh;
+        __syncthreads();
+        KZ_PHASE();
+        weights(0, K);
+        __syncthreads();
+        KZ_PHASE();
+        aggregate(lptr, lst, K, Nt, true, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
+      } else {
+        // exact block projection on the orthogonal group O (solvers.py:312-332)
+        refresh_list(optr, olst);
+        __syncthreads();
+        KZ_PHASE();
+        for (int e = tid; e < K * G; e += nthr) {
+          const int i = e / G, rr = e % G;
+          if (inset[i] != 1 || g0 + rr >= K) continue;
+          const T r = resid(i, rr);
+          const T gm = make_float2(r.x / en[i], r.y / en[i]);
+          const T q = Qs[xs(i, rr)];
+          Qs[xs(i, rr)] = make_float2(q.x + gm.x, q.y + gm.y);
+          Phi[xs(i, rr)] = gm;
+        }
+        if (tid < G && g0 + tid < K) flv[tid] += 2 * costO + (nN ? costN + 4LL * nN : 0);
+        __syncthreads();
+        KZ_PHASE();
+        for (int q = optr[w]; q < optr[w + 1]; ++q) {
+          const int i = olst[q].x >> 20;
+          project(m0, i, Phi[xs(i, g)]);
+          project(m1, i, Phi[xs(i, g + 16)]);
+        }
+        if (nN > 0) {
+          refresh_list(nptr, nlst);
+          __syncthreads();
+          KZ_PHASE();
+          weights(2, nN);
+          __syncthreads();
+          KZ_PHASE();
+          aggregate(nptr, nlst, nN, unionN, false, false, costN);
+        }
+        if (tid < G && g0 + tid < K) itv[tid] += 1;
+      }
+      __syncthreads();  // bookkeeping visible before the all-done test
+      KZ_PHASE();
     }
     bool all_done = true;
     for (int gg = 0; gg < G; ++gg)
@@ -503,6 +768,10 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   const int t_end = t > p.T ? p.T : t;
   __syncthreads();
   KZ_PHASE();
+  if constexpr (AGG) {
+    tmem::fence_after();
+    if (w == 0) tmem::dealloc(misc[0], 256);
+  }
 
   // ------------------------------------------------------------------ outputs
   if (tid == 0) p.tstop[blockIdx.x] = t_end;
@@ -528,7 +797,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     if (p.O.iters) p.O.iters[r] = itv[gg];
     if (p.O.converged) p.O.converged[r] = 0;
     if (p.O.done) p.O.done[r] = donev[gg] ? 1 : 0;
-    if (p.O.noop_steps) p.O.noop_steps[r] = 0;
+    if (p.O.noop_steps) p.O.noop_steps[r] = noopv[gg];
     if (p.O.flops) p.O.flops[r] = flv[gg];
   }
 }
@@ -578,6 +847,8 @@ inline int wide_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const
     case KZ_GK: return wide_launch<KZ_GK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
     case KZ_GRK: return wide_launch<KZ_GRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
     case KZ_VR_OGRK: return wide_launch<KZ_VR_OGRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_AHK: return wide_launch<KZ_AHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    case KZ_VR_OAHK: return wide_launch<KZ_VR_OAHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
   }
   return 0;
 }
