@@ -162,7 +162,9 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
 
 size_t kz_epilogue_workspace_bytes(const kz_problem* prob) {
   if (!prob) return 0;
-  return kz_align((size_t)prob->n_systems * prob->n_users * prob->n_users * sizeof(double2));
+  size_t gram = (size_t)prob->n_systems * prob->n_users * prob->n_users * sizeof(double2);
+  size_t fbuf = (size_t)prob->n_systems * prob->n_antennas * prob->n_users * (prob->dtype == KZ_C128 ? 16 : 8);
+  return kz_align(gram > fbuf ? gram : fbuf);
 }
 
 int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double* v_ref, const double* beta_ref,
@@ -178,6 +180,19 @@ int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double
   if (need && (!workspace || workspace_bytes < need))
     return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
   cudaStream_t s = (cudaStream_t)stream;
+  if (prob->flags & KZ_PROBLEM_CONTIGUOUS) {
+    size_t smem = epilogue_contig_smem(prob->n_users);
+    if (prob->dtype == KZ_C128)
+      kz_epilogue_contig_kernel<double2><<<prob->n_systems, DENSE_THREADS, smem, s>>>(
+          *prob, (const double2*)v, (double2*)f_out, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out,
+          sum_rate_out, (double2*)workspace);
+    else
+      kz_epilogue_contig_kernel<float2><<<prob->n_systems, DENSE_THREADS, smem, s>>>(
+          *prob, (const float2*)v, (float2*)f_out, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out,
+          sum_rate_out, (float2*)workspace);
+    g_launches = 1;
+    return cuda_check("kz_epilogue(contiguous)");
+  }
   if (prob->dtype == KZ_C128)
     kz_epilogue_kernel<double2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(
         *prob, (const double2*)v, (double2*)f_out, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out,

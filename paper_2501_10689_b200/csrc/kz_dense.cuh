@@ -286,3 +286,159 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_kernel(kz_problem P
 }
 
 }  // namespace kz
+
+namespace kz {
+
+// ---------------------------------------------------------------- K3 fast path (contiguous VRs)
+// One CTA per system.  Rows are ranked by VR start so the rows covering antenna n
+// form a short window found by two binary searches; F = H V is assembled per
+// antenna with lanes over the K columns.  Pass 1 gives beta = 1/||HV||_F, pass 2
+// stores F = beta H V and accumulates ||beta_ref H V_ref - beta H V||^2 directly
+// (no cancellation), pass 3 forms H^H F over each user's VR for the Eq. (7) rates.
+template <class T>
+__global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_contig_kernel(
+    kz_problem P, const T* v, T* f_out, const double* v_ref, const double* beta_ref, const double* snr_linear,
+    double* beta_out, double* nmse_out, double* rates_out, double* sum_rate_out, T* fws) {
+  using R = typename Cx<T>::real;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.x, K = P.n_users, Nt = P.n_antennas;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int* st = (int*)sm;            // starts, original order
+  int* ln = st + K;              // lengths
+  int* ord = ln + K;             // rows ranked by start
+  int* ss = ord + K;             // sorted starts
+  long long* off = (long long*)(ss + K + (K & 1));
+  __shared__ double red[32];
+  __shared__ int s_lmax;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    size_t r = (size_t)b * K + i;
+    int sg = P.row_seg_ptr[r];
+    st[i] = P.seg_start[sg];
+    ln[i] = P.seg_len[sg];
+    off[i] = P.row_val_ptr[r];
+  }
+  if (threadIdx.x == 0) s_lmax = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    int rk = 0;
+    for (int j = 0; j < K; ++j) rk += (st[j] < st[i]) || (st[j] == st[i] && j < i);
+    ord[rk] = i;
+    ss[rk] = st[i];
+    atomicMax(&s_lmax, ln[i]);
+  }
+  __syncthreads();
+  const int lmax = s_lmax;
+  const T* H = (const T*)P.heff;
+  const T* V = v + (size_t)b * K * K;
+  const double2* Vr = v_ref ? (const double2*)v_ref + (size_t)b * K * K : nullptr;
+  auto window = [&](int n, int& lo, int& hi) {  // sorted positions with n - lmax < start <= n
+    int a0 = 0, a1 = K;
+    while (a0 < a1) { int m = (a0 + a1) >> 1; if (ss[m] <= n) a0 = m + 1; else a1 = m; }
+    hi = a0;
+    a0 = 0; a1 = hi;
+    while (a0 < a1) { int m = (a0 + a1) >> 1; if (ss[m] <= n - lmax) a0 = m + 1; else a1 = m; }
+    lo = a0;
+  };
+  // pass 1: ||H V||_F^2
+  double s1 = 0.0;
+  for (int n = warp; n < Nt; n += nw) {
+    int lo, hi;
+    window(n, lo, hi);
+    for (int c0 = 0; c0 < K; c0 += 32) {
+      const int c = c0 + lane;
+      R fr = 0, fi = 0;
+      for (int j = lo; j < hi; ++j) {
+        const int i = ord[j];
+        if (n >= st[i] + ln[i]) continue;
+        const T h = H[off[i] + (n - st[i])];
+        if (c < K) {
+          const T x = V[(size_t)i * K + c];
+          fr = fma(h.x, x.x, fr); fr = fma(-h.y, x.y, fr);
+          fi = fma(h.x, x.y, fi); fi = fma(h.y, x.x, fi);
+        }
+      }
+      s1 += (double)fr * fr + (double)fi * fi;
+    }
+  }
+  s1 = block_reduce_sum(s1, red);
+  const double beta = 1.0 / sqrt(s1);
+  if (beta_out && threadIdx.x == 0) beta_out[b] = beta;
+  // pass 2: F = beta H V (stored), NMSE against beta_ref H V_ref
+  T* F = f_out ? f_out + (size_t)b * Nt * K : fws + (size_t)b * Nt * K;
+  const double br = Vr ? beta_ref[b] : 0.0;
+  double e2 = 0.0, r2 = 0.0;
+  for (int n = warp; n < Nt; n += nw) {
+    int lo, hi;
+    window(n, lo, hi);
+    for (int c0 = 0; c0 < K; c0 += 32) {
+      const int c = c0 + lane;
+      R fr = 0, fi = 0;
+      double gr = 0.0, gi = 0.0;
+      for (int j = lo; j < hi; ++j) {
+        const int i = ord[j];
+        if (n >= st[i] + ln[i]) continue;
+        const T h = H[off[i] + (n - st[i])];
+        if (c < K) {
+          const T x = V[(size_t)i * K + c];
+          fr = fma(h.x, x.x, fr); fr = fma(-h.y, x.y, fr);
+          fi = fma(h.x, x.y, fi); fi = fma(h.y, x.x, fi);
+          if (Vr) {
+            const double2 y = Vr[(size_t)i * K + c];
+            const double hx = h.x, hy = h.y;
+            gr = fma(hx, y.x, gr); gr = fma(-hy, y.y, gr);
+            gi = fma(hx, y.y, gi); gi = fma(hy, y.x, gi);
+          }
+        }
+      }
+      if (c < K) {
+        const double ox = beta * fr, oy = beta * fi;
+        F[(size_t)n * K + c] = from_d2<T>(make_double2(ox, oy));
+        if (Vr) {
+          const double dx = br * gr - ox, dy = br * gi - oy;
+          e2 += dx * dx + dy * dy;
+          r2 += br * br * (gr * gr + gi * gi);
+        }
+      }
+    }
+  }
+  if (Vr) {
+    e2 = block_reduce_sum(e2, red);
+    r2 = block_reduce_sum(r2, red);
+    if (nmse_out && threadIdx.x == 0) nmse_out[b] = sqrt(e2) / sqrt(r2);
+  }
+  if (!snr_linear) return;
+  __syncthreads();  // F visible to the block
+  // pass 3: Eq. (7) rates from cross = H^H F over each user's VR (metrics.py:74-77)
+  const double noise = 1.0 / snr_linear[b];
+  double rsum = 0.0;
+  for (int k = warp; k < K; k += nw) {
+    double sig = 0.0, tot = 0.0;
+    for (int c0 = 0; c0 < K; c0 += 32) {
+      const int c = c0 + lane;
+      double re = 0.0, im = 0.0;
+      if (c < K)
+        for (int j = 0; j < ln[k]; ++j) {
+          const double2 h = to_d2(H[off[k] + j]);
+          const double2 x = to_d2(F[(size_t)(st[k] + j) * K + c]);
+          re = fma(h.x, x.x, re); re = fma(h.y, x.y, re);
+          im = fma(h.x, x.y, im); im = fma(-h.y, x.x, im);
+        }
+      const double pw = c < K ? np_abs2(re, im) : 0.0;
+      if (c == k) sig = pw;
+      tot += pw;
+    }
+    tot = warp_sum(tot);
+    sig = warp_sum(sig);
+    if (lane == 0) {
+      const double rate = log2(1.0 + sig / ((tot - sig) + noise));
+      if (rates_out) rates_out[(size_t)b * K + k] = rate;
+      rsum += rate;
+    }
+  }
+  rsum = block_reduce_sum(rsum, red);
+  if (sum_rate_out && threadIdx.x == 0) sum_rate_out[b] = rsum;
+}
+
+inline size_t epilogue_contig_smem(int K) { return (size_t)4 * K * 4 + 8 + (size_t)8 * K + 64; }
+
+}  // namespace kz

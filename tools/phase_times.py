@@ -42,8 +42,7 @@ cs = 16 if a.dtype == "c128" else 8
 extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 44 * 8
 base = ws.numel() - extra
 off = base + (B * K * 4 + 7) // 8 * 8
-rk = a.scheme in ("urk", "swor-erk", "gk", "grk", "vr-ogrk")
-G = (32 if rk and K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype == "c64" else 8
+G = (32 if K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype == "c64" else 8
 ncta = B * ((K + G - 1) // G)
 raw = ws[off:off + ncta * 44 * 8].view(torch.int64).view(ncta, 44).cpu().numpy().astype(np.float64)
 ph = raw[:, :12].copy()
