@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   }
   __syncthreads();
   // per-chunk row lists (all rows / O / N), ascending rows: warp w compacts with ballots.
-  // entry = (h element offset of this chunk | row << 20, P offset of (row, slot) | (row & 15))
+  // entry = (h element offset of this chunk | row << 20,
+  //          P offset of (row, slot) | (row & 15) | half-chunk mask << 28)
   auto build_list = [&](int* ptr, int2* out, int which) {
     int n = 0;
     for (int base = 0; base < K; base += 32) {
@@ -204,7 +205,11 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       unsigned bal = __ballot_sync(FULL, ov);
       if (ov) {
         int slot = w - c0[i];
-        out[n + __popc(bal & ((1u << lane) - 1))] = make_int2((hoff[i] + slot * CH) | (i << 20), (i * SL + slot) * G | (i & 15));
+        // which 16-antenna halves of this chunk the row's support touches (the rest is zero padding)
+        const int lo = rowS[i] - w * CH, hi = rowS[i] + rowL[i] - w * CH;
+        const int hm = (lo < 16 && hi > 0 ? 1 : 0) | (lo < 32 && hi > 16 ? 2 : 0);
+        out[n + __popc(bal & ((1u << lane) - 1))] =
+            make_int2((hoff[i] + slot * CH) | (i << 20), (i * SL + slot) * G | (i & 15) | (hm << 28));
       }
       n += __popc(bal);
     }
@@ -290,28 +295,35 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
 
   // conj(h) . m for both rhs over the chunk; returns this lane's rhs partial after
   // the a-lane exchange (lane a keeps rhs g + 16a)
-  auto dot_chunk = [&](int h0) -> T {
+  auto dot_chunk = [&](int h0, int hm) -> T {
     const float4* hp = H4 + ((h0 + 2 * a) >> 1);
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
 #pragma unroll
-    for (int j = 0; j < E / 2; ++j) {
-      float4 h = hp[2 * j];
-      const int k = 2 * j;
-      x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
-      y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
-      x1 = fmaf(h.z, m0[k + 1].x, x1); x1 = fmaf(h.w, m0[k + 1].y, x1);
-      y1 = fmaf(h.z, m0[k + 1].y, y1); y1 = fmaf(-h.w, m0[k + 1].x, y1);
-      u0 = fmaf(h.x, m1[k].x, u0); u0 = fmaf(h.y, m1[k].y, u0);
-      v0 = fmaf(h.x, m1[k].y, v0); v0 = fmaf(-h.y, m1[k].x, v0);
-      u1 = fmaf(h.z, m1[k + 1].x, u1); u1 = fmaf(h.w, m1[k + 1].y, u1);
-      v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
+    for (int half = 0; half < 2; ++half) {
+      if (!((hm >> half) & 1)) continue;  // that half of the chunk is zero padding for this row
+#pragma unroll
+      for (int jj = 0; jj < E / 4; ++jj) {
+        const int j = half * (E / 4) + jj;
+        float4 h = hp[2 * j];
+        const int k = 2 * j;
+        x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
+        y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
+        x1 = fmaf(h.z, m0[k + 1].x, x1); x1 = fmaf(h.w, m0[k + 1].y, x1);
+        y1 = fmaf(h.z, m0[k + 1].y, y1); y1 = fmaf(-h.w, m0[k + 1].x, y1);
+        u0 = fmaf(h.x, m1[k].x, u0); u0 = fmaf(h.y, m1[k].y, u0);
+        v0 = fmaf(h.x, m1[k].y, v0); v0 = fmaf(-h.y, m1[k].x, v0);
+        u1 = fmaf(h.z, m1[k + 1].x, u1); u1 = fmaf(h.w, m1[k + 1].y, u1);
+        v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
+      }
     }
     const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
-    // lane a keeps rhs a: send the other rhs' partial to the partner lane
+    // lane a keeps rhs g + 16a: send the other rhs' partial to the partner lane
     const float sx = a ? px : qx, sy = a ? py : qy;
     const float rx = __shfl_xor_sync(FULL, sx, 16), ry = __shfl_xor_sync(FULL, sy, 16);
     return a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
   };
+  // P element of list entry e for this lane's rhs
+  auto pslot = [&](int ey) { return (ey & 0x0FFFFFE0) + ((g + 16 * a) ^ (ey & 15)); };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
@@ -374,99 +386,109 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       int q = l0;
       for (; q + 1 < l1; q += 2) {
         int2 e0 = lst[q], e1 = lst[q + 1];
-        T v0 = dot_chunk(e0.x & 0xFFFFF);
-        T v1 = dot_chunk(e1.x & 0xFFFFF);
-        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = v0;
-        Ps[(e1.y & ~31) + ((g + 16 * a) ^ (e1.y & 15))] = v1;
+        T v0 = dot_chunk(e0.x & 0xFFFFF, e0.y >> 28);
+        T v1 = dot_chunk(e1.x & 0xFFFFF, e1.y >> 28);
+        Ps[pslot(e0.y)] = v0;
+        Ps[pslot(e1.y)] = v1;
       }
       if (q < l1) {
         int2 e0 = lst[q];
-        Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x & 0xFFFFF);
+        Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF, e0.y >> 28);
       }
       KZ_WSTAMP();
       __syncthreads();
       KZ_PHASE();
-      // finalise + select, one warp per rhs (lanes over rows)
-      for (int gg = w; gg < G; gg += W) {
-        if (g0 + gg >= K || donev[gg]) {
-          if (lane == 0) sel[gg] = -1;
-          continue;
-        }
-        float wsum = 0.f;
-        for (int i = lane; i < K; i += 32) {
-          bool upd = true;
-          if constexpr (SCH == KZ_VR_OGRK) {
-            int pr = prevv[gg];
-            upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
-          }
-          T r = upd ? resid(i, gg) : Rs[xs(i, gg)];
-          if (upd) Rs[xs(i, gg)] = r;
-          wsum += r.x * r.x + r.y * r.y;
-        }
-        __syncwarp();
-        int isel;
-        long long f;
-        if constexpr (SCH == KZ_GK) {
-          float best = -1.f;
-          int bi = 0x7fffffff;
-          bool any = false;
-          for (int i = lane; i < K; i += 32) {
-            T r = Rs[xs(i, gg)];
-            float s = (r.x * r.x + r.y * r.y) / en[i];
-            if (s != 0.f) any = true;
-            if (s > best) { best = s; bi = i; }
-          }
-          for (int o = 16; o > 0; o >>= 1) {
-            float ob = __shfl_xor_sync(FULL, best, o);
-            int oi = __shfl_xor_sync(FULL, bi, o);
-            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-          }
-          isel = __any_sync(FULL, any) ? bi : -1;
-          f = dense_refresh + 4LL * K;
-        } else {
-          float tot = warp_sum(wsum);
-          f = (SCH == KZ_GRK ? dense_refresh : (prevv[gg] >= 0 ? cost[prevv[gg]] : 0)) + 4LL * K + 2;
-          if (tot == 0.f) {
-            isel = -1;
+      // finalise + select: each half-warp serves one rhs (lanes over rows, 16-lane scans)
+      {
+        const int hf = lane >> 4, hl = lane & 15;
+        const unsigned hmask = 0xFFFFu << (16 * hf);
+        for (int pair = w; pair < G / 2; pair += W) {
+          const int gg = pair + hf * (G / 2);
+          const bool act = g0 + gg < K && !donev[gg];
+          double u = 0.0;
+          if (SCH != KZ_GK && act) u = draw_u(gg);  // independent of the residuals: issue early
+          float wsum = 0.f;
+          if (act)
+            for (int i = hl; i < K; i += 16) {
+              bool upd = true;
+              if constexpr (SCH == KZ_VR_OGRK) {
+                int pr = prevv[gg];
+                upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
+              }
+              T r = upd ? resid(i, gg) : Rs[xs(i, gg)];
+              if (upd) Rs[xs(i, gg)] = r;
+              wsum += r.x * r.x + r.y * r.y;
+            }
+          __syncwarp();
+          int isel = -1;
+          long long f;
+          if constexpr (SCH == KZ_GK) {
+            float best = -1.f;
+            int bi = 0x7fffffff;
+            bool any = false;
+            if (act)
+              for (int i = hl; i < K; i += 16) {
+                T r = Rs[xs(i, gg)];
+                float sc = (r.x * r.x + r.y * r.y) / en[i];
+                if (sc != 0.f) any = true;
+                if (sc > best) { best = sc; bi = i; }
+              }
+            for (int o = 8; o > 0; o >>= 1) {
+              float ob = __shfl_xor_sync(FULL, best, o);
+              int oi = __shfl_xor_sync(FULL, bi, o);
+              if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            isel = (__ballot_sync(FULL, any) & hmask) ? bi : -1;
+            f = dense_refresh + 4LL * K;
           } else {
-            const float tau = (float)draw_u(gg) * tot;
+            float tot = wsum;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+            f = (SCH == KZ_GRK ? dense_refresh : (prevv[gg] >= 0 ? cost[prevv[gg]] : 0)) + 4LL * K + 2;
+            const float tau = (float)u * tot;
             float carry = 0.f;
             int lastnz = -1;
-            isel = -1;
-            for (int base = 0; base < K && isel < 0; base += 32) {
-              int i = base + lane;
+            bool found = !(tot > 0.f);  // tot == 0: None, no draw is consumed (solvers.py:235-236)
+            for (int base = 0; base < K; base += 16) {
+              if (__all_sync(FULL, found)) break;
+              const int i = base + hl;
               float v = 0.f;
-              if (i < K) {
+              if (act && i < K) {
                 T r = Rs[xs(i, gg)];
                 v = r.x * r.x + r.y * r.y;
               }
               float sc = v;
 #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                float t2 = __shfl_up_sync(FULL, sc, o);
-                if (lane >= o) sc += t2;
+              for (int o = 1; o < 16; o <<= 1) {
+                float t2 = __shfl_up_sync(FULL, sc, o, 16);
+                if (hl >= o) sc += t2;
               }
-              unsigned bal = __ballot_sync(FULL, i < K && v > 0.f && carry + sc > tau);
-              if (bal) isel = base + __ffs(bal) - 1;
-              unsigned nzb = __ballot_sync(FULL, i < K && v > 0.f);
+              const unsigned bal = (__ballot_sync(FULL, !found && i < K && v > 0.f && carry + sc > tau) & hmask) >> (16 * hf);
+              const unsigned nzb = (__ballot_sync(FULL, i < K && v > 0.f) & hmask) >> (16 * hf);
+              if (!found && bal) {
+                isel = base + __ffs(bal) - 1;
+                found = true;
+              }
               if (nzb) lastnz = base + 31 - __clz(nzb);
-              carry += __shfl_sync(FULL, sc, 31);
+              carry += __shfl_sync(FULL, sc, 15, 16);
             }
-            if (isel < 0) isel = lastnz;
+            if (tot > 0.f && isel < 0) isel = lastnz;
           }
-        }
-        if (lane == 0) {
-          if (isel < 0) {
-            donev[gg] = 1;
+          if (hl == 0 && act) {
+            if (isel < 0) {
+              donev[gg] = 1;
+              sel[gg] = -1;
+              flv[gg] += f;
+            } else {
+              long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[isel] + 2 : dense_rk;
+              take_step(gg, isel, Rs[xs(isel, gg)], f + fr);
+              if constexpr (SCH == KZ_VR_OGRK) prevv[gg] = isel;
+            }
+          } else if (hl == 0) {
             sel[gg] = -1;
-            flv[gg] += f;
-          } else {
-            long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[isel] + 2 : dense_rk;
-            take_step(gg, isel, Rs[xs(isel, gg)], f + fr);
-            if constexpr (SCH == KZ_VR_OGRK) prevv[gg] = isel;
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
       __syncthreads();
       KZ_PHASE();
@@ -555,14 +577,14 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         const int q1 = ptr[w + 1];
         for (; q + 1 < q1; q += 2) {
           int2 e0 = L[q], e1 = L[q + 1];
-          T v0 = dot_chunk(e0.x & 0xFFFFF);
-          T v1 = dot_chunk(e1.x & 0xFFFFF);
-          Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = v0;
-          Ps[(e1.y & ~31) + ((g + 16 * a) ^ (e1.y & 15))] = v1;
+          T v0 = dot_chunk(e0.x & 0xFFFFF, e0.y >> 28);
+          T v1 = dot_chunk(e1.x & 0xFFFFF, e1.y >> 28);
+          Ps[pslot(e0.y)] = v0;
+          Ps[pslot(e1.y)] = v1;
         }
         if (q < q1) {
           int2 e0 = L[q];
-          Ps[(e0.y & ~31) + ((g + 16 * a) ^ (e0.y & 15))] = dot_chunk(e0.x & 0xFFFFF);
+          Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF, e0.y >> 28);
         }
       };
       // residuals -> weights phi = r/e, num = vdot(phi, r), ||phi||^2 (warp per rhs; solvers.py:248-254, 274)
@@ -624,14 +646,20 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           const int i = e.x >> 20;
           const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
           const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
+          const int hm = e.y >> 28;
 #pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
-            float4 h = hp[2 * j];
-            const int k = 2 * j;
-            m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
-            m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
-            m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
-            m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
+          for (int half = 0; half < 2; ++half) {
+            if (!((hm >> half) & 1)) continue;
+#pragma unroll
+            for (int jj = 0; jj < E / 4; ++jj) {
+              const int j = half * (E / 4) + jj;
+              float4 h = hp[2 * j];
+              const int k = 2 * j;
+              m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
+              m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
+              m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
+              m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
+            }
           }
         }
         float s0 = 0.f, s1 = 0.f;
