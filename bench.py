@@ -147,9 +147,11 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- algorithmic bytes
 
-def h_bytes_per_launch(host, scheme, iters, csize):
-    """H_eff bytes the algorithm streams per rhs-iteration, summed over
-    every (system, rhs) of one launch of T iterations."""
+def h_elems_per_launch(host, scheme, iters):
+    """H_eff elements the algorithm streams per rhs-iteration
+    (sum over R_t of |Gamma_i| plus the projected row), summed over every
+    (system, rhs) of one launch of T iterations.  Bytes = elems * sizeof(complex);
+    real flops = 8 * elems (one complex MAC per streamed element)."""
     sup = host.support_sizes().astype(np.float64)        # (B, K)
     b, k = sup.shape
     tot_rows = sup.sum(axis=1)                            # sum_i |Gamma_i| per system
@@ -167,7 +169,35 @@ def h_bytes_per_launch(host, scheme, iters, csize):
         per = xs + mean_row
     else:  # ahk, vr-oahk: refresh + aggregation over every row
         per = 2 * tot_rows
-    return float(csize * iters * k * per.sum())
+    return float(iters * k * per.sum())
+
+
+MICRO = os.path.join(ROOT, "profiles", "r01_microbench.json")
+
+
+def measured_fp32_peak():
+    """FP32 FFMA peak (TFLOP/s) from tools/microbench.cu as committed under profiles/."""
+    try:
+        with open(MICRO) as fh:
+            for line in fh:
+                d = json.loads(line)
+                if d.get("probe") == "FFMA":
+                    return float(d["chip_TFLOPs_fp32"]), "measured (tools/microbench.cu, profiles/r01_microbench.json)"
+    except (OSError, ValueError):
+        pass
+    return 2 * 148 * 128 * 1.965e9 / 1e12, "nominal 148 SM x 128 FFMA/clk x 1.965 GHz"
+
+
+def measured_smem_peak():
+    try:
+        with open(MICRO) as fh:
+            for line in fh:
+                d = json.loads(line)
+                if d.get("probe") == "LDS.128 distinct":
+                    return float(d["chip_TBps"]) * 1e3
+    except (OSError, ValueError):
+        pass
+    return 148 * 128 * 1.965e9 / 1e9
 
 
 # --------------------------------------------------------------------------- main
@@ -290,7 +320,7 @@ def main():
     # dominant kernel: the scheme solve with the largest launch time
     avg = {sc: float(np.mean([x.elapsed_time(y) for x, y in ev])) for sc, ev in per_scheme.items()}
     dom = max(avg, key=avg.get)
-    bytes_dom = h_bytes_per_launch(host, dom, iters, csize)
+    elems_dom = h_elems_per_launch(host, dom, iters)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -298,8 +328,17 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bytes_dom / (avg[dom] / 1e3) / 1e9
-
+    fp32_peak, fp32_src = measured_fp32_peak()
+    smem_peak = measured_smem_peak()
+    t_dom = avg[dom] / 1e3
+    tflops = 8.0 * elems_dom / t_dom / 1e12
+    bytes_dom = csize * elems_dom
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)
+    except (OSError, ValueError):
+        pass
     # end to end through the public API: host buffers in, per-system results out
     e2e = None
     if not a.no_e2e:
@@ -354,11 +393,15 @@ def main():
                        "rng": "on-device Philox4x32-10 row draws", "parallelism": f"realizations sharded x{world}"},
             "rhs_iterations_per_s": rhs_iters,
             "per_scheme_launch_ms": avg,
-            "roofline": {"kernel": f"kz_solve[{dom}]", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
-                         "algorithmic_bytes_per_launch": bytes_dom,
-                         "note": "algorithmic H_eff bytes per SURVEY §8(d) / CUDA-event launch time; "
-                                 "peak = MEASURED_PEAKS.json hbm_gbs"},
+            "roofline": {"kernel": f"kz_solve[{dom}]", "bound": "fp32-fma", "achieved": tflops,
+                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": tflops / fp32_peak, "traffic": traffic,
+                         "algorithmic_flops_per_launch": 8.0 * elems_dom, "peak_source": fp32_src,
+                         "note": "H_eff is shared-memory resident and each streamed h element is reused by "
+                                 "4 rhs in registers, so the launch is CUDA-core FMA bound (SURVEY 8(d): report "
+                                 "the FMA roofline); flops = 8 x streamed H_eff elements per rhs-iteration",
+                         "smem_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": smem_peak},
+                         "hbm_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": hbm_peak,
+                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "stats": stats,
         }
