@@ -138,6 +138,7 @@ typedef struct kz_out {
   double* resid_trace;
   int64_t* flops_trace;
   int32_t* n_checks;        /* optional [B*K] (RESIDUAL/ORACLE): entries written per rhs */
+  void* iterates;           /* optional [B][K rhs][Nt] complex (dtype): final iterate m (SolverState.col) */
 } kz_out;
 
 /* Bytes of device workspace kz_solve needs for this problem (iterates M, residuals,
@@ -149,10 +150,6 @@ size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop);
    workspace (next host-stream chunk). */
 int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng,
              kz_out* out, void* workspace, size_t workspace_bytes, int32_t resume, void* stream);
-
-/* Device pointer to the iterate block M (col = H coef) inside a solve workspace:
-   [B][K rhs][Nt] complex (dtype). */
-void* kz_workspace_iterates(const kz_problem* prob, void* workspace);
 
 /* Batched direct RZF (rzf.py:38-83): Gram H^H H + reg I from the packed rows,
    Cholesky, V = Gram^{-1}, F = beta H V with ||F||_F = 1.  Always complex128.

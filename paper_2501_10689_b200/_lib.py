@@ -55,7 +55,7 @@ class KzOut(C.Structure):
         ("v", P), ("iters", P), ("converged", P), ("done", P), ("noop_steps", P), ("flops", P),
         ("n_outer", P), ("sys_converged", P), ("paused", P), ("rows", P),
         ("rows_cap", C.c_int32), ("trace_cap", C.c_int32),
-        ("nmse_trace", P), ("resid_trace", P), ("flops_trace", P), ("n_checks", P),
+        ("nmse_trace", P), ("resid_trace", P), ("flops_trace", P), ("n_checks", P), ("iterates", P),
     ]
 
 
@@ -93,7 +93,7 @@ def lib():
 
 EXPORTS = (
     "kz_abi_version", "kz_last_error", "kz_last_launch_count",
-    "kz_solve_workspace_bytes", "kz_solve", "kz_workspace_iterates",
+    "kz_solve_workspace_bytes", "kz_solve",
     "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue",
 )
 
@@ -107,8 +107,6 @@ def _declare(lb):
     lb.kz_solve.restype = C.c_int
     lb.kz_solve.argtypes = [C.POINTER(KzProblem), C.c_int32, C.POINTER(KzStop), C.POINTER(KzRng),
                             C.POINTER(KzOut), P, C.c_size_t, C.c_int32, P]
-    lb.kz_workspace_iterates.restype = P
-    lb.kz_workspace_iterates.argtypes = [C.POINTER(KzProblem), P]
     lb.kz_rzf_workspace_bytes.restype = C.c_size_t
     lb.kz_rzf_workspace_bytes.argtypes = [C.POINTER(KzProblem)]
     lb.kz_rzf.restype = C.c_int

@@ -685,8 +685,13 @@ __global__ void __launch_bounds__(GEN_WARPS * 32) kz_generic_kernel(Gen<T> g, in
     __syncthreads();
   }
 
-  // ---- outputs: v[b][i][c] = coef_i of rhs c, per-rhs counters
+  // ---- outputs: v[b][i][c] = coef_i of rhs c, per-rhs counters, optional iterates
   for (int c = warp; c < K; c += nw) {
+    if (g.O.iterates) {
+      const T* m = g.M(b, c);
+      T* mo = (T*)g.O.iterates + g.rid(b, c) * Nt;
+      for (int n = lane; n < Nt; n += 32) mo[n] = m[n];
+    }
     const T* q = g.Qv(b, c);
     T* v = (T*)g.O.v;
     for (int i = lane; i < K; i += 32) v[((size_t)b * K + i) * K + c] = q[i];

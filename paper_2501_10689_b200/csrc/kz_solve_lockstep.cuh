@@ -768,8 +768,8 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   {
     const int c = g0 + g;
-    if (c < K) {
-      T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt;
+    if (c < K && p.O.iterates) {
+      T* M = (T*)p.O.iterates + ((size_t)b * K + c) * Nt;
 #pragma unroll
       for (int k = 0; k < NPT; ++k) M[ant(k)] = m[k];
     }

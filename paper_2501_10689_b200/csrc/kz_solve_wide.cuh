@@ -788,8 +788,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
     const int c = g0 + g + 8 * r;
-    if (c < K) {
-      T* M = (T*)(p.ws + p.L.M) + ((size_t)b * K + c) * Nt + w * CH;
+    if (c < K && p.O.iterates) {
+      T* M = (T*)p.O.iterates + ((size_t)b * K + c) * Nt + w * CH;
 #pragma unroll
       for (int k = 0; k < E; ++k) M[8 * (k >> 1) + 2 * a + (k & 1)] = m[r][k];
     }

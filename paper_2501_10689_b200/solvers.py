@@ -238,15 +238,13 @@ class BatchResult:
     workspace: object = None
     launches: int = 0
 
+    m: object = None          # (B, K rhs, Nt) final iterates when requested
+
     def iterates(self):
-        """Device view of the iterate block M as (B, K rhs, Nt) complex."""
-        import torch
-        ptr = _lib.lib().kz_workspace_iterates(C.byref(self.dev.problem), self.workspace.data_ptr())
-        off = ptr - self.workspace.data_ptr()
-        b, k, nt = self.dev.n_systems, self.dev.n_users, self.dev.n_antennas
-        isz = 16 if self.dev.dtype == "c128" else 8
-        raw = self.workspace[off:off + b * k * nt * isz]
-        return raw.view(self.dev.complex_dtype).view(b, k, nt)
+        """Final iterate block M (col = H coef) as (B, K rhs, Nt); needs want_iterates=True."""
+        if self.m is None:
+            raise ValueError("solve_batch(..., want_iterates=True) was not requested")
+        return self.m
 
 
 def _stream_ptr(stream):
@@ -257,7 +255,8 @@ def _stream_ptr(stream):
 
 def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_iters: int, epsilon: float = 0.0,
                 check_every: int = 1, f_ref=None, v_ref=None, rng=None, rows_cap: int = 0, trace_cap: int = 0,
-                rhs_mask=None, chunk: int | None = None, stream=None, workspace=None) -> BatchResult:
+                rhs_mask=None, chunk: int | None = None, stream=None, workspace=None,
+                want_iterates: bool = False) -> BatchResult:
     """Run `scheme` on every (system, rhs) of `dev` with one kz_solve launch.
 
     mode: "lockstep" (run_precoding), "residual" / "oracle" (solve / solve_all).
@@ -279,6 +278,8 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
                       noop_steps=z(b, k, dt=torch.int32), flops=z(b, k, dt=torch.int64),
                       n_outer=z(b, dt=torch.int32), sys_converged=z(b, dt=torch.uint8))
     paused = z(b, k, dt=torch.uint8)
+    if want_iterates:
+        res.m = z(b, k, dev.n_antennas, dt=cdt)
     if rows_cap:
         res.rows = torch.full((b, k, rows_cap), -1, dtype=torch.int32, device=d)
     if trace_cap:
@@ -317,6 +318,8 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
     out.n_outer = res.n_outer.data_ptr()
     out.sys_converged = res.sys_converged.data_ptr()
     out.paused = paused.data_ptr()
+    if want_iterates:
+        out.iterates = res.m.data_ptr()
     if rows_cap:
         out.rows = res.rows.data_ptr()
         out.rows_cap = rows_cap
@@ -485,7 +488,7 @@ def solve(scheme: str, sys, rhs: int, stop: StoppingRule, rng: np.random.Generat
     cap_trace = max(1, cap // stop.check_every + 1)
     res = solve_batch(dev, scheme, mode=stop.mode, max_iters=cap, epsilon=stop.epsilon,
                       check_every=stop.check_every, v_ref=v_ref, rng=streams, rhs_mask=mask,
-                      trace_cap=min(cap_trace, 1 << 20))
+                      trace_cap=min(cap_trace, 1 << 20), want_iterates=True)
     st = _state_from(res, rhs)
     n = int(res.n_checks[0, rhs])
     tr = RunTrace(scheme=display_scheme(scheme))

@@ -363,7 +363,7 @@ def test_philox_full_cfg2_properties(scheme):
     rz = kz.rzf_batched(dev)
     errs = []
     for T in (25, 200):
-        res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rng=("philox", 1234))
+        res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rng=("philox", 1234), want_iterates=True)
         ep = kz.epilogue(dev, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, want_f=True)
         errs.append(ep["nmse"].cpu().numpy())
         assert torch.isfinite(ep["sum_rate"]).all()
@@ -424,7 +424,7 @@ def test_register_resident_iterates_are_h_coef():
     kz = _kz()
     ch = kz.generate("cfg2", range(8))
     dev = kz.HostBatch.from_contiguous(ch).to_device("c128")
-    res = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20)
+    res = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20, want_iterates=True)
     hv = kz.epilogue(dev, res.v, want_f=True)
     f = (hv["f"] / hv["beta"][:, None, None]).transpose(1, 2).cpu().numpy()
     assert rel(res.iterates().cpu().numpy(), f) <= 1e-12

@@ -36,7 +36,6 @@ import ctypes  # noqa: E402
 from paper_2501_10689_b200 import _lib  # noqa: E402
 lb = _lib.lib()
 ws = res.workspace
-m_off = lb.kz_workspace_iterates(ctypes.byref(dev.problem), ws.data_ptr()) - ws.data_ptr()
 cs = 16 if a.dtype == "c128" else 8
 # generic layout total = offset of tstop; recompute from the end: tstop region starts at ws.numel() - extra
 extra = ((B * K * 4 + 8 + 255) // 256 * 256) + B * K * 44 * 8
