@@ -1,22 +1,20 @@
 // Wide register-resident lockstep kernel for the single-row (RK) family in
 // complex64: urk, swor-erk, gk, grk, vr-ogrk (fixed T, contiguous VRs).
 //
-// One CTA = one system x 32 right-hand sides.  Lane (a, g), a = lane >> 3,
-// g = lane & 7, owns the four rhs c = g0 + g + 8r (r < 4, register blocking)
-// on the 8 antennas 32w + 8j + 2a + e (j < 4, e < 2) of warp w's chunk, so
-// thread (w, lane) keeps 4 x 8 iterate entries in 64 registers.  Rows live in
-// shared memory zero-padded to whole 32-antenna chunks; a (row, chunk)
-// product is 4 LDS.128 per thread feeding 128 FMAs (each h element reused by
-// four rhs) with no predicates.  The four a-lanes then exchange-reduce (six
-// shuffles) so that lane a holds the total of rhs g + 8a, and every lane
-// stores one partial into the slot array P[i][slot][rhs] (slot = chunk - first
-// chunk of the row), summed in a fixed order by the half-warp that selects for
-// that rhs (deterministic).
-// Why: shared memory delivers 128 B/clk/SM on B200 (tools/microbench.cu; a
+// One CTA = one system x 32 right-hand sides.  Lane (a, g), a = lane >> 4,
+// g = lane & 15, owns the two rhs c = g0 + g and c + 16 (register blocking)
+// on the 16 antennas 32w + 4j + 2a + e (j < 8, e < 2) of warp w's chunk, so
+// thread (w, lane) keeps 2 x 16 iterate entries in 64 registers.  Rows live
+// in shared memory zero-padded to whole 32-antenna chunks; a (row, chunk)
+// product is 8 LDS.128 per thread feeding 128 FMAs (each h element reused for
+// both rhs) with no predicates.  The two a-lanes exchange one partial each
+// (one shuffle pair), then every lane stores its own rhs partial into the slot
+// array P[i][slot][rhs] (slot = chunk - first chunk of the row), summed in a
+// fixed order by the warp that selects for that rhs (deterministic).
+// Why: shared memory delivers 128 B/clk/SM on B200 (tools/microbench.cu, a
 // broadcast LDS.128 costs as much as a distinct one) and FFMA issues 128
-// lanes/clk/SM: one rhs per h element (8 B -> 4 FMA) caps the refresh at 50% of
-// the FMA roofline, two balance the pipes exactly (measured ~60% of each),
-// four leave the SMEM pipe half idle so the refresh is FMA-bound.
+// lanes/clk/SM, so one rhs per h element (8 B -> 4 FMA) caps the refresh at
+// 50% of the FMA roofline; two rhs per element balance the two pipes.
 // Semantics: InstanceRun.step for urk / swor-erk / gk / grk / vr-ogrk
 // (solvers.py:382-406) with the FlopCounter charges of each primitive.
 #pragma once
@@ -286,63 +284,43 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
 
-  constexpr int RB = 4;  // rhs per thread (register blocking)
-  constexpr int E = 8;   // antennas per thread per chunk: 32w + 8j + 2a + e (j < 4, e < 2)
-  const int a = lane >> 3, g = lane & 7;  // thread rhs: g + 8r (r < 4); after a reduction lane a owns g + 8a
-  T m[RB][E];
+  constexpr int E = 16;  // antennas per thread per chunk
+  const int a = lane >> 4, g = lane & 15;
+  T m0[E], m1[E];  // rhs g and g + 16
 #pragma unroll
-  for (int r = 0; r < RB; ++r)
-#pragma unroll
-    for (int k = 0; k < E; ++k) m[r][k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
   const int l0 = lptr[w], l1 = lptr[w + 1];
   const float4* H4 = reinterpret_cast<const float4*>(Hs);
+  // antenna of element k of this thread within the chunk: 4*(k/2) + 2a + (k&1)
 
-  // exchange-reduce over the 4 a-lanes: in v[r] = partial of rhs g + 8r, out = total of rhs g + 8a
-  auto xreduce = [&](const float (&vx)[RB], const float (&vy)[RB]) -> T {
-    const bool hi = a & 2;
-    float k0x = hi ? vx[2] : vx[0], k0y = hi ? vy[2] : vy[0];
-    float k1x = hi ? vx[3] : vx[1], k1y = hi ? vy[3] : vy[1];
-    const float s0x = hi ? vx[0] : vx[2], s0y = hi ? vy[0] : vy[2];
-    const float s1x = hi ? vx[1] : vx[3], s1y = hi ? vy[1] : vy[3];
-    k0x += __shfl_xor_sync(FULL, s0x, 16);
-    k0y += __shfl_xor_sync(FULL, s0y, 16);
-    k1x += __shfl_xor_sync(FULL, s1x, 16);
-    k1y += __shfl_xor_sync(FULL, s1y, 16);
-    const bool od = a & 1;
-    const float sx = od ? k0x : k1x, sy = od ? k0y : k1y;
-    float kx = od ? k1x : k0x, ky = od ? k1y : k0y;
-    kx += __shfl_xor_sync(FULL, sx, 8);
-    ky += __shfl_xor_sync(FULL, sy, 8);
-    return make_float2(kx, ky);
-  };
-  // conj(h) . m for the four rhs over this thread's 8 antennas of the chunk (16 FMA chains)
+  // conj(h) . m for both rhs over the chunk; returns this lane's rhs partial after
+  // the a-lane exchange (lane a keeps rhs g + 16a)
   auto dot_chunk = [&](int h0) -> T {
     const float4* hp = H4 + ((h0 + 2 * a) >> 1);
-    float ax[RB][2], ay[RB][2];
+    float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
+    {
 #pragma unroll
-    for (int r = 0; r < RB; ++r) ax[r][0] = ax[r][1] = ay[r][0] = ay[r][1] = 0.f;
-#pragma unroll
-    for (int j = 0; j < E / 2; ++j) {
-      const float4 h = hp[4 * j];
-      const int k = 2 * j;
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        ax[r][0] = fmaf(h.x, m[r][k].x, ax[r][0]); ax[r][0] = fmaf(h.y, m[r][k].y, ax[r][0]);
-        ay[r][0] = fmaf(h.x, m[r][k].y, ay[r][0]); ay[r][0] = fmaf(-h.y, m[r][k].x, ay[r][0]);
-        ax[r][1] = fmaf(h.z, m[r][k + 1].x, ax[r][1]); ax[r][1] = fmaf(h.w, m[r][k + 1].y, ax[r][1]);
-        ay[r][1] = fmaf(h.z, m[r][k + 1].y, ay[r][1]); ay[r][1] = fmaf(-h.w, m[r][k + 1].x, ay[r][1]);
+      for (int j = 0; j < E / 2; ++j) {
+        float4 h = hp[2 * j];
+        const int k = 2 * j;
+        x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
+        y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
+        x1 = fmaf(h.z, m0[k + 1].x, x1); x1 = fmaf(h.w, m0[k + 1].y, x1);
+        y1 = fmaf(h.z, m0[k + 1].y, y1); y1 = fmaf(-h.w, m0[k + 1].x, y1);
+        u0 = fmaf(h.x, m1[k].x, u0); u0 = fmaf(h.y, m1[k].y, u0);
+        v0 = fmaf(h.x, m1[k].y, v0); v0 = fmaf(-h.y, m1[k].x, v0);
+        u1 = fmaf(h.z, m1[k + 1].x, u1); u1 = fmaf(h.w, m1[k + 1].y, u1);
+        v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
       }
     }
-    float vx[RB], vy[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      vx[r] = ax[r][0] + ax[r][1];
-      vy[r] = ay[r][0] + ay[r][1];
-    }
-    return xreduce(vx, vy);
+    const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
+    // lane a keeps rhs g + 16a: send the other rhs' partial to the partner lane
+    const float sx = a ? px : qx, sy = a ? py : qy;
+    const float rx = __shfl_xor_sync(FULL, sx, 16), ry = __shfl_xor_sync(FULL, sy, 16);
+    return a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
   };
-  // P element of list entry e for this lane's reduced rhs
-  auto pslot = [&](int ey) { return (ey & 0x0FFFFFE0) + ((g + 8 * a) ^ (ey & 15)); };
+  // P element of list entry e for this lane's rhs
+  auto pslot = [&](int ey) { return (ey & 0x0FFFFFE0) + ((g + 16 * a) ^ (ey & 15)); };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
@@ -380,19 +358,18 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     itv[gg] = it + 1;
     flv[gg] += f;
   };
-  // m[r] += gm h_i on this thread's antennas of the chunk (rows zero padded => whole chunk)
-  auto project = [&](int r, int i, T gm) {
+  // m_r += gm h_i on this thread's antennas of the chunk (rows zero padded => whole chunk)
+  auto project = [&](T (&mr)[E], int i, T gm) {
     if (i < 0 || w < c0[i] || w > c1[i]) return;
     const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      if (rr != r) continue;
-#pragma unroll
-      for (int j = 0; j < E / 2; ++j) {
-        const float4 h = hp[4 * j];
-        m[rr][2 * j] = cfma(gm, make_float2(h.x, h.y), m[rr][2 * j]);
-        m[rr][2 * j + 1] = cfma(gm, make_float2(h.z, h.w), m[rr][2 * j + 1]);
-      }
+    for (int j = 0; j < E / 2; ++j) {
+      float4 h = hp[2 * j];
+      const int k = 2 * j;
+      mr[k].x = fmaf(gm.x, h.x, mr[k].x); mr[k].x = fmaf(-gm.y, h.y, mr[k].x);
+      mr[k].y = fmaf(gm.x, h.y, mr[k].y); mr[k].y = fmaf(gm.y, h.x, mr[k].y);
+      mr[k + 1].x = fmaf(gm.x, h.z, mr[k + 1].x); mr[k + 1].x = fmaf(-gm.y, h.w, mr[k + 1].x);
+      mr[k + 1].y = fmaf(gm.x, h.w, mr[k + 1].y); mr[k + 1].y = fmaf(gm.y, h.z, mr[k + 1].y);
     }
   };
 
@@ -402,8 +379,17 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   for (t = 1; t <= p.T; ++t) {
     KZ_ITER();
     if constexpr (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK) {
-      for (int q = l0; q < l1; ++q) {
-        const int2 e0 = lst[q];
+      // refresh every row overlapping this chunk, two rows in flight
+      int q = l0;
+      for (; q + 1 < l1; q += 2) {
+        int2 e0 = lst[q], e1 = lst[q + 1];
+        T v0 = dot_chunk(e0.x & 0xFFFFF);
+        T v1 = dot_chunk(e1.x & 0xFFFFF);
+        Ps[pslot(e0.y)] = v0;
+        Ps[pslot(e1.y)] = v1;
+      }
+      if (q < l1) {
+        int2 e0 = lst[q];
         Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF);
       }
       KZ_WSTAMP();
@@ -474,8 +460,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
                 float t2 = __shfl_up_sync(FULL, sc, o, 16);
                 if (hl >= o) sc += t2;
               }
-              const unsigned bal =
-                  (__ballot_sync(FULL, !found && i < K && v > 0.f && carry + sc > tau) & hmask) >> (16 * hf);
+              const unsigned bal = (__ballot_sync(FULL, !found && i < K && v > 0.f && carry + sc > tau) & hmask) >> (16 * hf);
               const unsigned nzb = (__ballot_sync(FULL, i < K && v > 0.f) & hmask) >> (16 * hf);
               if (!found && bal) {
                 isel = base + __ffs(bal) - 1;
@@ -504,8 +489,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-#pragma unroll
-      for (int r = 0; r < RB; ++r) project(r, sel[g + 8 * r], gam[g + 8 * r]);
+      project(m0, sel[g], gam[g]);
+      project(m1, sel[g + 16], gam[g + 16]);
     } else if constexpr (PER_LANE_ROW) {
       // row draw per rhs (host index stream / Philox), one thread per rhs
       if (tid < G) {
@@ -547,29 +532,29 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-      // partials of each rhs' own row on this chunk (gathered loads), full a-lane reduction
+      {  // partials of the lanes' own rows on this chunk (gathered loads), rhs g then g + 16
+        auto own_row = [&](const T (&mr)[E], int r) {
+          const int i = sel[g + 16 * r];
+          const bool ov = i >= 0 && w >= c0[i] && w <= c1[i];
+          float px = 0.f, py = 0.f;
+          if (ov) {
+            const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
 #pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const int i = sel[g + 8 * r];
-        const bool ov = i >= 0 && w >= c0[i] && w <= c1[i];
-        float px = 0.f, py = 0.f;
-        if (ov) {
-          const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
-#pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
-            const float4 h = hp[4 * j];
-            const int k = 2 * j;
-            px = fmaf(h.x, m[r][k].x, px); px = fmaf(h.y, m[r][k].y, px);
-            py = fmaf(h.x, m[r][k].y, py); py = fmaf(-h.y, m[r][k].x, py);
-            px = fmaf(h.z, m[r][k + 1].x, px); px = fmaf(h.w, m[r][k + 1].y, px);
-            py = fmaf(h.z, m[r][k + 1].y, py); py = fmaf(-h.w, m[r][k + 1].x, py);
+            for (int j = 0; j < E / 2; ++j) {
+              float4 h = hp[2 * j];
+              const int k = 2 * j;
+              px = fmaf(h.x, mr[k].x, px); px = fmaf(h.y, mr[k].y, px);
+              py = fmaf(h.x, mr[k].y, py); py = fmaf(-h.y, mr[k].x, py);
+              px = fmaf(h.z, mr[k + 1].x, px); px = fmaf(h.w, mr[k + 1].y, px);
+              py = fmaf(h.z, mr[k + 1].y, py); py = fmaf(-h.w, mr[k + 1].x, py);
+            }
           }
-        }
-        px += __shfl_xor_sync(FULL, px, 8);
-        py += __shfl_xor_sync(FULL, py, 8);
-        px += __shfl_xor_sync(FULL, px, 16);
-        py += __shfl_xor_sync(FULL, py, 16);
-        if (ov && a == r) Ps[(size_t)(i * SL + (w - c0[i])) * G + ((g + 8 * r) ^ (i & 15))] = make_float2(px, py);
+          px += __shfl_xor_sync(FULL, px, 16);
+          py += __shfl_xor_sync(FULL, py, 16);
+          if (ov && a == r) Ps[(size_t)(i * SL + (w - c0[i])) * G + ((g + 16 * r) ^ (i & 15))] = make_float2(px, py);
+        };
+        own_row(m0, 0);
+        own_row(m1, 1);
       }
       __syncthreads();
       KZ_PHASE();
@@ -579,13 +564,23 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       }
       __syncthreads();
       KZ_PHASE();
-#pragma unroll
-      for (int r = 0; r < RB; ++r) project(r, sel[g + 8 * r], gam[g + 8 * r]);
+      project(m0, sel[g], gam[g]);
+      project(m1, sel[g + 16], gam[g + 16]);
       __syncthreads();  // sel/gam are rewritten by the next draw
     } else {  // AHK / VR-OAHK (solvers.py:407-421)
+      // refresh partials of the rows in list (ptr, L) -> P
       auto refresh_list = [&](const int* ptr, const int2* L) {
-        for (int q = ptr[w]; q < ptr[w + 1]; ++q) {
-          const int2 e0 = L[q];
+        int q = ptr[w];
+        const int q1 = ptr[w + 1];
+        for (; q + 1 < q1; q += 2) {
+          int2 e0 = L[q], e1 = L[q + 1];
+          T v0 = dot_chunk(e0.x & 0xFFFFF);
+          T v1 = dot_chunk(e1.x & 0xFFFFF);
+          Ps[pslot(e0.y)] = v0;
+          Ps[pslot(e1.y)] = v1;
+        }
+        if (q < q1) {
+          int2 e0 = L[q];
           Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF);
         }
       };
@@ -621,54 +616,59 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         }
       };
       // aggregated projection (solvers.py:257-309): m parked in TMEM while y = sum phi h
-      // (ascending rows) occupies the same registers
-      auto aggregate = [&](const int* ptr, const int2* L, int nrows, int span, bool mark_done, long long ycost) {
+      // (ascending rows) occupies the registers
+      auto aggregate = [&](const int* ptr, const int2* L, int nrows, int span, bool dense, bool mark_done,
+                           long long ycost) {
+        {
+          float f0[16], f1[16];
 #pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          float f[16];
-#pragma unroll
-          for (int k = 0; k < E; ++k) {
-            f[2 * k] = m[r][k].x;
-            f[2 * k + 1] = m[r][k].y;
+          for (int k = 0; k < 8; ++k) {
+            f0[2 * k] = m0[k].x; f0[2 * k + 1] = m0[k].y;
+            f1[2 * k] = m0[k + 8].x; f1[2 * k + 1] = m0[k + 8].y;
           }
-          tmem::st16(my_tmem + 16 * r, f);
+          tmem::st16(my_tmem, f0);
+          tmem::st16(my_tmem + 16, f1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            f0[2 * k] = m1[k].x; f0[2 * k + 1] = m1[k].y;
+            f1[2 * k] = m1[k + 8].x; f1[2 * k + 1] = m1[k + 8].y;
+          }
+          tmem::st16(my_tmem + 32, f0);
+          tmem::st16(my_tmem + 48, f1);
         }
 #pragma unroll
-        for (int r = 0; r < RB; ++r)
-#pragma unroll
-          for (int k = 0; k < E; ++k) m[r][k] = make_float2(0.f, 0.f);  // registers now hold y
+        for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);  // registers now hold y
         for (int q = ptr[w]; q < ptr[w + 1]; ++q) {
           const int2 e = L[q];
           const int i = e.x >> 20;
-          T ph[RB];
-#pragma unroll
-          for (int r = 0; r < RB; ++r) ph[r] = Phi[xs(i, g + 8 * r)];
+          const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
           const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
+          {
 #pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
-            const float4 h = hp[4 * j];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-              m[r][2 * j] = cfma(ph[r], make_float2(h.x, h.y), m[r][2 * j]);
-              m[r][2 * j + 1] = cfma(ph[r], make_float2(h.z, h.w), m[r][2 * j + 1]);
+            for (int j = 0; j < E / 2; ++j) {
+              float4 h = hp[2 * j];
+              const int k = 2 * j;
+              m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
+              m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
+              m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
+              m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
             }
           }
         }
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          s0 = fmaf(m0[k].x, m0[k].x, fmaf(m0[k].y, m0[k].y, s0));
+          s1 = fmaf(m1[k].x, m1[k].x, fmaf(m1[k].y, m1[k].y, s1));
+        }
         {
-          float sx[RB], sy[RB];
-#pragma unroll
-          for (int r = 0; r < RB; ++r) {
-            float s = 0.f;
-#pragma unroll
-            for (int k = 0; k < E; ++k) s = fmaf(m[r][k].x, m[r][k].x, fmaf(m[r][k].y, m[r][k].y, s));
-            sx[r] = s;
-            sy[r] = 0.f;
-          }
-          Dp[w * G + g + 8 * a] = xreduce(sx, sy).x;
+          const float sd = a ? s0 : s1;
+          const float rv = __shfl_xor_sync(FULL, sd, 16);
+          Dp[w * G + g + 16 * a] = (a ? s1 : s0) + rv;
         }
         __syncthreads();
         KZ_PHASE();
-        // step lengths (fixed-order sums => identical in every thread)
+        // step lengths of this thread's two rhs (fixed-order sums => identical in every thread)
         auto gamma_of = [&](int rr, bool& step) -> T {
           step = false;
           if (!nzv[rr]) return make_float2(0.f, 0.f);
@@ -680,18 +680,28 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           T nm = numv[rr];
           return make_float2(nm.x / den, nm.y / den);
         };
+        bool st0, st1;
+        const T gm0 = gamma_of(g, st0), gm1 = gamma_of(g + 16, st1);
         tmem::wait_st();
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          bool st;
-          const T gm = gamma_of(g + 8 * r, st);
-          float f[16];
-          tmem::ld16(my_tmem + 16 * r, f);
+        {
+          float f0[16], f1[16];
+          tmem::ld16(my_tmem, f0);
+          tmem::ld16(my_tmem + 16, f1);
           tmem::wait_ld();
 #pragma unroll
-          for (int k = 0; k < E; ++k) {
-            const T o = make_float2(f[2 * k], f[2 * k + 1]);
-            m[r][k] = st ? cfma(gm, m[r][k], o) : o;
+          for (int k = 0; k < 8; ++k) {
+            T o0 = make_float2(f0[2 * k], f0[2 * k + 1]), o1 = make_float2(f1[2 * k], f1[2 * k + 1]);
+            m0[k] = st0 ? cfma(gm0, m0[k], o0) : o0;
+            m0[k + 8] = st0 ? cfma(gm0, m0[k + 8], o1) : o1;
+          }
+          tmem::ld16(my_tmem + 32, f0);
+          tmem::ld16(my_tmem + 48, f1);
+          tmem::wait_ld();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            T o0 = make_float2(f0[2 * k], f0[2 * k + 1]), o1 = make_float2(f1[2 * k], f1[2 * k + 1]);
+            m1[k] = st1 ? cfma(gm1, m1[k], o0) : o0;
+            m1[k + 8] = st1 ? cfma(gm1, m1[k + 8], o1) : o1;
           }
         }
         // q += gamma phi over the aggregated rows (threads over (row, rhs))
@@ -722,6 +732,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             flv[lane] += f;
           }
         }
+        (void)dense;
       };
 
       if constexpr (SCH == KZ_AHK) {
@@ -732,7 +743,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         weights(0, K);
         __syncthreads();
         KZ_PHASE();
-        aggregate(lptr, lst, K, Nt, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
+        aggregate(lptr, lst, K, Nt, true, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
       } else {
         // exact block projection on the orthogonal group O (solvers.py:312-332)
         refresh_list(optr, olst);
@@ -752,8 +763,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         KZ_PHASE();
         for (int q = optr[w]; q < optr[w + 1]; ++q) {
           const int i = olst[q].x >> 20;
-#pragma unroll
-          for (int r = 0; r < RB; ++r) project(r, i, Phi[xs(i, g + 8 * r)]);
+          project(m0, i, Phi[xs(i, g)]);
+          project(m1, i, Phi[xs(i, g + 16)]);
         }
         if (nN > 0) {
           refresh_list(nptr, nlst);
@@ -762,7 +773,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           weights(2, nN);
           __syncthreads();
           KZ_PHASE();
-          aggregate(nptr, nlst, nN, unionN, false, costN);
+          aggregate(nptr, nlst, nN, unionN, false, false, costN);
         }
         if (tid < G && g0 + tid < K) itv[tid] += 1;
       }
@@ -773,6 +784,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     for (int gg = 0; gg < G; ++gg)
       if (!donev[gg]) all_done = false;
     if (all_done) break;
+    // next iteration's writers of sel/gam run after the refresh barrier: no extra barrier needed
   }
   const int t_end = t > p.T ? p.T : t;
   __syncthreads();
@@ -785,15 +797,15 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   // ------------------------------------------------------------------ outputs
   if (tid == 0) p.tstop[blockIdx.x] = t_end;
   KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
+  auto store_m = [&](const T (&mr)[E], int r) {
+    const int c = g0 + g + 16 * r;
+    if (c >= K || !p.O.iterates) return;
+    T* M = (T*)p.O.iterates + ((size_t)b * K + c) * Nt + w * CH;
 #pragma unroll
-  for (int r = 0; r < RB; ++r) {
-    const int c = g0 + g + 8 * r;
-    if (c < K && p.O.iterates) {
-      T* M = (T*)p.O.iterates + ((size_t)b * K + c) * Nt + w * CH;
-#pragma unroll
-      for (int k = 0; k < E; ++k) M[8 * (k >> 1) + 2 * a + (k & 1)] = m[r][k];
-    }
-  }
+    for (int k = 0; k < E; ++k) M[4 * (k >> 1) + 2 * a + (k & 1)] = mr[k];
+  };
+  store_m(m0, 0);
+  store_m(m1, 1);
   T* vout = (T*)p.O.v;
   for (int e = tid; e < K * G; e += nthr) {
     int i = e / G, gg = e % G;
