@@ -9,7 +9,7 @@ Batched entry points (`solve_batch`, `run_precoding_batched`, `rzf_batched`,
 """
 
 from .assembly import assemble_dense, assemble_vr, epilogue
-from .batch import DeviceBatch, HostBatch
+from .batch import DeviceBatch, HostBatch, pin_host
 from .channel import CONFIGS, ContiguousChannels, NearFieldConfig, generate, solver_seed_sequence
 from .metrics import CADD, CMUL, nmse, spectral_efficiency
 from .rzf import Precoder, apply_auxiliary, auxiliary_matrix, mrc_precoder, rzf_batched, rzf_precoder
@@ -33,6 +33,7 @@ from .solvers import (
     solve_all,
     solve_batch,
 )
+from .shard import gather_stats, shard_range
 from .vrgraph import UserPartition, build_partition
 
 __version__ = "0.1.0"
@@ -42,7 +43,7 @@ __all__ = [
     "FlopCounter", "HostBatch", "HostStreams", "NearFieldConfig", "Precoder", "PrecodingRun", "RunTrace",
     "SCHEMES", "STOCHASTIC_SCHEMES", "SolverState", "StoppingRule", "UserPartition", "VR_SCHEMES",
     "apply_auxiliary", "assemble_dense", "assemble_vr", "auxiliary_matrix", "build_partition",
-    "canonical_scheme", "display_scheme", "epilogue", "generate", "mrc_precoder", "nmse", "rzf_batched",
+    "canonical_scheme", "display_scheme", "epilogue", "generate", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
     "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",
-    "solver_seed_sequence", "spectral_efficiency",
+    "solver_seed_sequence", "spectral_efficiency", "gather_stats", "shard_range",
 ]

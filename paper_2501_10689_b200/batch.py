@@ -188,10 +188,29 @@ class HostBatch:
             "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"))
 
 
+def pin_host(host: HostBatch, dtype: str = "c128", pin: bool = True) -> dict:
+    """Host tensors of a batch (page-locked when `pin`), heff already in the compute dtype."""
+    import torch
+    cdt = torch.complex128 if dtype == "c128" else torch.complex64
+    out = {}
+    for name in DeviceBatch.FIELDS + (("snr_linear",) if host.snr_linear is not None else ()):
+        t = torch.from_numpy(np.ascontiguousarray(getattr(host, name)))
+        if name == "heff":
+            t = t.to(cdt)
+        out[name] = t.pin_memory() if pin else t
+    return out
+
+
 class DeviceBatch:
     """Device-resident copy of a HostBatch plus the KzProblem that points at it."""
 
-    def __init__(self, host: HostBatch, dtype: str = "c128", device=None, pinned: bool = False, stream=None):
+    FIELDS = ("row_seg_ptr", "seg_start", "seg_len", "row_val_ptr", "heff", "row_energy", "reg", "coupled_ptr",
+              "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size")
+
+    def __init__(self, host: HostBatch, dtype: str = "c128", device=None, pinned=None):
+        """Upload `host`.  `pinned` may be the dict returned by `pin_host(host, dtype)`:
+        the copies then come from page-locked memory and are asynchronous on the
+        current stream (the end-to-end path)."""
         import torch
         if dtype not in ("c128", "c64"):
             raise ValueError(f"dtype must be 'c128' or 'c64', got {dtype!r}")
@@ -200,25 +219,8 @@ class DeviceBatch:
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the Kaczmarz path runs on CUDA devices only (no CPU fallback)")
-        cdt = torch.complex128 if dtype == "c128" else torch.complex64
-
-        def up(a, dt=None):
-            t = torch.from_numpy(np.ascontiguousarray(a))
-            if dt is not None:
-                t = t.to(dt)
-            if pinned:
-                t = t.pin_memory()
-            return t.to(self.device, non_blocking=pinned)
-
-        self.t = {
-            "row_seg_ptr": up(host.row_seg_ptr), "seg_start": up(host.seg_start), "seg_len": up(host.seg_len),
-            "row_val_ptr": up(host.row_val_ptr), "heff": up(host.heff, cdt), "row_energy": up(host.row_energy),
-            "reg": up(host.reg), "coupled_ptr": up(host.coupled_ptr), "coupled_idx": up(host.coupled_idx),
-            "orth_ptr": up(host.orth_ptr), "orth_idx": up(host.orth_idx), "non_ptr": up(host.non_ptr),
-            "non_idx": up(host.non_idx), "non_union_size": up(host.non_union_size),
-        }
-        if host.snr_linear is not None:
-            self.t["snr_linear"] = up(host.snr_linear)
+        src = pinned if pinned is not None else pin_host(host, dtype, pin=False)
+        self.t = {k: v.to(self.device, non_blocking=pinned is not None) for k, v in src.items()}
         self.problem = self._make_problem(self.t)
 
     def _make_problem(self, t):
@@ -227,8 +229,7 @@ class DeviceBatch:
         p.n_users = self.host.n_users
         p.n_antennas = self.host.n_antennas
         p.dtype = _lib.KZ_C128 if self.dtype == "c128" else _lib.KZ_C64
-        for name in ("row_seg_ptr", "seg_start", "seg_len", "row_val_ptr", "heff", "row_energy", "reg",
-                     "coupled_ptr", "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"):
+        for name in self.FIELDS:
             ten = t[name]
             setattr(p, name, ten.data_ptr() if ten.numel() else None)
         sup = np.diff(self.host.row_val_ptr)
