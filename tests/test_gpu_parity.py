@@ -428,3 +428,82 @@ def test_register_resident_iterates_are_h_coef():
     hv = kz.epilogue(dev, res.v, want_f=True)
     f = (hv["f"] / hv["beta"][:, None, None]).transpose(1, 2).cpu().numpy()
     assert rel(res.iterates().cpu().numpy(), f) <= 1e-12
+
+
+# --------------------------------------------------------------------------- BASELINE cfg3/4/5 shapes (reduced B)
+
+def test_cfg4_residual_tolerance_solve_all():
+    """cfg4 semantics (Nt=4096, K=256, VR=512): per-rhs residual tolerance 1e-4 (solve_all,
+    solvers.py:510-537) for GRK and VR-OAHK on one realization, complex128, vs the oracle."""
+    kz = _kz()
+    ch = kz.generate("cfg4", [0])
+    chan = oracle_channel_contiguous(ch, 0)
+    reg = float(ch.reg[0])
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    for sc in ("vr-oahk", "grk"):
+        # a fresh SeedSequence per generator: Generator.spawn advances the shared sequence
+        stop = kz.StoppingRule(mode="residual", epsilon=1e-4)
+        v_gpu = kz.solve_all(sc, sys_, stop, rng=np.random.default_rng(kz.solver_seed_sequence(0)))
+        traces = []
+        v_ref = O.solve_all(sc, sys_, O.StoppingRule(mode="residual", epsilon=1e-4),
+                            rng=np.random.default_rng(kz.solver_seed_sequence(0)), traces=traces)
+        assert rel(v_gpu, v_ref) <= REL_C128, sc
+        assert all(t.converged for t in traces)
+
+
+def test_cfg5_wideband_subcarriers_c128():
+    """cfg5 shape: Nt=2048, K=128, frequency-dependent channels on shared VRs, AHK and
+    VR-OAHK at T=10 on two subcarriers, complex128 vs the oracle."""
+    kz = _kz()
+    ch = kz.generate("cfg5", [0, [0, 1023]])
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    for sc in ("ahk", "vr-oahk"):
+        res = kz.solve_batch(dev, sc, mode="lockstep", max_iters=10)
+        for b in range(2):
+            chan = oracle_channel_contiguous(ch, b)
+            sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+            run = O.run_precoding(sc, sys_, O.rzf_precoder(chan, float(ch.reg[b])), epsilon=0.0,
+                                  max_iters=10, traces=False)
+            assert rel(res.v[b].cpu().numpy(), run.v) <= REL_C128, (sc, b)
+
+
+def test_cfg3_c64_vr_oahk_nmse_and_rate():
+    """cfg3 shape (Nt=1024, K=128, VR ~ U[128,512]) in complex64: VR-OAHK T=30 NMSE and
+    sum-rate within the c64 criterion of the complex128 oracle."""
+    kz = _kz()
+    ch = kz.generate("cfg3", [5, 6])
+    dev64 = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    dev128 = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    rz = kz.rzf_batched(dev128)
+    out = kz.run_precoding_batched("vr-oahk", dev64, max_iters=30, v_ref=rz["v"], beta_ref=rz["beta"])
+    for b in range(2):
+        chan = oracle_channel_contiguous(ch, b)
+        reg = float(ch.reg[b])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        run = O.run_precoding("vr-oahk", sys_, ref, epsilon=0.0, max_iters=30, traces=False)
+        n128 = O.nmse(run.precoder.f, ref.f)
+        s128 = O.spectral_efficiency(chan.h, run.precoder.f, float(ch.snr_linear[b]))[1]
+        _c64_ok(float(out["nmse"][b]), n128, float(out["sum_rate"][b]), s128)
+
+
+def test_c_abi_direct_call_as_in_integration_md():
+    """The ctypes binding shown in INTEGRATION.md §3 drives kz_solve directly."""
+    import ctypes as C
+    import torch
+    from paper_2501_10689_b200._lib import KzOut, KzRng, KzStop, SCHEME_IDS, check, lib
+    kz = _kz()
+    ch = kz.generate("cfg2", range(4))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    lb = lib()
+    stop = KzStop(mode=0, max_iters=50, check_every=1, epsilon=0.0)
+    rng = KzRng(kind=3, seed=1)
+    b, k = dev.n_systems, dev.n_users
+    v = torch.zeros((b, k, k), dtype=torch.complex64, device="cuda")
+    out = KzOut(v=v.data_ptr())
+    ws = torch.empty(lb.kz_solve_workspace_bytes(C.byref(dev.problem), C.byref(stop)), dtype=torch.uint8,
+                     device="cuda")
+    check(lb.kz_solve(C.byref(dev.problem), SCHEME_IDS["grk"], C.byref(stop), C.byref(rng), C.byref(out),
+                      ws.data_ptr(), ws.numel(), 0, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    res = kz.solve_batch(dev, "grk", mode="lockstep", max_iters=50, rng=("philox", 1))
+    torch.testing.assert_close(v, res.v, rtol=0, atol=0)  # deterministic: identical bits
