@@ -705,12 +705,15 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           }
         }
         // q += gamma phi over the aggregated rows (threads over (row, rhs))
-        for (int e = tid; e < K * G; e += nthr) {
-          const int i = e / G, rr = e % G;
-          if ((SCH == KZ_VR_OAHK && inset[i] != 2) || g0 + rr >= K) continue;
-          bool st;
-          const T gm = gamma_of(rr, st);
-          if (st) Qs[xs(i, rr)] = cfma(gm, Phi[xs(i, rr)], Qs[xs(i, rr)]);
+        {  // rhs of entry e is e % G == lane (nthr is a multiple of 32): one step length per thread
+          bool stq;
+          const T gq = gamma_of(lane, stq);
+          if (stq && g0 + lane < K)
+            for (int e = tid; e < K * G; e += nthr) {
+              const int i = e / G;
+              if (SCH == KZ_VR_OAHK && inset[i] != 2) continue;
+              Qs[xs(i, lane)] = cfma(gq, Phi[xs(i, lane)], Qs[xs(i, lane)]);
+            }
         }
         // bookkeeping once per rhs (warp 0: lane = rhs slot)
         if (w == 0 && g0 + lane < K && !donev[lane]) {
