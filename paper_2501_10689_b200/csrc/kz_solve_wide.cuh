@@ -446,28 +446,46 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             float carry = 0.f;
             int lastnz = -1;
             bool found = !(tot > 0.f);  // tot == 0: None, no draw is consumed (solvers.py:235-236)
-            for (int base = 0; base < K; base += 16) {
+            // rows in blocks of 64, lane hl owning 4 consecutive rows: one 16-lane scan per block
+            for (int base = 0; base < K; base += 64) {
               if (__all_sync(FULL, found)) break;
-              const int i = base + hl;
-              float v = 0.f;
-              if (act && i < K) {
-                T r = Rs[xs(i, gg)];
-                v = r.x * r.x + r.y * r.y;
+              float wt[4], ls = 0.f;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int i = base + 4 * hl + t;
+                float v = 0.f;
+                if (act && i < K) {
+                  const T r = Rs[xs(i, gg)];
+                  v = r.x * r.x + r.y * r.y;
+                }
+                wt[t] = v;
+                ls += v;
               }
-              float sc = v;
+              float sc = ls;
 #pragma unroll
               for (int o = 1; o < 16; o <<= 1) {
-                float t2 = __shfl_up_sync(FULL, sc, o, 16);
+                const float t2 = __shfl_up_sync(FULL, sc, o, 16);
                 if (hl >= o) sc += t2;
               }
-              const unsigned bal = (__ballot_sync(FULL, !found && i < K && v > 0.f && carry + sc > tau) & hmask) >> (16 * hf);
-              const unsigned nzb = (__ballot_sync(FULL, i < K && v > 0.f) & hmask) >> (16 * hf);
+              float run = carry + sc - ls;  // weight before this lane's first row
+              int lt = -1, lnz = -1;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                run += wt[t];
+                if (lt < 0 && wt[t] > 0.f && run > tau) lt = t;
+                if (wt[t] > 0.f) lnz = t;
+              }
+              const unsigned bal = (__ballot_sync(FULL, !found && lt >= 0) & hmask) >> (16 * hf);
+              const unsigned nzb = (__ballot_sync(FULL, lnz >= 0) & hmask) >> (16 * hf);
+              const int srcl = bal ? __ffs(bal) - 1 : 0, srcn = nzb ? 31 - __clz(nzb) : 0;
+              const int lt_s = __shfl_sync(FULL, lt, 16 * hf + srcl);
+              const int lnz_s = __shfl_sync(FULL, lnz, 16 * hf + srcn);
               if (!found && bal) {
-                isel = base + __ffs(bal) - 1;
+                isel = base + 4 * srcl + lt_s;
                 found = true;
               }
-              if (nzb) lastnz = base + 31 - __clz(nzb);
-              carry += __shfl_sync(FULL, sc, 15, 16);
+              if (nzb) lastnz = base + 4 * srcn + lnz_s;
+              carry += __shfl_sync(FULL, sc, 16 * hf + 15);
             }
             if (tot > 0.f && isel < 0) isel = lastnz;
           }
