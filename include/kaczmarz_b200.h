@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 1
+#define KZ_ABI_VERSION 2
 
 /* status codes */
 #define KZ_OK 0
@@ -93,6 +93,10 @@ typedef struct kz_problem {
   /* shape hints, set by the packer (trusted): enable the register-resident fast path */
   int32_t max_support;          /* max_r |Gamma_r| */
   int32_t flags;                /* KZ_PROBLEM_CONTIGUOUS: every row is exactly one segment */
+  /* max over systems of the (row, 32-antenna chunk) pairs inside one aligned 128- / 256-antenna slice
+     (contiguous supports; 0 = unknown): sizes the shared-memory layout of the cluster path for large arrays */
+  int32_t slice_pairs_128;
+  int32_t slice_pairs_256;
 } kz_problem;
 
 #define KZ_PROBLEM_CONTIGUOUS 1

@@ -178,6 +178,26 @@ class HostBatch:
     def support_sizes(self) -> np.ndarray:
         return np.diff(self.row_val_ptr).reshape(self.n_systems, self.n_users)
 
+    def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024) -> int:
+        """Max over systems and aligned `width`-antenna slices of the (row, `chunk`-antenna chunk)
+        pairs inside the slice (contiguous supports): the shared-memory layout bound of the
+        cluster kernel (kz_problem.slice_pairs_*)."""
+        if not self.contiguous or self.n_systems == 0:
+            return 0
+        per = width // chunk
+        nsl = -(-self.n_antennas // width)
+        seg = self.row_seg_ptr[:-1]
+        c0 = (self.seg_start[seg] // chunk).astype(np.int64).reshape(self.n_systems, self.n_users)
+        c1 = ((self.seg_start[seg] + self.seg_len[seg] - 1) // chunk).astype(np.int64).reshape(self.n_systems,
+                                                                                                 self.n_users)
+        lo = (np.arange(nsl) * per)[None, None, :]
+        best = 0
+        for s in range(0, self.n_systems, block):
+            a, b = c0[s:s + block, :, None], c1[s:s + block, :, None]
+            n = np.clip(np.minimum(b, lo + per - 1) - np.maximum(a, lo) + 1, 0, None).sum(axis=1)
+            best = max(best, int(n.max()))
+        return best
+
     def to_device(self, dtype: str = "c128", device=None) -> "DeviceBatch":
         return DeviceBatch(self, dtype, device)
 
@@ -235,6 +255,9 @@ class DeviceBatch:
         sup = np.diff(self.host.row_val_ptr)
         p.max_support = int(sup.max()) if sup.size else 0
         p.flags = 1 if self.host.contiguous else 0
+        if self.host.contiguous:
+            p.slice_pairs_128 = self.host.slice_pairs(128)
+            p.slice_pairs_256 = self.host.slice_pairs(256)
         return p
 
     @property

@@ -11,6 +11,7 @@
 #include "kz_dense.cuh"
 #include "kz_solve_generic.cuh"
 #include "kz_solve_lockstep.cuh"
+#include "kz_solve_cluster.cuh"
 
 namespace {
 
@@ -113,6 +114,11 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
                                  &g_launches);
   if (fast == 1) return cuda_check("kz_solve(lockstep)");
   if (fast < 0) return fail(KZ_ERR_CUDA, "lockstep launch failed");
+  // large arrays / residual tolerance: one thread-block cluster per (system, 16 rhs) (kz_solve_cluster.cuh)
+  fast = cluster_try_launch(*prob, scheme, *stop, *rng, *out, resume, (char*)workspace, workspace_bytes, s,
+                            &g_launches);
+  if (fast == 1) return cuda_check("kz_solve(cluster)");
+  if (fast < 0) return fail(KZ_ERR_CUDA, "cluster launch failed");
 
   const int nw = GEN_WARPS;
   size_t cs = prob->dtype == KZ_C128 ? 16 : 8;

@@ -1,0 +1,1191 @@
+// Cluster kernel for large arrays (complex64): gk, grk, vr-ogrk, ahk, vr-oahk over contiguous VRs, fixed T
+// (LOCKSTEP, epsilon = 0) or a per-rhs residual tolerance (RESIDUAL, solve / solve_all semantics).
+//
+// One thread-block cluster = one system x 16 right-hand sides.  CTA c of the cluster owns the antenna slice
+// [32 W c, 32 W (c + 1)) (warp w: the 32-antenna chunk W c + w) and keeps in shared memory only the pieces
+// of the rows that touch its slice, zero padded to whole chunks; the iterate of its 16 rhs on the slice stays
+// in registers: lane (a, g), a = lane >> 3, g = lane & 7, holds rhs g and g + 8 on the antennas
+// 8j + 2a + e (j < 4, e < 2) of its warp's chunk, so each h element loaded feeds two rhs (the SMEM/FFMA
+// balance of the wide kernel, csrc/kz_solve_wide.cuh) while the per-CTA footprint is half the wide layout's.
+// Rows are owned in contiguous blocks of KO = ceil(K / CL): the owner keeps q_i and r_i.
+//
+// Per iteration (grk; the other schemes follow the same pattern):
+//   refresh  every CTA: per-(row, chunk) partials -> P; fixed-order sum over the slice's chunks, pushed into
+//            the owner's inbox IN[row][slice][rhs] with a DSMEM store                     -- cluster barrier
+//   finalise owner: r_i = e - sum_slices IN - xi q_i (fixed order), block sums of |r_i|^2 pushed to every CTA
+//                                                                                            -- cluster barrier
+//   select   every CTA: the same prefix over the block sums -> the block holding the draw; its owner picks the
+//            row, updates q_i, pushes (row, gamma) to every CTA                              -- cluster barrier
+//   project  every CTA: m += gamma h on its slice.
+// Residual mode fuses the convergence test into the next refresh: ||r_true||^2 of the state after step t is
+// the sum of the block sums of step t + 1 (grk / gk / ahk), so the stopping rule costs no extra pass; vr-oahk
+// refreshes all rows (instead of its orthogonal group) at the start of each iteration for the same purpose.
+// Semantics: InstanceRun.step (solvers.py:382-421), solve / StoppingRule (solvers.py:426-507).
+#pragma once
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "kz_common.cuh"
+#include "kz_solve_generic.cuh"
+
+namespace kz {
+
+namespace clu {
+
+constexpr int G = 16;   // rhs per cluster
+constexpr int CH = 32;  // antennas per warp
+
+// [owned row][rhs] arrays are XOR-swizzled so lanes-over-rows and lanes-over-rhs are both conflict free
+__device__ __forceinline__ int xo(int il, int gg) { return il * G + (gg ^ (il & 15)); }
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctas() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t remote(const void* p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_remote(float2* p, int rank, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(remote(p, rank)), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_remote(float* p, int rank, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote(p, rank)), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote(int* p, int rank, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(remote(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote(float4* p, int rank, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote(p, rank)), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ int ld_remote(const int* p, int rank) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(remote(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(remote(p, rank)) : "memory");
+  return v;
+}
+
+struct Plan {
+  int K, W, CL, KO, NS, pcap, nlcap;
+  size_t rowS, rowL, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, P, Qo,
+      Ro, Fo, IN, Phl, dloc, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
+      misc, total;
+};
+
+__host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap) {
+  Plan p;
+  p.K = K;
+  p.W = W;
+  p.CL = CL;
+  p.KO = (K + CL - 1) / CL;
+  p.NS = NS;
+  p.pcap = pcap;
+  p.nlcap = K < pcap ? K : pcap;
+  const int KW = (K + 31) / 32;
+  const bool ogrk = scheme == KZ_VR_OGRK, oahk = scheme == KZ_VR_OAHK;
+  size_t o = 0;
+  p.rowS = o; o = al(o + 4 * K);
+  p.rowL = o; o = al(o + 4 * K);
+  p.c0 = o; o = al(o + 4 * K);
+  p.c1 = o; o = al(o + 4 * K);
+  p.en = o; o = al(o + 4 * K);
+  p.inset = o; o = al(o + K);
+  p.loc = o; o = al(o + 4 * K);
+  p.cost = o; o = al(o + (ogrk ? 8 * K : 0));
+  p.cmask = o; o = al(o + (ogrk ? 4 * (size_t)p.KO * KW : 0));
+  p.lrow = o; o = al(o + 4 * p.nlcap);
+  p.lh = o; o = al(o + 4 * p.nlcap);
+  p.lcc = o; o = al(o + 4 * p.nlcap);
+  p.lptr = o; o = al(o + 4 * (W + 1));
+  p.lst = o; o = al(o + 4 * (size_t)pcap);
+  p.optr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
+  p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
+  p.olst = o; o = al(o + (oahk ? 4 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
+  p.nlst = p.olst;
+  p.H = o; o = al(o + 8 * (size_t)pcap * CH);
+  p.P = o; o = al(o + 8 * (size_t)pcap * G);
+  p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
+  p.Ro = o; o = al(o + 8 * (size_t)p.KO * G);
+  p.Fo = o; o = al(o + 8 * (size_t)p.KO * G);
+  p.IN = o; o = al(o + 8 * (size_t)p.KO * NS * G);
+  p.Phl = p.P;  // phi / gamma of local rows reuse P (disjoint phases; nlcap <= pcap)
+  p.dloc = o; o = al(o + 4 * (size_t)p.KO * NS);
+  p.AG4 = o; o = al(o + 16 * (size_t)CL * G);
+  p.GAMv = o; o = al(o + 8 * G);
+  p.stepv = o; o = al(o + 4 * G);
+  p.BS = o; o = al(o + 4 * (size_t)CL * G);
+  p.BI = o; o = al(o + 4 * (size_t)CL * G);
+  p.SPP = o; o = al(o + 4 * (size_t)CL * G);
+  p.NZP = o; o = al(o + 4 * (size_t)CL * G);
+  p.DY = o; o = al(o + 4 * (size_t)CL * G);
+  p.Dp = o; o = al(o + 4 * (size_t)W * G);
+  p.SEL = o; o = al(o + 4 * G);
+  p.GAM = o; o = al(o + 8 * G);
+  p.done = o; o = al(o + 4 * G);
+  p.sdone = o; o = al(o + 4 * G);
+  p.live = o; o = al(o + 4 * G);
+  p.iters = o; o = al(o + 4 * G);
+  p.prev = o; o = al(o + 4 * G);
+  p.noop = o; o = al(o + 4 * G);
+  p.conv = o; o = al(o + 4 * G);
+  p.nchk = o; o = al(o + 4 * G);
+  p.flops = o; o = al(o + 8 * G);
+  p.misc = o; o = al(o + 64);
+  p.total = o;
+  return p;
+}
+
+}  // namespace clu
+
+struct CluArgs {
+  kz_problem P;
+  kz_rng R;
+  kz_out O;
+  int mode;     // KZ_STOP_LOCKSTEP (fixed T) or KZ_STOP_RESIDUAL
+  int cap;      // T (lockstep) or the per-rhs iteration cap
+  int every;    // check_every
+  float eps;    // residual tolerance
+  int NS;       // max slices a row spans
+  int pcap;     // (row, chunk) pairs reserved per CTA
+  int32_t* tstop;
+};
+
+template <int SCH>
+__global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
+  using namespace clu;
+  using T = float2;
+  constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
+  constexpr bool GREEDY = SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK;
+
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int K = p.P.n_users, Nt = p.P.n_antennas;
+  const int CL = (int)cluster_ctas(), c = (int)cta_rank();
+  const int ngroups = (K + G - 1) / G;
+  const int cid = blockIdx.x / CL;
+  const int b = cid / ngroups, grp = cid % ngroups, g0 = grp * G;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
+  const int W = nthr >> 5;
+  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap);
+  const int KO = pl.KO, NS = pl.NS, KW = (K + 31) / 32;
+  const int cW = c * W;
+  const int o_lo = c * KO, nown = max(0, min(K, o_lo + KO) - o_lo);
+  const bool residual = p.mode == KZ_STOP_RESIDUAL;
+
+  int* rowS = (int*)(sm + pl.rowS);
+  int* rowL = (int*)(sm + pl.rowL);
+  int* c0 = (int*)(sm + pl.c0);
+  int* c1 = (int*)(sm + pl.c1);
+  float* en = (float*)(sm + pl.en);
+  uint8_t* inset = (uint8_t*)(sm + pl.inset);
+  int* loc = (int*)(sm + pl.loc);
+  long long* cost = (long long*)(sm + pl.cost);
+  uint32_t* cmask = (uint32_t*)(sm + pl.cmask);
+  int* lrow = (int*)(sm + pl.lrow);
+  int* lh = (int*)(sm + pl.lh);    // H element offset of local row n's first chunk
+  int* lcc = (int*)(sm + pl.lcc);  // local chunk range of row n: lc0 | lc1 << 8
+  int* lptr = (int*)(sm + pl.lptr);
+  int* lst = (int*)(sm + pl.lst);  // H element offset of the (row, chunk) piece | local row << 20
+  int* optr = (int*)(sm + pl.optr);
+  int* olst = (int*)(sm + pl.olst);
+  int* nptr = (int*)(sm + pl.nptr);
+  int* nlst = (int*)(sm + pl.nlst);
+  T* Hs = (T*)(sm + pl.H);
+  T* Ps = (T*)(sm + pl.P);
+  T* Qo = (T*)(sm + pl.Qo);
+  T* Ro = (T*)(sm + pl.Ro);
+  T* Fo = (T*)(sm + pl.Fo);  // owned phi (aggregation weights) or gamma (orthogonal block)
+  T* INs = (T*)(sm + pl.IN);
+  T* Phl = (T*)(sm + pl.Phl);  // phi / gamma of the local rows, pulled from their owners
+  int* dloc = (int*)(sm + pl.dloc);  // [owned row][slice slot] -> local row index in that CTA
+  float4* AG4 = (float4*)(sm + pl.AG4);
+  T* GAMv = (T*)(sm + pl.GAMv);
+  int* stepv = (int*)(sm + pl.stepv);
+  float* BS = (float*)(sm + pl.BS);
+  int* BI = (int*)(sm + pl.BI);
+  float* SPP = (float*)(sm + pl.SPP);
+  int* NZP = (int*)(sm + pl.NZP);
+  float* DY = (float*)(sm + pl.DY);
+  float* Dp = (float*)(sm + pl.Dp);
+  int* SEL = (int*)(sm + pl.SEL);
+  T* GAM = (T*)(sm + pl.GAM);
+  int* donev = (int*)(sm + pl.done);
+  int* sdone = (int*)(sm + pl.sdone);  // scheme termination (InstanceRun.done)
+  int* livev = (int*)(sm + pl.live);
+  int* itv = (int*)(sm + pl.iters);
+  int* prevv = (int*)(sm + pl.prev);
+  int* noopv = (int*)(sm + pl.noop);
+  int* convv = (int*)(sm + pl.conv);
+  int* nchk = (int*)(sm + pl.nchk);
+  long long* flv = (long long*)(sm + pl.flops);
+  int* misc = (int*)(sm + pl.misc);
+
+  const float regf = (float)p.P.reg[b];
+  const T* heff = (const T*)p.P.heff;
+  KZ_TSTART
+
+  // ------------------------------------------------------------------ setup
+  for (int i = tid; i < K; i += nthr) {
+    size_t r = (size_t)b * K + i;
+    int sg = p.P.row_seg_ptr[r];
+    int s = p.P.seg_start[sg], L = p.P.seg_len[sg];
+    rowS[i] = s;
+    rowL[i] = L;
+    c0[i] = s / CH;
+    c1[i] = (s + L - 1) / CH;
+    en[i] = (float)p.P.row_energy[r];
+    inset[i] = 0;
+  }
+  __syncthreads();
+  if (AGG && p.P.orth_ptr) {
+    for (int q = p.P.orth_ptr[b] + tid; q < p.P.orth_ptr[b + 1]; q += nthr) inset[p.P.orth_idx[q]] = 1;
+    for (int q = p.P.non_ptr[b] + tid; q < p.P.non_ptr[b + 1]; q += nthr) inset[p.P.non_idx[q]] = 2;
+  }
+  // rows touching this slice, ascending (warp 0 compacts with ballots)
+  if (w == 0) {
+    int n = 0, hcar = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int i = base + lane;
+      const bool ov = i < K && c0[i] <= cW + W - 1 && c1[i] >= cW;
+      const unsigned bal = __ballot_sync(FULL, ov);
+      int l0 = 0, l1 = 0, np = 0;
+      if (ov) {
+        l0 = max(c0[i], cW) - cW;
+        l1 = min(c1[i], cW + W - 1) - cW;
+        np = l1 - l0 + 1;
+      }
+      int sc = np;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += t2;
+      }
+      const int idx = n + __popc(bal & ((1u << lane) - 1));
+      if (i < K) loc[i] = ov ? idx : -1;
+      if (ov && idx < pl.nlcap) {
+        lrow[idx] = i;
+        lh[idx] = (hcar + sc - np) * CH;
+        lcc[idx] = l0 | (l1 << 8);
+      }
+      n += __popc(bal);
+      hcar += __shfl_sync(FULL, sc, 31);
+    }
+    if (lane == 0) {
+      misc[1] = n;
+      misc[2] = hcar;
+    }
+  }
+  __syncthreads();
+  const int NL = misc[1], npairs = misc[2];
+  if (npairs > p.pcap || NL > pl.nlcap) __trap();  // layout hint violated: fail loudly
+  // row pieces -> shared memory, zero padded to whole chunks
+  for (int e = tid; e < npairs * CH; e += nthr) {
+    int lo = 0, hi = NL - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (lh[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int i = lrow[lo];
+    const int ant = (cW + (lcc[lo] & 0xFF)) * CH + (e - lh[lo]);
+    const int s = rowS[i];
+    Hs[e] = (ant >= s && ant < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (ant - s)]
+                                             : make_float2(0.f, 0.f);
+  }
+  // per-chunk piece lists (ascending rows)
+  auto build_list = [&](int* ptr, int* out, int which, int base0) {
+    int cnt = 0;
+    for (int base = 0; base < NL; base += 32) {
+      const int n = base + lane;
+      bool ov = false;
+      if (n < NL) {
+        const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
+        ov = l0 <= w && w <= l1 && (which == 0 || inset[lrow[n]] == which);
+      }
+      cnt += __popc(__ballot_sync(FULL, ov));
+    }
+    if (lane == 0) ptr[w + 1] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      ptr[0] = base0;
+      for (int ww = 0; ww < W; ++ww) ptr[ww + 1] += ptr[ww];
+    }
+    __syncthreads();
+    int q = ptr[w];
+    for (int base = 0; base < NL; base += 32) {
+      const int n = base + lane;
+      bool ov = false;
+      int l0 = 0;
+      if (n < NL) {
+        l0 = lcc[n] & 0xFF;
+        const int l1 = lcc[n] >> 8;
+        ov = l0 <= w && w <= l1 && (which == 0 || inset[lrow[n]] == which);
+      }
+      const unsigned bal = __ballot_sync(FULL, ov);
+      if (ov) out[q + __popc(bal & ((1u << lane) - 1))] = (lh[n] + (w - l0) * CH) | (n << 20);
+      q += __popc(bal);
+    }
+  };
+  __syncthreads();
+  if (SCH != KZ_VR_OAHK || residual) build_list(lptr, lst, 0, 0);
+  if (SCH == KZ_VR_OAHK) {
+    build_list(optr, olst, 1, 0);
+    __syncthreads();
+    build_list(nptr, nlst, 2, optr[W]);
+  }
+  if constexpr (SCH == KZ_VR_OGRK) {
+    // owner: bitmask of X_i for its rows (coupling is symmetric: i in X_j <=> j in X_i, vrgraph.py:60-82);
+    // every CTA: the refresh cost of each X_j (flop charge)
+    for (int i = tid; i < K; i += nthr) {
+      const size_t r = (size_t)b * K + i;
+      const int il = i - o_lo;
+      const bool own = il >= 0 && il < nown;
+      if (own)
+        for (int q = 0; q < KW; ++q) cmask[il * KW + q] = 0;
+      long long cst = 0;
+      for (int q = p.P.coupled_ptr[r]; q < p.P.coupled_ptr[r + 1]; ++q) {
+        const int j = p.P.coupled_idx[q];
+        if (own) cmask[il * KW + (j >> 5)] |= 1u << (j & 31);
+        cst += 8LL * rowL[j] + 4;
+      }
+      cost[i] = cst;
+    }
+  }
+  for (int e = tid; e < KO * G; e += nthr) {
+    const int il = e / G, gg = e % G;
+    Qo[xo(il, gg)] = make_float2(0.f, 0.f);
+    Ro[xo(il, gg)] = make_float2(o_lo + il == g0 + gg ? 1.f : 0.f, 0.f);
+    Fo[xo(il, gg)] = make_float2(0.f, 0.f);
+  }
+  for (int gg = tid; gg < G; gg += nthr) {
+    donev[gg] = g0 + gg < K ? 0 : 1;
+    sdone[gg] = 0;
+    livev[gg] = 0;
+    itv[gg] = 0;
+    prevv[gg] = -1;
+    noopv[gg] = 0;
+    convv[gg] = 0;
+    nchk[gg] = 0;
+    flv[gg] = 0;
+    SEL[gg] = -1;
+  }
+  long long costO = 0, costN = 0;
+  int nN = 0;
+  for (int i = 0; i < K; ++i) {
+    if (inset[i] == 1) costO += 8LL * rowL[i] + 4;
+    if (inset[i] == 2) { costN += 8LL * rowL[i]; ++nN; }
+  }
+  const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
+  cluster_sync();  // every CTA of the cluster is resident and initialised before any DSMEM traffic
+  if (AGG)
+    for (int e = tid; e < nown * NS; e += nthr) {
+      const int il = e / NS, s = e % NS, i = o_lo + il, s0 = c0[i] / W;
+      if (s <= c1[i] / W - s0) dloc[e] = s0 + s == c ? loc[i] : ld_remote(loc + i, s0 + s);
+    }
+  __syncthreads();
+  KZ_PHASE();
+
+  const int a = lane >> 3, g = lane & 7;
+  const int hf = lane >> 4, hl = lane & 15;  // half-warp serving one rhs in the owner / selection phases
+  const unsigned hmask = 0xFFFFu << (16 * hf);
+  T m0[8], m1[8];  // rhs g and g + 8
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
+  const float4* H4 = reinterpret_cast<const float4*>(Hs);
+
+  // conj(h) . m over this warp's chunk for both rhs, reduced over the four a-lanes; lane < 16 ends with rhs lane
+  auto dot16 = [&](int h0) -> T {
+    const float4* hp = H4 + (h0 >> 1) + a;
+    float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 h = hp[4 * j];
+      const int k = 2 * j;
+      x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
+      y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
+      x1 = fmaf(h.z, m0[k + 1].x, x1); x1 = fmaf(h.w, m0[k + 1].y, x1);
+      y1 = fmaf(h.z, m0[k + 1].y, y1); y1 = fmaf(-h.w, m0[k + 1].x, y1);
+      u0 = fmaf(h.x, m1[k].x, u0); u0 = fmaf(h.y, m1[k].y, u0);
+      v0 = fmaf(h.x, m1[k].y, v0); v0 = fmaf(-h.y, m1[k].x, v0);
+      u1 = fmaf(h.z, m1[k + 1].x, u1); u1 = fmaf(h.w, m1[k + 1].y, u1);
+      v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
+    }
+    const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
+    const bool odd = a & 1;  // odd a-lanes keep rhs g + 8
+    const float sx = odd ? px : qx, sy = odd ? py : qy;
+    const float rx = __shfl_xor_sync(FULL, sx, 8), ry = __shfl_xor_sync(FULL, sy, 8);
+    float kx = (odd ? qx : px) + rx, ky = (odd ? qy : py) + ry;
+    kx += __shfl_xor_sync(FULL, kx, 16);
+    ky += __shfl_xor_sync(FULL, ky, 16);
+    return make_float2(kx, ky);
+  };
+  auto refresh = [&](const int* ptr, const int* L) {
+    int q = ptr[w];
+    const int q1 = ptr[w + 1];
+    for (; q + 3 < q1; q += 4) {  // four pieces in flight
+      const int h0 = L[q] & 0xFFFFF, h1 = L[q + 1] & 0xFFFFF, h2 = L[q + 2] & 0xFFFFF, h3 = L[q + 3] & 0xFFFFF;
+      const T v0 = dot16(h0);
+      const T v1 = dot16(h1);
+      const T v2 = dot16(h2);
+      const T v3 = dot16(h3);
+      if (lane < 16) {
+        Ps[(h0 >> 5) * G + lane] = v0;
+        Ps[(h1 >> 5) * G + lane] = v1;
+        Ps[(h2 >> 5) * G + lane] = v2;
+        Ps[(h3 >> 5) * G + lane] = v3;
+      }
+    }
+    for (; q + 1 < q1; q += 2) {
+      const int h0 = L[q] & 0xFFFFF, h1 = L[q + 1] & 0xFFFFF;
+      const T v0 = dot16(h0);
+      const T v1 = dot16(h1);
+      if (lane < 16) {
+        Ps[(h0 >> 5) * G + lane] = v0;
+        Ps[(h1 >> 5) * G + lane] = v1;
+      }
+    }
+    if (q < q1) {
+      const int h0 = L[q] & 0xFFFFF;
+      const T v0 = dot16(h0);
+      if (lane < 16) Ps[(h0 >> 5) * G + lane] = v0;
+    }
+  };
+  // slice sums (fixed chunk order) -> owner inbox IN[row][slice slot][rhs]
+  auto push = [&](int which) {
+    for (int e = tid; e < NL * G; e += nthr) {
+      const int n = e >> 4, gg = e & 15;
+      const int i = lrow[n];
+      if (which && inset[i] != which) continue;
+      const int ns = (lcc[n] >> 8) - (lcc[n] & 0xFF);
+      const T* pp = Ps + (size_t)(lh[n] >> 5) * G + gg;
+      float dx = 0.f, dy = 0.f;
+      for (int s = 0; s <= ns; ++s) {
+        const T v = pp[s * G];
+        dx += v.x;
+        dy += v.y;
+      }
+      const int o = i / KO, il = i - o * KO;
+      T* dst = INs + (size_t)(il * NS + (c - c0[i] / W)) * G + (gg ^ (il & 15));
+      if (o == c) *dst = make_float2(dx, dy);
+      else st_remote(dst, o, make_float2(dx, dy));
+    }
+  };
+  // owner: residual of owned row il for rhs gg from the slice sums (fixed slice order)
+  auto oresid = [&](int il, int gg, bool dense) -> T {
+    const int i = o_lo + il;
+    const int ns = c1[i] / W - c0[i] / W;
+    const T* pp = INs + (size_t)il * NS * G + (gg ^ (il & 15));
+    float dx = 0.f, dy = 0.f;
+    for (int s = 0; s <= ns; ++s) {
+      const T v = pp[s * G];
+      dx += v.x;
+      dy += v.y;
+    }
+    const T q = Qo[xo(il, gg)];
+    if (dense) {  // solvers.py:149-153
+      T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
+      if (i == g0 + gg) r.x += 1.f;
+      return r;
+    }
+    const float tg = i == g0 + gg ? 1.f : 0.f;  // solvers.py:166
+    return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
+  };
+  auto push_phi = [&](int il, int gg, T v) {
+    const int i = o_lo + il, s0 = c0[i] / W, ns = c1[i] / W - s0;
+    for (int s = 0; s <= ns; ++s) {
+      const int d = s0 + s;
+      T* dst = Phl + dloc[il * NS + s] * G + gg;
+      if (d == c) *dst = v; else st_remote(dst, d, v);
+    }
+  };
+  // owner: phi = r / e on its rows of set `which` (0 = all), pushed to the slices; block partials of
+  // vdot(phi, r), ||phi||^2, ||r||^2 and any(phi != 0) pushed to every CTA (solvers.py:240-254, 274)
+  auto owner_weights = [&](int which, bool gate_live) {
+    for (int pair = w; pair < G / 2; pair += W) {
+      const int gg = pair + hf * (G / 2);
+      float nx = 0.f, ny = 0.f, sp = 0.f, n2 = 0.f;
+      bool nz = false;
+      if (gate_live ? livev[gg] != 0 : !donev[gg])
+        for (int il = hl; il < nown; il += 16) {
+          const int i = o_lo + il;
+          if (which && inset[i] != which) continue;
+          const T r = oresid(il, gg, which == 0);
+          const T ph = make_float2(r.x / en[i], r.y / en[i]);
+          Fo[xo(il, gg)] = ph;
+          push_phi(il, gg, ph);
+          nz |= (ph.x != 0.f || ph.y != 0.f);
+          nx = fmaf(ph.x, r.x, nx); nx = fmaf(ph.y, r.y, nx);
+          ny = fmaf(ph.x, r.y, ny); ny = fmaf(-ph.y, r.x, ny);
+          sp = fmaf(ph.x, ph.x, sp); sp = fmaf(ph.y, ph.y, sp);
+          n2 = fmaf(r.x, r.x, fmaf(r.y, r.y, n2));
+        }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        nx += __shfl_xor_sync(FULL, nx, o);
+        ny += __shfl_xor_sync(FULL, ny, o);
+        sp += __shfl_xor_sync(FULL, sp, o);
+        n2 += __shfl_xor_sync(FULL, n2, o);
+      }
+      const int anz = (__ballot_sync(FULL, nz) & hmask) ? 1 : 0;
+      if (hl < CL) {
+        const int d = hl, k = c * G + gg;
+        const float4 v = make_float4(nx, ny, sp, n2);
+        if (d == c) {
+          AG4[k] = v;
+          NZP[k] = anz;
+        } else {
+          st_remote(AG4 + k, d, v);
+          st_remote(NZP + k, d, anz);
+        }
+      }
+    }
+  };
+  auto project = [&](T (&mr)[8], int n, T gm) {  // m += gm h on this warp's chunk of local row n
+    const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
+    if (w < l0 || w > l1) return;
+    const float4* hp = H4 + ((lh[n] + (w - l0) * CH) >> 1) + a;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 h = hp[4 * j];
+      const int k = 2 * j;
+      mr[k].x = fmaf(gm.x, h.x, mr[k].x); mr[k].x = fmaf(-gm.y, h.y, mr[k].x);
+      mr[k].y = fmaf(gm.x, h.y, mr[k].y); mr[k].y = fmaf(gm.y, h.x, mr[k].y);
+      mr[k + 1].x = fmaf(gm.x, h.z, mr[k + 1].x); mr[k + 1].x = fmaf(-gm.y, h.w, mr[k + 1].x);
+      mr[k + 1].y = fmaf(gm.x, h.w, mr[k + 1].y); mr[k + 1].y = fmaf(gm.y, h.z, mr[k + 1].y);
+    }
+  };
+  auto draw_u = [&](int gg) -> double {
+    const int cc = g0 + gg, d = itv[gg];
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)cc, (uint64_t)d);
+    return p.R.uniforms[((size_t)b * K + cc) * p.R.stream_len + d];
+  };
+  // residual-mode stopping test of the state after step itv (solvers.py:480-503); returns true if the rhs stops
+  auto stop_test = [&](int gg, float nrm2) -> bool {
+    if (!residual) return false;
+    const int it = itv[gg];
+    if (it >= 1 && it % p.every == 0) {
+      nchk[gg] += 1;
+      if (sqrtf(nrm2) <= p.eps) {
+        convv[gg] = 1;
+        donev[gg] = 1;
+        return true;
+      }
+    }
+    if (it >= p.cap) {
+      donev[gg] = 1;
+      return true;
+    }
+    return false;
+  };
+
+  const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
+  const long long dense_rk = 2 + 8LL * Nt + 2;
+  // charge of one greedy selection pass (refresh + selection), before the step itself
+  auto sel_cost = [&](int gg) -> long long {
+    if (SCH == KZ_GK) return dense_refresh + 4LL * K;
+    if (SCH == KZ_GRK) return dense_refresh + 4LL * K + 2;
+    return (prevv[gg] >= 0 ? cost[prevv[gg]] : 0) + 4LL * K + 2;
+  };
+  int t;
+  for (t = 1;; ++t) {
+    KZ_ITER();
+    if constexpr (GREEDY) {
+      refresh(lptr, lst);
+      __syncthreads();
+      KZ_PHASE();
+      push(0);
+      cluster_sync();
+      KZ_PHASE();
+      // owner: residuals of its rows, block sums (grk / vr-ogrk) or block argmax (gk); half-warp per rhs
+      for (int pair = w; pair < G / 2; pair += W) {
+        const int gg = pair + hf * (G / 2);
+        const bool act = !donev[gg];
+        float ws = 0.f, fresh = 0.f, best = -1.f;
+        int bi = 0x7fffffff;
+        if (act)
+          for (int il = hl; il < nown; il += 16) {
+            const int i = o_lo + il;
+            bool upd = true;
+            if constexpr (SCH == KZ_VR_OGRK) {
+              const int pr = prevv[gg];
+              upd = pr >= 0 && ((cmask[il * KW + (pr >> 5)] >> (pr & 31)) & 1u);
+            }
+            T r;
+            if (upd || residual) {
+              const T rf = oresid(il, gg, SCH != KZ_VR_OGRK);
+              fresh += rf.x * rf.x + rf.y * rf.y;
+              r = upd ? rf : Ro[xo(il, gg)];
+            } else {
+              r = Ro[xo(il, gg)];
+            }
+            if (upd) Ro[xo(il, gg)] = r;
+            const float w2 = r.x * r.x + r.y * r.y;
+            ws += w2;
+            if constexpr (SCH == KZ_GK) {
+              const float sc = w2 / en[i];
+              if (sc > best) { best = sc; bi = i; }
+            }
+          }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          ws += __shfl_xor_sync(FULL, ws, o);
+          fresh += __shfl_xor_sync(FULL, fresh, o);
+          if constexpr (SCH == KZ_GK) {
+            const float ob = __shfl_xor_sync(FULL, best, o);
+            const int oi = __shfl_xor_sync(FULL, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          }
+        }
+        if (hl < CL) {
+          const int d = hl;
+          if (SCH == KZ_GK) {
+            float* bs = BS + c * G + gg;
+            int* bx = BI + c * G + gg;
+            if (d == c) { *bs = best; *bx = bi; } else { st_remote(bs, d, best); st_remote(bx, d, bi); }
+          } else {
+            float* bs = BS + c * G + gg;
+            if (d == c) *bs = ws; else st_remote(bs, d, ws);
+          }
+          float* fs = SPP + c * G + gg;  // fresh ||r||^2 partial (the stopping test)
+          if (d == c) *fs = SCH == KZ_VR_OGRK ? fresh : ws; else st_remote(fs, d, SCH == KZ_VR_OGRK ? fresh : ws);
+        }
+      }
+      cluster_sync();
+      KZ_PHASE();
+      // selection: the same block-level decision in every CTA, the owner of the chosen row does the step.
+      // Control flow stays warp-uniform (the two half-warps serve different rhs): predicates, no early exits.
+      for (int pair = w; pair < G / 2; pair += W) {
+        const int gg = pair + hf * (G / 2);
+        bool act = !donev[gg];
+        float nrm2 = 0.f;
+        for (int d = 0; d < CL; ++d) nrm2 += SPP[d * G + gg];
+        bool stopped = false;
+        if (act && hl == 0) stopped = stop_test(gg, nrm2);
+        stopped = __shfl_sync(FULL, stopped, 16 * hf);
+        act = act && !stopped;
+        const long long f = sel_cost(gg);
+        int cstar = -1, isel = -1;
+        if constexpr (SCH == KZ_GK) {
+          float bb = act && hl < CL ? BS[hl * G + gg] : -1.f;
+          int bx = act && hl < CL ? BI[hl * G + gg] : 0x7fffffff;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(FULL, bb, o);
+            const int oi = __shfl_xor_sync(FULL, bx, o);
+            if (ob > bb || (ob == bb && oi < bx)) { bb = ob; bx = oi; }
+          }
+          if (act && bb > 0.f) {  // greedy-max: None if every score is zero (solvers.py:210-215)
+            isel = bx;
+            cstar = bx / KO;
+          }
+        } else {
+          const float v = act && hl < CL ? BS[hl * G + gg] : 0.f;
+          float incl = v;
+#pragma unroll
+          for (int o = 1; o < 16; o <<= 1) {
+            const float t2 = __shfl_up_sync(FULL, incl, o, 16);
+            if (hl >= o) incl += t2;
+          }
+          const float tot = __shfl_sync(FULL, incl, 16 * hf + 15);
+          const bool draw = act && tot > 0.f;  // tot == 0: None, no draw consumed (solvers.py:235-236)
+          const float tau = draw ? (float)draw_u(gg) * tot : 0.f;
+          const unsigned hit = (__ballot_sync(FULL, draw && v > 0.f && incl > tau) & hmask) >> (16 * hf);
+          const unsigned nzb = (__ballot_sync(FULL, draw && v > 0.f) & hmask) >> (16 * hf);
+          if (draw) cstar = hit ? __ffs(hit) - 1 : 31 - __clz(nzb);
+          const float excl = __shfl_sync(FULL, incl - v, 16 * hf + (cstar < 0 ? 0 : cstar));
+          // the chosen block's owner scans its rows, 16 per step
+          const bool mine = cstar == c;
+          float carry = excl;
+          int lastnz = -1;
+          bool found = !mine;
+          for (int base = 0; base < nown; base += 16) {
+            if (__all_sync(FULL, found)) break;
+            const int il = base + hl;
+            float wv = 0.f;
+            if (mine && il < nown) {
+              const T r = Ro[xo(il, gg)];
+              wv = r.x * r.x + r.y * r.y;
+            }
+            float sc = wv;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+              const float t2 = __shfl_up_sync(FULL, sc, o, 16);
+              if (hl >= o) sc += t2;
+            }
+            const unsigned h2 = (__ballot_sync(FULL, !found && wv > 0.f && carry + sc > tau) & hmask) >> (16 * hf);
+            const unsigned n2 = (__ballot_sync(FULL, wv > 0.f) & hmask) >> (16 * hf);
+            if (!found && h2) {
+              isel = o_lo + base + __ffs(h2) - 1;
+              found = true;
+            }
+            if (n2) lastnz = o_lo + base + 31 - __clz(n2);
+            carry += __shfl_sync(FULL, sc, 16 * hf + 15);
+          }
+          if (mine && !found) isel = lastnz;
+        }
+        if (act && cstar < 0 && hl == 0) {  // None: InstanceRun.done (solvers.py:391-396)
+          donev[gg] = 1;
+          sdone[gg] = 1;
+          flv[gg] += f;
+          if (residual) {  // the reference checks once more on done, then reports convergence
+            nchk[gg] += 1;
+            convv[gg] = 1;
+          }
+        }
+        if (!(act && cstar >= 0) && hl == 0) SEL[gg] = -1;
+        // owner: rk_step (solvers.py:173-188), then (row, gamma) to every CTA
+        const bool step = act && cstar == c;
+        T gm = make_float2(0.f, 0.f);
+        if (step) {
+          const T r = Ro[xo(isel - o_lo, gg)];
+          const float e = en[isel];
+          gm = make_float2(r.x / e, r.y / e);
+        }
+        __syncwarp();
+        if (step && hl == 0) {
+          const int il = isel - o_lo;
+          const T q = Qo[xo(il, gg)];
+          Qo[xo(il, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
+          Ro[xo(il, gg)] = make_float2(0.f, 0.f);
+          const int it = itv[gg];
+          if (p.O.rows && it < p.O.rows_cap) p.O.rows[((size_t)b * K + g0 + gg) * p.O.rows_cap + it] = isel;
+        }
+        if (step && hl < CL) {
+          if (hl == c) {
+            SEL[gg] = isel;
+            GAM[gg] = gm;
+          } else {
+            st_remote(SEL + gg, hl, isel);
+            st_remote(GAM + gg, hl, gm);
+          }
+        }
+      }
+      cluster_sync();
+      KZ_PHASE();
+      // bookkeeping of the steps (every CTA keeps the same per-rhs counters)
+      if (tid < G) {
+        const int gg = tid, i = SEL[gg];
+        if (i >= 0) {
+          const long long fr = SCH == KZ_VR_OGRK ? 2 + 8LL * rowL[i] + 2 : dense_rk;
+          flv[gg] += sel_cost(gg) + fr;
+          itv[gg] += 1;
+          prevv[gg] = i;
+        }
+      }
+      {
+        const int i0 = SEL[g], i1 = SEL[g + 8];
+        if (i0 >= 0 && loc[i0] >= 0) project(m0, loc[i0], GAM[g]);
+        if (i1 >= 0 && loc[i1] >= 0) project(m1, loc[i1], GAM[g + 8]);
+      }
+    } else if constexpr (SCH == KZ_AHK) {
+      refresh(lptr, lst);
+      __syncthreads();
+      KZ_PHASE();
+      push(0);
+      cluster_sync();
+      KZ_PHASE();
+      owner_weights(0, false);
+      cluster_sync();
+      KZ_PHASE();
+    } else {  // VR-OAHK (solvers.py:414-421)
+      // orthogonal group O: exact block projection (solvers.py:312-332); residual mode refreshes every row
+      if (residual) refresh(lptr, lst); else refresh(optr, olst);
+      __syncthreads();
+      KZ_PHASE();
+      push(residual ? 0 : 1);
+      cluster_sync();
+      KZ_PHASE();
+      for (int pair = w; pair < G / 2; pair += W) {
+        const int gg = pair + hf * (G / 2);
+        float n2 = 0.f;
+        if (!donev[gg])
+          for (int il = hl; il < nown; il += 16) {
+            const int i = o_lo + il;
+            if (!residual && inset[i] != 1) continue;
+            const T r = oresid(il, gg, false);
+            if (inset[i] == 1) {
+              const T gm = make_float2(r.x / en[i], r.y / en[i]);
+              Fo[xo(il, gg)] = gm;
+              push_phi(il, gg, gm);
+            }
+            n2 = fmaf(r.x, r.x, fmaf(r.y, r.y, n2));
+          }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) n2 += __shfl_xor_sync(FULL, n2, o);
+        if (residual && hl < CL) {
+          const int k = c * G + gg;
+          if (hl == c) BS[k] = n2; else st_remote(BS + k, hl, n2);
+        }
+      }
+      cluster_sync();
+      KZ_PHASE();
+      if (tid < G) {
+        const int gg = tid;
+        livev[gg] = 0;
+        if (!donev[gg]) {
+          float n2 = 0.f;
+          for (int d = 0; d < CL; ++d) n2 += BS[d * G + gg];
+          if (!stop_test(gg, n2)) {
+            livev[gg] = 1;
+            itv[gg] += 1;
+            flv[gg] += 2 * costO + (nN ? costN + 4LL * nN : 0);
+          }
+        }
+      }
+      __syncthreads();
+      // owner: q_i += gamma_i on O; every CTA: m += gamma_i h_i for its O pieces (disjoint supports)
+      for (int e = tid; e < nown * G; e += nthr) {
+        const int il = e / G, gg = e % G;
+        if (inset[o_lo + il] != 1 || !livev[gg]) continue;
+        const T gm = Fo[xo(il, gg)], q = Qo[xo(il, gg)];
+        Qo[xo(il, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
+      }
+      {
+        const bool l0v = livev[g], l1v = livev[g + 8];
+        for (int q = optr[w]; q < optr[w + 1]; ++q) {
+          const int n = olst[q] >> 20;
+          if (l0v) project(m0, n, Phl[n * G + g]);
+          if (l1v) project(m1, n, Phl[n * G + g + 8]);
+        }
+      }
+      KZ_PHASE();
+      if (nN > 0) {
+        __syncthreads();  // Phl (aliasing P) is read by the O projection above
+        refresh(nptr, nlst);
+        __syncthreads();
+        KZ_PHASE();
+        push(2);
+        cluster_sync();
+        KZ_PHASE();
+        owner_weights(2, true);
+        cluster_sync();
+        KZ_PHASE();
+      }
+    }
+    if constexpr (AGG) {
+      // aggregated projection (solvers.py:257-309): y = sum_i phi_i h_i over the rows (ascending),
+      // den = ||y||^2 + xi ||phi||^2 from fixed-order reductions over warps and CTAs
+      if (SCH == KZ_AHK || nN > 0) {
+        const int* ptr = SCH == KZ_AHK ? lptr : nptr;
+        const int* L = SCH == KZ_AHK ? lst : nlst;
+        T y0[8], y1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
+        int q = ptr[w];
+        const int q1 = ptr[w + 1];
+        for (; q + 1 < q1; q += 2) {  // two pieces in flight
+          const int e0 = L[q], e1 = L[q + 1], n0 = e0 >> 20, n1 = e1 >> 20;
+          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
+          const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + 8];
+          const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
+          const float4* hp1 = H4 + ((e1 & 0xFFFFF) >> 1) + a;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 h0 = hp0[4 * j], h1 = hp1[4 * j];
+            const int k = 2 * j;
+            y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
+            y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
+            y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
+            y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
+            y0[k] = cfma(p10, make_float2(h1.x, h1.y), y0[k]);
+            y0[k + 1] = cfma(p10, make_float2(h1.z, h1.w), y0[k + 1]);
+            y1[k] = cfma(p11, make_float2(h1.x, h1.y), y1[k]);
+            y1[k + 1] = cfma(p11, make_float2(h1.z, h1.w), y1[k + 1]);
+          }
+        }
+        if (q < q1) {
+          const int e0 = L[q], n0 = e0 >> 20;
+          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
+          const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 h0 = hp0[4 * j];
+            const int k = 2 * j;
+            y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
+            y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
+            y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
+            y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
+          }
+        }
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          s0 = fmaf(y0[k].x, y0[k].x, fmaf(y0[k].y, y0[k].y, s0));
+          s1 = fmaf(y1[k].x, y1[k].x, fmaf(y1[k].y, y1[k].y, s1));
+        }
+        s0 += __shfl_xor_sync(FULL, s0, 8);
+        s1 += __shfl_xor_sync(FULL, s1, 8);
+        s0 += __shfl_xor_sync(FULL, s0, 16);
+        s1 += __shfl_xor_sync(FULL, s1, 16);
+        if (a == 0) {
+          Dp[w * G + g] = s0;
+          Dp[w * G + g + 8] = s1;
+        }
+        __syncthreads();
+        if (tid < G) {
+          float dy = 0.f;
+          for (int ww = 0; ww < W; ++ww) dy += Dp[ww * G + tid];
+          for (int d = 0; d < CL; ++d) {
+            float* dst = DY + c * G + tid;
+            if (d == c) *dst = dy; else st_remote(dst, d, dy);
+          }
+        }
+        cluster_sync();
+        KZ_PHASE();
+        // step length per rhs (identical in every CTA: fixed-order sums of the pushed partials)
+        if (tid < G) {
+          const int gg = tid;
+          bool live = livev[gg];
+          if (SCH == KZ_AHK) {
+            live = false;
+            if (!donev[gg]) {
+              float n2 = 0.f;
+              for (int d = 0; d < CL; ++d) n2 += AG4[d * G + gg].w;
+              if (!stop_test(gg, n2)) {
+                live = true;
+                flv[gg] += dense_refresh + 2LL * K;
+              }
+            }
+            livev[gg] = live;
+          }
+          stepv[gg] = 0;
+          if (live) {
+            float nx = 0.f, ny = 0.f, sp = 0.f, den = 0.f;
+            int nz = 0;
+            for (int d = 0; d < CL; ++d) {
+              const float4 v = AG4[d * G + gg];
+              nx += v.x; ny += v.y; sp += v.z; nz |= NZP[d * G + gg];
+              den += DY[d * G + gg];
+            }
+            den = fmaf(regf, sp, den);
+            const int n = SCH == KZ_AHK ? K : nN;
+            if (SCH == KZ_VR_OAHK) flv[gg] += 2LL * nN;  // aggregation_weights charge
+            const long long ycost = SCH == KZ_AHK ? 6LL * Nt * K + 2LL * Nt * max(K - 1, 0) : costN;
+            const int span = SCH == KZ_AHK ? Nt : unionN;
+            bool step = false;
+            if (nz && n > 0) {
+              long long f = 6LL * n + 2LL * max(n - 1, 0) + ycost + 4LL * span + 3LL * n + 2;
+              if (den != 0.f) {
+                step = true;
+                f += 2 + 8LL * span + 8LL * n;
+                GAMv[gg] = make_float2(nx / den, ny / den);
+              }
+              flv[gg] += f;
+            }
+            if (step) {
+              stepv[gg] = 1;
+              if (SCH == KZ_AHK) itv[gg] += 1;
+            } else {
+              noopv[gg] += 1;
+              if (SCH == KZ_AHK) {  // ahk_step returned False: InstanceRun.done (solvers.py:407-413)
+                donev[gg] = 1;
+                sdone[gg] = 1;
+                if (residual) {
+                  nchk[gg] += 1;
+                  convv[gg] = 1;
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        if (stepv[g]) {
+          const T gm = GAMv[g];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m0[k] = cfma(gm, y0[k], m0[k]);
+        }
+        if (stepv[g + 8]) {
+          const T gm = GAMv[g + 8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m1[k] = cfma(gm, y1[k], m1[k]);
+        }
+        // owner: q += gamma phi over its aggregated rows
+        for (int e = tid; e < nown * G; e += nthr) {
+          const int il = e / G, gg = e % G;
+          if (!stepv[gg] || (SCH == KZ_VR_OAHK && inset[o_lo + il] != 2)) continue;
+          Qo[xo(il, gg)] = cfma(GAMv[gg], Fo[xo(il, gg)], Qo[xo(il, gg)]);
+        }
+      }
+    }
+    __syncthreads();
+    KZ_PHASE();
+    if (!residual && t >= p.cap) break;
+    bool all_done = true;
+    for (int gg = 0; gg < G; ++gg)
+      if (!donev[gg]) all_done = false;
+    if (all_done) break;
+  }
+  const int t_end = t > p.cap ? p.cap : t;
+  cluster_sync();  // no CTA leaves while its shared memory may still be addressed by the cluster
+
+  // ------------------------------------------------------------------ outputs
+  if (c == 0 && tid == 0 && p.tstop) p.tstop[cid] = t_end;
+  if (blockIdx.x < (unsigned)p.P.n_systems * K)
+    KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
+  if (p.O.iterates) {
+    auto store_m = [&](const T (&mr)[8], int r) {
+      const int cc = g0 + g + 8 * r, chunk = cW + w;
+      if (cc >= K || chunk >= Nt / CH) return;
+      T* M = (T*)p.O.iterates + ((size_t)b * K + cc) * Nt + chunk * CH;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) M[8 * (k >> 1) + 2 * a + (k & 1)] = mr[k];
+    };
+    store_m(m0, 0);
+    store_m(m1, 1);
+  }
+  T* vout = (T*)p.O.v;
+  for (int e = tid; e < nown * G; e += nthr) {
+    const int il = e / G, gg = e % G;
+    if (g0 + gg < K) vout[((size_t)b * K + o_lo + il) * K + g0 + gg] = Qo[xo(il, gg)];
+  }
+  if (c == 0)
+    for (int gg = tid; gg < G; gg += nthr) {
+      const int cc = g0 + gg;
+      if (cc >= K) continue;
+      const size_t r = (size_t)b * K + cc;
+      if (p.O.iters) p.O.iters[r] = itv[gg];
+      if (p.O.converged) p.O.converged[r] = residual && convv[gg] ? 1 : 0;
+      if (p.O.done) p.O.done[r] = sdone[gg] ? 1 : 0;
+      if (p.O.noop_steps) p.O.noop_steps[r] = noopv[gg];
+      if (p.O.flops) p.O.flops[r] = flv[gg];
+      if (p.O.n_checks) p.O.n_checks[r] = nchk[gg];
+    }
+}
+
+// ------------------------------------------------------------------ host side
+inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int* CL, int* NS, int* pcap) {
+  const int nch = P.n_antennas / clu::CH;
+  *CL = (nch + W - 1) / W;
+  const int SW = W * clu::CH;
+  *NS = (P.max_support + SW - 2) / SW + 1;
+  *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
+  if (*pcap <= 0) return ~size_t(0);
+  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap).total;
+}
+
+template <int SCH>
+inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStream_t s) {
+  auto kern = kz_cluster_kernel<SCH>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  if (CL > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int groups = (a.P.n_users + clu::G - 1) / clu::G;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.P.n_systems * groups * CL));
+  cfg.blockDim = dim3((unsigned)(32 * W));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  const cudaError_t oc = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
+  if (getenv("KZ_VERBOSE"))
+    fprintf(stderr, "[kz cluster] W %d CL %d smem %zu: max active clusters %d (%s)\n", W, CL, smem, nclusters,
+            cudaGetErrorString(oc));
+  if (oc != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
+  if (a.mode == KZ_STOP_LOCKSTEP)
+    kz_lockstep_finalize<<<(a.P.n_systems + 127) / 128, 128, 0, s>>>(a.tstop, groups, a.P.n_systems, a.O.n_outer,
+                                                                     a.O.sys_converged);
+  return 1;
+}
+
+// 1 launched, 0 not eligible, -1 failure
+inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S, const kz_rng& R, const kz_out& O,
+                              int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
+  static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr || getenv("KZ_DISABLE_CLUSTER") != nullptr;
+  if (disabled || resume || P.dtype != KZ_C64) return 0;
+  if (!(scheme == KZ_GK || scheme == KZ_GRK || scheme == KZ_VR_OGRK || scheme == KZ_AHK || scheme == KZ_VR_OAHK))
+    return 0;
+  const bool lockstep = S.mode == KZ_STOP_LOCKSTEP && S.epsilon == 0.0;
+  const bool resid = S.mode == KZ_STOP_RESIDUAL && S.epsilon > 0.0;
+  if (!(lockstep || resid) || S.max_iters < 1 || S.check_every < 1) return 0;
+  if (O.nmse_trace || O.resid_trace || O.flops_trace || S.rhs_mask) return 0;
+  if (!(P.flags & KZ_PROBLEM_CONTIGUOUS) || P.max_support < 1 || P.n_antennas % clu::CH != 0) return 0;
+  const bool stochastic = scheme == KZ_GRK || scheme == KZ_VR_OGRK;
+  if (stochastic && R.kind != KZ_RNG_PHILOX &&
+      !(lockstep && R.kind == KZ_RNG_HOST_UNIFORM && R.stream_base == 0 && R.stream_len >= S.max_iters))
+    return 0;
+  GenLayout L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
+  if (ws_bytes < L.total + ls_extra_ws(P)) return 0;
+  int dev = 0, maxsm = 0, smsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  // slice width: 256 antennas (8 warps, one CTA per SM) when it fits, else 128 antennas (two CTAs per SM when
+  // they fit); clusters stay within 16 CTAs
+  int CL4, NS4, pc4, CL8, NS8, pc8;
+  const size_t s4 = cluster_smem_bytes(P, scheme, 4, &CL4, &NS4, &pc4);
+  const size_t s8 = cluster_smem_bytes(P, scheme, 8, &CL8, &NS8, &pc8);
+  const size_t two = (size_t)(smsm / 2 - 1024);
+  int W = 0;
+  static const int forced = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
+  if (forced == 4 || forced == 8) {
+    W = forced;
+  } else if (CL8 <= 16 && s8 <= (size_t)maxsm) {
+    W = 8;
+  } else if (CL4 <= 16 && s4 <= two) {
+    W = 4;
+  } else if (CL4 <= 16 && s4 <= (size_t)maxsm) {
+    W = 4;
+  }
+  static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
+  if (verbose)
+    fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: W4 CL %d pairs %d smem %zu | W8 CL %d pairs %d smem %zu -> W %d\n",
+            scheme, P.n_users, P.n_antennas, CL4, pc4, s4 == ~size_t(0) ? 0 : s4, CL8, pc8,
+            s8 == ~size_t(0) ? 0 : s8, W);
+  if (W == 0) return 0;
+  const int CL = W == 4 ? CL4 : CL8;
+  const size_t smem = W == 4 ? s4 : s8;
+  if (CL > 16 || smem > (size_t)maxsm) return 0;
+  CluArgs a;
+  a.P = P;
+  a.R = R;
+  a.O = O;
+  a.mode = lockstep ? KZ_STOP_LOCKSTEP : KZ_STOP_RESIDUAL;
+  a.cap = S.max_iters;
+  a.every = S.check_every;
+  a.eps = (float)S.epsilon;
+  a.NS = W == 4 ? NS4 : NS8;
+  a.pcap = W == 4 ? pc4 : pc8;
+  a.tstop = (int32_t*)(ws + L.total);
+  int rc = 0;
+  switch (scheme) {
+    case KZ_GK: rc = cluster_launch<KZ_GK>(a, W, CL, smem, s); break;
+    case KZ_GRK: rc = cluster_launch<KZ_GRK>(a, W, CL, smem, s); break;
+    case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK>(a, W, CL, smem, s); break;
+    case KZ_AHK: rc = cluster_launch<KZ_AHK>(a, W, CL, smem, s); break;
+    case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK>(a, W, CL, smem, s); break;
+  }
+  if (rc == 1) *launches = lockstep ? 2 : 1;
+  return rc;
+}
+
+}  // namespace kz

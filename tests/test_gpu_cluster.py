@@ -1,0 +1,191 @@
+"""GPU parity of the cluster kernel (csrc/kz_solve_cluster.cuh): large arrays (Nt > 512, one
+thread-block cluster per system x 16 rhs) in complex64, fixed-T lockstep and per-rhs residual
+tolerance, against the complex128 CPU oracle.
+
+Criteria (BASELINE.json north_star, complex64 throughput mode): deterministic schemes (AHK,
+VR-OAHK) match the oracle's V within 1e-4 relative after T steps (fp32 accumulation); greedy
+schemes may break near-ties differently in fp32, so their recorded row sequence is replayed in
+float64 and must reproduce the kernel's V, and the greedy choice itself is checked on the first
+step (identical to the oracle's); the residual mode must converge every rhs with the true
+residual (recomputed in float64 from V) at the tolerance, and deterministic VR-OAHK must stop
+at the oracle's iteration counts.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import oracle_channel_contiguous
+
+pytestmark = pytest.mark.gpu
+
+
+def _kz():
+    import paper_2501_10689_b200 as kz
+    return kz
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (n if n > 0 else 1.0)
+
+
+def _large(nt=1024, k=40, vr=(96, 400), name="t_large"):
+    kz = _kz()
+    return kz.NearFieldConfig(name, nt, k, vr)
+
+
+def _replay(ch, b, rows, vr_form):
+    """Float64 replay of a recorded RK row sequence (rk_step with the refreshed residual of the
+    projected row, solvers.py:143-188): returns V (K x K)."""
+    h = ch.dense(b)
+    k = ch.n_users
+    reg = float(ch.reg[b])
+    e = np.sum(np.abs(h) ** 2, axis=0) + reg
+    v = np.zeros((k, k), dtype=np.complex128)
+    for c in range(k):
+        m = np.zeros(h.shape[0], dtype=np.complex128)
+        q = np.zeros(k, dtype=np.complex128)
+        for i in rows[c]:
+            if i < 0:
+                break
+            r = (1.0 if i == c else 0.0) - np.vdot(h[:, i], m) - reg * q[i]
+            g = r / e[i]
+            m += g * h[:, i]
+            q[i] += g
+        v[:, c] = q
+    return v
+
+
+@pytest.mark.parametrize("scheme", ["gk", "grk", "vr-ogrk", "ahk", "vr-oahk"])
+def test_cluster_lockstep_vs_oracle(scheme):
+    kz = _kz()
+    T = 25
+    ch = kz.generate(_large(), range(3))
+    host = kz.HostBatch.from_contiguous(ch)
+    dev = host.to_device("c64")
+    k = host.n_users
+    streams = None
+    if scheme in kz.STOCHASTIC_SCHEMES:
+        gens = [np.random.default_rng(kz.solver_seed_sequence(s)).spawn(k) for s in range(3)]
+        streams = kz.HostStreams(scheme, gens, host.row_energy.reshape(3, k))
+    res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rng=streams, rows_cap=T)
+    assert res.launches == 2  # cluster kernel + n_outer finaliser
+    for b in range(3):
+        chan = oracle_channel_contiguous(ch, b)
+        sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+        run = O.run_precoding(scheme, sys_, O.rzf_precoder(chan, float(ch.reg[b])), epsilon=0.0, max_iters=T,
+                              traces=False, rng=np.random.default_rng(kz.solver_seed_sequence(b)))
+        v = res.v[b].cpu().numpy()
+        assert int(res.n_outer[b]) == T
+        if scheme in ("ahk", "vr-oahk"):
+            # iteration / no-op counts are not compared: at the fp32 floor the aggregated step can
+            # become an exact no-op (phi == 0 or den == 0), which ends AHK early (the generic c64
+            # kernel does the same); V is what the criterion is about
+            assert rel(v, run.v) <= 1e-4, b
+        else:
+            rows = res.rows[b].cpu().numpy()
+            assert (rows >= 0).sum(axis=1).min() == T  # no early None on these drops
+            assert rel(v, _replay(ch, b, rows, scheme == "vr-ogrk")) <= 1e-4, b
+            first = [r[0] for r in run.rows]
+            np.testing.assert_array_equal(rows[:, 0], first)
+            same = np.mean([np.array_equal(rows[c], run.rows[c]) for c in range(k)])
+            assert same >= 0.5, same  # fp32 vs fp64 near-ties only
+
+
+def test_cluster_flops_match_oracle_counter():
+    """FlopCounter totals of the deterministic schemes equal the oracle's (setup and assembly
+    charges added as in test_register_resident_path_all_schemes)."""
+    kz = _kz()
+    T = 12
+    ch = kz.generate(_large(nt=768, k=24, vr=(64, 300)), range(2))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    k, nt = ch.n_users, ch.n_antennas
+    for scheme in ("ahk", "vr-oahk", "gk"):
+        res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=T, rows_cap=T)
+        if scheme != "gk":
+            assert int(res.noop_steps.sum()) == 0  # T = 12 stays above the fp32 floor
+        for b in range(2):
+            chan = oracle_channel_contiguous(ch, b)
+            sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+            run = O.run_precoding(scheme, sys_, O.rzf_precoder(chan, float(ch.reg[b])), epsilon=0.0,
+                                  max_iters=T, traces=False)
+            if scheme == "gk" and any(list(res.rows[b, c, :T].cpu().numpy()) != list(run.rows[c]) for c in range(k)):
+                continue  # an fp32 near-tie changed a greedy pick: counts legitimately differ
+            setup = 4 * nt * k
+            if scheme in kz.VR_SCHEMES:
+                asm = sum(6 * q * k + 2 * (q - 1) * k for q in
+                          [sum(1 for vr in chan.vrs if n in vr.visible_subarrays) for n in range(nt)] if q)
+            else:
+                asm = 6 * nt * k * k + 2 * nt * k * (k - 1)
+            assert int(res.flops[b].sum()) + setup + asm == run.flops_measured, (scheme, b)
+
+
+@pytest.mark.parametrize("cfg,nsys", [("mid", 2), ("cfg4", 1)])
+def test_cluster_residual_tolerance(cfg, nsys):
+    """solve_all residual semantics (solvers.py:460-537) in complex64 on the cluster kernel: every
+    rhs converges, the float64 true residual of V is at the tolerance, VR-OAHK stops at the
+    oracle's iteration counts (+-1 where the fp32 norm sits on the threshold)."""
+    kz = _kz()
+    eps = 1e-4
+    conf = _large(nt=2048, k=64, vr=(256, 256), name="mid") if cfg == "mid" else kz.CONFIGS["cfg4"]
+    ch = kz.generate(conf, range(nsys))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    k = ch.n_users
+    for scheme in ("vr-oahk", "grk"):
+        rng = ("philox", 3) if scheme == "grk" else None
+        res = kz.solve_batch(dev, scheme, mode="residual", epsilon=eps, max_iters=10000 * k, rng=rng)
+        assert res.launches == 1
+        assert bool(res.converged.all()), scheme
+        its = res.iters.cpu().numpy()
+        for b in range(nsys):
+            h = ch.dense(b)
+            reg = float(ch.reg[b])
+            gram = h.conj().T @ h + reg * np.eye(k)
+            v = res.v[b].cpu().numpy().astype(np.complex128)
+            r = np.eye(k) - gram @ v
+            rn = np.linalg.norm(r, axis=0)
+            assert rn.max() <= 2 * eps, (scheme, rn.max())
+            if scheme == "vr-oahk" and b == 0:
+                chan = oracle_channel_contiguous(ch, b)
+                sys_ = O.AugmentedSystem.from_channel(chan, reg)
+                traces = []
+                O.solve_all(scheme, sys_, O.StoppingRule(mode="residual", epsilon=eps), traces=traces)
+                want = np.array([t.n_iters for t in traces])
+                assert np.abs(its[b] - want).max() <= 1, (its[b], want)
+                assert np.mean(its[b] == want) >= 0.9
+        if scheme == "grk":
+            assert its.min() >= 1
+
+
+def test_cluster_iterates_are_h_coef():
+    """The iterate written back by the cluster kernel equals H v (col = H coef) to fp32 accuracy."""
+    import torch
+    kz = _kz()
+    ch = kz.generate(_large(), range(2))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    for scheme in ("vr-oahk", "grk"):
+        rng = ("philox", 5) if scheme == "grk" else None
+        res = kz.solve_batch(dev, scheme, mode="lockstep", max_iters=20, rng=rng, want_iterates=True)
+        hv = kz.epilogue(dev, res.v, want_f=True)
+        f = (hv["f"].to(torch.complex128) / hv["beta"][:, None, None]).transpose(1, 2).cpu().numpy()
+        assert rel(res.iterates().to(torch.complex128).cpu().numpy(), f) <= 1e-4, scheme
+
+
+def test_cluster_cfg5_ahk_nmse_vs_rzf():
+    """cfg5 shape (Nt=2048, K=128, wideband, shared VRs) in complex64: AHK / VR-OAHK at T=3 and
+    T=20 give the complex128 path's NMSE to RZF (c64 criterion) and sum-rate within 1e-3."""
+    kz = _kz()
+    ch = kz.generate("cfg5", [0, [3, 700]])
+    dev64 = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    dev128 = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    rz = kz.rzf_batched(dev128)
+    for sc, T in (("ahk", 3), ("vr-oahk", 3), ("ahk", 20), ("vr-oahk", 20)):
+        out = kz.run_precoding_batched(sc, dev64, max_iters=T, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
+        ref = kz.run_precoding_batched(sc, dev128, max_iters=T, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
+        got, want = out["nmse"].cpu().numpy(), ref["nmse"].cpu().numpy()
+        above = want >= 1e-5  # relative criterion above the fp32 floor, else NMSE_64 <= 1e-6
+        np.testing.assert_allclose(got[above], want[above], rtol=1e-3)
+        assert np.all(got[~above] <= 1e-6), got
+        np.testing.assert_allclose(out["sum_rate"].cpu().numpy(), ref["sum_rate"].cpu().numpy(), rtol=1e-3)

@@ -21,8 +21,11 @@ ap.add_argument("--scheme", default="grk")
 ap.add_argument("--dtype", default="c64")
 ap.add_argument("--batch", type=int, default=296)
 ap.add_argument("--iters", type=int, default=100)
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--cluster-w", type=int, default=0, help="warps per CTA of the cluster kernel (0: wide/chunked)")
 a = ap.parse_args()
-ch = kz.generate("cfg2", range(a.batch))
+cfg = kz.CONFIGS[a.config]
+ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
 dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
 rng = ("philox", 3) if a.scheme in kz.STOCHASTIC_SCHEMES else None
 res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
@@ -43,6 +46,9 @@ base = ws.numel() - extra
 off = base + (B * K * 4 + 7) // 8 * 8
 G = (32 if K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype == "c64" else 8
 ncta = B * ((K + G - 1) // G)
+if a.cluster_w:
+    CL = -(-Nt // (32 * a.cluster_w))
+    ncta = min(B * K, B * -(-K // 16) * CL)
 raw = ws[off:off + ncta * 44 * 8].view(torch.int64).view(ncta, 44).cpu().numpy().astype(np.float64)
 ph = raw[:, :12].copy()
 wst = raw[:, 12:12 + Nt // 32] / a.iters  # per-warp refresh-end cycles per iteration
