@@ -137,8 +137,17 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
   return cuda_check("kz_solve(generic)");
 }
 
+// the blocked Gauss-Jordan kernel inverts in place in v_out; only the legacy kernel needs a workspace
+static bool rzf_uses_gj(const kz_problem* prob) {
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return getenv("KZ_RZF_LEGACY") == nullptr && maxsm > 0 && rzf_smem(prob->n_users) <= (size_t)maxsm;
+}
+
 size_t kz_rzf_workspace_bytes(const kz_problem* prob) {
   if (!prob) return 0;
+  if (rzf_uses_gj(prob)) return 0;
   return kz_align((size_t)prob->n_systems * 2 * prob->n_users * prob->n_users * sizeof(double2));
 }
 
@@ -150,13 +159,25 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
   if (!v_out) return fail(KZ_ERR_INVALID, "v_out must be non-null");
   if (prob->n_systems == 0) return KZ_OK;
   size_t need = kz_rzf_workspace_bytes(prob);
-  if (!workspace || workspace_bytes < need)
+  if (need && (!workspace || workspace_bytes < need))
     return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
   cudaStream_t s = (cudaStream_t)stream;
-  if (prob->dtype == KZ_C128)
+  const size_t smem = rzf_smem(prob->n_users);
+  if (rzf_uses_gj(prob)) {  // KZ_RZF_LEGACY=1: A/B switch to the unblocked Cholesky kernel
+    const int nb = rzf_nb(prob->n_users);
+    const int nthr = prob->n_users <= 96 ? 256 : RZF_THREADS;  // small Grams: fewer threads, cheaper barriers
+    if (prob->dtype == KZ_C128) {
+      cudaFuncSetAttribute(kz_rzf_gj_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kz_rzf_gj_kernel<double2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb);
+    } else {
+      cudaFuncSetAttribute(kz_rzf_gj_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kz_rzf_gj_kernel<float2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb);
+    }
+  } else if (prob->dtype == KZ_C128) {
     kz_rzf_kernel<double2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(*prob, v_out, f_out, beta_out, pd_ok, (double2*)workspace);
-  else
+  } else {
     kz_rzf_kernel<float2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(*prob, v_out, f_out, beta_out, pd_ok, (double2*)workspace);
+  }
   g_launches = 1;
   return cuda_check("kz_rzf");
 }

@@ -220,6 +220,226 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_rzf_kernel(kz_problem P, dou
   if (beta_out && threadIdx.x == 0) beta_out[b] = beta;
 }
 
+// ---------------------------------------------------------------- K2: RZF, blocked Gauss-Jordan
+// V = (H^H H + xi I)^{-1} in place in v_out: the Gram (full Hermitian) is built from the pairwise support
+// intersections, then inverted by blocked Gauss-Jordan (block NB: the NB x NB pivot block is inverted in shared
+// memory, the row panel D^{-1} A[kb,:] and the column panel A[:,kb] are staged in shared memory, the trailing
+// matrix gets a rank-NB update in 4 x 4 register tiles).  No pivoting: for a Hermitian positive definite
+// Gram the pivots are the squared Cholesky diagonals, so "pivot > 0" is exactly cho_factor's test (rzf.py:55-59).
+// beta = 1 / ||H V||_F from ||H V||_F^2 = tr(V) - xi ||V||_F^2 (H^H H = V^{-1} - xi I), so H V is only formed
+// when F is requested.  Work ~ K^3 complex MACs in fp64 per system.
+constexpr int RZF_THREADS = 512;
+inline int rzf_nb(int K) { return K <= 256 ? 16 : 8; }
+inline size_t rzf_smem(int K) {
+  const int nb = rzf_nb(K);
+  return (size_t)(2 * (size_t)K * nb + (size_t)nb * nb) * sizeof(double2);
+}
+
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 zfms(double2 a, double2 b, double2 acc) {  // acc - a b (4 DFMA)
+  return make_double2(fma(a.y, b.y, fma(-a.x, b.x, acc.x)), fma(-a.y, b.x, fma(-a.x, b.y, acc.y)));
+}
+__device__ __forceinline__ double2 zfma(double2 a, double2 b, double2 acc) {  // acc + a b (4 DFMA)
+  return make_double2(fma(-a.y, b.y, fma(a.x, b.x, acc.x)), fma(a.y, b.x, fma(a.x, b.y, acc.y)));
+}
+
+template <class TH>
+__global__ void __launch_bounds__(RZF_THREADS, 1) kz_rzf_gj_kernel(kz_problem P, double* v_out, double* f_out,
+                                                                double* beta_out, uint8_t* pd_ok, int NB) {
+  extern __shared__ __align__(16) unsigned char rzf_sm[];
+  const int b = blockIdx.x;
+  const int K = P.n_users, Nt = P.n_antennas;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  RowView R{P.row_seg_ptr, P.seg_start, P.seg_len, P.row_val_ptr};
+  double2* A = (double2*)v_out + (size_t)b * K * K;
+  double2* Cs = (double2*)rzf_sm;          // [K][nb]  column panel A[:, kb]
+  double2* Rs = Cs + (size_t)K * NB;       // [nb][K]  row panel D^{-1} A[kb, :]
+  double2* Ds = Rs + (size_t)NB * K;       // [nb][nb] pivot block -> its inverse
+  __shared__ double red[32];
+  __shared__ int s_bad;
+  const double reg = P.reg[b];
+
+  // Gram H^H H + xi I (rzf.py:38-40), both triangles.  Contiguous supports: one warp per pair with the
+  // lanes over the overlap (coalesced loads, fixed-order shuffle reduction); general supports: one
+  // thread per pair walking the segment intersections.
+  const int npair = K * (K + 1) / 2;
+  auto pair_of = [&](int e, int& i, int& j) {
+    i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > e) --i;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    j = e - i * (i + 1) / 2;
+  };
+  auto put = [&](int i, int j, double2 g) {
+    if (i == j) {
+      A[(size_t)i * K + i] = make_double2(g.x + reg, 0.0);
+    } else {
+      A[(size_t)i * K + j] = g;
+      A[(size_t)j * K + i] = make_double2(g.x, -g.y);
+    }
+  };
+  if (P.flags & KZ_PROBLEM_CONTIGUOUS) {
+    const int lane = tid & 31, nw = nthr >> 5;
+    const TH* hv = (const TH*)P.heff;
+    for (int e = tid >> 5; e < npair; e += nw) {
+      int i, j;
+      pair_of(e, i, j);
+      const size_t ri = (size_t)b * K + i, rj = (size_t)b * K + j;
+      const int si = P.seg_start[P.row_seg_ptr[ri]], li = P.seg_len[P.row_seg_ptr[ri]];
+      const int sj = P.seg_start[P.row_seg_ptr[rj]], lj = P.seg_len[P.row_seg_ptr[rj]];
+      const int lo = max(si, sj), hi = min(si + li, sj + lj);
+      if (lo >= hi) {  // disjoint supports: structural zero, no reduction
+        if (lane == 0) put(i, j, make_double2(0.0, 0.0));
+        continue;
+      }
+      const TH* hi_p = hv + R.val_ptr[ri] - si;
+      const TH* hj_p = hv + R.val_ptr[rj] - sj;
+      double re = 0.0, im = 0.0;
+      for (int n = lo + lane; n < hi; n += 32) {
+        const double2 x = to_d2(hi_p[n]), y = to_d2(hj_p[n]);
+        re = fma(x.x, y.x, re);
+        re = fma(x.y, y.y, re);
+        im = fma(x.x, y.y, im);
+        im = fma(-x.y, y.x, im);
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) put(i, j, make_double2(re, im));
+    }
+  } else {
+    for (int e = tid; e < npair; e += nthr) {
+      int i, j;
+      pair_of(e, i, j);
+      put(i, j, gram_entry<TH>(R, P.heff, (size_t)b * K + i, (size_t)b * K + j));
+    }
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  const int TI = (K + 3) / 4;
+  for (int k0 = 0; k0 < K; k0 += NB) {
+    const int nb = min(NB, K - k0);
+    for (int e = tid; e < nb * nb; e += nthr) Ds[e] = A[(size_t)(k0 + e / nb) * K + k0 + e % nb];
+    __syncthreads();
+    // scalar Gauss-Jordan on the pivot block, warp 0 alone (warp-synchronous steps)
+    if (tid < 32) {
+      for (int k = 0; k < nb; ++k) {
+        const double2 dkk = Ds[k * nb + k];
+        const bool bad = !(dkk.x > 0.0);
+        const double2 piv = make_double2(1.0 / (bad ? 1.0 : dkk.x), 0.0);  // Hermitian PD: the pivot is real
+        __syncwarp();
+        if (bad && tid == 0) s_bad = 1;
+        for (int j = tid; j < nb; j += 32)
+          if (j != k) Ds[k * nb + j] = zmul(piv, Ds[k * nb + j]);
+        __syncwarp();
+        for (int e = tid; e < nb * nb; e += 32) {
+          const int i = e / nb, j = e % nb;
+          if (i != k && j != k) Ds[e] = zfms(Ds[i * nb + k], Ds[k * nb + j], Ds[e]);
+        }
+        __syncwarp();
+        for (int i = tid; i < nb; i += 32) {
+          const double2 x = Ds[i * nb + k];
+          Ds[i * nb + k] = i == k ? piv : make_double2(-(x.x * piv.x), -(x.y * piv.x));
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // panels: rows kb of A -> Rs (coalesced), then R = D^{-1} A[kb, :] in place one column per thread;
+    // C = A[:, kb]
+    for (int e = tid; e < nb * K; e += nthr) Rs[e] = A[(size_t)(k0 + e / K) * K + e % K];
+    for (int e = tid; e < K * nb; e += nthr) {
+      const int i = e / nb, t = e % nb;
+      Cs[i * nb + t] = A[(size_t)i * K + k0 + t];
+    }
+    __syncthreads();
+    for (int j = tid; j < K; j += nthr) {
+      if (j >= k0 && j < k0 + nb) continue;
+      double2 col[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) col[q] = q < nb ? Rs[q * K + j] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        if (t >= nb) break;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < nb) acc = zfma(Ds[t * nb + q], col[q], acc);
+        Rs[t * K + j] = acc;
+        A[(size_t)(k0 + t) * K + j] = acc;
+      }
+    }
+    __syncthreads();
+    // rank-nb trailing update in 4 x 4 register tiles (columns strided by TI: conflict-free shared loads and
+    // coalesced global accesses), column panel -C D^{-1}, pivot block D^{-1}
+    for (int tile = tid; tile < TI * TI; tile += nthr) {
+      const int i0 = (tile / TI) * 4, tj = tile % TI;
+      bool okr[4], okc[4], any_r = false, any_c = false;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int j = tj + r * TI;
+        okr[r] = i0 + r < K && (i0 + r < k0 || i0 + r >= k0 + nb);
+        okc[r] = j < K && (j < k0 || j >= k0 + nb);
+        any_r |= okr[r];
+        any_c |= okc[r];
+      }
+      if (!any_r || !any_c) continue;
+      double2 acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          acc[r][q] = okr[r] && okc[q] ? A[(size_t)(i0 + r) * K + tj + q * TI] : make_double2(0.0, 0.0);
+      for (int t = 0; t < nb; ++t) {
+        double2 cv[4], rv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          cv[r] = i0 + r < K ? Cs[(i0 + r) * nb + t] : make_double2(0.0, 0.0);
+          rv[r] = tj + r * TI < K ? Rs[t * K + tj + r * TI] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[r][q] = zfms(cv[r], rv[q], acc[r][q]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (okr[r] && okc[q]) A[(size_t)(i0 + r) * K + tj + q * TI] = acc[r][q];
+    }
+    for (int e = tid; e < K * nb; e += nthr) {
+      const int i = e / nb, t = e % nb;
+      double2 x;
+      if (i >= k0 && i < k0 + nb) {
+        x = Ds[(i - k0) * nb + t];
+      } else {
+        x = make_double2(0.0, 0.0);
+        for (int q = 0; q < nb; ++q) x = zfms(Cs[i * nb + q], Ds[q * nb + t], x);
+      }
+      A[(size_t)i * K + k0 + t] = x;
+    }
+    __syncthreads();
+  }
+  if (pd_ok && tid == 0) pd_ok[b] = s_bad ? 0 : 1;
+  // beta = 1 / ||H V||_F with ||H V||_F^2 = tr(V) - xi ||V||_F^2 (rzf.py:77-83)
+  double tr = 0.0, fro = 0.0;
+  for (int e = tid; e < K * K; e += nthr) {
+    const double2 x = A[e];
+    fro += x.x * x.x + x.y * x.y;
+    if (e / K == e % K) tr += x.x;
+  }
+  tr = block_reduce_sum(tr, red);
+  fro = block_reduce_sum(fro, red);
+  const double beta = 1.0 / sqrt(tr - reg * fro);
+  if (beta_out && tid == 0) beta_out[b] = beta;
+  if (f_out) {  // F = beta H V (assembly.py:51-56), only on request
+    double2* F = (double2*)f_out + (size_t)b * Nt * K;
+    (void)assemble<TH, double2, double2>(P, b, A, beta, nullptr, 0.0, F, nullptr, red);
+  }
+}
+
 // ---------------------------------------------------------------- K3: epilogue
 template <class T>
 __global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_kernel(kz_problem P, const T* v, T* f_out, const double* v_ref,
