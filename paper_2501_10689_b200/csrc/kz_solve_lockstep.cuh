@@ -862,6 +862,7 @@ inline int ls_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const k
 }  // namespace kz
 
 #include "kz_solve_wide.cuh"
+#include "kz_solve_rkwarp.cuh"
 
 namespace kz {
 
@@ -887,7 +888,8 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
   int rc;
   static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: 16-rhs chunked kernel only
   if (P.dtype == KZ_C64) {
-    rc = chunked ? 0 : wide_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
+    rc = chunked ? 0 : rkwarp_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
+    if (rc == 0 && !chunked) rc = wide_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
     if (rc == 0) {
       size_t smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
       if ((int)smem > maxsm) return 0;

@@ -1,0 +1,242 @@
+// Warp-per-rhs kernel for the one-row-per-iteration schemes (urk, swor-erk) in complex64, fixed T,
+// contiguous VRs (solvers.py:382-389 with rk_step, solvers.py:173-188).
+//
+// An RK iteration touches one row (|Gamma_i| antennas) per rhs, so the wide kernel's CTA-wide barriers
+// (draw -> partials -> step -> projection) dominate its time.  Here each warp owns one rhs and runs its T
+// iterations without any CTA barrier: the iterate m of its rhs lives in shared memory (Nt complex), the
+// rows of the system are shared by the warps of the CTA (packed, unpadded).  Per iteration the lanes
+// stride the row's support (antenna s + lane + 32 j): one conflict-free LDS.64 of h and of m per element,
+// a shuffle reduction for h^H m, the step, and the m update from the same registers.
+#pragma once
+
+#include "kz_common.cuh"
+#include "kz_solve_generic.cuh"
+
+namespace kz {
+
+namespace rkw {
+
+struct Plan {
+  size_t rowS, rowL, hoff, en, M, Q, pool, total;
+};
+
+__host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+
+// nw warps (rhs) per CTA, hcap packed H elements
+__host__ __device__ inline Plan plan(int K, int Nt, int nw, int hcap) {
+  Plan p;
+  const int KW = (K + 31) / 32;
+  size_t o = 0;
+  p.rowS = o; o = al(o + 4 * (size_t)K);
+  p.rowL = o; o = al(o + 4 * (size_t)K);
+  p.hoff = o; o = al(o + 4 * (size_t)K);
+  p.en = o; o = al(o + 8 * (size_t)K);
+  p.M = o; o = al(o + 8 * (size_t)nw * Nt);
+  p.Q = o; o = al(o + 8 * (size_t)nw * K);
+  p.pool = o; o = al(o + 4 * (size_t)nw * KW);
+  o = al(o + 8 * (size_t)hcap);  // H last
+  p.total = o;
+  return p;
+}
+
+}  // namespace rkw
+
+template <int SCH>
+__global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
+  using namespace rkw;
+  using T = float2;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int K = p.P.n_users, Nt = p.P.n_antennas;
+  const int ngroups = (K + nw - 1) / nw;
+  const int b = blockIdx.x / ngroups, c0g = (blockIdx.x % ngroups) * nw;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
+  const int KW = (K + 31) / 32;
+  const Plan pl = plan(K, Nt, nw, p.hcap);
+  int* rowS = (int*)(sm + pl.rowS);
+  int* rowL = (int*)(sm + pl.rowL);
+  int* hoff = (int*)(sm + pl.hoff);
+  double* en = (double*)(sm + pl.en);
+  T* Ms = (T*)(sm + pl.M) + (size_t)w * Nt;
+  T* Qs = (T*)(sm + pl.Q) + (size_t)w * K;
+  uint32_t* pool = (uint32_t*)(sm + pl.pool) + (size_t)w * KW;
+  T* Hs = (T*)(sm + pl.pool + al(4 * (size_t)nw * KW));
+  const float regf = (float)p.P.reg[b];
+
+  for (int i = tid; i < K; i += nthr) {
+    const size_t r = (size_t)b * K + i;
+    const int sg = p.P.row_seg_ptr[r];
+    rowS[i] = p.P.seg_start[sg];
+    rowL[i] = p.P.seg_len[sg];
+    en[i] = p.P.row_energy[r];
+  }
+  __syncthreads();
+  if (w == 0) {  // packed row offsets
+    int carry = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int i = base + lane;
+      const int v = i < K ? rowL[i] : 0;
+      int sc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += t2;
+      }
+      if (i < K) hoff[i] = carry + sc - v;
+      carry += __shfl_sync(FULL, sc, 31);
+    }
+  }
+  __syncthreads();
+  {
+    const T* heff = (const T*)p.P.heff;
+    for (int i = w; i < K; i += nthr >> 5) {
+      const T* src = heff + p.P.row_val_ptr[(size_t)b * K + i];
+      for (int e = lane; e < rowL[i]; e += 32) Hs[hoff[i] + e] = src[e];
+    }
+  }
+  for (int n = lane; n < Nt; n += 32) Ms[n] = make_float2(0.f, 0.f);
+  for (int i = lane; i < K; i += 32) Qs[i] = make_float2(0.f, 0.f);
+  for (int q = lane; q < KW; q += 32) pool[q] = 0;
+  int poolcnt = 0;
+  __syncthreads();
+
+  const int c = c0g + w;
+  const bool active = c < K && w < nw;
+  long long flops = 0;
+  int it = 0;
+  if (active) {
+    const size_t rid = (size_t)b * K + c;
+    for (it = 0; it < p.T; ++it) {
+      // ---- draw (solvers.py:218-230)
+      int i;
+      if (p.R.kind == KZ_RNG_HOST_INDEX) {
+        i = p.R.indices[rid * p.R.stream_len + it];
+      } else if (SCH == KZ_URK) {
+        const double u = p.R.kind == KZ_RNG_PHILOX ? philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)it)
+                                                   : p.R.uniforms[rid * p.R.stream_len + it];
+        i = (int)(u * K);
+        i = i >= K ? K - 1 : i;
+      } else {  // energy-weighted pick without replacement from the epoch pool (warp-parallel scan)
+        if (poolcnt == 0) {
+          for (int q = lane; q < KW; q += 32) pool[q] = 0xFFFFFFFFu >> (q == KW - 1 && (K & 31) ? 32 - (K & 31) : 0);
+          poolcnt = K;
+          __syncwarp();
+        }
+        const double u = p.R.kind == KZ_RNG_PHILOX ? philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)it)
+                                                   : p.R.uniforms[rid * p.R.stream_len + it];
+        double tot = 0.0;
+        for (int j = lane; j < K; j += 32)
+          if ((pool[j >> 5] >> (j & 31)) & 1u) tot += en[j];
+        tot = warp_sum(tot);
+        const double tau = u * tot;
+        double carry = 0.0;
+        int pick = -1, last = -1;
+        for (int base = 0; base < K; base += 32) {
+          const int j = base + lane;
+          const bool in = j < K && ((pool[j >> 5] >> (j & 31)) & 1u);
+          const double v = in ? en[j] : 0.0;
+          double sc = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double t2 = __shfl_up_sync(FULL, sc, o);
+            if (lane >= o) sc += t2;
+          }
+          const unsigned hit = __ballot_sync(FULL, in && carry + sc > tau);
+          const unsigned nz = __ballot_sync(FULL, in);
+          if (pick < 0 && hit) pick = base + __ffs(hit) - 1;
+          if (nz) last = base + 31 - __clz(nz);
+          carry += __shfl_sync(FULL, sc, 31);
+        }
+        i = pick >= 0 ? pick : last;
+        __syncwarp();
+        if (lane == 0) pool[i >> 5] &= ~(1u << (i & 31));
+        __syncwarp();
+        poolcnt -= 1;
+      }
+      if (SCH == KZ_SWOR_ERK) flops += (K - it % K) + 2;  // pool bookkeeping charge (as the wide kernel)
+      // ---- refresh of row i (solvers.py:159-170) and rk_step (solvers.py:173-188)
+      const int s = rowS[i], L = rowL[i];
+      const T* h = Hs + hoff[i];
+      float dx = 0.f, dy = 0.f;
+      for (int e = lane; e < L; e += 32) {
+        const T hv = h[e], mv = Ms[s + e];
+        dx = fmaf(hv.x, mv.x, dx); dx = fmaf(hv.y, mv.y, dx);
+        dy = fmaf(hv.x, mv.y, dy); dy = fmaf(-hv.y, mv.x, dy);
+      }
+      dx = warp_sum(dx);
+      dy = warp_sum(dy);
+      const T q = Qs[i];
+      const float tg = i == c ? 1.f : 0.f;
+      const T r = make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
+      const float e = (float)en[i];
+      const T gm = make_float2(r.x / e, r.y / e);
+      for (int e2 = lane; e2 < L; e2 += 32) {
+        const T hv = h[e2];
+        T mv = Ms[s + e2];
+        mv.x = fmaf(gm.x, hv.x, mv.x); mv.x = fmaf(-gm.y, hv.y, mv.x);
+        mv.y = fmaf(gm.x, hv.y, mv.y); mv.y = fmaf(gm.y, hv.x, mv.y);
+        Ms[s + e2] = mv;
+      }
+      if (lane == 0) {
+        Qs[i] = make_float2(q.x + gm.x, q.y + gm.y);
+        if (p.O.rows && it < p.O.rows_cap) p.O.rows[rid * p.O.rows_cap + it] = i;
+      }
+      flops += 2 * (8LL * Nt + 4);
+      __syncwarp();
+    }
+  }
+  // ---- outputs
+  if (active) {
+    const size_t rid = (size_t)b * K + c;
+    T* vout = (T*)p.O.v;
+    for (int i = lane; i < K; i += 32) vout[((size_t)b * K + i) * K + c] = Qs[i];
+    if (p.O.iterates) {
+      T* M = (T*)p.O.iterates + rid * Nt;
+      for (int n = lane; n < Nt; n += 32) M[n] = Ms[n];
+    }
+    if (lane == 0) {
+      if (p.O.iters) p.O.iters[rid] = it;
+      if (p.O.converged) p.O.converged[rid] = 0;
+      if (p.O.done) p.O.done[rid] = 0;
+      if (p.O.noop_steps) p.O.noop_steps[rid] = 0;
+      if (p.O.flops) p.O.flops[rid] = flops;
+    }
+  }
+  if (tid == 0) p.tstop[blockIdx.x] = p.T;
+}
+
+// 1 launched, 0 not eligible, -1 failure
+inline int rkwarp_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
+                           int32_t* tstop, int maxsm, cudaStream_t s) {
+  if (scheme != KZ_URK && scheme != KZ_SWOR_ERK) return 0;
+  if (P.dtype != KZ_C64 || !(P.flags & KZ_PROBLEM_CONTIGUOUS)) return 0;
+  static const bool off = getenv("KZ_DISABLE_RKWARP") != nullptr;  // A/B switch
+  if (off) return 0;
+  const int K = P.n_users, Nt = P.n_antennas;
+  const int hcap = K * P.max_support;
+  int nw = K < 32 ? K : 32;
+  size_t smem = 0;
+  for (; nw >= 1; nw = nw > 8 ? nw - 8 : nw - 1) {
+    smem = rkw::plan(K, Nt, nw, hcap).total;
+    if (smem <= (size_t)maxsm) break;
+  }
+  if (nw < 1) return 0;
+  LsArgs a;
+  a.P = P;
+  a.R = R;
+  a.O = O;
+  a.T = T_iters;
+  a.S = 0;
+  a.hcap = hcap;
+  a.ws = ws;
+  a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
+  a.tstop = tstop;
+  const int groups = (K + nw - 1) / nw;
+  auto kern = scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK> : kz_rkwarp_kernel<KZ_SWOR_ERK>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  kern<<<P.n_systems * groups, 32 * nw, smem, s>>>(a, nw);
+  kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
+                                                                  O.sys_converged);
+  return 1;
+}
+
+}  // namespace kz

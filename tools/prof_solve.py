@@ -21,7 +21,8 @@ ap.add_argument("--batch", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
-ch = kz.generate(a.config, range(a.batch))
+cfg = kz.CONFIGS[a.config]
+ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
 dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
 rng = ("philox", 7) if a.scheme in kz.STOCHASTIC_SCHEMES else None
 for r in range(a.reps):
