@@ -182,9 +182,15 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
   return cuda_check("kz_rzf");
 }
 
+// Gram-form epilogue for large K (contiguous VRs, F not requested): G0 and G0 V per system
+static bool epilogue_gram_path(const kz_problem* prob) {
+  return (prob->flags & KZ_PROBLEM_CONTIGUOUS) && prob->n_users >= 96 && getenv("KZ_EPILOGUE_ANTENNA") == nullptr;
+}
+
 size_t kz_epilogue_workspace_bytes(const kz_problem* prob) {
   if (!prob) return 0;
-  size_t gram = (size_t)prob->n_systems * prob->n_users * prob->n_users * sizeof(double2);
+  size_t gram = (size_t)prob->n_systems * prob->n_users * prob->n_users * sizeof(double2) *
+                (epilogue_gram_path(prob) ? 2 : 1);
   size_t fbuf = (size_t)prob->n_systems * prob->n_antennas * prob->n_users * (prob->dtype == KZ_C128 ? 16 : 8);
   return kz_align(gram > fbuf ? gram : fbuf);
 }
@@ -198,10 +204,29 @@ int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double
   if (!v) return fail(KZ_ERR_INVALID, "v must be non-null");
   if (v_ref && !beta_ref) return fail(KZ_ERR_INVALID, "v_ref needs beta_ref");
   if (prob->n_systems == 0) return KZ_OK;
-  size_t need = snr_linear ? kz_epilogue_workspace_bytes(prob) : 0;
+  const bool gram_path = epilogue_gram_path(prob) && !f_out;
+  size_t need = (snr_linear || gram_path) ? kz_epilogue_workspace_bytes(prob) : 0;
   if (need && (!workspace || workspace_bytes < need))
     return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
   cudaStream_t s = (cudaStream_t)stream;
+  if (gram_path) {
+    const size_t smem = epilogue_gram_smem();
+    if (prob->dtype == KZ_C128) {
+      cudaFuncSetAttribute(kz_epilogue_gram_kernel<double2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      kz_epilogue_gram_kernel<double2, double2><<<prob->n_systems, EPG_THREADS, smem, s>>>(
+          *prob, (const double2*)v, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out, sum_rate_out,
+          (double2*)workspace);
+    } else {
+      cudaFuncSetAttribute(kz_epilogue_gram_kernel<float2, float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      kz_epilogue_gram_kernel<float2, float2><<<prob->n_systems, EPG_THREADS, smem, s>>>(
+          *prob, (const float2*)v, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out, sum_rate_out,
+          (double2*)workspace);
+    }
+    g_launches = 1;
+    return cuda_check("kz_epilogue(gram)");
+  }
   if (prob->flags & KZ_PROBLEM_CONTIGUOUS) {
     size_t smem = epilogue_contig_smem(prob->n_users);
     if (prob->dtype == KZ_C128)

@@ -661,4 +661,163 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_contig_kernel(
 
 inline size_t epilogue_contig_smem(int K) { return (size_t)4 * K * 4 + 8 + (size_t)8 * K + 64; }
 
+// ---------------------------------------------------------------- K3 for large K: Gram form
+// For K >= 96 the per-antenna assembly costs Nt K |coverage| MACs per pass; with G0 = H^H H (no ridge) every
+// epilogue quantity is a quadratic form in G0 instead (H is zero off the VRs, so these are exact identities):
+//   ||H V||_F^2 = Re tr(V^H G0 V)                        -> beta          (assembly.py:51-56)
+//   ||beta_ref H V_ref - beta H V||_F^2 = Re tr(D^H G0 D), D = beta_ref V_ref - beta V (formed in fp64,
+//                                          a direct quadratic form: no cancellation)   (metrics.py:44-51)
+//   H^H F = beta G0 V                                     -> Eq. (7) rates (metrics.py:54-78)
+// G0 is built like the RZF Gram (warp per row pair, fixed order), the K x K x K products run as a shared-memory
+// tiled fp64 GEMM (64 x 128 output blocks, 4 x 4 register tiles, k panels of 16).  F is not formed.
+constexpr int EPG_THREADS = 512;
+constexpr int EPG_BM = 64, EPG_BN = 128, EPG_BK = 16;
+inline size_t epilogue_gram_smem() { return (size_t)(EPG_BM * EPG_BK + EPG_BK * EPG_BN) * sizeof(double2); }
+
+template <class TH, class TV>
+__global__ void __launch_bounds__(EPG_THREADS, 1) kz_epilogue_gram_kernel(
+    kz_problem P, const TV* v, const double* v_ref, const double* beta_ref, const double* snr_linear,
+    double* beta_out, double* nmse_out, double* rates_out, double* sum_rate_out, double2* ws) {
+  extern __shared__ __align__(16) unsigned char epg_sm[];
+  double2* Ap = (double2*)epg_sm;     // [BM][BK]
+  double2* Bp = Ap + EPG_BM * EPG_BK;  // [BK][BN]
+  __shared__ double red[32];
+  const int b = blockIdx.x, K = P.n_users;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, nw = nthr >> 5;
+  RowView R{P.row_seg_ptr, P.seg_start, P.seg_len, P.row_val_ptr};
+  double2* G0 = ws + (size_t)b * 2 * K * K;
+  double2* W1 = G0 + (size_t)K * K;
+  const TV* V = v + (size_t)b * K * K;
+  const double2* Vr = v_ref ? (const double2*)v_ref + (size_t)b * K * K : nullptr;
+
+  // G0 = H^H H, both triangles (one warp per pair, lanes over the overlap)
+  {
+    const TH* hv = (const TH*)P.heff;
+    const int npair = K * (K + 1) / 2;
+    for (int e = tid >> 5; e < npair; e += nw) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      const int j = e - i * (i + 1) / 2;
+      const size_t ri = (size_t)b * K + i, rj = (size_t)b * K + j;
+      const int si = P.seg_start[P.row_seg_ptr[ri]], li = P.seg_len[P.row_seg_ptr[ri]];
+      const int sj = P.seg_start[P.row_seg_ptr[rj]], lj = P.seg_len[P.row_seg_ptr[rj]];
+      const int lo = max(si, sj), hi = min(si + li, sj + lj);
+      double re = 0.0, im = 0.0;
+      if (lo < hi) {
+        const TH* hi_p = hv + R.val_ptr[ri] - si;
+        const TH* hj_p = hv + R.val_ptr[rj] - sj;
+        for (int n = lo + lane; n < hi; n += 32) {
+          const double2 x = to_d2(hi_p[n]), y = to_d2(hj_p[n]);
+          re = fma(x.x, y.x, re); re = fma(x.y, y.y, re);
+          im = fma(x.x, y.y, im); im = fma(-x.y, y.x, im);
+        }
+        re = warp_sum(re);
+        im = warp_sum(im);
+      }
+      if (lane == 0) {
+        G0[(size_t)i * K + j] = make_double2(re, im);
+        if (i != j) G0[(size_t)j * K + i] = make_double2(re, -im);
+      }
+    }
+  }
+  __syncthreads();
+
+  // C = G0 X (X given element-wise by xval(j, c)); per output: either stored (W1) or folded into
+  // sum_{i,c} Re(conj(X[i][c]) C[i][c]) (returned, block-reduced)
+  const int tr = tid / 32, tc = tid % 32;  // 16 x 32 grid of 4 x 4 tiles per 64 x 128 block
+  auto gemm = [&](auto xval, double2* out) -> double {
+    double quad = 0.0;
+    for (int i0 = 0; i0 < K; i0 += EPG_BM)
+      for (int c0 = 0; c0 < K; c0 += EPG_BN) {
+        double2 acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[r][q] = make_double2(0.0, 0.0);
+        for (int k0 = 0; k0 < K; k0 += EPG_BK) {
+          for (int e = tid; e < EPG_BM * EPG_BK; e += nthr) {
+            const int r = e / EPG_BK, k = e % EPG_BK;
+            Ap[e] = (i0 + r < K && k0 + k < K) ? G0[(size_t)(i0 + r) * K + k0 + k] : make_double2(0.0, 0.0);
+          }
+          for (int e = tid; e < EPG_BK * EPG_BN; e += nthr) {
+            const int k = e / EPG_BN, cc = e % EPG_BN;
+            Bp[e] = (k0 + k < K && c0 + cc < K) ? xval(k0 + k, c0 + cc) : make_double2(0.0, 0.0);
+          }
+          __syncthreads();
+#pragma unroll 4
+          for (int k = 0; k < EPG_BK; ++k) {
+            double2 av[4], bv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              av[r] = Ap[(tr * 4 + r) * EPG_BK + k];
+              bv[r] = Bp[k * EPG_BN + tc + 32 * r];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[r][q] = zfma(av[r], bv[q], acc[r][q]);
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + tr * 4 + r, c = c0 + tc + 32 * q;
+            if (i < K && c < K) {
+              if (out) out[(size_t)i * K + c] = acc[r][q];
+              const double2 x = xval(i, c);
+              quad = fma(x.x, acc[r][q].x, fma(x.y, acc[r][q].y, quad));
+            }
+          }
+      }
+    return block_reduce_sum(quad, red);
+  };
+
+  // beta from tr(V^H G0 V), W1 = G0 V kept for the rates
+  const double s1 = gemm([&](int j, int c) { return to_d2(V[(size_t)j * K + c]); }, W1);
+  const double beta = 1.0 / sqrt(s1);
+  if (beta_out && tid == 0) beta_out[b] = beta;
+  if (Vr && nmse_out) {
+    const double br = beta_ref[b];
+    const double num = gemm(
+        [&](int j, int c) {
+          const double2 x = to_d2(V[(size_t)j * K + c]), y = Vr[(size_t)j * K + c];
+          return make_double2(br * y.x - beta * x.x, br * y.y - beta * x.y);
+        },
+        nullptr);
+    const double ref = gemm(
+        [&](int j, int c) {
+          const double2 y = Vr[(size_t)j * K + c];
+          return make_double2(br * y.x, br * y.y);
+        },
+        nullptr);
+    if (tid == 0) nmse_out[b] = sqrt(fmax(num, 0.0)) / sqrt(ref);
+  }
+  if (!snr_linear) return;
+  __syncthreads();
+  // rates: cross = H^H F = beta W1 (metrics.py:74-77)
+  const double noise = 1.0 / snr_linear[b];
+  double rsum = 0.0;
+  for (int k = tid >> 5; k < K; k += nw) {
+    double sig = 0.0, tot = 0.0;
+    for (int c = lane; c < K; c += 32) {
+      const double2 x = W1[(size_t)k * K + c];
+      const double pw = np_abs2(beta * x.x, beta * x.y);
+      if (c == k) sig = pw;
+      tot += pw;
+    }
+    tot = warp_sum(tot);
+    sig = warp_sum(sig);
+    if (lane == 0) {
+      const double rate = log2(1.0 + sig / ((tot - sig) + noise));
+      if (rates_out) rates_out[(size_t)b * K + k] = rate;
+      rsum += rate;
+    }
+  }
+  rsum = block_reduce_sum(rsum, red);
+  if (sum_rate_out && tid == 0) sum_rate_out[b] = rsum;
+}
+
 }  // namespace kz
