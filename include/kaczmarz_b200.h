@@ -93,8 +93,10 @@ typedef struct kz_problem {
   /* shape hints, set by the packer (trusted): enable the register-resident fast path */
   int32_t max_support;          /* max_r |Gamma_r| */
   int32_t flags;                /* KZ_PROBLEM_CONTIGUOUS: every row is exactly one segment */
-  /* max over systems of the (row, 32-antenna chunk) pairs inside one aligned 128- / 256-antenna slice
-     (contiguous supports; 0 = unknown): sizes the shared-memory layout of the cluster path for large arrays */
+  /* max over systems and CTAs of the (row, 32-antenna chunk) pairs one CTA of the large-array cluster path
+     holds, for 128- / 256-antenna CTAs in its block-interleaved layout (CL = ceil(Nt / width) CTAs; with
+     CL > 1 CTA c owns two blocks of width/2 antennas, block j starting at antenna (j*CL + c) * width/2);
+     contiguous supports only, 0 = unknown (cluster path disabled) */
   int32_t slice_pairs_128;
   int32_t slice_pairs_256;
 } kz_problem;

@@ -179,23 +179,30 @@ class HostBatch:
         return np.diff(self.row_val_ptr).reshape(self.n_systems, self.n_users)
 
     def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024) -> int:
-        """Max over systems and aligned `width`-antenna slices of the (row, `chunk`-antenna chunk)
-        pairs inside the slice (contiguous supports): the shared-memory layout bound of the
-        cluster kernel (kz_problem.slice_pairs_*)."""
+        """Max over systems and CTAs of the (row, `chunk`-antenna chunk) pairs a CTA of the cluster kernel
+        holds, for CTAs of `width` antennas in the block-interleaved layout of csrc/kz_solve_cluster.cuh
+        (CL = ceil(Nt / width) CTAs; with CL > 1 each CTA owns two blocks of width/2 antennas, block j of
+        CTA c at chunk (j CL + c) * (width/2) / chunk).  Contiguous supports only; this is the shared-memory
+        layout bound kz_problem.slice_pairs_* (the kernel traps if it is exceeded)."""
         if not self.contiguous or self.n_systems == 0:
             return 0
-        per = width // chunk
-        nsl = -(-self.n_antennas // width)
+        w = width // chunk
+        nch = self.n_antennas // chunk
+        ncl = -(-nch // w)
+        nblk = 2 if ncl > 1 else 1
+        bc = w // nblk
+        # chunk ranges [lo, hi) of block j of CTA c
+        lo = np.array([[(j * ncl + c) * bc for j in range(nblk)] for c in range(ncl)], dtype=np.int64)
+        hi = np.minimum(lo + bc, nch)
         seg = self.row_seg_ptr[:-1]
         c0 = (self.seg_start[seg] // chunk).astype(np.int64).reshape(self.n_systems, self.n_users)
         c1 = ((self.seg_start[seg] + self.seg_len[seg] - 1) // chunk).astype(np.int64).reshape(self.n_systems,
                                                                                                  self.n_users)
-        lo = (np.arange(nsl) * per)[None, None, :]
         best = 0
         for s in range(0, self.n_systems, block):
-            a, b = c0[s:s + block, :, None], c1[s:s + block, :, None]
-            n = np.clip(np.minimum(b, lo + per - 1) - np.maximum(a, lo) + 1, 0, None).sum(axis=1)
-            best = max(best, int(n.max()))
+            a, b = c0[s:s + block, :, None, None], c1[s:s + block, :, None, None]
+            n = np.clip(np.minimum(b + 1, hi[None, None]) - np.maximum(a, lo[None, None]), 0, None)
+            best = max(best, int(n.sum(axis=(1, 3)).max()))
         return best
 
     def to_device(self, dtype: str = "c128", device=None) -> "DeviceBatch":

@@ -29,6 +29,13 @@
 #include "kz_common.cuh"
 #include "kz_solve_generic.cuh"
 
+// timing build: close a phase before each cluster barrier so the barrier wait is its own phase
+#ifdef KZ_TIMING
+#define KZ_CLU_SPLIT() do { __syncthreads(); KZ_PHASE(); } while (0)
+#else
+#define KZ_CLU_SPLIT() do {} while (0)
+#endif
+
 namespace kz {
 
 namespace clu {
@@ -85,7 +92,7 @@ __device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
 struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
   size_t rowS, rowL, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, P, Qo,
-      Ro, Fo, IN, Phl, dloc, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
+      Ro, Fo, IN, Phl, dloc, dlst, dcnt, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
       misc, total;
 };
 
@@ -129,6 +136,8 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.IN = o; o = al(o + 8 * (size_t)p.KO * NS * G);
   p.Phl = p.P;  // phi / gamma of local rows reuse P (disjoint phases; nlcap <= pcap)
   p.dloc = o; o = al(o + 4 * (size_t)p.KO * NS);
+  p.dlst = o; o = al(o + 4 * (size_t)p.KO * NS);
+  p.dcnt = o; o = al(o + 4 * (size_t)p.KO);
   p.AG4 = o; o = al(o + 16 * (size_t)CL * G);
   p.GAMv = o; o = al(o + 8 * G);
   p.stepv = o; o = al(o + 4 * G);
@@ -164,7 +173,8 @@ struct CluArgs {
   int cap;      // T (lockstep) or the per-rhs iteration cap
   int every;    // check_every
   float eps;    // residual tolerance
-  int NS;       // max slices a row spans
+  int NS;       // inbox slots per row (= CL: any CTA may hold a piece of a row)
+  int nblk;     // chunk blocks per CTA (block-interleaved slices)
   int pcap;     // (row, chunk) pairs reserved per CTA
   int32_t* tstop;
 };
@@ -186,7 +196,12 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   const int W = nthr >> 5;
   const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap);
   const int KO = pl.KO, NS = pl.NS, KW = (K + 31) / 32;
-  const int cW = c * W;
+  // block-interleaved slices: CTA c owns nblk blocks of Bc = W / nblk chunks, block j at chunk
+  // (j CL + c) Bc, so every CTA samples the whole array and the VR-coverage ramps at the array edges no
+  // longer leave some CTAs with a fraction of the others' rows (the cluster barriers wait for the max)
+  const int nblk = p.nblk, Bc = W / nblk;
+  auto chunk_of = [&](int ww) { return ((ww / Bc) * CL + c) * Bc + (ww % Bc); };
+  const int nch = Nt / CH;
   const int o_lo = c * KO, nown = max(0, min(K, o_lo + KO) - o_lo);
   const bool residual = p.mode == KZ_STOP_RESIDUAL;
 
@@ -215,7 +230,9 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   T* Fo = (T*)(sm + pl.Fo);  // owned phi (aggregation weights) or gamma (orthogonal block)
   T* INs = (T*)(sm + pl.IN);
   T* Phl = (T*)(sm + pl.Phl);  // phi / gamma of the local rows, pulled from their owners
-  int* dloc = (int*)(sm + pl.dloc);  // [owned row][slice slot] -> local row index in that CTA
+  int* dloc = (int*)(sm + pl.dloc);  // [owned row][CTA] -> local row index of the row in that CTA (-1: none)
+  int* dlst = (int*)(sm + pl.dlst);  // [owned row][k] -> k-th CTA holding pieces of the row (ascending)
+  int* dcnt = (int*)(sm + pl.dcnt);
   float4* AG4 = (float4*)(sm + pl.AG4);
   T* GAMv = (T*)(sm + pl.GAMv);
   int* stepv = (int*)(sm + pl.stepv);
@@ -264,14 +281,18 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     int n = 0, hcar = 0;
     for (int base = 0; base < K; base += 32) {
       const int i = base + lane;
-      const bool ov = i < K && c0[i] <= cW + W - 1 && c1[i] >= cW;
+      int l0 = W, l1 = -1;  // local warps whose chunks lie in [c0_i, c1_i] (contiguous: chunk_of is increasing)
+      if (i < K)
+        for (int ww = 0; ww < W; ++ww) {
+          const int ch = chunk_of(ww);
+          if (ch >= c0[i] && ch <= c1[i] && ch < nch) {
+            l0 = min(l0, ww);
+            l1 = ww;
+          }
+        }
+      const bool ov = l0 <= l1;
       const unsigned bal = __ballot_sync(FULL, ov);
-      int l0 = 0, l1 = 0, np = 0;
-      if (ov) {
-        l0 = max(c0[i], cW) - cW;
-        l1 = min(c1[i], cW + W - 1) - cW;
-        np = l1 - l0 + 1;
-      }
+      const int np = ov ? l1 - l0 + 1 : 0;
       int sc = np;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -304,7 +325,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       if (lh[mid] <= e) lo = mid; else hi = mid - 1;
     }
     const int i = lrow[lo];
-    const int ant = (cW + (lcc[lo] & 0xFF)) * CH + (e - lh[lo]);
+    const int ant = chunk_of((lcc[lo] & 0xFF) + (e - lh[lo]) / CH) * CH + (e - lh[lo]) % CH;
     const int s = rowS[i];
     Hs[e] = (ant >= s && ant < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (ant - s)]
                                              : make_float2(0.f, 0.f);
@@ -394,11 +415,17 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
   cluster_sync();  // every CTA of the cluster is resident and initialised before any DSMEM traffic
-  if (AGG)
-    for (int e = tid; e < nown * NS; e += nthr) {
-      const int il = e / NS, s = e % NS, i = o_lo + il, s0 = c0[i] / W;
-      if (s <= c1[i] / W - s0) dloc[e] = s0 + s == c ? loc[i] : ld_remote(loc + i, s0 + s);
-    }
+  for (int e = tid; e < nown * NS; e += nthr) {  // owner: where each CTA keeps its piece of an owned row
+    const int il = e / NS, d = e % NS, i = o_lo + il;
+    dloc[e] = d == c ? loc[i] : ld_remote(loc + i, d);
+  }
+  __syncthreads();
+  for (int il = tid; il < nown; il += nthr) {
+    int n = 0;
+    for (int d = 0; d < NS; ++d)
+      if (dloc[il * NS + d] >= 0) dlst[il * NS + n++] = d;
+    dcnt[il] = n;
+  }
   __syncthreads();
   KZ_PHASE();
 
@@ -482,7 +509,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         dy += v.y;
       }
       const int o = i / KO, il = i - o * KO;
-      T* dst = INs + (size_t)(il * NS + (c - c0[i] / W)) * G + (gg ^ (il & 15));
+      T* dst = INs + (size_t)(il * NS + c) * G + (gg ^ (il & 15));
       if (o == c) *dst = make_float2(dx, dy);
       else st_remote(dst, o, make_float2(dx, dy));
     }
@@ -490,11 +517,12 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   // owner: residual of owned row il for rhs gg from the slice sums (fixed slice order)
   auto oresid = [&](int il, int gg, bool dense) -> T {
     const int i = o_lo + il;
-    const int ns = c1[i] / W - c0[i] / W;
     const T* pp = INs + (size_t)il * NS * G + (gg ^ (il & 15));
+    const int* dl = dlst + il * NS;
+    const int nd = dcnt[il];
     float dx = 0.f, dy = 0.f;
-    for (int s = 0; s <= ns; ++s) {
-      const T v = pp[s * G];
+    for (int k = 0; k < nd; ++k) {  // the CTAs holding pieces of row i, ascending (fixed order)
+      const T v = pp[dl[k] * G];
       dx += v.x;
       dy += v.y;
     }
@@ -508,10 +536,10 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
   };
   auto push_phi = [&](int il, int gg, T v) {
-    const int i = o_lo + il, s0 = c0[i] / W, ns = c1[i] / W - s0;
-    for (int s = 0; s <= ns; ++s) {
-      const int d = s0 + s;
-      T* dst = Phl + dloc[il * NS + s] * G + gg;
+    const int nd = dcnt[il];
+    for (int k = 0; k < nd; ++k) {
+      const int d = dlst[il * NS + k];
+      T* dst = Phl + dloc[il * NS + d] * G + gg;
       if (d == c) *dst = v; else st_remote(dst, d, v);
     }
   };
@@ -611,6 +639,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       __syncthreads();
       KZ_PHASE();
       push(0);
+      KZ_CLU_SPLIT();
       cluster_sync();
       KZ_PHASE();
       // owner: residuals of its rows, block sums (grk / vr-ogrk) or block argmax (gk); half-warp per rhs
@@ -667,6 +696,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
           if (d == c) *fs = SCH == KZ_VR_OGRK ? fresh : ws; else st_remote(fs, d, SCH == KZ_VR_OGRK ? fresh : ws);
         }
       }
+      KZ_CLU_SPLIT();
       cluster_sync();
       KZ_PHASE();
       // selection: the same block-level decision in every CTA, the owner of the chosen row does the step.
@@ -777,6 +807,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
           }
         }
       }
+      KZ_CLU_SPLIT();
       cluster_sync();
       KZ_PHASE();
       // bookkeeping of the steps (every CTA keeps the same per-rhs counters)
@@ -1041,7 +1072,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   if (p.O.iterates) {
     auto store_m = [&](const T (&mr)[8], int r) {
-      const int cc = g0 + g + 8 * r, chunk = cW + w;
+      const int cc = g0 + g + 8 * r, chunk = chunk_of(w);
       if (cc >= K || chunk >= Nt / CH) return;
       T* M = (T*)p.O.iterates + ((size_t)b * K + cc) * Nt + chunk * CH;
 #pragma unroll
@@ -1073,8 +1104,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
 inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int* CL, int* NS, int* pcap) {
   const int nch = P.n_antennas / clu::CH;
   *CL = (nch + W - 1) / W;
-  const int SW = W * clu::CH;
-  *NS = (P.max_support + SW - 2) / SW + 1;
+  *NS = *CL;
   *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
   if (*pcap <= 0) return ~size_t(0);
   return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap).total;
@@ -1174,6 +1204,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.every = S.check_every;
   a.eps = (float)S.epsilon;
   a.NS = W == 4 ? NS4 : NS8;
+  a.nblk = CL > 1 ? 2 : 1;  // must match the layout hint (HostBatch.slice_pairs)
   a.pcap = W == 4 ? pc4 : pc8;
   a.tstop = (int32_t*)(ws + L.total);
   int rc = 0;
