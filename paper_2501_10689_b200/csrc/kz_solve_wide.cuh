@@ -36,7 +36,7 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 
 struct Plan {
   int K, W, SL, hcap;
-  size_t rowS, rowL, c0, c1, hoff, en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
+  size_t rowS, rowL, c0, c1, hoff, en, inv_en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
       gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, total;
 };
 
@@ -56,6 +56,7 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.c1 = o; o = al(o + 4 * K);
   p.hoff = o; o = al(o + 4 * K);
   p.en = o; o = al(o + 4 * K);
+  p.inv_en = o; o = al(o + 4 * K);
   p.cost = o; o = al(o + 8 * K);
   p.cmask = o; o = al(o + 4 * (size_t)K * KW);
   p.inset = o; o = al(o + K);
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   int* c1 = (int*)(sm + pl.c1);
   int* hoff = (int*)(sm + pl.hoff);  // element index of antenna CH*c0 of row i
   float* en = (float*)(sm + pl.en);
+  float* inv_en = (float*)(sm + pl.inv_en);  // 1 / e_i (aggregation weights phi = r / e)
   long long* cost = (long long*)(sm + pl.cost);
   uint32_t* cmask = (uint32_t*)(sm + pl.cmask);
   int* lptr = (int*)(sm + pl.lptr);
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     c0[i] = s / CH;
     c1[i] = (s + L - 1) / CH;
     en[i] = (float)p.P.row_energy[r];
+    inv_en[i] = (float)(1.0 / p.P.row_energy[r]);
   }
   __syncthreads();
   // padded row offsets (prefix over rows) by warp 0
@@ -604,32 +607,41 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       };
       // residuals -> weights phi = r/e, num = vdot(phi, r), ||phi||^2 (warp per rhs; solvers.py:248-254, 274)
       auto weights = [&](int which, int nrows) {
-        for (int gg = w; gg < G; gg += W) {
-          if (g0 + gg >= K || donev[gg]) {
-            if (lane == 0) nzv[gg] = 0;
-            continue;
-          }
+        const int hf = lane >> 4, hl = lane & 15;  // one half-warp per rhs, lanes over rows
+        const unsigned hmask = 0xFFFFu << (16 * hf);
+        for (int pair = w; pair < G / 2; pair += W) {
+          const int gg = pair + hf * (G / 2);
+          const bool act = g0 + gg < K && !donev[gg];
           float nx = 0.f, ny = 0.f, sp = 0.f;
           bool nz = false;
-          for (int i = lane; i < K; i += 32) {
-            if (which && inset[i] != which) continue;
-            T r = resid(i, gg);
-            T ph = make_float2(r.x / en[i], r.y / en[i]);
-            Phi[xs(i, gg)] = ph;
-            nz |= (ph.x != 0.f || ph.y != 0.f);
-            nx = fmaf(ph.x, r.x, nx); nx = fmaf(ph.y, r.y, nx);
-            ny = fmaf(ph.x, r.y, ny); ny = fmaf(-ph.y, r.x, ny);
-            sp = fmaf(ph.x, ph.x, sp); sp = fmaf(ph.y, ph.y, sp);
+          if (act)
+            for (int i = hl; i < K; i += 16) {
+              if (which && inset[i] != which) continue;
+              const T r = resid(i, gg);
+              const float ie = inv_en[i];
+              const T ph = make_float2(r.x * ie, r.y * ie);
+              Phi[xs(i, gg)] = ph;
+              nz |= (ph.x != 0.f || ph.y != 0.f);
+              nx = fmaf(ph.x, r.x, nx); nx = fmaf(ph.y, r.y, nx);
+              ny = fmaf(ph.x, r.y, ny); ny = fmaf(-ph.y, r.x, ny);
+              sp = fmaf(ph.x, ph.x, sp); sp = fmaf(ph.y, ph.y, sp);
+            }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            nx += __shfl_xor_sync(FULL, nx, o);
+            ny += __shfl_xor_sync(FULL, ny, o);
+            sp += __shfl_xor_sync(FULL, sp, o);
           }
-          nx = warp_sum(nx);
-          ny = warp_sum(ny);
-          sp = warp_sum(sp);
-          nz = __any_sync(FULL, nz);
-          if (lane == 0) {
-            numv[gg] = make_float2(nx, ny);
-            spv[gg] = sp;
-            nzv[gg] = (nz && nrows > 0) ? 1 : 0;
-            flv[gg] += 2LL * nrows;
+          const bool anz = (__ballot_sync(FULL, nz) & hmask) != 0;
+          if (hl == 0) {
+            if (act) {
+              numv[gg] = make_float2(nx, ny);
+              spv[gg] = sp;
+              nzv[gg] = (anz && nrows > 0) ? 1 : 0;
+              flv[gg] += 2LL * nrows;
+            } else {
+              nzv[gg] = 0;
+            }
           }
         }
       };
