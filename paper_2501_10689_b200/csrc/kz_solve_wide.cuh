@@ -691,19 +691,32 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           s0 = fmaf(m0[k].x, m0[k].x, fmaf(m0[k].y, m0[k].y, s0));
           s1 = fmaf(m1[k].x, m1[k].x, fmaf(m1[k].y, m1[k].y, s1));
         }
-        {
+        {  // ||y||^2 partial of this warp, stored [rhs][warp] so a rhs' partials are one contiguous run
           const float sd = a ? s0 : s1;
           const float rv = __shfl_xor_sync(FULL, sd, 16);
-          Dp[w * G + g + 16 * a] = (a ? s1 : s0) + rv;
+          Dp[(g + 16 * a) * W + w] = (a ? s1 : s0) + rv;
         }
         __syncthreads();
         KZ_PHASE();
-        // step lengths of this thread's two rhs (fixed-order sums => identical in every thread)
+        tmem::wait_st();
+        float f0[16], f1[16];
+        tmem::ld16(my_tmem, f0);  // the parked iterate streams in while the step lengths are formed
+        tmem::ld16(my_tmem + 16, f1);
+        // step lengths of this thread's two rhs (fixed-order pairwise sums => identical in every thread)
         auto gamma_of = [&](int rr, bool& step) -> T {
           step = false;
           if (!nzv[rr]) return make_float2(0.f, 0.f);
-          float den = 0.f;
-          for (int ww = 0; ww < W; ++ww) den += Dp[ww * G + rr];
+          const float* dp = Dp + rr * W;
+          float den;
+          if (W == 16) {
+            const float4* d4 = reinterpret_cast<const float4*>(dp);
+            const float4 u0 = d4[0], u1 = d4[1], u2 = d4[2], u3 = d4[3];
+            den = ((u0.x + u0.y) + (u0.z + u0.w) + ((u1.x + u1.y) + (u1.z + u1.w))) +
+                  ((u2.x + u2.y) + (u2.z + u2.w) + ((u3.x + u3.y) + (u3.z + u3.w)));
+          } else {
+            den = 0.f;
+            for (int ww = 0; ww < W; ++ww) den += dp[ww];
+          }
           den = fmaf(regf, spv[rr], den);
           if (den == 0.f) return make_float2(0.f, 0.f);
           step = true;
@@ -712,11 +725,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         };
         bool st0, st1;
         const T gm0 = gamma_of(g, st0), gm1 = gamma_of(g + 16, st1);
-        tmem::wait_st();
         {
-          float f0[16], f1[16];
-          tmem::ld16(my_tmem, f0);
-          tmem::ld16(my_tmem + 16, f1);
           tmem::wait_ld();
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -735,9 +744,9 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           }
         }
         // q += gamma phi over the aggregated rows (threads over (row, rhs))
-        {  // rhs of entry e is e % G == lane (nthr is a multiple of 32): one step length per thread
-          bool stq;
-          const T gq = gamma_of(lane, stq);
+        {  // rhs of entry e is e % G == lane = g + 16 a (nthr is a multiple of 32): this thread's own step
+          const bool stq = a ? st1 : st0;
+          const T gq = a ? gm1 : gm0;
           if (stq && g0 + lane < K)
             for (int e = tid; e < K * G; e += nthr) {
               const int i = e / G;
@@ -747,8 +756,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         }
         // bookkeeping once per rhs (warp 0: lane = rhs slot)
         if (w == 0 && g0 + lane < K && !donev[lane]) {
-          bool st;
-          (void)gamma_of(lane, st);
+          const bool st = a ? st1 : st0;
           const int n = nrows;
           if (!nzv[lane]) {
             noopv[lane] += 1;
