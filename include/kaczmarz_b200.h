@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 2
+#define KZ_ABI_VERSION 3
 
 /* status codes */
 #define KZ_OK 0
@@ -181,6 +181,39 @@ size_t kz_epilogue_workspace_bytes(const kz_problem* prob);
 int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double* v_ref, const double* beta_ref,
                 const double* snr_linear, double* beta_out, double* nmse_out, double* rates_out,
                 double* sum_rate_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * On-device input preparation for contiguous-VR near-field drops: a batch of B
+ * systems described by their user drop; the packed layout of kz_problem is built on the device.
+ */
+typedef struct kz_drop {
+  int32_t n_systems;          /* B */
+  int32_t n_users;            /* K */
+  int32_t n_antennas;         /* Nt (ULA, element n at x_n = (n - (Nt-1)/2) * element_spacing) */
+  int32_t dtype;              /* kz_dtype of heff */
+  double element_spacing;     /* metres (lambda_carrier / 2 in the BASELINE configs) */
+  const double* wavelength;   /* [B] wavelength of each system (per subcarrier for wideband OFDM) */
+  const double* r0;           /* [B*K] user distance to the array centre (m) */
+  const double* theta;        /* [B*K] user angle from broadside (rad) */
+  const int32_t* vr_start;    /* [B*K] first visible antenna */
+  const int32_t* vr_len;      /* [B*K] visible antennas (>= 1) */
+  const double* reg;          /* [B] ridge weight xi */
+} kz_drop;
+
+/* heff rows lambda/(4 pi r_n) exp(-j 2 pi r_n / lambda) on [vr_start, vr_start + vr_len), unit-norm per user,
+   at heff + row_val_ptr[b*K+i] (caller-computed exclusive prefix of vr_len, [B*K+1]); row_energy [B*K] =
+   ||h_bi||^2 + reg_b.  Replaces host channel generation + packing (channel.py, solvers.py:80-92). */
+int kz_channel_synth(const kz_drop* drop, const int64_t* row_val_ptr, void* heff, double* row_energy, void* stream);
+
+/* VR partition on the device (vrgraph.py:31-114).  Pass 1 counts: coupled_cnt [B*K] = |X_bi|,
+   orth_cnt [B] = |O_b|, non_union_size [B], inset [B*K] (1 = O, 2 = N).  The caller forms the exclusive
+   prefixes coupled_ptr [B*K+1], orth_ptr [B+1], non_ptr [B+1] (N_b has K - |O_b| rows); pass 2 fills
+   coupled_idx, orth_idx, non_idx in ascending order. */
+int kz_partition_counts(const kz_drop* drop, int32_t* coupled_cnt, int32_t* orth_cnt, int32_t* non_union_size,
+                        uint8_t* inset, void* stream);
+int kz_partition_fill(const kz_drop* drop, const int32_t* coupled_ptr, const int32_t* orth_ptr,
+                      const int32_t* non_ptr, int32_t* coupled_idx, int32_t* orth_idx, int32_t* non_idx,
+                      void* stream);
 
 /* Number of kernels the last kz_* call on this thread launched (benchmark
    bookkeeping for the gpu_launches count). */

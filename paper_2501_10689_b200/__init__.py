@@ -10,7 +10,7 @@ Batched entry points (`solve_batch`, `run_precoding_batched`, `rzf_batched`,
 
 from .assembly import assemble_dense, assemble_vr, epilogue
 from .batch import DeviceBatch, HostBatch, pin_host
-from .channel import CONFIGS, ContiguousChannels, NearFieldConfig, generate, solver_seed_sequence
+from .channel import CONFIGS, ContiguousChannels, Drops, NearFieldConfig, generate, generate_drops, solver_seed_sequence
 from .metrics import CADD, CMUL, nmse, spectral_efficiency
 from .rzf import Precoder, apply_auxiliary, auxiliary_matrix, mrc_precoder, rzf_batched, rzf_precoder
 from .solvers import (
@@ -39,11 +39,11 @@ from .vrgraph import UserPartition, build_partition
 __version__ = "0.1.0"
 
 __all__ = [
-    "AugmentedSystem", "BatchResult", "CADD", "CMUL", "CONFIGS", "ContiguousChannels", "DeviceBatch",
+    "AugmentedSystem", "BatchResult", "CADD", "CMUL", "CONFIGS", "ContiguousChannels", "DeviceBatch", "Drops",
     "FlopCounter", "HostBatch", "HostStreams", "NearFieldConfig", "Precoder", "PrecodingRun", "RunTrace",
     "SCHEMES", "STOCHASTIC_SCHEMES", "SolverState", "StoppingRule", "UserPartition", "VR_SCHEMES",
     "apply_auxiliary", "assemble_dense", "assemble_vr", "auxiliary_matrix", "build_partition",
-    "canonical_scheme", "display_scheme", "epilogue", "generate", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
+    "canonical_scheme", "display_scheme", "epilogue", "generate", "generate_drops", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
     "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",
     "solver_seed_sequence", "spectral_efficiency", "gather_stats", "shard_range",
 ]

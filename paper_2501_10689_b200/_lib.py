@@ -51,6 +51,14 @@ class KzRng(C.Structure):
     ]
 
 
+class KzDrop(C.Structure):
+    _fields_ = [
+        ("n_systems", C.c_int32), ("n_users", C.c_int32), ("n_antennas", C.c_int32), ("dtype", C.c_int32),
+        ("element_spacing", C.c_double), ("wavelength", P), ("r0", P), ("theta", P), ("vr_start", P),
+        ("vr_len", P), ("reg", P),
+    ]
+
+
 class KzOut(C.Structure):
     _fields_ = [
         ("v", P), ("iters", P), ("converged", P), ("done", P), ("noop_steps", P), ("flops", P),
@@ -96,6 +104,7 @@ EXPORTS = (
     "kz_abi_version", "kz_last_error", "kz_last_launch_count",
     "kz_solve_workspace_bytes", "kz_solve",
     "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue",
+    "kz_channel_synth", "kz_partition_counts", "kz_partition_fill",
 )
 
 
@@ -116,6 +125,12 @@ def _declare(lb):
     lb.kz_epilogue_workspace_bytes.argtypes = [C.POINTER(KzProblem)]
     lb.kz_epilogue.restype = C.c_int
     lb.kz_epilogue.argtypes = [C.POINTER(KzProblem), P, P, P, P, P, P, P, P, P, P, C.c_size_t, P]
+    lb.kz_channel_synth.restype = C.c_int
+    lb.kz_channel_synth.argtypes = [C.POINTER(KzDrop), P, P, P, P]
+    lb.kz_partition_counts.restype = C.c_int
+    lb.kz_partition_counts.argtypes = [C.POINTER(KzDrop), P, P, P, P, P]
+    lb.kz_partition_fill.restype = C.c_int
+    lb.kz_partition_fill.argtypes = [C.POINTER(KzDrop), P, P, P, P, P, P, P]
 
 
 def check(status: int):

@@ -168,6 +168,52 @@ def generate(cfg: NearFieldConfig | str, seeds) -> ContiguousChannels:
                               np.full(b, cfg.reg), np.full(b, cfg.snr_linear))
 
 
+@dataclass
+class Drops:
+    """User drops of B systems (the inputs of on-device channel synthesis):
+    everything `generate` draws, without the channel entries."""
+
+    n_antennas: int
+    n_users: int
+    r0: np.ndarray           # (B, K) float64 distance to the array centre (m)
+    theta: np.ndarray        # (B, K) float64 angle from broadside (rad)
+    start: np.ndarray        # (B, K) int32 first visible antenna
+    length: np.ndarray       # (B, K) int32 VR length
+    wavelength: np.ndarray   # (B,) float64 per system (subcarrier)
+    element_spacing: float   # lambda_carrier / 2
+    reg: np.ndarray          # (B,)
+    snr_linear: np.ndarray   # (B,)
+
+    @property
+    def n_systems(self) -> int:
+        return self.start.shape[0]
+
+
+def generate_drops(cfg: NearFieldConfig | str, seeds) -> Drops:
+    """The drops `generate(cfg, seeds)` uses, from the same seeded streams (same draw order)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    seeds = list(seeds)
+    r0s, ths, starts, lens, lams = [], [], [], [], []
+    if cfg.n_subcarriers > 1:
+        r0, theta, start, length = _user_drop(cfg, np.random.default_rng(seeds[0]))
+        m = cfg.n_subcarriers
+        for mi in (seeds[1] if len(seeds) > 1 else range(m)):
+            f = cfg.carrier_freq + (mi - (m - 1) / 2.0) * cfg.bandwidth / m
+            r0s.append(r0); ths.append(theta); starts.append(start); lens.append(length)
+            lams.append(SPEED_OF_LIGHT / f)
+    else:
+        for s in seeds:
+            r0, theta, start, length = _user_drop(cfg, np.random.default_rng(s))
+            r0s.append(r0); ths.append(theta); starts.append(start); lens.append(length)
+            lams.append(cfg.wavelength)
+    b = len(starts)
+    return Drops(cfg.n_antennas, cfg.n_users, np.asarray(r0s, dtype=np.float64), np.asarray(ths, dtype=np.float64),
+                 np.asarray(starts, dtype=np.int32), np.asarray(lens, dtype=np.int32),
+                 np.asarray(lams, dtype=np.float64), cfg.wavelength / 2.0, np.full(b, cfg.reg),
+                 np.full(b, cfg.snr_linear))
+
+
 def solver_seed_sequence(seed: int) -> np.random.SeedSequence:
     """Solver RNG of realization `seed`, distinct from its channel draw (experiments.py:226-228)."""
     return np.random.SeedSequence(entropy=seed, spawn_key=(1,))

@@ -12,6 +12,7 @@
 #include "kz_solve_generic.cuh"
 #include "kz_solve_lockstep.cuh"
 #include "kz_solve_cluster.cuh"
+#include "kz_channel.cuh"
 
 namespace {
 
@@ -250,6 +251,75 @@ int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double
         sum_rate_out, (double2*)workspace);
   g_launches = 1;
   return cuda_check("kz_epilogue");
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ on-device input preparation
+static int check_drop(const kz_drop* d) {
+  if (!d) return fail(KZ_ERR_INVALID, "drop is null");
+  if (d->n_systems < 0 || d->n_users < 1 || d->n_antennas < 1)
+    return fail(KZ_ERR_INVALID, "bad drop shape: B=%d K=%d Nt=%d", d->n_systems, d->n_users, d->n_antennas);
+  if (d->dtype != KZ_C128 && d->dtype != KZ_C64) return fail(KZ_ERR_INVALID, "bad dtype %d", d->dtype);
+  if (d->n_systems && (!d->wavelength || !d->r0 || !d->theta || !d->vr_start || !d->vr_len || !d->reg))
+    return fail(KZ_ERR_INVALID, "drop arrays must be non-null");
+  if (!(d->element_spacing > 0.0)) return fail(KZ_ERR_INVALID, "element_spacing must be positive");
+  return KZ_OK;
+}
+
+extern "C" {
+
+int kz_channel_synth(const kz_drop* drop, const int64_t* row_val_ptr, void* heff, double* row_energy,
+                     void* stream) {
+  g_launches = 0;
+  int st = check_drop(drop);
+  if (st) return st;
+  if (drop->n_systems == 0) return KZ_OK;
+  if (!row_val_ptr || !heff || !row_energy) return fail(KZ_ERR_INVALID, "outputs must be non-null");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rows = (size_t)drop->n_systems * drop->n_users;
+  const int wpb = 8;
+  const unsigned grid = (unsigned)((rows + wpb - 1) / wpb);
+  if (drop->dtype == KZ_C128)
+    kz_channel_synth_kernel<double2><<<grid, 32 * wpb, 0, s>>>(*drop, row_val_ptr, (double2*)heff, row_energy);
+  else
+    kz_channel_synth_kernel<float2><<<grid, 32 * wpb, 0, s>>>(*drop, row_val_ptr, (float2*)heff, row_energy);
+  g_launches = 1;
+  return cuda_check("kz_channel_synth");
+}
+
+int kz_partition_counts(const kz_drop* drop, int32_t* coupled_cnt, int32_t* orth_cnt, int32_t* non_union_size,
+                        uint8_t* inset, void* stream) {
+  g_launches = 0;
+  int st = check_drop(drop);
+  if (st) return st;
+  if (drop->n_systems == 0) return KZ_OK;
+  if (!coupled_cnt || !orth_cnt || !non_union_size || !inset) return fail(KZ_ERR_INVALID, "outputs must be non-null");
+  const size_t smem = partition_smem(drop->n_users, drop->n_antennas);
+  if (cudaFuncSetAttribute(kz_partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(KZ_ERR_UNSUPPORTED, "partition: K=%d too large for shared memory", drop->n_users);
+  kz_partition_kernel<<<drop->n_systems, 256, smem, (cudaStream_t)stream>>>(
+      *drop, 0, coupled_cnt, orth_cnt, non_union_size, inset, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  g_launches = 1;
+  return cuda_check("kz_partition_counts");
+}
+
+int kz_partition_fill(const kz_drop* drop, const int32_t* coupled_ptr, const int32_t* orth_ptr,
+                      const int32_t* non_ptr, int32_t* coupled_idx, int32_t* orth_idx, int32_t* non_idx,
+                      void* stream) {
+  g_launches = 0;
+  int st = check_drop(drop);
+  if (st) return st;
+  if (drop->n_systems == 0) return KZ_OK;
+  if (!coupled_ptr || !orth_ptr || !non_ptr || !coupled_idx)
+    return fail(KZ_ERR_INVALID, "CSR arrays must be non-null");
+  const size_t smem = partition_smem(drop->n_users, drop->n_antennas);
+  if (cudaFuncSetAttribute(kz_partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(KZ_ERR_UNSUPPORTED, "partition: K=%d too large for shared memory", drop->n_users);
+  kz_partition_kernel<<<drop->n_systems, 256, smem, (cudaStream_t)stream>>>(
+      *drop, 1, nullptr, nullptr, nullptr, nullptr, coupled_ptr, orth_ptr, non_ptr, coupled_idx, orth_idx, non_idx);
+  g_launches = 1;
+  return cuda_check("kz_partition_fill");
 }
 
 }  // extern "C"

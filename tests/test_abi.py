@@ -45,7 +45,7 @@ def test_python_binding_lists_the_exports(libpath):
     from paper_2501_10689_b200 import _lib
     assert set(_lib.EXPORTS) == set(declared_functions())
     lb = _lib.lib()
-    assert lb.kz_abi_version() == 2
+    assert lb.kz_abi_version() == 3
 
 
 def test_library_is_sm100a(libpath):
@@ -58,7 +58,7 @@ def test_struct_layouts_match_header():
     from paper_2501_10689_b200 import _lib
     src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
     for cname, py in (("kz_problem", _lib.KzProblem), ("kz_stop", _lib.KzStop), ("kz_rng", _lib.KzRng),
-                      ("kz_out", _lib.KzOut)):
+                      ("kz_out", _lib.KzOut), ("kz_drop", _lib.KzDrop)):
         body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (cname, cname), src, flags=re.S).group(1)
         names = re.findall(r"\b([a-z_0-9]+)\s*;", body)
         assert names == [f[0] for f in py._fields_], cname

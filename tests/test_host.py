@@ -134,3 +134,15 @@ def test_product_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_generate_drops_matches_generate():
+    """generate_drops draws exactly the drops generate() uses (narrowband and wideband)."""
+    import paper_2501_10689_b200 as kz
+    for cfg, seeds in (("cfg2", range(3)), ("cfg3", [5, 9]), ("cfg5", [0, [0, 1023]])):
+        ch = kz.generate(cfg, seeds)
+        dr = kz.generate_drops(cfg, seeds)
+        np.testing.assert_array_equal(dr.start, ch.start)
+        np.testing.assert_array_equal(dr.length, ch.length)
+        np.testing.assert_array_equal(dr.reg, ch.reg)
+        assert dr.n_systems == ch.n_systems and dr.n_antennas == ch.n_antennas
