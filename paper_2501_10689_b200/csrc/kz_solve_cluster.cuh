@@ -317,18 +317,20 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   __syncthreads();
   const int NL = misc[1], npairs = misc[2];
   if (npairs > p.pcap || NL > pl.nlcap) __trap();  // layout hint violated: fail loudly
-  // row pieces -> shared memory, zero padded to whole chunks
-  for (int e = tid; e < npairs * CH; e += nthr) {
-    int lo = 0, hi = NL - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (lh[mid] <= e) lo = mid; else hi = mid - 1;
+  // row pieces -> shared memory, zero padded to whole chunks: one warp per (local row, piece), lanes over
+  // the 32 antennas of the piece (coalesced 256 B loads)
+  {
+    int n = 0, pc = 0;  // this warp's current (local row, piece), advanced by W pieces at a time
+    for (int q = w; q < npairs; q += W) {
+      while (n < NL - 1 && lh[n + 1] <= q * CH) ++n;
+      pc = q - (lh[n] >> 5);
+      const int i = lrow[n];
+      const int ant = chunk_of((lcc[n] & 0xFF) + pc) * CH + lane;
+      const int s = rowS[i];
+      Hs[q * CH + lane] = (ant >= s && ant < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (ant - s)]
+                                                           : make_float2(0.f, 0.f);
     }
-    const int i = lrow[lo];
-    const int ant = chunk_of((lcc[lo] & 0xFF) + (e - lh[lo]) / CH) * CH + (e - lh[lo]) % CH;
-    const int s = rowS[i];
-    Hs[e] = (ant >= s && ant < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (ant - s)]
-                                             : make_float2(0.f, 0.f);
+    (void)pc;
   }
   // per-chunk piece lists (ascending rows)
   auto build_list = [&](int* ptr, int* out, int which, int base0) {
