@@ -189,3 +189,56 @@ def test_cluster_cfg5_ahk_nmse_vs_rzf():
         np.testing.assert_allclose(got[above], want[above], rtol=1e-3)
         assert np.all(got[~above] <= 1e-6), got
         np.testing.assert_allclose(out["sum_rate"].cpu().numpy(), ref["sum_rate"].cpu().numpy(), rtol=1e-3)
+
+
+@pytest.mark.parametrize("scheme", ["gk", "grk", "vr-ogrk", "ahk", "vr-oahk"])
+def test_cluster_residual_check_every_and_partial_slices(scheme):
+    """Residual mode with check_every=3 on an array whose chunk count is not a multiple of the slice
+    (Nt=800: idle warps in the last CTA) and K=40 (a partial 16-rhs group): every converged rhs stops at a
+    multiple of check_every, n_checks counts the checks, the float64 true residual is at the tolerance;
+    the deterministic schemes stop within one check of the complex128 oracle."""
+    kz = _kz()
+    eps, every = 1e-4, 3
+    ch = kz.generate(_large(nt=800, k=40, vr=(90, 300), name="odd"), range(2))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    k = ch.n_users
+    rng = ("philox", 11) if scheme in kz.STOCHASTIC_SCHEMES else None
+    res = kz.solve_batch(dev, scheme, mode="residual", epsilon=eps, max_iters=10000 * k, check_every=every, rng=rng)
+    assert res.launches == 1  # the cluster kernel (residual mode has no finaliser)
+    conv = res.converged.cpu().numpy().astype(bool)
+    assert conv.all(), scheme
+    its = res.iters.cpu().numpy()
+    done = res.done.cpu().numpy().astype(bool)
+    assert np.all((its % every == 0) | done), its
+    for b in range(2):
+        h = ch.dense(b)
+        reg = float(ch.reg[b])
+        v = res.v[b].cpu().numpy().astype(np.complex128)
+        rn = np.linalg.norm(np.eye(k) - (h.conj().T @ h + reg * np.eye(k)) @ v, axis=0)
+        assert rn.max() <= 2 * eps, (scheme, rn.max())
+        if scheme in ("gk", "ahk", "vr-oahk") and b == 0:
+            chan = oracle_channel_contiguous(ch, b)
+            sys_ = O.AugmentedSystem.from_channel(chan, reg)
+            traces = []
+            O.solve_all(scheme, sys_, O.StoppingRule(mode="residual", epsilon=eps, check_every=every),
+                        traces=traces)
+            want = np.array([t.n_iters for t in traces])
+            assert np.abs(its[b] - want).max() <= every, (its[b], want)
+
+
+def test_cluster_gk_lockstep_rows_log_and_noop_free():
+    """GK on the cluster kernel logs one row per step and, far from the fp32 floor, equals the oracle's
+    row sequence exactly (greedy-max ties are measure-zero on these drops)."""
+    kz = _kz()
+    T = 8
+    ch = kz.generate(_large(nt=1024, k=24, vr=(200, 400), name="gk"), range(2))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    res = kz.solve_batch(dev, "gk", mode="lockstep", max_iters=T, rows_cap=T)
+    for b in range(2):
+        chan = oracle_channel_contiguous(ch, b)
+        sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[b]))
+        run = O.run_precoding("gk", sys_, O.rzf_precoder(chan, float(ch.reg[b])), epsilon=0.0, max_iters=T,
+                              traces=False)
+        rows = res.rows[b].cpu().numpy()
+        same = np.mean([np.array_equal(rows[c], run.rows[c]) for c in range(ch.n_users)])
+        assert same >= 0.9, same
