@@ -6,7 +6,7 @@ for sc in urk grk vr-ogrk ahk vr-oahk; do
   cmd="python tools/prof_solve.py --scheme $sc --iters 200 --reps 1"
   $cmd > gpurun_out/ncu/plain_$sc.log 2>&1 && \
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum \
-      --clock-control none -k regex:wide_kernel -c 1 --csv $cmd > gpurun_out/ncu/traffic_$sc.csv 2> gpurun_out/ncu/traffic_$sc.err
+      --clock-control none -k regex:"wide_kernel|rkwarp" -c 1 --csv $cmd > gpurun_out/ncu/traffic_$sc.csv 2> gpurun_out/ncu/traffic_$sc.err
 done
 # full section set of the dominant kernel (vr-oahk), smaller T to bound replay time
 cmd="python tools/prof_solve.py --scheme vr-oahk --iters 50 --reps 1"
