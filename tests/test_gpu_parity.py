@@ -513,3 +513,25 @@ def test_c_abi_direct_call_as_in_integration_md():
                       ws.data_ptr(), ws.numel(), 0, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     res = kz.solve_batch(dev, "grk", mode="lockstep", max_iters=50, rng=("philox", 1))
     torch.testing.assert_close(v, res.v, rtol=0, atol=0)  # deterministic: identical bits
+
+
+def test_gpu_traces_match_kaczplot_golden_csv():
+    """The reference's cross-machine golden traces (pkg/kaczplot/tests/data/convergence.csv, kept as
+    tests/golden/kaczplot_convergence.npz) through the GPU run_precoding in complex128: iteration
+    counts and FlopCounter traces exact, NMSE within 1e-9 relative above 1e-9, true residual traces."""
+    kz = _kz()
+    z = load("kaczplot_convergence.npz")
+    cfg = O.ArrayConfig(32, 100e9, 4)
+    for seed in (0, 1):
+        chan, reg = O.power_control(O.random_channel(cfg, 4, 5, 0.6, np.random.default_rng(seed)), 0.0)
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        for sc in O.SCHEMES:
+            rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(1,)))
+            run = kz.run_precoding(sc, sys_, ref, epsilon=1e-6, max_iters=20_000, rng=rng)
+            want_n = z[f"{sc}/{seed}/nmse"]
+            assert run.n_iters == want_n.size, (sc, seed)
+            np.testing.assert_array_equal(run.flops_trace, z[f"{sc}/{seed}/flops"])
+            big = want_n > 1e-9
+            np.testing.assert_allclose(np.asarray(run.nmse_trace)[big], want_n[big], rtol=1e-9)
+            np.testing.assert_allclose(run.resid_trace, z[f"{sc}/{seed}/resid"], rtol=1e-8, atol=1e-14)
