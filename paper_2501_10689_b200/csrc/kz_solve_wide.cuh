@@ -668,23 +668,28 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         }
 #pragma unroll
         for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);  // registers now hold y
-        for (int q = ptr[w]; q < ptr[w + 1]; ++q) {
-          const int2 e = L[q];
+        auto agg_entry = [&](int2 e) {
           const int i = e.x >> 20;
           const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
           const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
-          {
 #pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-              float4 h = hp[2 * j];
-              const int k = 2 * j;
-              m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
-              m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
-              m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
-              m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
-            }
+          for (int j = 0; j < E / 2; ++j) {
+            float4 h = hp[2 * j];
+            const int k = 2 * j;
+            m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
+            m0[k + 1] = cfma(p0, make_float2(h.z, h.w), m0[k + 1]);
+            m1[k] = cfma(p1, make_float2(h.x, h.y), m1[k]);
+            m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
           }
+        };
+        int q = ptr[w];
+        const int q1 = ptr[w + 1];
+        for (; q + 1 < q1; q += 2) {  // two entries per trip: the next entry's loads overlap this one's FMAs
+          const int2 ea = L[q], eb = L[q + 1];
+          agg_entry(ea);
+          agg_entry(eb);
         }
+        if (q < q1) agg_entry(L[q]);
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
