@@ -180,6 +180,17 @@ class HostBatch:
     def support_sizes(self) -> np.ndarray:
         return np.diff(self.row_val_ptr).reshape(self.n_systems, self.n_users)
 
+    def layout_hints(self) -> dict:
+        """kz_problem shape hints of this batch (computed once: host packing work, not per upload)."""
+        h = self.__dict__.get("_hints")
+        if h is None:
+            sup = np.diff(self.row_val_ptr)
+            h = {"max_support": int(sup.max()) if sup.size else 0,
+                 "slice_pairs_128": self.slice_pairs(128) if self.contiguous else 0,
+                 "slice_pairs_256": self.slice_pairs(256) if self.contiguous else 0}
+            self.__dict__["_hints"] = h
+        return h
+
     def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024) -> int:
         """Max over systems and CTAs of the (row, `chunk`-antenna chunk) pairs a CTA of the cluster kernel
         holds, for CTAs of `width` antennas in the block-interleaved layout of csrc/kz_solve_cluster.cuh
@@ -261,12 +272,11 @@ class DeviceBatch:
         for name in self.FIELDS:
             ten = t[name]
             setattr(p, name, ten.data_ptr() if ten.numel() else None)
-        sup = np.diff(self.host.row_val_ptr)
-        p.max_support = int(sup.max()) if sup.size else 0
+        hints = self.host.layout_hints()
+        p.max_support = hints["max_support"]
         p.flags = 1 if self.host.contiguous else 0
-        if self.host.contiguous:
-            p.slice_pairs_128 = self.host.slice_pairs(128)
-            p.slice_pairs_256 = self.host.slice_pairs(256)
+        p.slice_pairs_128 = hints["slice_pairs_128"]
+        p.slice_pairs_256 = hints["slice_pairs_256"]
         return p
 
     @classmethod
