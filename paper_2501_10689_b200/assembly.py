@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -42,7 +44,7 @@ def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = Fa
     r = torch.zeros((b, k), dtype=torch.float64, device=d) if rates else None
     sr = torch.zeros(b, dtype=torch.float64, device=d) if rates else None
     # the Gram-form epilogue (contiguous VRs, K >= 96, F not stored) always needs its G0 / G0 V workspace
-    gram_form = dev.host.contiguous and k >= 96 and not want_f
+    gram_form = dev.host.contiguous and k >= int(os.environ.get("KZ_EPILOGUE_GRAM_KMIN", 32)) and not want_f
     need = lb.kz_epilogue_workspace_bytes(C.byref(dev.problem)) if (rates or gram_form) else 0
     ws = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
     s = stream if stream is not None else torch.cuda.current_stream()

@@ -185,7 +185,8 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
 
 // Gram-form epilogue for large K (contiguous VRs, F not requested): G0 and G0 V per system
 static bool epilogue_gram_path(const kz_problem* prob) {
-  return (prob->flags & KZ_PROBLEM_CONTIGUOUS) && prob->n_users >= 96 && getenv("KZ_EPILOGUE_ANTENNA") == nullptr;
+  static const int kmin = getenv("KZ_EPILOGUE_GRAM_KMIN") ? atoi(getenv("KZ_EPILOGUE_GRAM_KMIN")) : 32;
+  return (prob->flags & KZ_PROBLEM_CONTIGUOUS) && prob->n_users >= kmin && getenv("KZ_EPILOGUE_ANTENNA") == nullptr;
 }
 
 size_t kz_epilogue_workspace_bytes(const kz_problem* prob) {
