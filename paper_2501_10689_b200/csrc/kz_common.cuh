@@ -75,6 +75,19 @@ template <class T> __device__ __forceinline__ T cfma(T a, T b, T acc) {
   acc.y = fma(a.y, b.x, acc.y);
   return acc;
 }
+// packed fp32x2 FMA (sm_100a FFMA2): d = a * b + c per half, one rounding per half (bitwise the same as two
+// fmaf calls); a broadcast scalar operand (fma2s) is folded into the instruction by ptxas
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long A, B, C, D;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D) : "l"(A), "l"(B), "l"(C));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(D));
+  return r;
+}
+__device__ __forceinline__ float2 fma2s(float s, float2 b, float2 c) { return fma2(make_float2(s, s), b, c); }
 template <class T> __device__ __forceinline__ T cscale(T a, typename Cx<T>::real s) { return Cx<T>::make(a.x * s, a.y * s); }
 template <class T> __device__ __forceinline__ T cdivr(T a, double e) {
   using R = typename Cx<T>::real;
