@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 oracle-mode step")
     return ap.parse_args()
 
 
@@ -394,6 +395,26 @@ def main():
         stats[sc] = {"median_nmse": float(g["nmse"].median()), "mean_sum_rate": float(g["sum_rate"].mean()),
                      "systems": int(g["nmse"].numel())}
 
+    # the same step in complex128 oracle mode (BASELINE cfg2 quotes both modes): one warm + one timed step
+    c128 = None
+    if not a.no_c128 and a.dtype == "c64":
+        dev128 = host.to_device("c128", device=dev_id)
+        step(dev128, 7)
+        torch.cuda.synchronize()
+        ev128 = {}
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(dev128, 8, ev128)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t128 = e0.elapsed_time(e1)
+        c128 = {"value": len(schemes) * B * world / (t128 / 1e3), "unit": UNIT, "ms_per_step": t128,
+                "dtype": "complex128",
+                "per_scheme_launch_ms": {sc: ev[0][0].elapsed_time(ev[0][1]) for sc, ev in ev128.items()},
+                "note": "one timed step, same workload; the exact-arithmetic kernels of the oracle-mode parity tests"}
+        del dev128
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -409,13 +430,14 @@ def main():
                          "peak": fp32_peak, "unit": "TFLOP/s", "frac": tflops / fp32_peak, "traffic": traffic,
                          "algorithmic_flops_per_launch": 8.0 * elems_dom, "peak_source": fp32_src,
                          "note": "H_eff is shared-memory resident and each streamed h element is reused by "
-                                 "4 rhs in registers, so the launch is CUDA-core FMA bound (SURVEY 8(d): report "
-                                 "the FMA roofline); flops = 8 x streamed H_eff elements per rhs-iteration",
+                                 "2 rhs in registers (8 FFMA per complex element), so the launch is CUDA-core "
+                                 "FMA bound (SURVEY 8(d): report the FMA roofline); flops = 8 x streamed H_eff "
+                                 "elements per rhs-iteration",
                          "smem_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": smem_peak},
                          "hbm_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": hbm_peak,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "stats": stats,
+            "clocks": clk.summary(), "stats": stats, "complex128_oracle_mode": c128,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
