@@ -382,8 +382,19 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   for (t = 1; t <= p.T; ++t) {
     KZ_ITER();
     if constexpr (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK) {
-      // refresh every row overlapping this chunk, two rows in flight
+      // refresh every row overlapping this chunk, up to four rows in flight
       int q = l0;
+      for (; q + 3 < l1; q += 4) {
+        const int2 e0 = lst[q], e1 = lst[q + 1], e2 = lst[q + 2], e3 = lst[q + 3];
+        const T v0 = dot_chunk(e0.x & 0xFFFFF);
+        const T v1 = dot_chunk(e1.x & 0xFFFFF);
+        const T v2 = dot_chunk(e2.x & 0xFFFFF);
+        const T v3 = dot_chunk(e3.x & 0xFFFFF);
+        Ps[pslot(e0.y)] = v0;
+        Ps[pslot(e1.y)] = v1;
+        Ps[pslot(e2.y)] = v2;
+        Ps[pslot(e3.y)] = v3;
+      }
       for (; q + 1 < l1; q += 2) {
         int2 e0 = lst[q], e1 = lst[q + 1];
         T v0 = dot_chunk(e0.x & 0xFFFFF);
@@ -593,6 +604,18 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
       auto refresh_list = [&](const int* ptr, const int2* L) {
         int q = ptr[w];
         const int q1 = ptr[w + 1];
+        // up to four rows in flight (vr-oahk keeps two: its larger live state would spill)
+        for (; SCH != KZ_VR_OAHK && q + 3 < q1; q += 4) {
+          const int2 e0 = L[q], e1 = L[q + 1], e2 = L[q + 2], e3 = L[q + 3];
+          const T v0 = dot_chunk(e0.x & 0xFFFFF);
+          const T v1 = dot_chunk(e1.x & 0xFFFFF);
+          const T v2 = dot_chunk(e2.x & 0xFFFFF);
+          const T v3 = dot_chunk(e3.x & 0xFFFFF);
+          Ps[pslot(e0.y)] = v0;
+          Ps[pslot(e1.y)] = v1;
+          Ps[pslot(e2.y)] = v2;
+          Ps[pslot(e3.y)] = v3;
+        }
         for (; q + 1 < q1; q += 2) {
           int2 e0 = L[q], e1 = L[q + 1];
           T v0 = dot_chunk(e0.x & 0xFFFFF);
