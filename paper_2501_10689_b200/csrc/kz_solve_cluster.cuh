@@ -91,7 +91,7 @@ __device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
 
 struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
-  size_t rowS, rowL, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, P, Qo,
+  size_t rowS, rowL, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
       misc, total;
 };
@@ -123,20 +123,19 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.lh = o; o = al(o + 4 * p.nlcap);
   p.lcc = o; o = al(o + 4 * p.nlcap);
   p.lptr = o; o = al(o + 4 * (W + 1));
-  p.lst = o; o = al(o + 4 * (size_t)pcap);
+  p.lst = o; o = al(o + 8 * (size_t)pcap);
   p.optr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
   p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
-  p.olst = o; o = al(o + (oahk ? 4 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
+  p.olst = o; o = al(o + (oahk ? 8 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
   p.nlst = p.olst;
   p.H = o; o = al(o + 8 * (size_t)pcap * CH);
-  p.P = o; o = al(o + 8 * (size_t)pcap * G);
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Ro = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Fo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.IN = o; o = al(o + 8 * (size_t)p.KO * NS * G);
-  p.Phl = p.P;  // phi / gamma of local rows reuse P (disjoint phases; nlcap <= pcap)
-  p.dloc = o; o = al(o + 4 * (size_t)p.KO * NS);
-  p.dlst = o; o = al(o + 4 * (size_t)p.KO * NS);
+  p.Phl = o; o = al(o + 8 * (size_t)p.nlcap * G);
+  p.dloc = o; o = al(o + 4 * (size_t)p.KO * CL);
+  p.dlst = o; o = al(o + 4 * (size_t)p.KO * CL);
   p.dcnt = o; o = al(o + 4 * (size_t)p.KO);
   p.AG4 = o; o = al(o + 16 * (size_t)CL * G);
   p.GAMv = o; o = al(o + 8 * G);
@@ -218,19 +217,21 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   int* lh = (int*)(sm + pl.lh);    // H element offset of local row n's first chunk
   int* lcc = (int*)(sm + pl.lcc);  // local chunk range of row n: lc0 | lc1 << 8
   int* lptr = (int*)(sm + pl.lptr);
-  int* lst = (int*)(sm + pl.lst);  // H element offset of the (row, chunk) piece | local row << 20
+  // piece lists: x = H element offset of the (row, chunk) piece | local row << 20,
+  //              y = inbox offset (row, chunk slot) in the owner | (row & 15) << 20 | owner << 24
+  int2* lst = (int2*)(sm + pl.lst);
   int* optr = (int*)(sm + pl.optr);
-  int* olst = (int*)(sm + pl.olst);
+  int2* olst = (int2*)(sm + pl.olst);
   int* nptr = (int*)(sm + pl.nptr);
-  int* nlst = (int*)(sm + pl.nlst);
+  int2* nlst = (int2*)(sm + pl.nlst);
   T* Hs = (T*)(sm + pl.H);
-  T* Ps = (T*)(sm + pl.P);
   T* Qo = (T*)(sm + pl.Qo);
   T* Ro = (T*)(sm + pl.Ro);
   T* Fo = (T*)(sm + pl.Fo);  // owned phi (aggregation weights) or gamma (orthogonal block)
   T* INs = (T*)(sm + pl.IN);
-  T* Phl = (T*)(sm + pl.Phl);  // phi / gamma of the local rows, pulled from their owners
+  T* Phl = (T*)(sm + pl.Phl);  // phi / gamma of the local rows, pushed by their owners
   int* dloc = (int*)(sm + pl.dloc);  // [owned row][CTA] -> local row index of the row in that CTA (-1: none)
+  // (inbox: IN[owned row][chunk slot][rhs], slot = chunk - first chunk of the row, NS = max chunks per row)
   int* dlst = (int*)(sm + pl.dlst);  // [owned row][k] -> k-th CTA holding pieces of the row (ascending)
   int* dcnt = (int*)(sm + pl.dcnt);
   float4* AG4 = (float4*)(sm + pl.AG4);
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     (void)pc;
   }
   // per-chunk piece lists (ascending rows)
-  auto build_list = [&](int* ptr, int* out, int which, int base0) {
+  auto build_list = [&](int* ptr, int2* out, int which, int base0) {
     int cnt = 0;
     for (int base = 0; base < NL; base += 32) {
       const int n = base + lane;
@@ -362,7 +363,12 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         ov = l0 <= w && w <= l1 && (which == 0 || inset[lrow[n]] == which);
       }
       const unsigned bal = __ballot_sync(FULL, ov);
-      if (ov) out[q + __popc(bal & ((1u << lane) - 1))] = (lh[n] + (w - l0) * CH) | (n << 20);
+      if (ov) {
+        const int i = lrow[n], o = i / KO, il = i - o * KO;
+        const int slot = chunk_of(w) - c0[i];
+        out[q + __popc(bal & ((1u << lane) - 1))] =
+            make_int2((lh[n] + (w - l0) * CH) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
+      }
       q += __popc(bal);
     }
   };
@@ -417,15 +423,15 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
   cluster_sync();  // every CTA of the cluster is resident and initialised before any DSMEM traffic
-  for (int e = tid; e < nown * NS; e += nthr) {  // owner: where each CTA keeps its piece of an owned row
-    const int il = e / NS, d = e % NS, i = o_lo + il;
+  for (int e = tid; e < nown * CL; e += nthr) {  // owner: where each CTA keeps its piece of an owned row
+    const int il = e / CL, d = e % CL, i = o_lo + il;
     dloc[e] = d == c ? loc[i] : ld_remote(loc + i, d);
   }
   __syncthreads();
   for (int il = tid; il < nown; il += nthr) {
     int n = 0;
-    for (int d = 0; d < NS; ++d)
-      if (dloc[il * NS + d] >= 0) dlst[il * NS + n++] = d;
+    for (int d = 0; d < CL; ++d)
+      if (dloc[il * CL + d] >= 0) dlst[il * CL + n++] = d;
     dcnt[il] = n;
   }
   __syncthreads();
@@ -465,66 +471,46 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     ky += __shfl_xor_sync(FULL, ky, 16);
     return make_float2(kx, ky);
   };
-  auto refresh = [&](const int* ptr, const int* L) {
+  // partial of each (row, chunk) piece straight into the owner's inbox (local or DSMEM store): no slice-level
+  // staging, the remote stores drain while the warp computes its next pieces
+  auto deliver = [&](int2 e, T v) {
+    if (lane < 16) {
+      T* dst = INs + (e.y & 0xFFFFF) + (lane ^ ((e.y >> 20) & 15));
+      const int o = e.y >> 24;
+      if (o == c) *dst = v; else st_remote(dst, o, v);
+    }
+  };
+  auto refresh = [&](const int* ptr, const int2* L) {
     int q = ptr[w];
     const int q1 = ptr[w + 1];
     for (; q + 3 < q1; q += 4) {  // four pieces in flight
-      const int h0 = L[q] & 0xFFFFF, h1 = L[q + 1] & 0xFFFFF, h2 = L[q + 2] & 0xFFFFF, h3 = L[q + 3] & 0xFFFFF;
-      const T v0 = dot16(h0);
-      const T v1 = dot16(h1);
-      const T v2 = dot16(h2);
-      const T v3 = dot16(h3);
-      if (lane < 16) {
-        Ps[(h0 >> 5) * G + lane] = v0;
-        Ps[(h1 >> 5) * G + lane] = v1;
-        Ps[(h2 >> 5) * G + lane] = v2;
-        Ps[(h3 >> 5) * G + lane] = v3;
-      }
+      const int2 e0 = L[q], e1 = L[q + 1], e2 = L[q + 2], e3 = L[q + 3];
+      const T v0 = dot16(e0.x & 0xFFFFF);
+      const T v1 = dot16(e1.x & 0xFFFFF);
+      const T v2 = dot16(e2.x & 0xFFFFF);
+      const T v3 = dot16(e3.x & 0xFFFFF);
+      deliver(e0, v0);
+      deliver(e1, v1);
+      deliver(e2, v2);
+      deliver(e3, v3);
     }
     for (; q + 1 < q1; q += 2) {
-      const int h0 = L[q] & 0xFFFFF, h1 = L[q + 1] & 0xFFFFF;
-      const T v0 = dot16(h0);
-      const T v1 = dot16(h1);
-      if (lane < 16) {
-        Ps[(h0 >> 5) * G + lane] = v0;
-        Ps[(h1 >> 5) * G + lane] = v1;
-      }
+      const int2 e0 = L[q], e1 = L[q + 1];
+      const T v0 = dot16(e0.x & 0xFFFFF);
+      const T v1 = dot16(e1.x & 0xFFFFF);
+      deliver(e0, v0);
+      deliver(e1, v1);
     }
-    if (q < q1) {
-      const int h0 = L[q] & 0xFFFFF;
-      const T v0 = dot16(h0);
-      if (lane < 16) Ps[(h0 >> 5) * G + lane] = v0;
-    }
-  };
-  // slice sums (fixed chunk order) -> owner inbox IN[row][slice slot][rhs]
-  auto push = [&](int which) {
-    for (int e = tid; e < NL * G; e += nthr) {
-      const int n = e >> 4, gg = e & 15;
-      const int i = lrow[n];
-      if (which && inset[i] != which) continue;
-      const int ns = (lcc[n] >> 8) - (lcc[n] & 0xFF);
-      const T* pp = Ps + (size_t)(lh[n] >> 5) * G + gg;
-      float dx = 0.f, dy = 0.f;
-      for (int s = 0; s <= ns; ++s) {
-        const T v = pp[s * G];
-        dx += v.x;
-        dy += v.y;
-      }
-      const int o = i / KO, il = i - o * KO;
-      T* dst = INs + (size_t)(il * NS + c) * G + (gg ^ (il & 15));
-      if (o == c) *dst = make_float2(dx, dy);
-      else st_remote(dst, o, make_float2(dx, dy));
-    }
+    if (q < q1) deliver(L[q], dot16(L[q].x & 0xFFFFF));
   };
   // owner: residual of owned row il for rhs gg from the slice sums (fixed slice order)
   auto oresid = [&](int il, int gg, bool dense) -> T {
     const int i = o_lo + il;
     const T* pp = INs + (size_t)il * NS * G + (gg ^ (il & 15));
-    const int* dl = dlst + il * NS;
-    const int nd = dcnt[il];
+    const int ns = c1[i] - c0[i];
     float dx = 0.f, dy = 0.f;
-    for (int k = 0; k < nd; ++k) {  // the CTAs holding pieces of row i, ascending (fixed order)
-      const T v = pp[dl[k] * G];
+    for (int sl = 0; sl <= ns; ++sl) {  // the row's chunk pieces, ascending (fixed order)
+      const T v = pp[sl * G];
       dx += v.x;
       dy += v.y;
     }
@@ -540,8 +526,8 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   auto push_phi = [&](int il, int gg, T v) {
     const int nd = dcnt[il];
     for (int k = 0; k < nd; ++k) {
-      const int d = dlst[il * NS + k];
-      T* dst = Phl + dloc[il * NS + d] * G + gg;
+      const int d = dlst[il * CL + k];
+      T* dst = Phl + dloc[il * CL + d] * G + gg;
       if (d == c) *dst = v; else st_remote(dst, d, v);
     }
   };
@@ -638,9 +624,6 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     KZ_ITER();
     if constexpr (GREEDY) {
       refresh(lptr, lst);
-      __syncthreads();
-      KZ_PHASE();
-      push(0);
       KZ_CLU_SPLIT();
       cluster_sync();
       KZ_PHASE();
@@ -829,9 +812,6 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       }
     } else if constexpr (SCH == KZ_AHK) {
       refresh(lptr, lst);
-      __syncthreads();
-      KZ_PHASE();
-      push(0);
       cluster_sync();
       KZ_PHASE();
       owner_weights(0, false);
@@ -840,9 +820,6 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     } else {  // VR-OAHK (solvers.py:414-421)
       // orthogonal group O: exact block projection (solvers.py:312-332); residual mode refreshes every row
       if (residual) refresh(lptr, lst); else refresh(optr, olst);
-      __syncthreads();
-      KZ_PHASE();
-      push(residual ? 0 : 1);
       cluster_sync();
       KZ_PHASE();
       for (int pair = w; pair < G / 2; pair += W) {
@@ -893,18 +870,14 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       {
         const bool l0v = livev[g], l1v = livev[g + 8];
         for (int q = optr[w]; q < optr[w + 1]; ++q) {
-          const int n = olst[q] >> 20;
+          const int n = olst[q].x >> 20;
           if (l0v) project(m0, n, Phl[n * G + g]);
           if (l1v) project(m1, n, Phl[n * G + g + 8]);
         }
       }
       KZ_PHASE();
       if (nN > 0) {
-        __syncthreads();  // Phl (aliasing P) is read by the O projection above
         refresh(nptr, nlst);
-        __syncthreads();
-        KZ_PHASE();
-        push(2);
         cluster_sync();
         KZ_PHASE();
         owner_weights(2, true);
@@ -917,14 +890,14 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       // den = ||y||^2 + xi ||phi||^2 from fixed-order reductions over warps and CTAs
       if (SCH == KZ_AHK || nN > 0) {
         const int* ptr = SCH == KZ_AHK ? lptr : nptr;
-        const int* L = SCH == KZ_AHK ? lst : nlst;
+        const int2* L = SCH == KZ_AHK ? lst : nlst;
         T y0[8], y1[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
         int q = ptr[w];
         const int q1 = ptr[w + 1];
         for (; q + 1 < q1; q += 2) {  // two pieces in flight
-          const int e0 = L[q], e1 = L[q + 1], n0 = e0 >> 20, n1 = e1 >> 20;
+          const int e0 = L[q].x, e1 = L[q + 1].x, n0 = e0 >> 20, n1 = e1 >> 20;
           const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
           const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + 8];
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
@@ -944,7 +917,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
           }
         }
         if (q < q1) {
-          const int e0 = L[q], n0 = e0 >> 20;
+          const int e0 = L[q].x, n0 = e0 >> 20;
           const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
 #pragma unroll
@@ -1106,7 +1079,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
 inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int* CL, int* NS, int* pcap) {
   const int nch = P.n_antennas / clu::CH;
   *CL = (nch + W - 1) / W;
-  *NS = *CL;
+  *NS = (P.max_support + clu::CH - 2) / clu::CH + 1;  // inbox slots: chunks a row can touch
   *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
   if (*pcap <= 0) return ~size_t(0);
   return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap).total;
