@@ -40,11 +40,10 @@ namespace kz {
 
 namespace clu {
 
-constexpr int G = 16;   // rhs per cluster
 constexpr int CH = 32;  // antennas per warp
 
 // [owned row][rhs] arrays are XOR-swizzled so lanes-over-rows and lanes-over-rhs are both conflict free
-__device__ __forceinline__ int xo(int il, int gg) { return il * G + (gg ^ (il & 15)); }
+template <int G> __device__ __forceinline__ int xo(int il, int gg) { return il * G + (gg ^ (il & 15)); }
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -98,7 +97,7 @@ struct Plan {
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap) {
+__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap, int G) {
   Plan p;
   p.K = K;
   p.W = W;
@@ -178,9 +177,17 @@ struct CluArgs {
   int32_t* tstop;
 };
 
-template <int SCH>
+// GG = rhs per cluster: 16 (lane (a, g), a = lane >> 3: rhs g, g + 8 on 8 antennas) or 32 (a = lane >> 4:
+// rhs g, g + 16 on 16 antennas, the wide kernel's mapping: twice the FMAs per loaded element set and per
+// piece overhead, when the larger inbox fits)
+template <int SCH, int GG>
 __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   using namespace clu;
+  constexpr int G = GG;
+  constexpr int NA = G == 16 ? 4 : 2;  // a-lanes sharing a (row, chunk) piece
+  constexpr int LPA = 32 / NA;         // lanes per a-lane group = rhs offset of the second rhs
+  constexpr int E = CH / NA;           // antennas per thread per chunk
+  auto xo = [](int il, int gg) { return clu::xo<G>(il, gg); };
   using T = float2;
   constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
   constexpr bool GREEDY = SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK;
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   const int b = cid / ngroups, grp = cid % ngroups, g0 = grp * G;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int W = nthr >> 5;
-  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap);
+  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap, G);
   const int KO = pl.KO, NS = pl.NS, KW = (K + 31) / 32;
   // block-interleaved slices: CTA c owns nblk blocks of Bc = W / nblk chunks, block j at chunk
   // (j CL + c) Bc, so every CTA samples the whole array and the VR-coverage ramps at the array edges no
@@ -437,21 +444,21 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   __syncthreads();
   KZ_PHASE();
 
-  const int a = lane >> 3, g = lane & 7;
+  const int a = lane / LPA, g = lane % LPA;
   const int hf = lane >> 4, hl = lane & 15;  // half-warp serving one rhs in the owner / selection phases
   const unsigned hmask = 0xFFFFu << (16 * hf);
-  T m0[8], m1[8];  // rhs g and g + 8
+  T m0[E], m1[E];  // rhs g and g + LPA
 #pragma unroll
-  for (int k = 0; k < 8; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
   const float4* H4 = reinterpret_cast<const float4*>(Hs);
 
-  // conj(h) . m over this warp's chunk for both rhs, reduced over the four a-lanes; lane < 16 ends with rhs lane
+  // conj(h) . m over this warp's chunk for both rhs, reduced over the a-lanes; lane < G ends with rhs lane
   auto dot16 = [&](int h0) -> T {
     const float4* hp = H4 + (h0 >> 1) + a;
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 h = hp[4 * j];
+    for (int j = 0; j < E / 2; ++j) {
+      const float4 h = hp[NA * j];
       const int k = 2 * j;
       x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
       y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
@@ -463,18 +470,20 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       v1 = fmaf(h.z, m1[k + 1].y, v1); v1 = fmaf(-h.w, m1[k + 1].x, v1);
     }
     const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
-    const bool odd = a & 1;  // odd a-lanes keep rhs g + 8
+    const bool odd = a & 1;  // odd a-lanes keep rhs g + LPA
     const float sx = odd ? px : qx, sy = odd ? py : qy;
-    const float rx = __shfl_xor_sync(FULL, sx, 8), ry = __shfl_xor_sync(FULL, sy, 8);
+    const float rx = __shfl_xor_sync(FULL, sx, LPA), ry = __shfl_xor_sync(FULL, sy, LPA);
     float kx = (odd ? qx : px) + rx, ky = (odd ? qy : py) + ry;
-    kx += __shfl_xor_sync(FULL, kx, 16);
-    ky += __shfl_xor_sync(FULL, ky, 16);
+    if constexpr (NA == 4) {
+      kx += __shfl_xor_sync(FULL, kx, 16);
+      ky += __shfl_xor_sync(FULL, ky, 16);
+    }
     return make_float2(kx, ky);
   };
   // partial of each (row, chunk) piece straight into the owner's inbox (local or DSMEM store): no slice-level
   // staging, the remote stores drain while the warp computes its next pieces
   auto deliver = [&](int2 e, T v) {
-    if (lane < 16) {
+    if (lane < G) {
       T* dst = INs + (e.y & 0xFFFFF) + (lane ^ ((e.y >> 20) & 15));
       const int o = e.y >> 24;
       if (o == c) *dst = v; else st_remote(dst, o, v);
@@ -573,13 +582,13 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       }
     }
   };
-  auto project = [&](T (&mr)[8], int n, T gm) {  // m += gm h on this warp's chunk of local row n
+  auto project = [&](T (&mr)[E], int n, T gm) {  // m += gm h on this warp's chunk of local row n
     const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
     if (w < l0 || w > l1) return;
     const float4* hp = H4 + ((lh[n] + (w - l0) * CH) >> 1) + a;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 h = hp[4 * j];
+    for (int j = 0; j < E / 2; ++j) {
+      const float4 h = hp[NA * j];
       const int k = 2 * j;
       mr[k].x = fmaf(gm.x, h.x, mr[k].x); mr[k].x = fmaf(-gm.y, h.y, mr[k].x);
       mr[k].y = fmaf(gm.x, h.y, mr[k].y); mr[k].y = fmaf(gm.y, h.x, mr[k].y);
@@ -806,9 +815,9 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         }
       }
       {
-        const int i0 = SEL[g], i1 = SEL[g + 8];
+        const int i0 = SEL[g], i1 = SEL[g + LPA];
         if (i0 >= 0 && loc[i0] >= 0) project(m0, loc[i0], GAM[g]);
-        if (i1 >= 0 && loc[i1] >= 0) project(m1, loc[i1], GAM[g + 8]);
+        if (i1 >= 0 && loc[i1] >= 0) project(m1, loc[i1], GAM[g + LPA]);
       }
     } else if constexpr (SCH == KZ_AHK) {
       refresh(lptr, lst);
@@ -868,11 +877,11 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         Qo[xo(il, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
       }
       {
-        const bool l0v = livev[g], l1v = livev[g + 8];
+        const bool l0v = livev[g], l1v = livev[g + LPA];
         for (int q = optr[w]; q < optr[w + 1]; ++q) {
           const int n = olst[q].x >> 20;
           if (l0v) project(m0, n, Phl[n * G + g]);
-          if (l1v) project(m1, n, Phl[n * G + g + 8]);
+          if (l1v) project(m1, n, Phl[n * G + g + LPA]);
         }
       }
       KZ_PHASE();
@@ -891,20 +900,20 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       if (SCH == KZ_AHK || nN > 0) {
         const int* ptr = SCH == KZ_AHK ? lptr : nptr;
         const int2* L = SCH == KZ_AHK ? lst : nlst;
-        T y0[8], y1[8];
+        T y0[E], y1[E];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
+        for (int k = 0; k < E; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
         int q = ptr[w];
         const int q1 = ptr[w + 1];
         for (; q + 1 < q1; q += 2) {  // two pieces in flight
           const int e0 = L[q].x, e1 = L[q + 1].x, n0 = e0 >> 20, n1 = e1 >> 20;
-          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
-          const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + 8];
+          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
+          const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + LPA];
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
           const float4* hp1 = H4 + ((e1 & 0xFFFFF) >> 1) + a;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 h0 = hp0[4 * j], h1 = hp1[4 * j];
+          for (int j = 0; j < E / 2; ++j) {
+            const float4 h0 = hp0[NA * j], h1 = hp1[NA * j];
             const int k = 2 * j;
             y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
             y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
@@ -918,11 +927,11 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         }
         if (q < q1) {
           const int e0 = L[q].x, n0 = e0 >> 20;
-          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + 8];
+          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 h0 = hp0[4 * j];
+          for (int j = 0; j < E / 2; ++j) {
+            const float4 h0 = hp0[NA * j];
             const int k = 2 * j;
             y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
             y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
@@ -932,17 +941,18 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         }
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < E; ++k) {
           s0 = fmaf(y0[k].x, y0[k].x, fmaf(y0[k].y, y0[k].y, s0));
           s1 = fmaf(y1[k].x, y1[k].x, fmaf(y1[k].y, y1[k].y, s1));
         }
-        s0 += __shfl_xor_sync(FULL, s0, 8);
-        s1 += __shfl_xor_sync(FULL, s1, 8);
-        s0 += __shfl_xor_sync(FULL, s0, 16);
-        s1 += __shfl_xor_sync(FULL, s1, 16);
+#pragma unroll
+        for (int o = LPA; o < 32; o <<= 1) {
+          s0 += __shfl_xor_sync(FULL, s0, o);
+          s1 += __shfl_xor_sync(FULL, s1, o);
+        }
         if (a == 0) {
           Dp[w * G + g] = s0;
-          Dp[w * G + g + 8] = s1;
+          Dp[w * G + g + LPA] = s1;
         }
         __syncthreads();
         if (tid < G) {
@@ -1015,12 +1025,12 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
         if (stepv[g]) {
           const T gm = GAMv[g];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) m0[k] = cfma(gm, y0[k], m0[k]);
+          for (int k = 0; k < E; ++k) m0[k] = cfma(gm, y0[k], m0[k]);
         }
-        if (stepv[g + 8]) {
-          const T gm = GAMv[g + 8];
+        if (stepv[g + LPA]) {
+          const T gm = GAMv[g + LPA];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) m1[k] = cfma(gm, y1[k], m1[k]);
+          for (int k = 0; k < E; ++k) m1[k] = cfma(gm, y1[k], m1[k]);
         }
         // owner: q += gamma phi over its aggregated rows
         for (int e = tid; e < nown * G; e += nthr) {
@@ -1046,12 +1056,12 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   if (blockIdx.x < (unsigned)p.P.n_systems * K)
     KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   if (p.O.iterates) {
-    auto store_m = [&](const T (&mr)[8], int r) {
-      const int cc = g0 + g + 8 * r, chunk = chunk_of(w);
+    auto store_m = [&](const T (&mr)[E], int r) {
+      const int cc = g0 + g + LPA * r, chunk = chunk_of(w);
       if (cc >= K || chunk >= Nt / CH) return;
       T* M = (T*)p.O.iterates + ((size_t)b * K + cc) * Nt + chunk * CH;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) M[8 * (k >> 1) + 2 * a + (k & 1)] = mr[k];
+      for (int k = 0; k < E; ++k) M[2 * NA * (k >> 1) + 2 * a + (k & 1)] = mr[k];
     };
     store_m(m0, 0);
     store_m(m1, 1);
@@ -1076,24 +1086,24 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
 }
 
 // ------------------------------------------------------------------ host side
-inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int* CL, int* NS, int* pcap) {
+inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int G, int* CL, int* NS, int* pcap) {
   const int nch = P.n_antennas / clu::CH;
   *CL = (nch + W - 1) / W;
   *NS = (P.max_support + clu::CH - 2) / clu::CH + 1;  // inbox slots: chunks a row can touch
   *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
   if (*pcap <= 0) return ~size_t(0);
-  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap).total;
+  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap, G).total;
 }
 
-template <int SCH>
+template <int SCH, int GG>
 inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStream_t s) {
-  auto kern = kz_cluster_kernel<SCH>;
+  auto kern = kz_cluster_kernel<SCH, GG>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
   if (CL > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  const int groups = (a.P.n_users + clu::G - 1) / clu::G;
+  const int groups = (a.P.n_users + GG - 1) / GG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.P.n_systems * groups * CL));
   cfg.blockDim = dim3((unsigned)(32 * W));
@@ -1146,30 +1156,34 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   // slice width: 256 antennas (8 warps, one CTA per SM) when it fits, else 128 antennas (two CTAs per SM when
   // they fit); clusters stay within 16 CTAs
-  int CL4, NS4, pc4, CL8, NS8, pc8;
-  const size_t s4 = cluster_smem_bytes(P, scheme, 4, &CL4, &NS4, &pc4);
-  const size_t s8 = cluster_smem_bytes(P, scheme, 8, &CL8, &NS8, &pc8);
+  // candidates in order of preference: 32 rhs x 256-antenna CTAs, 16 rhs x 256, 16 rhs x 128 (two CTAs per
+  // SM when they fit), 16 rhs x 128; clusters stay within 16 CTAs
+  struct Cand { int G, W, CL, NS, pcap; size_t smem; bool two_per_sm; };
+  Cand cands[4] = {{32, 8}, {16, 8}, {16, 4}, {16, 4}};
   const size_t two = (size_t)(smsm / 2 - 1024);
-  int W = 0;
-  static const int forced = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
-  if (forced == 4 || forced == 8) {
-    W = forced;
-  } else if (CL8 <= 16 && s8 <= (size_t)maxsm) {
-    W = 8;
-  } else if (CL4 <= 16 && s4 <= two) {
-    W = 4;
-  } else if (CL4 <= 16 && s4 <= (size_t)maxsm) {
-    W = 4;
+  for (int k = 0; k < 4; ++k) {
+    Cand& cd = cands[k];
+    cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap);
+    cd.two_per_sm = k == 2;
+  }
+  static const int forced_w = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
+  static const int forced_g = getenv("KZ_CLUSTER_G") ? atoi(getenv("KZ_CLUSTER_G")) : 0;
+  int pick = -1;
+  for (int k = 0; k < 4 && pick < 0; ++k) {
+    const Cand& cd = cands[k];
+    if ((forced_w && cd.W != forced_w) || (forced_g && cd.G != forced_g)) continue;
+    if (cd.CL > 16 || cd.smem > (cd.two_per_sm ? two : (size_t)maxsm)) continue;
+    pick = k;
   }
   static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: W4 CL %d pairs %d smem %zu | W8 CL %d pairs %d smem %zu -> W %d\n",
-            scheme, P.n_users, P.n_antennas, CL4, pc4, s4 == ~size_t(0) ? 0 : s4, CL8, pc8,
-            s8 == ~size_t(0) ? 0 : s8, W);
-  if (W == 0) return 0;
-  const int CL = W == 4 ? CL4 : CL8;
-  const size_t smem = W == 4 ? s4 : s8;
-  if (CL > 16 || smem > (size_t)maxsm) return 0;
+    for (int k = 0; k < 4; ++k)
+      fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: G %d W %d CL %d pairs %d smem %zu%s\n", scheme,
+              P.n_users, P.n_antennas, cands[k].G, cands[k].W, cands[k].CL, cands[k].pcap,
+              cands[k].smem == ~size_t(0) ? 0 : cands[k].smem, k == pick ? "  <- picked" : "");
+  if (pick < 0) return 0;
+  const int W = cands[pick].W, CL = cands[pick].CL, GG = cands[pick].G;
+  const size_t smem = cands[pick].smem;
   CluArgs a;
   a.P = P;
   a.R = R;
@@ -1178,17 +1192,27 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.cap = S.max_iters;
   a.every = S.check_every;
   a.eps = (float)S.epsilon;
-  a.NS = W == 4 ? NS4 : NS8;
+  a.NS = cands[pick].NS;
   a.nblk = CL > 1 ? 2 : 1;  // must match the layout hint (HostBatch.slice_pairs)
-  a.pcap = W == 4 ? pc4 : pc8;
+  a.pcap = cands[pick].pcap;
   a.tstop = (int32_t*)(ws + L.total);
   int rc = 0;
-  switch (scheme) {
-    case KZ_GK: rc = cluster_launch<KZ_GK>(a, W, CL, smem, s); break;
-    case KZ_GRK: rc = cluster_launch<KZ_GRK>(a, W, CL, smem, s); break;
-    case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK>(a, W, CL, smem, s); break;
-    case KZ_AHK: rc = cluster_launch<KZ_AHK>(a, W, CL, smem, s); break;
-    case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK>(a, W, CL, smem, s); break;
+  if (GG == 32) {
+    switch (scheme) {
+      case KZ_GK: rc = cluster_launch<KZ_GK, 32>(a, W, CL, smem, s); break;
+      case KZ_GRK: rc = cluster_launch<KZ_GRK, 32>(a, W, CL, smem, s); break;
+      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 32>(a, W, CL, smem, s); break;
+      case KZ_AHK: rc = cluster_launch<KZ_AHK, 32>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 32>(a, W, CL, smem, s); break;
+    }
+  } else {
+    switch (scheme) {
+      case KZ_GK: rc = cluster_launch<KZ_GK, 16>(a, W, CL, smem, s); break;
+      case KZ_GRK: rc = cluster_launch<KZ_GRK, 16>(a, W, CL, smem, s); break;
+      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 16>(a, W, CL, smem, s); break;
+      case KZ_AHK: rc = cluster_launch<KZ_AHK, 16>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 16>(a, W, CL, smem, s); break;
+    }
   }
   if (rc == 1) *launches = lockstep ? 2 : 1;
   return rc;
