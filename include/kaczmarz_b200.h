@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 3
+#define KZ_ABI_VERSION 4
 
 /* status codes */
 #define KZ_OK 0
@@ -99,6 +99,10 @@ typedef struct kz_problem {
      contiguous supports only, 0 = unknown (cluster path disabled) */
   int32_t slice_pairs_128;
   int32_t slice_pairs_256;
+  /* max over systems and CTAs of the rows with at least one piece in one CTA of the same layouts (0 = use
+     min(K, pairs)) */
+  int32_t slice_rows_128;
+  int32_t slice_rows_256;
 } kz_problem;
 
 #define KZ_PROBLEM_CONTIGUOUS 1

@@ -34,6 +34,7 @@ class KzProblem(C.Structure):
         ("non_ptr", P), ("non_idx", P), ("non_union_size", P),
         ("max_support", C.c_int32), ("flags", C.c_int32),
         ("slice_pairs_128", C.c_int32), ("slice_pairs_256", C.c_int32),
+        ("slice_rows_128", C.c_int32), ("slice_rows_256", C.c_int32),
     ]
 
 

@@ -187,16 +187,19 @@ class HostBatch:
             sup = np.diff(self.row_val_ptr)
             h = {"max_support": int(sup.max()) if sup.size else 0,
                  "slice_pairs_128": self.slice_pairs(128) if self.contiguous else 0,
-                 "slice_pairs_256": self.slice_pairs(256) if self.contiguous else 0}
+                 "slice_pairs_256": self.slice_pairs(256) if self.contiguous else 0,
+                 "slice_rows_128": self.slice_pairs(128, rows=True) if self.contiguous else 0,
+                 "slice_rows_256": self.slice_pairs(256, rows=True) if self.contiguous else 0}
             self.__dict__["_hints"] = h
         return h
 
-    def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024) -> int:
+    def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024, rows: bool = False) -> int:
         """Max over systems and CTAs of the (row, `chunk`-antenna chunk) pairs a CTA of the cluster kernel
         holds, for CTAs of `width` antennas in the block-interleaved layout of csrc/kz_solve_cluster.cuh
         (CL = ceil(Nt / width) CTAs; with CL > 1 each CTA owns two blocks of width/2 antennas, block j of
         CTA c at chunk (j CL + c) * (width/2) / chunk).  Contiguous supports only; this is the shared-memory
-        layout bound kz_problem.slice_pairs_* (the kernel traps if it is exceeded)."""
+        layout bound kz_problem.slice_pairs_* (the kernel traps if it is exceeded).  rows=True: the number of
+        rows with at least one piece in the CTA instead (kz_problem.slice_rows_*)."""
         if not self.contiguous or self.n_systems == 0:
             return 0
         w = width // chunk
@@ -215,7 +218,10 @@ class HostBatch:
         for s in range(0, self.n_systems, block):
             a, b = c0[s:s + block, :, None, None], c1[s:s + block, :, None, None]
             n = np.clip(np.minimum(b + 1, hi[None, None]) - np.maximum(a, lo[None, None]), 0, None)
-            best = max(best, int(n.sum(axis=(1, 3)).max()))
+            if rows:
+                best = max(best, int((n.sum(axis=3) > 0).sum(axis=1).max()))
+            else:
+                best = max(best, int(n.sum(axis=(1, 3)).max()))
         return best
 
     def to_device(self, dtype: str = "c128", device=None) -> "DeviceBatch":
@@ -277,6 +283,8 @@ class DeviceBatch:
         p.flags = 1 if self.host.contiguous else 0
         p.slice_pairs_128 = hints["slice_pairs_128"]
         p.slice_pairs_256 = hints["slice_pairs_256"]
+        p.slice_rows_128 = hints["slice_rows_128"]
+        p.slice_rows_256 = hints["slice_rows_256"]
         return p
 
     @classmethod

@@ -97,7 +97,7 @@ struct Plan {
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap, int G) {
+__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap, int G, int rcap) {
   Plan p;
   p.K = K;
   p.W = W;
@@ -106,8 +106,10 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.NS = NS;
   p.pcap = pcap;
   p.nlcap = K < pcap ? K : pcap;
+  if (rcap > 0 && rcap < p.nlcap) p.nlcap = rcap;
   const int KW = (K + 31) / 32;
   const bool ogrk = scheme == KZ_VR_OGRK, oahk = scheme == KZ_VR_OAHK;
+  const bool agg = scheme == KZ_AHK || oahk, greedy = !agg;  // arrays only one family touches are sized 0
   size_t o = 0;
   p.rowS = o; o = al(o + 4 * K);
   p.rowL = o; o = al(o + 4 * K);
@@ -129,22 +131,22 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nlst = p.olst;
   p.H = o; o = al(o + 8 * (size_t)pcap * CH);
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
-  p.Ro = o; o = al(o + 8 * (size_t)p.KO * G);
-  p.Fo = o; o = al(o + 8 * (size_t)p.KO * G);
+  p.Ro = o; o = al(o + (greedy ? 8 * (size_t)p.KO * G : 0));
+  p.Fo = o; o = al(o + (agg ? 8 * (size_t)p.KO * G : 0));
   p.IN = o; o = al(o + 8 * (size_t)p.KO * NS * G);
-  p.Phl = o; o = al(o + 8 * (size_t)p.nlcap * G);
+  p.Phl = o; o = al(o + (agg ? 8 * (size_t)p.nlcap * G : 0));
   p.dloc = o; o = al(o + 4 * (size_t)p.KO * CL);
   p.dlst = o; o = al(o + 4 * (size_t)p.KO * CL);
   p.dcnt = o; o = al(o + 4 * (size_t)p.KO);
-  p.AG4 = o; o = al(o + 16 * (size_t)CL * G);
+  p.AG4 = o; o = al(o + (agg ? 16 * (size_t)CL * G : 0));
   p.GAMv = o; o = al(o + 8 * G);
   p.stepv = o; o = al(o + 4 * G);
   p.BS = o; o = al(o + 4 * (size_t)CL * G);
-  p.BI = o; o = al(o + 4 * (size_t)CL * G);
-  p.SPP = o; o = al(o + 4 * (size_t)CL * G);
-  p.NZP = o; o = al(o + 4 * (size_t)CL * G);
-  p.DY = o; o = al(o + 4 * (size_t)CL * G);
-  p.Dp = o; o = al(o + 4 * (size_t)W * G);
+  p.BI = o; o = al(o + (scheme == KZ_GK ? 4 * (size_t)CL * G : 0));
+  p.SPP = o; o = al(o + (greedy ? 4 * (size_t)CL * G : 0));
+  p.NZP = o; o = al(o + (agg ? 4 * (size_t)CL * G : 0));
+  p.DY = o; o = al(o + (agg ? 4 * (size_t)CL * G : 0));
+  p.Dp = o; o = al(o + (agg ? 4 * (size_t)W * G : 0));
   p.SEL = o; o = al(o + 4 * G);
   p.GAM = o; o = al(o + 8 * G);
   p.done = o; o = al(o + 4 * G);
@@ -174,6 +176,7 @@ struct CluArgs {
   int NS;       // inbox slots per row (= CL: any CTA may hold a piece of a row)
   int nblk;     // chunk blocks per CTA (block-interleaved slices)
   int pcap;     // (row, chunk) pairs reserved per CTA
+  int rcap;     // local rows reserved per CTA (0: min(K, pcap))
   int32_t* tstop;
 };
 
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   const int b = cid / ngroups, grp = cid % ngroups, g0 = grp * G;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int W = nthr >> 5;
-  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap, G);
+  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap, G, p.rcap);
   const int KO = pl.KO, NS = pl.NS, KW = (K + 31) / 32;
   // block-interleaved slices: CTA c owns nblk blocks of Bc = W / nblk chunks, block j at chunk
   // (j CL + c) Bc, so every CTA samples the whole array and the VR-coverage ramps at the array edges no
@@ -1086,13 +1089,15 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
 }
 
 // ------------------------------------------------------------------ host side
-inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int G, int* CL, int* NS, int* pcap) {
+inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int G, int* CL, int* NS, int* pcap,
+                                 int* rcap) {
   const int nch = P.n_antennas / clu::CH;
   *CL = (nch + W - 1) / W;
   *NS = (P.max_support + clu::CH - 2) / clu::CH + 1;  // inbox slots: chunks a row can touch
   *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
+  *rcap = W == 4 ? P.slice_rows_128 : (W == 8 ? P.slice_rows_256 : 0);
   if (*pcap <= 0) return ~size_t(0);
-  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap, G).total;
+  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap, G, *rcap).total;
 }
 
 template <int SCH, int GG>
@@ -1158,12 +1163,12 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   // they fit); clusters stay within 16 CTAs
   // candidates in order of preference: 32 rhs x 256-antenna CTAs, 16 rhs x 256, 16 rhs x 128 (two CTAs per
   // SM when they fit), 16 rhs x 128; clusters stay within 16 CTAs
-  struct Cand { int G, W, CL, NS, pcap; size_t smem; bool two_per_sm; };
+  struct Cand { int G, W, CL, NS, pcap, rcap; size_t smem; bool two_per_sm; };
   Cand cands[4] = {{32, 8}, {16, 8}, {16, 4}, {16, 4}};
   const size_t two = (size_t)(smsm / 2 - 1024);
   for (int k = 0; k < 4; ++k) {
     Cand& cd = cands[k];
-    cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap);
+    cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap, &cd.rcap);
     cd.two_per_sm = k == 2;
   }
   static const int forced_w = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
@@ -1195,6 +1200,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.NS = cands[pick].NS;
   a.nblk = CL > 1 ? 2 : 1;  // must match the layout hint (HostBatch.slice_pairs)
   a.pcap = cands[pick].pcap;
+  a.rcap = cands[pick].rcap;
   a.tstop = (int32_t*)(ws + L.total);
   int rc = 0;
   if (GG == 32) {
