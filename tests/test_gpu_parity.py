@@ -535,3 +535,26 @@ def test_gpu_traces_match_kaczplot_golden_csv():
             big = want_n > 1e-9
             np.testing.assert_allclose(np.asarray(run.nmse_trace)[big], want_n[big], rtol=1e-9)
             np.testing.assert_allclose(run.resid_trace, z[f"{sc}/{seed}/resid"], rtol=1e-8, atol=1e-14)
+
+
+@pytest.mark.parametrize("scheme", ["urk", "grk", "vr-ogrk", "ahk", "vr-oahk"])
+def test_bench_workload_c64_vs_c128_same_draws(scheme):
+    """The benchmark workload (cfg2, T=200, on-device Philox draws) on 48 realizations: the complex64
+    throughput kernels against the complex128 oracle-mode kernels fed the same Philox draws — NMSE vs RZF
+    and sum-rate per system within the c64 criterion."""
+    kz = _kz()
+    ch = kz.generate("cfg2", range(48))
+    host = kz.HostBatch.from_contiguous(ch)
+    d64, d128 = host.to_device("c64"), host.to_device("c128")
+    rz = kz.rzf_batched(d128)
+    rng = ("philox", 2024) if scheme in kz.STOCHASTIC_SCHEMES else None
+    o64 = kz.run_precoding_batched(scheme, d64, max_iters=200, rng=rng, v_ref=rz["v"], beta_ref=rz["beta"],
+                                   rates=True)
+    o128 = kz.run_precoding_batched(scheme, d128, max_iters=200, rng=rng, v_ref=rz["v"], beta_ref=rz["beta"],
+                                    rates=True)
+    n64, n128 = o64["nmse"].cpu().numpy(), o128["nmse"].cpu().numpy()
+    above = n128 >= 1e-5
+    if scheme == "urk" or above.any():
+        np.testing.assert_allclose(n64[above], n128[above], rtol=1e-3)
+    assert np.all(n64[~above] <= 1e-6), n64[~above].max()
+    np.testing.assert_allclose(o64["sum_rate"].cpu().numpy(), o128["sum_rate"].cpu().numpy(), rtol=1e-3)
