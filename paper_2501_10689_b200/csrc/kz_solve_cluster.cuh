@@ -1,22 +1,23 @@
 // Cluster kernel for large arrays (complex64): gk, grk, vr-ogrk, ahk, vr-oahk over contiguous VRs, fixed T
 // (LOCKSTEP, epsilon = 0) or a per-rhs residual tolerance (RESIDUAL, solve / solve_all semantics).
 //
-// One thread-block cluster = one system x 16 right-hand sides.  CTA c of the cluster owns the antenna slice
-// [32 W c, 32 W (c + 1)) (warp w: the 32-antenna chunk W c + w) and keeps in shared memory only the pieces
-// of the rows that touch its slice, zero padded to whole chunks; the iterate of its 16 rhs on the slice stays
-// in registers: lane (a, g), a = lane >> 3, g = lane & 7, holds rhs g and g + 8 on the antennas
-// 8j + 2a + e (j < 4, e < 2) of its warp's chunk, so each h element loaded feeds two rhs (the SMEM/FFMA
-// balance of the wide kernel, csrc/kz_solve_wide.cuh) while the per-CTA footprint is half the wide layout's.
+// One thread-block cluster = one system x G right-hand sides (G = 32 or 16).  CTA c of the cluster owns W
+// 32-antenna chunks in two blocks spread over the array (block j at chunk (j CL + c) W/2: every CTA samples
+// the whole array, so the VR coverage ramps at the edges do not unbalance the cluster) and keeps in shared
+// memory only the pieces of the rows that touch its chunks, zero padded to whole chunks.  The iterate of its
+// rhs stays in registers: G = 32: lane (a, g), a = lane >> 4, holds rhs g and g + 16 on 16 antennas of its
+// warp's chunk (the wide kernel's mapping); G = 16: a = lane >> 3, rhs g and g + 8 on 8 antennas.  Each h
+// element loaded feeds two rhs (the SMEM/FFMA balance of csrc/kz_solve_wide.cuh).
 // Rows are owned in contiguous blocks of KO = ceil(K / CL): the owner keeps q_i and r_i.
 //
 // Per iteration (grk; the other schemes follow the same pattern):
-//   refresh  every CTA: per-(row, chunk) partials -> P; fixed-order sum over the slice's chunks, pushed into
-//            the owner's inbox IN[row][slice][rhs] with a DSMEM store                     -- cluster barrier
-//   finalise owner: r_i = e - sum_slices IN - xi q_i (fixed order), block sums of |r_i|^2 pushed to every CTA
+//   refresh  every CTA: each (row, chunk) partial goes straight into the owner's inbox IN[row][chunk slot][rhs]
+//            (local store or DSMEM st.shared::cluster, drained while the next pieces compute)  -- cluster barrier
+//   finalise owner: r_i = e - sum_slots IN - xi q_i (chunk order), block sums of |r_i|^2 pushed to every CTA
 //                                                                                            -- cluster barrier
 //   select   every CTA: the same prefix over the block sums -> the block holding the draw; its owner picks the
 //            row, updates q_i, pushes (row, gamma) to every CTA                              -- cluster barrier
-//   project  every CTA: m += gamma h on its slice.
+//   project  every CTA: m += gamma h on its chunks.
 // Residual mode fuses the convergence test into the next refresh: ||r_true||^2 of the state after step t is
 // the sum of the block sums of step t + 1 (grk / gk / ahk), so the stopping rule costs no extra pass; vr-oahk
 // refreshes all rows (instead of its orthogonal group) at the start of each iteration for the same purpose.
