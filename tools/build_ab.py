@@ -1,0 +1,30 @@
+"""Build libkaczmarz_b200_ab.so from the current sources with some csrc files replaced (same-box A/B):
+
+    python tools/build_ab.py csrc/kz_solve_wide.cuh=/tmp/old_wide.cuh [...]
+then run the same command with KZ_LIB_VARIANT=ab (A) and without (B) in one gpurun call.
+"""
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2501_10689_b200 import build as B  # noqa: E402
+
+tmp = tempfile.mkdtemp()
+src = os.path.join(tmp, "pkg", "csrc")  # keeps csrc/../../include valid
+shutil.copytree(B.CSRC, src)
+shutil.copytree(os.path.join(ROOT, "include"), os.path.join(tmp, "include"))
+for arg in sys.argv[1:]:
+    rel, path = arg.split("=", 1)
+    shutil.copy(path, os.path.join(tmp, "pkg", rel))
+out = B.lib_path("ab")
+cmd = [B._nvcc(), *B.NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *[os.path.join(src, s) for s in B.SOURCES],
+       "-o", out]
+res = subprocess.run(cmd, capture_output=True, text=True)
+if res.returncode:
+    sys.stderr.write(res.stderr[-4000:])
+    sys.exit(1)
+print(out)
