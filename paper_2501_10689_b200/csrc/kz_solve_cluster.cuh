@@ -1165,9 +1165,9 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   // candidates in order of preference: 32 rhs x 256-antenna CTAs, 16 rhs x 256, 16 rhs x 128 (two CTAs per
   // SM when they fit), 16 rhs x 128; clusters stay within 16 CTAs
   struct Cand { int G, W, CL, NS, pcap, rcap; size_t smem; bool two_per_sm; };
-  Cand cands[4] = {{32, 8}, {16, 8}, {16, 4}, {16, 4}};
+  Cand cands[5] = {{32, 8}, {16, 8}, {16, 4}, {16, 4}, {32, 4}};
   const size_t two = (size_t)(smsm / 2 - 1024);
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 5; ++k) {
     Cand& cd = cands[k];
     cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap, &cd.rcap);
     cd.two_per_sm = k == 2;
@@ -1175,7 +1175,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   static const int forced_w = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
   static const int forced_g = getenv("KZ_CLUSTER_G") ? atoi(getenv("KZ_CLUSTER_G")) : 0;
   int pick = -1;
-  for (int k = 0; k < 4 && pick < 0; ++k) {
+  for (int k = 0; k < 5 && pick < 0; ++k) {
     const Cand& cd = cands[k];
     if ((forced_w && cd.W != forced_w) || (forced_g && cd.G != forced_g)) continue;
     if (cd.CL > 16 || cd.smem > (cd.two_per_sm ? two : (size_t)maxsm)) continue;
@@ -1183,7 +1183,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   }
   static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
   if (verbose)
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 5; ++k)
       fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: G %d W %d CL %d pairs %d smem %zu%s\n", scheme,
               P.n_users, P.n_antennas, cands[k].G, cands[k].W, cands[k].CL, cands[k].pcap,
               cands[k].smem == ~size_t(0) ? 0 : cands[k].smem, k == pick ? "  <- picked" : "");
