@@ -100,6 +100,14 @@ template <class T> __device__ __forceinline__ T from_d2(double2 a) {
 }
 template <class T> __device__ __forceinline__ T czero() { return Cx<T>::make(0, 0); }
 
+// asynchronous global -> shared copy of one 8-byte element (LDGSTS), zero-filled when !valid: the setup
+// loops issue every row piece without waiting on each load (cp_async_wait_all + a barrier before use)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // numpy SIMD complex abs (verified bit-exact against np.abs on AVX-512 hosts).
 __device__ __forceinline__ double np_cabs(double re, double im) {
   double a = fabs(re), b = fabs(im);

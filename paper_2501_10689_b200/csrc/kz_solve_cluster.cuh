@@ -91,7 +91,7 @@ __device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
 
 struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
-  size_t rowS, rowL, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
+  size_t rowS, rowL, rvo, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
       misc, total;
 };
@@ -114,6 +114,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   size_t o = 0;
   p.rowS = o; o = al(o + 4 * K);
   p.rowL = o; o = al(o + 4 * K);
+  p.rvo = o; o = al(o + 8 * (size_t)K);
   p.c0 = o; o = al(o + 4 * K);
   p.c1 = o; o = al(o + 4 * K);
   p.en = o; o = al(o + 4 * K);
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
 
   int* rowS = (int*)(sm + pl.rowS);
   int* rowL = (int*)(sm + pl.rowL);
+  long long* rvo = (long long*)(sm + pl.rvo);  // heff offset of row i (row_val_ptr)
   int* c0 = (int*)(sm + pl.c0);
   int* c1 = (int*)(sm + pl.c1);
   float* en = (float*)(sm + pl.en);
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     int s = p.P.seg_start[sg], L = p.P.seg_len[sg];
     rowS[i] = s;
     rowL[i] = L;
+    rvo[i] = p.P.row_val_ptr[r];
     c0[i] = s / CH;
     c1[i] = (s + L - 1) / CH;
     en[i] = (float)p.P.row_energy[r];
@@ -330,19 +333,20 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   const int NL = misc[1], npairs = misc[2];
   if (npairs > p.pcap || NL > pl.nlcap) __trap();  // layout hint violated: fail loudly
   // row pieces -> shared memory, zero padded to whole chunks: one warp per (local row, piece), lanes over
-  // the 32 antennas of the piece (coalesced 256 B loads)
+  // the 32 antennas of the piece (coalesced 256 B), all issued as asynchronous copies (no load latency per
+  // piece; the row offsets come from shared memory, so no dependent global load either)
   {
-    int n = 0, pc = 0;  // this warp's current (local row, piece), advanced by W pieces at a time
+    int n = 0;  // this warp's current local row, advanced by W pieces at a time
     for (int q = w; q < npairs; q += W) {
       while (n < NL - 1 && lh[n + 1] <= q * CH) ++n;
-      pc = q - (lh[n] >> 5);
+      const int pc = q - (lh[n] >> 5);
       const int i = lrow[n];
       const int ant = chunk_of((lcc[n] & 0xFF) + pc) * CH + lane;
       const int s = rowS[i];
-      Hs[q * CH + lane] = (ant >= s && ant < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (ant - s)]
-                                                           : make_float2(0.f, 0.f);
+      const bool in = ant >= s && ant < s + rowL[i];
+      cp_async8(Hs + q * CH + lane, heff + rvo[i] + (in ? ant - s : 0), in);
     }
-    (void)pc;
+    cp_async_wait_all();
   }
   // per-chunk piece lists (ascending rows)
   auto build_list = [&](int* ptr, int2* out, int which, int base0) {
@@ -428,9 +432,17 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   }
   long long costO = 0, costN = 0;
   int nN = 0;
-  for (int i = 0; i < K; ++i) {
-    if (inset[i] == 1) costO += 8LL * rowL[i] + 4;
-    if (inset[i] == 2) { costN += 8LL * rowL[i]; ++nN; }
+  if constexpr (AGG) {  // lanes over rows, every warp the same fixed-order reduction
+    for (int i = lane; i < K; i += 32) {
+      if (inset[i] == 1) costO += 8LL * rowL[i] + 4;
+      if (inset[i] == 2) { costN += 8LL * rowL[i]; ++nN; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      costO += __shfl_xor_sync(FULL, costO, o);
+      costN += __shfl_xor_sync(FULL, costN, o);
+      nN += __shfl_xor_sync(FULL, nN, o);
+    }
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
   cluster_sync();  // every CTA of the cluster is resident and initialised before any DSMEM traffic

@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
     const T* heff = (const T*)p.P.heff;
     for (int i = w; i < K; i += nthr >> 5) {
       const T* src = heff + p.P.row_val_ptr[(size_t)b * K + i];
-      for (int e = lane; e < rowL[i]; e += 32) Hs[hoff[i] + e] = src[e];
+      for (int e = lane; e < rowL[i]; e += 32) cp_async8(Hs + hoff[i] + e, src + e, true);  // no wait per row
     }
+    cp_async_wait_all();
   }
   for (int n = lane; n < Nt; n += 32) Ms[n] = make_float2(0.f, 0.f);
   for (int i = lane; i < K; i += 32) Qs[i] = make_float2(0.f, 0.f);

@@ -1,7 +1,8 @@
 """Build libkaczmarz_b200_ab.so from the current sources with some csrc files replaced (same-box A/B):
 
     python tools/build_ab.py csrc/kz_solve_wide.cuh=/tmp/old_wide.cuh [...]
-then run the same command with KZ_LIB_VARIANT=ab (A) and without (B) in one gpurun call.
+then run the same command with KZ_LIB_VARIANT=ab (A) and without (B) in one gpurun call
+(--name=X as the first argument builds libkaczmarz_b200_X.so for a third arm, KZ_LIB_VARIANT=X).
 """
 import os
 import shutil
@@ -17,13 +18,18 @@ tmp = tempfile.mkdtemp()
 src = os.path.join(tmp, "pkg", "csrc")  # keeps csrc/../../include valid
 shutil.copytree(B.CSRC, src)
 shutil.copytree(os.path.join(ROOT, "include"), os.path.join(tmp, "include"))
-for arg in sys.argv[1:]:
+name = "ab"
+args = sys.argv[1:]
+if args and args[0].startswith("--name="):
+    name = args.pop(0).split("=", 1)[1]
+for arg in args:
     rel, path = arg.split("=", 1)
     shutil.copy(path, os.path.join(tmp, "pkg", rel))
-out = B.lib_path("ab")
+out = B.lib_path(name)
 cmd = [B._nvcc(), *B.NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *[os.path.join(src, s) for s in B.SOURCES],
        "-o", out]
 res = subprocess.run(cmd, capture_output=True, text=True)
+open(out + ".log", "w").write(res.stderr)
 if res.returncode:
     sys.stderr.write(res.stderr[-4000:])
     sys.exit(1)

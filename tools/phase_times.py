@@ -23,15 +23,27 @@ ap.add_argument("--batch", type=int, default=296)
 ap.add_argument("--iters", type=int, default=100)
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--cluster-w", type=int, default=0, help="warps per CTA of the cluster kernel (0: wide/chunked)")
+ap.add_argument("--cluster-g", type=int, default=16, help="rhs per cluster of the cluster kernel (KZ_VERBOSE=1 shows the pick)")
+ap.add_argument("--residual", type=float, default=0.0, help="residual-tolerance mode (solve_all semantics) instead of fixed T")
 a = ap.parse_args()
 cfg = kz.CONFIGS[a.config]
 ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
 dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
 rng = ("philox", 3) if a.scheme in kz.STOCHASTIC_SCHEMES else None
-res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
+if a.residual:
+    def run(ws=None):
+        return kz.solve_batch(dev, a.scheme, mode="residual", epsilon=a.residual, max_iters=10000 * dev.n_users,
+                              check_every=1, rng=rng, workspace=ws)
+else:
+    def run(ws=None):
+        return kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng, workspace=ws)
+res = run()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng, workspace=res.workspace)
+res = run(res.workspace)
+if a.residual:
+    a.iters = max(1, int(round(res.iters.double().mean().item())))
+    print(f"residual mode: mean iters {res.iters.double().mean().item():.2f}, max {res.iters.max().item()}")
 e1.record()
 torch.cuda.synchronize()
 B, K, Nt = dev.n_systems, dev.n_users, dev.n_antennas
@@ -48,7 +60,7 @@ G = (32 if K > 16 and not os.environ.get("KZ_CHUNKED_C64") else 16) if a.dtype =
 ncta = B * ((K + G - 1) // G)
 if a.cluster_w:
     CL = -(-Nt // (32 * a.cluster_w))
-    ncta = min(B * K, B * -(-K // 16) * CL)
+    ncta = min(B * K, B * -(-K // a.cluster_g) * CL)
 raw = ws[off:off + ncta * 44 * 8].view(torch.int64).view(ncta, 44).cpu().numpy().astype(np.float64)
 ph = raw[:, :12].copy()
 wst = raw[:, 12:12 + Nt // 32] / a.iters  # per-warp refresh-end cycles per iteration

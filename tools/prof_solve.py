@@ -20,15 +20,25 @@ ap.add_argument("--dtype", default="c64")
 ap.add_argument("--batch", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--residual", type=float, default=0.0, help="residual tolerance (solve_all semantics); 0: fixed T")
 a = ap.parse_args()
 cfg = kz.CONFIGS[a.config]
 ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
 dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
 rng = ("philox", 7) if a.scheme in kz.STOCHASTIC_SCHEMES else None
+times = []
 for r in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
+    if a.residual:
+        res = kz.solve_batch(dev, a.scheme, mode="residual", epsilon=a.residual, max_iters=10000 * dev.n_users,
+                             check_every=1, rng=rng)
+    else:
+        res = kz.solve_batch(dev, a.scheme, mode="lockstep", max_iters=a.iters, rng=rng)
     e1.record()
     torch.cuda.synchronize()
-    print(f"{a.scheme} {a.dtype} B={a.batch} T={a.iters}: {e0.elapsed_time(e1):.3f} ms (launches {res.launches})")
+    times.append(e0.elapsed_time(e1))
+    print(f"{a.scheme} {a.dtype} B={a.batch} T={a.iters}: {times[-1]:.3f} ms (launches {res.launches})")
+times.sort()
+print(f"{a.scheme} {a.dtype} B={a.batch} T={a.iters}: min {times[0]:.3f} ms, median {times[len(times) // 2]:.3f} ms "
+      f"over {len(times)} (launches {res.launches})")
