@@ -189,6 +189,19 @@ def measured_fp32_peak():
     return 2 * 148 * 128 * 1.965e9 / 1e12, "nominal 148 SM x 128 FFMA/clk x 1.965 GHz"
 
 
+def measured_fp32_reg3_peak():
+    """FP32 FFMA rate when every FMA reads three registers (the kernels' form), tools/fma_forms.cu."""
+    try:
+        with open(MICRO) as fh:
+            for line in fh:
+                d = json.loads(line)
+                if d.get("probe") == "FFMA reg3":
+                    return float(d["chip_TFLOPs_fp32"])
+    except (OSError, ValueError):
+        pass
+    return None
+
+
 def measured_smem_peak():
     try:
         with open(MICRO) as fh:
@@ -331,6 +344,7 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     fp32_peak, fp32_src = measured_fp32_peak()
+    reg3_peak = measured_fp32_reg3_peak()
     smem_peak = measured_smem_peak()
     t_dom = avg[dom] / 1e3
     tflops = 8.0 * elems_dom / t_dom / 1e12
@@ -433,6 +447,11 @@ def main():
                                  "2 rhs in registers (8 FFMA per complex element), so the launch is CUDA-core "
                                  "FMA bound (SURVEY 8(d): report the FMA roofline); flops = 8 x streamed H_eff "
                                  "elements per rhs-iteration",
+                         "ffma_3reg_view": ({"peak_TFLOPs": reg3_peak, "frac": tflops / reg3_peak,
+                                             "peak_source": "tools/fma_forms.cu (profiles/r01_microbench.json): "
+                                                            "FFMA with three register operands issues at 0.81/clk "
+                                                            "per SMSP vs 0.97 for the immediate form"}
+                                            if reg3_peak else None),
                          "smem_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": smem_peak},
                          "hbm_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": hbm_peak,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},

@@ -78,6 +78,9 @@ __device__ __forceinline__ void st_remote(float4* p, int rank, float4 v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ void st_cluster(uint32_t addr, float2 v) {  // addr from remote() (any CTA, own included)
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
 __device__ __forceinline__ int ld_remote(const int* p, int rank) {
   int v;
   asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(remote(p, rank)) : "memory");
@@ -91,7 +94,7 @@ __device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
 
 struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
-  size_t rowS, rowL, rvo, c0, c1, en, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
+  size_t rowS, rowL, rvo, c0, c1, en, ien, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
       misc, total;
 };
@@ -118,6 +121,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.c0 = o; o = al(o + 4 * K);
   p.c1 = o; o = al(o + 4 * K);
   p.en = o; o = al(o + 4 * K);
+  p.ien = o; o = al(o + 4 * K);
   p.inset = o; o = al(o + K);
   p.loc = o; o = al(o + 4 * K);
   p.cost = o; o = al(o + (ogrk ? 8 * K : 0));
@@ -222,6 +226,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   int* c0 = (int*)(sm + pl.c0);
   int* c1 = (int*)(sm + pl.c1);
   float* en = (float*)(sm + pl.en);
+  float* ien = (float*)(sm + pl.ien);  // 1 / e_i: aggregation / block-step weights by multiplication
   uint8_t* inset = (uint8_t*)(sm + pl.inset);
   int* loc = (int*)(sm + pl.loc);
   long long* cost = (long long*)(sm + pl.cost);
@@ -245,7 +250,9 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   T* Phl = (T*)(sm + pl.Phl);  // phi / gamma of the local rows, pushed by their owners
   int* dloc = (int*)(sm + pl.dloc);  // [owned row][CTA] -> local row index of the row in that CTA (-1: none)
   // (inbox: IN[owned row][chunk slot][rhs], slot = chunk - first chunk of the row, NS = max chunks per row)
-  int* dlst = (int*)(sm + pl.dlst);  // [owned row][k] -> k-th CTA holding pieces of the row (ascending)
+  // [owned row][k] -> cluster shared address of Phl[local row] in the k-th CTA holding pieces of the row
+  // (ascending CTAs; the phi push is one precomputed address per destination)
+  uint32_t* dlst = (uint32_t*)(sm + pl.dlst);
   int* dcnt = (int*)(sm + pl.dcnt);
   float4* AG4 = (float4*)(sm + pl.AG4);
   T* GAMv = (T*)(sm + pl.GAMv);
@@ -284,6 +291,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     c0[i] = s / CH;
     c1[i] = (s + L - 1) / CH;
     en[i] = (float)p.P.row_energy[r];
+    ien[i] = (float)(1.0 / p.P.row_energy[r]);
     inset[i] = 0;
   }
   __syncthreads();
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   for (int il = tid; il < nown; il += nthr) {
     int n = 0;
     for (int d = 0; d < CL; ++d)
-      if (dloc[il * CL + d] >= 0) dlst[il * CL + n++] = d;
+      if (dloc[il * CL + d] >= 0) dlst[il * CL + n++] = remote(Phl + (size_t)dloc[il * CL + d] * G, d);
     dcnt[il] = n;
   }
   __syncthreads();
@@ -550,11 +558,10 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   };
   auto push_phi = [&](int il, int gg, T v) {
     const int nd = dcnt[il];
-    for (int k = 0; k < nd; ++k) {
-      const int d = dlst[il * CL + k];
-      T* dst = Phl + dloc[il * CL + d] * G + gg;
-      if (d == c) *dst = v; else st_remote(dst, d, v);
-    }
+    const uint32_t* da = dlst + il * CL;
+    const uint32_t off = 8u * (uint32_t)gg;
+#pragma unroll 4
+    for (int k = 0; k < nd; ++k) st_cluster(da[k] + off, v);
   };
   // owner: phi = r / e on its rows of set `which` (0 = all), pushed to the slices; block partials of
   // vdot(phi, r), ||phi||^2, ||r||^2 and any(phi != 0) pushed to every CTA (solvers.py:240-254, 274)
@@ -568,7 +575,8 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
           const int i = o_lo + il;
           if (which && inset[i] != which) continue;
           const T r = oresid(il, gg, which == 0);
-          const T ph = make_float2(r.x / en[i], r.y / en[i]);
+          const float ie = ien[i];
+          const T ph = make_float2(r.x * ie, r.y * ie);
           Fo[xo(il, gg)] = ph;
           push_phi(il, gg, ph);
           nz |= (ph.x != 0.f || ph.y != 0.f);
@@ -856,7 +864,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
             if (!residual && inset[i] != 1) continue;
             const T r = oresid(il, gg, false);
             if (inset[i] == 1) {
-              const T gm = make_float2(r.x / en[i], r.y / en[i]);
+              const T gm = make_float2(r.x * ien[i], r.y * ien[i]);
               Fo[xo(il, gg)] = gm;
               push_phi(il, gg, gm);
             }
