@@ -20,6 +20,8 @@ from dataclasses import dataclass
 
 import ctypes as C
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -40,6 +42,13 @@ def _union_size_intervals(start, length):
             tot += cur_e - cur_s
             cur_s, cur_e = int(a), int(b)
     return tot + cur_e - cur_s
+
+
+def cluster_blocks(warps: int) -> int:
+    """Chunk blocks per CTA of the cluster kernel's interleaved layout (must match kz_solve_cluster.cuh:
+    KZ_CLUSTER_NBLK, default 2)."""
+    n = int(os.environ.get("KZ_CLUSTER_NBLK", "2"))
+    return n if n > 0 and warps % n == 0 else 2
 
 
 @dataclass
@@ -193,7 +202,7 @@ class HostBatch:
             self.__dict__["_hints"] = h
         return h
 
-    def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024, rows: bool = False) -> int:
+    def slice_pairs(self, width: int, chunk: int = 32, block: int = 1024, rows: bool = False) -> int:  # noqa: C901
         """Max over systems and CTAs of the (row, `chunk`-antenna chunk) pairs a CTA of the cluster kernel
         holds, for CTAs of `width` antennas in the block-interleaved layout of csrc/kz_solve_cluster.cuh
         (CL = ceil(Nt / width) CTAs; with CL > 1 each CTA owns two blocks of width/2 antennas, block j of
@@ -205,7 +214,7 @@ class HostBatch:
         w = width // chunk
         nch = self.n_antennas // chunk
         ncl = -(-nch // w)
-        nblk = 2 if ncl > 1 else 1
+        nblk = cluster_blocks(w) if ncl > 1 else 1
         bc = w // nblk
         # chunk ranges [lo, hi) of block j of CTA c
         lo = np.array([[(j * ncl + c) * bc for j in range(nblk)] for c in range(ncl)], dtype=np.int64)

@@ -1219,7 +1219,9 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.every = S.check_every;
   a.eps = (float)S.epsilon;
   a.NS = cands[pick].NS;
-  a.nblk = CL > 1 ? 2 : 1;  // must match the layout hint (HostBatch.slice_pairs)
+  static const int env_nblk = getenv("KZ_CLUSTER_NBLK") ? atoi(getenv("KZ_CLUSTER_NBLK")) : 2;
+  const int nb = env_nblk > 0 && W % env_nblk == 0 ? env_nblk : 2;
+  a.nblk = CL > 1 ? nb : 1;  // must match the layout hint (HostBatch.slice_pairs / batch.cluster_blocks)
   a.pcap = cands[pick].pcap;
   a.rcap = cands[pick].rcap;
   a.tstop = (int32_t*)(ws + L.total);
