@@ -13,6 +13,7 @@ import io
 import json
 import os
 import subprocess
+import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -45,6 +46,67 @@ def to_bytes(v, unit):
 def to_ms(v, unit):
     return v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
                 "second": 1e3, "s": 1e3}.get(unit, 1.0)
+
+
+# (capture, title, kernel symbol substring for the line map, output suffix)
+FULL_SETS = [
+    ("full_vroahk", "kz_wide_kernel<6> (vr-oahk), cfg2 c64 B=1024 T=50", "kz_wide_kernelILi6E", "ncu_wide_vroahk"),
+    ("full_wide_grk", "kz_wide_kernel<4> (grk), cfg2 c64 B=1024 T=50", "kz_wide_kernelILi4E", "ncu_wide_grk"),
+    ("full_wide_ahk", "kz_wide_kernel<5> (ahk), cfg2 c64 B=1024 T=50", "kz_wide_kernelILi5E", "ncu_wide_ahk"),
+    ("full_cfg3_vr-oahk", "kz_cluster_kernel<6,16> (vr-oahk), cfg3 c64 B=128 T=20", "kz_cluster_kernelILi6ELi16",
+     "ncu_cluster_cfg3_vroahk"),
+    ("full_cfg5_ahk", "kz_cluster_kernel<5,32> (ahk), cfg5 c64 B=64 T=20", "kz_cluster_kernelILi5ELi32",
+     "ncu_cluster_cfg5_ahk"),
+]
+KEEP = ("Duration", "Elapsed Cycles", "SM Frequency", "Compute (SM) Throughput", "Memory Throughput",
+        "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy", "L1/TEX Hit Rate", "No Eligible",
+        "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction", "Executed Instructions",
+        "Registers Per Thread", "Dynamic Shared Memory Per Block", "Achieved Occupancy")
+
+
+def full_summary(rep, title, ksub):
+    """Details-page metrics, stall samples grouped by straight-line SASS blocks (same execution count: one
+    block is one loop body / phase), and the hottest source lines (tools/sass_lines.py, current build)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    lines = [f"# ncu --set full --clock-control none --import-source on, {title} (tools/prof_solve.py)",
+             f"# source: {os.path.relpath(rep, ROOT)}", ""]
+    for row in csv.DictReader(io.StringIO(raw)):
+        if row.get("Metric Name") in KEEP:
+            lines.append(f"{row['Section Name']} | {row['Metric Name']} | {row['Metric Unit']} | "
+                         f"{row['Metric Value']}")
+    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                          capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(sass)))
+    if len(rows) > 2:
+        hdr = rows[1]
+        col = {n: i for i, n in enumerate(hdr)}
+        data = rows[2:]
+        S = "Warp Stall Sampling (All Samples)"
+        tot = sum(float(r[col[S]] or 0) for r in data) or 1.0
+        base = int(data[0][col["Address"]], 16)
+        blocks = []
+        for r in data:
+            ex = int(float(r[col["Instructions Executed"]] or 0))
+            ad = int(r[col["Address"]], 16) - base
+            st = float(r[col[S]] or 0)
+            if blocks and blocks[-1][2] == ex:
+                blocks[-1][1] = ad
+                blocks[-1][3] += st
+                blocks[-1][4] += 1
+            else:
+                blocks.append([ad, ad, ex, st, 1])
+        lines += ["", "## stall samples by SASS block (contiguous instructions with one execution count)",
+                  "   offsets            executions  instrs  stall%"]
+        for b in sorted(blocks, key=lambda x: -x[3])[:14]:
+            lines.append(f"  {b[0]:#07x}-{b[1]:#07x} {b[2]:12d} {b[4]:7d}  {100 * b[3] / tot:5.1f}")
+        tmp = rep + ".sass.csv"
+        with open(tmp, "w") as fh:
+            fh.write(sass)
+        lib = os.path.join(ROOT, "paper_2501_10689_b200", "libkaczmarz_b200.so")
+        hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_lines.py"), lib, ksub, tmp, "15"],
+                             capture_output=True, text=True).stdout
+        lines += ["", "## hottest source lines (tools/sass_lines.py against the build that was profiled)", hot.rstrip()]
+    return "\n".join(lines)
 
 
 def main():
@@ -95,22 +157,12 @@ def main():
         with open(os.path.join(prof, f"{a.tag}_launches_summary.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
         subprocess.run(["cp", lpath, os.path.join(prof, f"{a.tag}_launches.csv")])
-    # full-set capture of the dominant kernel
-    rep = os.path.join(a.dir, "full_vroahk.ncu-rep")
-    if os.path.exists(rep):
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-        keep = ("Duration", "Elapsed Cycles", "SM Frequency", "Compute (SM) Throughput", "Memory Throughput",
-                "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy", "L1/TEX Hit Rate", "No Eligible",
-                "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction", "Executed Instructions",
-                "Registers Per Thread", "Dynamic Shared Memory Per Block", "Achieved Occupancy")
-        lines = ["# ncu --set full --clock-control none, kz_wide_kernel<6> (vr-oahk), cfg2 c64 B=1024 T=50 "
-                 "(tools/prof_solve.py)", f"# source: {os.path.relpath(rep, ROOT)}", ""]
-        for row in csv.DictReader(io.StringIO(raw)):
-            if row.get("Metric Name") in keep:
-                lines.append(f"{row['Section Name']} | {row['Metric Name']} | {row['Metric Unit']} | "
-                             f"{row['Metric Value']}")
-        with open(os.path.join(prof, f"{a.tag}_ncu_wide_vroahk.txt"), "w") as fh:
-            fh.write("\n".join(lines) + "\n")
+    # full-set captures: key metrics, stall samples by straight-line SASS block, hottest source lines
+    for rep_name, title, ksub, out in FULL_SETS:
+        rep = os.path.join(a.dir, rep_name + ".ncu-rep")
+        if os.path.exists(rep):
+            with open(os.path.join(prof, f"{a.tag}_{out}.txt"), "w") as fh:
+                fh.write(full_summary(rep, title, ksub) + "\n")
     print(json.dumps(traffic))
 
 
