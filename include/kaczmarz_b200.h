@@ -10,6 +10,9 @@
  *                   solve / solve_all (solvers.py:460-537)
  *                   InstanceRun.step + step primitives (solvers.py:143-423)
  *   kz_rzf       <- rzf_precoder / auxiliary_matrix (pkg/src/kaczprec/rzf.py:38-83)
+ *   kz_residual_refresh / kz_project_rows / kz_ahk_step
+ *                <- residual_refresh, rk_step + orthogonal_block_step, ahk_step (solvers.py:143-309, 312-332):
+ *                   the per-call step primitives on one rhs of one system (InstanceRun.step's building blocks)
  *   kz_epilogue  <- assemble_dense / assemble_vr (pkg/src/kaczprec/assembly.py:51-92),
  *                   nmse / spectral_efficiency (pkg/src/kaczprec/metrics.py:44-78)
  *
@@ -33,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 4
+#define KZ_ABI_VERSION 5
 
 /* status codes */
 #define KZ_OK 0
@@ -218,6 +221,29 @@ int kz_partition_counts(const kz_drop* drop, int32_t* coupled_cnt, int32_t* orth
 int kz_partition_fill(const kz_drop* drop, const int32_t* coupled_ptr, const int32_t* orth_ptr,
                       const int32_t* non_ptr, int32_t* coupled_idx, int32_t* orth_idx, int32_t* non_idx,
                       void* stream);
+
+/*
+ * Per-call step primitives on ONE right-hand side of system `system` of `prob` (solvers.py:143-332).  The
+ * state is SolverState (solvers.py:112-136) in device memory, prob->dtype complex: col [Nt], coef [K],
+ * resid [K]; rows / span are device int32 index arrays.  Flop charges and iteration / no-op counters are the
+ * caller's (they depend only on sizes, metrics.py:25-41).
+ */
+/* residual_refresh(state, sys, rows, use_vr) (solvers.py:143-170): resid_i = s_i - h_i^H col - reg coef_i for
+   the n_rows rows (rows = NULL: i = 0..n_rows-1); dense = 1 evaluates the h_adj @ col form (:149-153). */
+int kz_residual_refresh(const kz_problem* prob, int32_t system, int32_t rhs, const void* col, const void* coef,
+                        void* resid, const int32_t* rows, int32_t n_rows, int32_t dense, void* stream);
+/* rk_step (solvers.py:173-188) for n_rows = 1, orthogonal_block_step (:312-332) for a row list: per row, in
+   order, gamma = resid_i / e_i, col[Gamma_i] += gamma h_i, coef_i += gamma, resid_i = 0. */
+int kz_project_rows(const kz_problem* prob, int32_t system, void* col, void* coef, void* resid,
+                    const int32_t* rows, int32_t n_rows, void* stream);
+/* ahk_step (solvers.py:257-309) with weights phi [K] (complex, prob->dtype) on the sorted rows: y = sum phi_i h_i,
+   den = ||y||^2 + reg ||phi_rows||^2; den == 0 leaves the state untouched and writes *stepped = 0 (device
+   int32); else gamma = phi_rows^H resid_rows / den, col[span] += gamma y[span] (span = the support union, or
+   NULL for every antenna), coef[rows] += gamma phi_rows, *stepped = 1.  The caller handles the empty / all-zero
+   phi no-op (:270-273) before calling. */
+int kz_ahk_step(const kz_problem* prob, int32_t system, void* col, void* coef, const void* resid, const void* phi,
+                const int32_t* rows, int32_t n_rows, const int32_t* span, int32_t n_span, int32_t* stepped,
+                void* stream);
 
 /* Number of kernels the last kz_* call on this thread launched (benchmark
    bookkeeping for the gpu_launches count). */

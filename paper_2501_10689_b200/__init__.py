@@ -15,6 +15,15 @@ from .metrics import CADD, CMUL, nmse, spectral_efficiency
 from .rzf import Precoder, apply_auxiliary, auxiliary_matrix, mrc_precoder, rzf_batched, rzf_precoder
 from .solvers import (
     SCHEMES,
+    AggregationWeights,
+    InstanceRun,
+    SelectionStrategy,
+    ahk_step,
+    aggregation_weights,
+    orthogonal_block_step,
+    residual_refresh,
+    rk_step,
+    select_row,
     STOCHASTIC_SCHEMES,
     VR_SCHEMES,
     AugmentedSystem,
@@ -46,4 +55,6 @@ __all__ = [
     "canonical_scheme", "display_scheme", "epilogue", "generate", "generate_drops", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
     "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",
     "solver_seed_sequence", "spectral_efficiency", "gather_stats", "shard_range",
+    "AggregationWeights", "InstanceRun", "SelectionStrategy", "ahk_step", "aggregation_weights",
+    "orthogonal_block_step", "residual_refresh", "rk_step", "select_row",
 ]

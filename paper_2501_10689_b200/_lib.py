@@ -106,6 +106,7 @@ EXPORTS = (
     "kz_solve_workspace_bytes", "kz_solve",
     "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue",
     "kz_channel_synth", "kz_partition_counts", "kz_partition_fill",
+    "kz_residual_refresh", "kz_project_rows", "kz_ahk_step",
 )
 
 
@@ -132,6 +133,13 @@ def _declare(lb):
     lb.kz_partition_counts.argtypes = [C.POINTER(KzDrop), P, P, P, P, P]
     lb.kz_partition_fill.restype = C.c_int
     lb.kz_partition_fill.argtypes = [C.POINTER(KzDrop), P, P, P, P, P, P, P]
+    i32 = C.c_int32
+    lb.kz_residual_refresh.restype = C.c_int
+    lb.kz_residual_refresh.argtypes = [C.POINTER(KzProblem), i32, i32, P, P, P, P, i32, i32, P]
+    lb.kz_project_rows.restype = C.c_int
+    lb.kz_project_rows.argtypes = [C.POINTER(KzProblem), i32, P, P, P, P, i32, P]
+    lb.kz_ahk_step.restype = C.c_int
+    lb.kz_ahk_step.argtypes = [C.POINTER(KzProblem), i32, P, P, P, P, P, i32, P, i32, P, P]
 
 
 def check(status: int):

@@ -13,6 +13,7 @@
 #include "kz_solve_lockstep.cuh"
 #include "kz_solve_cluster.cuh"
 #include "kz_channel.cuh"
+#include "kz_primitives.cuh"
 
 namespace {
 
@@ -324,3 +325,90 @@ int kz_partition_fill(const kz_drop* drop, const int32_t* coupled_ptr, const int
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ per-call step primitives
+namespace {
+
+int check_prim(const kz_problem* p, int32_t system, const void* a, const void* b2, const void* c) {
+  int st = check_problem(p);
+  if (st) return st;
+  if (system < 0 || system >= p->n_systems)
+    return fail(KZ_ERR_INVALID, "system %d out of range [0, %d)", (int)system, (int)p->n_systems);
+  if (!a || !b2 || !c) return fail(KZ_ERR_INVALID, "state arrays must be non-null");
+  return KZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kz_residual_refresh(const kz_problem* prob, int32_t system, int32_t rhs, const void* col, const void* coef,
+                        void* resid, const int32_t* rows, int32_t n_rows, int32_t dense, void* stream) {
+  g_launches = 0;
+  int st = check_prim(prob, system, col, coef, resid);
+  if (st) return st;
+  if (rhs < 0 || rhs >= prob->n_users) return fail(KZ_ERR_INVALID, "rhs index %d out of range", (int)rhs);
+  if (n_rows < 0 || (!rows && n_rows > prob->n_users)) return fail(KZ_ERR_INVALID, "bad row count %d", (int)n_rows);
+  if (n_rows == 0) return KZ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prob->dtype == KZ_C128)
+    kz_prim_refresh<double2><<<1, PRIM_THREADS, 0, s>>>(*prob, system, rhs, (const double2*)col,
+                                                         (const double2*)coef, (double2*)resid, rows, n_rows, dense);
+  else
+    kz_prim_refresh<float2><<<1, PRIM_THREADS, 0, s>>>(*prob, system, rhs, (const float2*)col, (const float2*)coef,
+                                                        (float2*)resid, rows, n_rows, dense);
+  g_launches = 1;
+  return cuda_check("kz_residual_refresh");
+}
+
+int kz_project_rows(const kz_problem* prob, int32_t system, void* col, void* coef, void* resid,
+                    const int32_t* rows, int32_t n_rows, void* stream) {
+  g_launches = 0;
+  int st = check_prim(prob, system, col, coef, resid);
+  if (st) return st;
+  if (n_rows < 0 || (n_rows > 0 && !rows)) return fail(KZ_ERR_INVALID, "rows must be non-null");
+  if (n_rows == 0) return KZ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prob->dtype == KZ_C128)
+    kz_prim_project<double2><<<1, PRIM_THREADS, 0, s>>>(*prob, system, (double2*)col, (double2*)coef,
+                                                         (double2*)resid, rows, n_rows);
+  else
+    kz_prim_project<float2><<<1, PRIM_THREADS, 0, s>>>(*prob, system, (float2*)col, (float2*)coef, (float2*)resid,
+                                                        rows, n_rows);
+  g_launches = 1;
+  return cuda_check("kz_project_rows");
+}
+
+int kz_ahk_step(const kz_problem* prob, int32_t system, void* col, void* coef, const void* resid, const void* phi,
+                const int32_t* rows, int32_t n_rows, const int32_t* span, int32_t n_span, int32_t* stepped,
+                void* stream) {
+  g_launches = 0;
+  int st = check_prim(prob, system, col, coef, resid);
+  if (st) return st;
+  if (!phi || !rows || n_rows < 1) return fail(KZ_ERR_INVALID, "ahk_step needs phi and at least one row");
+  if (span && n_span < 0) return fail(KZ_ERR_INVALID, "bad span size %d", (int)n_span);
+  const size_t smem = (size_t)prob->n_antennas * (prob->dtype == KZ_C128 ? 16 : 8);
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (smem + 1024 > (size_t)maxsm)
+    return fail(KZ_ERR_UNSUPPORTED, "ahk_step: %d antennas exceed the shared-memory aggregation buffer",
+                (int)prob->n_antennas);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prob->dtype == KZ_C128) {
+    cudaFuncSetAttribute(kz_prim_ahk<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kz_prim_ahk<double2><<<1, PRIM_THREADS, smem, s>>>(*prob, system, (double2*)col, (double2*)coef,
+                                                        (const double2*)resid, (const double2*)phi, rows, n_rows,
+                                                        span, n_span, stepped);
+  } else {
+    cudaFuncSetAttribute(kz_prim_ahk<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kz_prim_ahk<float2><<<1, PRIM_THREADS, smem, s>>>(*prob, system, (float2*)col, (float2*)coef,
+                                                       (const float2*)resid, (const float2*)phi, rows, n_rows, span,
+                                                       n_span, stepped);
+  }
+  g_launches = 1;
+  return cuda_check("kz_ahk_step");
+}
+
+}  // extern "C"
+

@@ -30,6 +30,7 @@ import numpy as np
 
 from . import _lib
 from .batch import DeviceBatch, HostBatch
+from .metrics import CADD, CMUL
 from .vrgraph import UserPartition, build_partition
 
 SCHEMES = ("urk", "swor-erk", "gk", "grk", "vr-ogrk", "ahk", "vr-oahk")
@@ -114,12 +115,22 @@ class StoppingRule:
 
 
 class FlopCounter:
-    """metrics.py:25-41 (totals come back from the device)."""
+    """metrics.py:25-41 (batched totals come back from the device; the per-call primitives charge on the host,
+    the charges depend only on sizes)."""
 
     __slots__ = ("total",)
 
     def __init__(self, total: int = 0):
         self.total = int(total)
+
+    def cmul(self, n: int) -> None:
+        self.total += CMUL * n
+
+    def cadd(self, n: int) -> None:
+        self.total += CADD * n
+
+    def real(self, n: int) -> None:
+        self.total += n
 
 
 @dataclass
@@ -131,6 +142,16 @@ class SolverState:
     counter: FlopCounter = field(default_factory=FlopCounter)
     iters: int = 0
     noop_steps: int = 0
+
+    @classmethod
+    def initial(cls, sys, rhs: int, col_buffer: np.ndarray | None = None) -> "SolverState":
+        """solvers.py:129-136: m = 0, q = 0, r = e_rhs."""
+        if not 0 <= rhs < sys.n_users:
+            raise ValueError(f"rhs index {rhs} out of range")
+        col = col_buffer if col_buffer is not None else np.zeros(sys.n_antennas, dtype=np.complex128)
+        resid = np.zeros(sys.n_users, dtype=np.complex128)
+        resid[rhs] = 1.0
+        return cls(rhs=rhs, col=col, coef=np.zeros(sys.n_users, dtype=np.complex128), resid=resid)
 
 
 @dataclass
@@ -543,3 +564,274 @@ def run_precoding_batched(scheme: str, dev: DeviceBatch, *, max_iters: int, rng=
     out = {"solve": res, **ep}
     out["launches"] = res.launches + ep["launches"]
     return out
+
+
+# ---------------------------------------------------------------------------
+# per-call step primitives and InstanceRun (solvers.py:143-423): one rhs of one system, state on the GPU
+# for the duration of each call (kz_residual_refresh / kz_project_rows / kz_ahk_step)
+# ---------------------------------------------------------------------------
+
+def _prim_device(sys) -> DeviceBatch:
+    """The system as a one-system complex128 batch on the current GPU, built once per AugmentedSystem."""
+    dev = sys.__dict__.get("_kz_prim_dev")
+    if dev is None:
+        dev = HostBatch.from_systems([sys]).to_device("c128")
+        sys.__dict__["_kz_prim_dev"] = dev
+    return dev
+
+
+class _DeviceState:
+    """col / coef / resid of a SolverState uploaded for one primitive call and written back in place."""
+
+    def __init__(self, state: SolverState, sys):
+        import torch
+        self.state, self.dev = state, _prim_device(sys)
+        d = self.dev.device
+        self.col = torch.from_numpy(np.ascontiguousarray(state.col, dtype=np.complex128)).to(d)
+        self.coef = torch.from_numpy(np.ascontiguousarray(state.coef, dtype=np.complex128)).to(d)
+        self.resid = torch.from_numpy(np.ascontiguousarray(state.resid, dtype=np.complex128)).to(d)
+
+    def rows(self, rows):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev.device)
+
+    def write_back(self, col=True, coef=True, resid=True):
+        if col:
+            self.state.col[...] = self.col.cpu().numpy()
+        if coef:
+            self.state.coef[...] = self.coef.cpu().numpy()
+        if resid:
+            self.state.resid[...] = self.resid.cpu().numpy()
+
+
+def _sizes(sys, rows):
+    return [int(np.asarray(sys.supports[i]).size) for i in rows]
+
+
+def residual_refresh(state: SolverState, sys, rows=None, use_vr: bool = True) -> None:
+    """solvers.py:143-170 on the GPU: r_i = s_i - h_i^H col - reg coef_i for `rows` (None: all)."""
+    k, nt = sys.n_users, sys.n_antennas
+    dense_all = rows is None and not use_vr
+    idx = np.arange(k) if rows is None else np.asarray([int(r) for r in rows], dtype=np.int64)
+    if idx.size == 0:
+        return
+    ds = _DeviceState(state, sys)
+    r = ds.rows(idx)
+    _lib.check(_lib.lib().kz_residual_refresh(C.byref(ds.dev.problem), 0, int(state.rhs), _lib.ptr(ds.col),
+                                              _lib.ptr(ds.coef), _lib.ptr(ds.resid), _lib.ptr(r), int(idx.size),
+                                              1 if dense_all else 0, _stream_ptr(None)))
+    ds.write_back(col=False, coef=False)
+    if dense_all:
+        state.counter.cmul(k * nt)
+        state.counter.cadd(k * (nt + 1))
+        state.counter.real(2 * k)
+        return
+    for n in (_sizes(sys, idx) if use_vr else [nt] * idx.size):
+        state.counter.cmul(n)
+        state.counter.cadd(n + 1)
+        state.counter.real(2)
+
+
+def _project(state: SolverState, sys, rows, use_vr: bool) -> None:
+    ds = _DeviceState(state, sys)
+    r = ds.rows(rows)
+    _lib.check(_lib.lib().kz_project_rows(C.byref(ds.dev.problem), 0, _lib.ptr(ds.col), _lib.ptr(ds.coef),
+                                          _lib.ptr(ds.resid), _lib.ptr(r), len(rows), _stream_ptr(None)))
+    ds.write_back()
+    for n in (_sizes(sys, rows) if use_vr else [sys.n_antennas] * len(rows)):
+        state.counter.real(2)
+        state.counter.cmul(n)
+        state.counter.cadd(n + 1)
+
+
+def rk_step(state: SolverState, sys, i: int, use_vr: bool = True) -> None:
+    """solvers.py:173-188 on the GPU: project onto row i with the stored residual."""
+    _project(state, sys, [int(i)], use_vr)
+    state.iters += 1
+
+
+def orthogonal_block_step(state: SolverState, sys, rows, use_vr: bool = True) -> None:
+    """solvers.py:312-332 on the GPU: exact projections onto the (pairwise orthogonal) rows, in order."""
+    rows = [int(r) for r in rows]
+    if rows:
+        _project(state, sys, rows, use_vr)
+
+
+@dataclass
+class SelectionStrategy:
+    """solvers.py:191-203: row-choice rule; `pool` holds the without-replacement epoch state."""
+
+    variant: str
+    pool: list = field(default_factory=list)
+
+    _VARIANTS = ("uniform", "energy", "energy-swor", "greedy-max", "greedy-weighted")
+
+    def __post_init__(self):
+        if self.variant not in self._VARIANTS:
+            raise ValueError(f"unknown selection variant {self.variant!r}")
+
+
+def select_row(strategy: SelectionStrategy, state: SolverState, sys, rng: np.random.Generator | None = None):
+    """solvers.py:205-237.  The draw consumes the caller's numpy Generator on the host, exactly as the
+    reference (and as HostStreams does for the batched kernels); the K-entry residual it reads is the one the
+    GPU primitives wrote back."""
+    k = sys.n_users
+    variant = strategy.variant
+    if variant == "greedy-max":
+        score = np.abs(state.resid) ** 2 / sys.row_energies
+        state.counter.real(4 * k)
+        if not score.any():
+            return None
+        return int(np.argmax(score))
+    if rng is None:
+        raise ValueError(f"selection variant {variant!r} needs an rng")
+    if variant == "uniform":
+        return int(rng.integers(k))
+    if variant == "energy":
+        w = sys.row_energies
+        state.counter.real(k + 2)
+        return int(rng.choice(k, p=w / w.sum()))
+    if variant == "energy-swor":
+        if not strategy.pool:
+            strategy.pool = list(range(k))
+        w = sys.row_energies[strategy.pool]
+        state.counter.real(len(strategy.pool) + 2)
+        return strategy.pool.pop(int(rng.choice(len(strategy.pool), p=w / w.sum())))
+    w = np.abs(state.resid) ** 2
+    state.counter.real(4 * k + 2)
+    total = w.sum()
+    if total == 0.0:
+        return None
+    return int(rng.choice(k, p=w / total))
+
+
+@dataclass(frozen=True)
+class AggregationWeights:
+    """solvers.py:240-245: phi (K complex, zero off `rows`) and the sorted rows."""
+
+    phi: np.ndarray
+    rows: np.ndarray
+
+
+def aggregation_weights(state: SolverState, sys, rows) -> AggregationWeights:
+    """solvers.py:248-254: phi_i = r_i / e_i on the sorted rows."""
+    rows = np.asarray(sorted(int(r) for r in rows), dtype=np.intp)
+    phi = np.zeros(sys.n_users, dtype=np.complex128)
+    phi[rows] = state.resid[rows] / sys.row_energies[rows]
+    state.counter.real(2 * rows.size)
+    return AggregationWeights(phi=phi, rows=rows)
+
+
+def ahk_step(state: SolverState, sys, weights: AggregationWeights, use_vr: bool = True,
+             union: np.ndarray | None = None) -> bool:
+    """solvers.py:257-309 on the GPU: one projection onto the aggregated hyperplane; False (no-op flag) when
+    phi vanishes or the aggregated row is zero."""
+    import torch
+    rows = np.asarray(weights.rows, dtype=np.int64)
+    m = rows.size
+    if m == 0 or not weights.phi[rows].any():
+        state.noop_steps += 1
+        return False
+    state.counter.cmul(m)
+    state.counter.cadd(max(m - 1, 0))
+    nt = sys.n_antennas
+    if use_vr:
+        if union is None:
+            union = np.unique(np.concatenate([np.asarray(sys.supports[i]) for i in rows]))
+        for n in _sizes(sys, rows):
+            state.counter.cmul(n)
+            state.counter.cadd(n)
+        span_size = int(np.asarray(union).size)
+    else:
+        state.counter.cmul(nt * m)
+        state.counter.cadd(nt * max(m - 1, 0))
+        span_size = nt
+    state.counter.real(4 * span_size + 3 * m + 2)
+    ds = _DeviceState(state, sys)
+    d = ds.dev.device
+    phi = torch.from_numpy(np.ascontiguousarray(weights.phi, dtype=np.complex128)).to(d)
+    r = ds.rows(rows)
+    span = ds.rows(np.asarray(union)) if use_vr else None
+    stepped = torch.zeros(1, dtype=torch.int32, device=d)
+    _lib.check(_lib.lib().kz_ahk_step(C.byref(ds.dev.problem), 0, _lib.ptr(ds.col), _lib.ptr(ds.coef),
+                                      _lib.ptr(ds.resid), _lib.ptr(phi), _lib.ptr(r), int(m), _lib.ptr(span),
+                                      0 if span is None else int(span.numel()), _lib.ptr(stepped),
+                                      _stream_ptr(None)))
+    if not int(stepped.item()):
+        state.noop_steps += 1
+        return False
+    ds.write_back(resid=False)
+    state.counter.real(2)
+    state.counter.cmul(span_size)
+    state.counter.cadd(span_size)
+    state.counter.cmul(m)
+    state.counter.cadd(m)
+    return True
+
+
+class InstanceRun:
+    """solvers.py:345-423: one right-hand side advanced one scheme iteration at a time, composed from the GPU
+    primitives above exactly as the reference composes its numpy ones."""
+
+    def __init__(self, scheme: str, sys, rhs: int, rng: np.random.Generator | None,
+                 col_buffer: np.ndarray | None = None):
+        self.scheme = canonical_scheme(scheme)
+        if self.scheme in STOCHASTIC_SCHEMES and rng is None:
+            raise ValueError(f"scheme {self.scheme!r} draws rows at random; pass an rng")
+        self.sys = sys
+        self.rng = rng
+        self.state = SolverState.initial(sys, rhs, col_buffer=col_buffer)
+        self.done = False
+        self.strategy = {"urk": SelectionStrategy("uniform"), "swor-erk": SelectionStrategy("energy-swor"),
+                         "gk": SelectionStrategy("greedy-max"), "grk": SelectionStrategy("greedy-weighted"),
+                         "vr-ogrk": SelectionStrategy("greedy-weighted")}.get(self.scheme)
+        if self.scheme == "vr-ogrk":
+            self.prev_row = None
+            self.coupled = [np.asarray(sorted(c), dtype=np.intp) for c in sys.partition.coupled]
+        if self.scheme == "vr-oahk":
+            self.orth_rows = np.asarray(sys.partition.orthogonal_sorted, dtype=np.intp)
+            self.non_rows = np.asarray(sys.partition.non_orthogonal, dtype=np.intp)
+            self.non_union = (np.unique(np.concatenate([np.asarray(sys.supports[i]) for i in self.non_rows]))
+                              if self.non_rows.size else None)
+        if self.scheme == "ahk":
+            self.all_rows = np.arange(sys.n_users)
+
+    def step(self) -> None:
+        if self.done:
+            return
+        scheme, state, sys = self.scheme, self.state, self.sys
+        if scheme in ("urk", "swor-erk"):
+            i = select_row(self.strategy, state, sys, self.rng)
+            residual_refresh(state, sys, rows=(i,), use_vr=False)
+            rk_step(state, sys, i, use_vr=False)
+        elif scheme in ("gk", "grk"):
+            residual_refresh(state, sys, use_vr=False)
+            i = select_row(self.strategy, state, sys, self.rng)
+            if i is None:
+                self.done = True
+                return
+            rk_step(state, sys, i, use_vr=False)
+        elif scheme == "vr-ogrk":
+            if self.prev_row is not None:
+                residual_refresh(state, sys, rows=self.coupled[self.prev_row], use_vr=True)
+            i = select_row(self.strategy, state, sys, self.rng)
+            if i is None:
+                self.done = True
+                return
+            rk_step(state, sys, i, use_vr=True)
+            self.prev_row = i
+        elif scheme == "ahk":
+            residual_refresh(state, sys, use_vr=False)
+            weights = aggregation_weights(state, sys, self.all_rows)
+            if not ahk_step(state, sys, weights, use_vr=False):
+                self.done = True
+                return
+            state.iters += 1
+        else:  # vr-oahk
+            residual_refresh(state, sys, rows=self.orth_rows, use_vr=True)
+            orthogonal_block_step(state, sys, self.orth_rows, use_vr=True)
+            if self.non_rows.size:
+                residual_refresh(state, sys, rows=self.non_rows, use_vr=True)
+                weights = aggregation_weights(state, sys, self.non_rows)
+                ahk_step(state, sys, weights, use_vr=True, union=self.non_union)
+            state.iters += 1

@@ -146,3 +146,38 @@ def test_generate_drops_matches_generate():
         np.testing.assert_array_equal(dr.length, ch.length)
         np.testing.assert_array_equal(dr.reg, ch.reg)
         assert dr.n_systems == ch.n_systems and dr.n_antennas == ch.n_antennas
+
+
+def test_step_api_validates_like_the_reference():
+    """InstanceRun / SelectionStrategy / select_row argument errors (solvers.py:196-203, 216-217, 351-352),
+    and the host-side selection and weights equal the oracle's (no GPU needed)."""
+    import oracle as O
+    import paper_2501_10689_b200 as kz
+    ch = kz.generate(kz.CONFIGS["cfg1"], [0])
+    from helpers import oracle_channel_contiguous
+    sys_ = O.AugmentedSystem.from_channel(oracle_channel_contiguous(ch, 0), float(ch.reg[0]))
+    with pytest.raises(ValueError):
+        kz.InstanceRun("grk", sys_, 0, None)
+    with pytest.raises(ValueError):
+        kz.InstanceRun("nope", sys_, 0, None)
+    with pytest.raises(ValueError):
+        kz.SelectionStrategy("bogus")
+    with pytest.raises(ValueError):
+        kz.SolverState.initial(sys_, sys_.n_users)
+    st = kz.SolverState.initial(sys_, 1)
+    with pytest.raises(ValueError):
+        kz.select_row(kz.SelectionStrategy("uniform"), st, sys_)
+    rng = np.random.default_rng(3)
+    k = sys_.n_users
+    for variant in ("uniform", "energy", "energy-swor", "greedy-max", "greedy-weighted"):
+        a = O.SolverState.initial(sys_, 1)
+        a.resid[:] = rng.standard_normal(k) + 1j * rng.standard_normal(k)
+        b = kz.SolverState(rhs=1, col=a.col.copy(), coef=a.coef.copy(), resid=a.resid.copy())
+        sa, sb = O.SelectionStrategy(variant), kz.SelectionStrategy(variant)
+        ga, gb = np.random.default_rng(9), np.random.default_rng(9)
+        for _ in range(2 * k):
+            assert O.select_row(sa, a, sys_, ga) == kz.select_row(sb, b, sys_, gb)
+        assert a.counter.total == b.counter.total
+        wa, wb = O.aggregation_weights(a, sys_, [3, 1]), kz.aggregation_weights(b, sys_, [3, 1])
+        np.testing.assert_array_equal(wa.phi, wb.phi)
+        np.testing.assert_array_equal(wa.rows, wb.rows)
