@@ -8,7 +8,7 @@ Batched entry points (`solve_batch`, `run_precoding_batched`, `rzf_batched`,
 `epilogue`) run thousands of systems per launch.  There is no CPU fallback.
 """
 
-from .assembly import assemble_dense, assemble_vr, epilogue
+from .assembly import SubarrayChannel, assemble_dense, assemble_vr, epilogue
 from .batch import DeviceBatch, HostBatch, pin_host
 from .channel import CONFIGS, ContiguousChannels, Drops, NearFieldConfig, generate, generate_drops, solver_seed_sequence
 from .metrics import CADD, CMUL, nmse, spectral_efficiency
@@ -55,6 +55,6 @@ __all__ = [
     "canonical_scheme", "display_scheme", "epilogue", "generate", "generate_drops", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
     "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",
     "solver_seed_sequence", "spectral_efficiency", "gather_stats", "shard_range",
-    "AggregationWeights", "InstanceRun", "SelectionStrategy", "ahk_step", "aggregation_weights",
+    "AggregationWeights", "InstanceRun", "SubarrayChannel", "SelectionStrategy", "ahk_step", "aggregation_weights",
     "orthogonal_block_step", "residual_refresh", "rk_step", "select_row",
 ]

@@ -10,6 +10,7 @@ gathered across GPUs.
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 
 import os
 
@@ -55,15 +56,51 @@ def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = Fa
     return {"f": f, "beta": beta, "nmse": nm, "rates": r, "sum_rate": sr, "launches": lb.kz_last_launch_count()}
 
 
+@dataclass(frozen=True)
+class SubarrayChannel:
+    """assembly.py:20-48: the channel as S row blocks with the users active on each block."""
+
+    blocks: tuple
+    active_users: tuple
+    n_users: int
+
+    @classmethod
+    def from_channel(cls, chan) -> "SubarrayChannel":
+        h = np.asarray(chan.h)
+        s_count, m = chan.cfg.n_subarrays, chan.cfg.subarray_size
+        blocks, active = [], []
+        for s in range(s_count):
+            block = h[s * m:(s + 1) * m, :]
+            users = np.asarray(sorted(k for k, vr in enumerate(chan.vrs) if s in vr.visible_subarrays),
+                               dtype=np.intp)
+            inactive = np.setdiff1d(np.arange(h.shape[1]), users)
+            if inactive.size and np.any(block[:, inactive] != 0.0):
+                raise ValueError(f"subarray {s}: channel is nonzero for a user outside its visibility region")
+            blocks.append(block)
+            active.append(users)
+        return cls(blocks=tuple(blocks), active_users=tuple(active), n_users=h.shape[1])
+
+
 class _VrSystem:
-    """Batch view of a ChannelMatrix (VR supports) for the epilogue."""
+    """Batch view of a ChannelMatrix (VR supports) or a SubarrayChannel (block supports) for the epilogue."""
 
     def __init__(self, chan):
         from .vrgraph import UserPartition
-        h = np.asarray(chan.h)
+        if hasattr(chan, "blocks"):  # SubarrayChannel: user k is supported on the blocks listing it
+            h = np.vstack(chan.blocks)
+            starts = np.cumsum([0] + [b.shape[0] for b in chan.blocks])
+            sup = [[] for _ in range(chan.n_users)]
+            for s, users in enumerate(chan.active_users):
+                for k in np.asarray(users).tolist():
+                    sup[k].append(np.arange(starts[s], starts[s + 1]))
+            supports = tuple(np.concatenate(x) if x else np.zeros(0, np.intp) for x in sup)
+        else:
+            h = np.asarray(chan.h)
+            supports = tuple(np.asarray(vr.antenna_indices) for vr in chan.vrs)
+        self.h = h
         self.n_antennas, self.n_users = h.shape
         self.reg = 0.0
-        self.supports = tuple(np.asarray(vr.antenna_indices) for vr in chan.vrs)
+        self.supports = supports
         self.eff_rows = tuple(np.ascontiguousarray(h[s, i]) for i, s in enumerate(self.supports))
         self.row_energies = np.array([np.sum(np.abs(e) ** 2) for e in self.eff_rows])
         k = self.n_users
@@ -72,12 +109,15 @@ class _VrSystem:
 
 def _assemble(chan, v, counter, scheme, blocked):
     from .rzf import Precoder, _DenseSystem
-    h = np.asarray(chan.h if hasattr(chan, "h") else chan)
+    vr_view = hasattr(chan, "vrs") or hasattr(chan, "blocks")
+    sysv = _VrSystem(chan) if vr_view else None
+    h = sysv.h if vr_view else np.asarray(chan.h if hasattr(chan, "h") else chan)
     nt, k = h.shape
     v = np.asarray(v)
     if v.shape != (k, k):
         raise ValueError(f"expected a ({k}, {k}) solution block, got {v.shape}")
-    sysv = _VrSystem(chan) if hasattr(chan, "vrs") else _DenseSystem(h, 0.0)
+    if sysv is None:
+        sysv = _DenseSystem(h, 0.0)
     dev = HostBatch.from_systems([sysv]).to_device("c128")
     import torch
     ep = epilogue(dev, torch.as_tensor(v[None], dtype=torch.complex128, device="cuda"), want_f=True)
@@ -85,7 +125,12 @@ def _assemble(chan, v, counter, scheme, blocked):
     if not np.isfinite(beta):
         raise ValueError("degenerate precoder: H V vanished")
     if counter is not None:
-        if blocked:
+        if blocked and hasattr(chan, "blocks"):
+            for block, users in zip(chan.blocks, chan.active_users):
+                m, q = block.shape[0], int(np.asarray(users).size)
+                if q:
+                    counter.total += 6 * m * q * k + 2 * m * (q - 1) * k
+        elif blocked:
             m = chan.cfg.subarray_size
             for s in range(chan.cfg.n_subarrays):
                 q = sum(1 for vr in chan.vrs if s in vr.visible_subarrays)
@@ -101,9 +146,7 @@ def assemble_dense(chan, v, counter=None, scheme: str = ""):
     return _assemble(chan, v, counter, scheme, blocked=False)
 
 
-def assemble_vr(chan, v, counter=None, scheme: str = ""):
-    """Subarray-blocked F = H V (assembly.py:74-92); takes the ChannelMatrix (the
-    reference's SubarrayChannel view is implicit in the VR supports)."""
-    if hasattr(chan, "blocks"):
-        raise TypeError("pass the ChannelMatrix; the VR blocking is derived on the device")
-    return _assemble(chan, v, counter, scheme, blocked=True)
+def assemble_vr(sub, v, counter=None, scheme: str = ""):
+    """Subarray-blocked F = H V (assembly.py:74-92).  Takes the reference's SubarrayChannel (or this
+    package's), or the ChannelMatrix itself (its VR supports give the same blocking)."""
+    return _assemble(sub, v, counter, scheme, blocked=True)

@@ -263,6 +263,11 @@ def test_assembly_and_metrics_match_oracle():
     r1, s1 = kz.spectral_efficiency(chan.h, a.f, 1.0)
     r2, s2 = O.spectral_efficiency(chan.h, b.f, 1.0)
     np.testing.assert_allclose(r1, r2, rtol=1e-12)
+    # the reference's calling form: assemble_vr(SubarrayChannel.from_channel(chan), v, counter)
+    ca, cb = kz.FlopCounter(), O.FlopCounter()
+    d = kz.assemble_vr(kz.SubarrayChannel.from_channel(chan), v, counter=ca)
+    e = O.assemble_vr(chan, v, counter=cb)
+    assert rel(d.f, e.f) <= 1e-13 and ca.total == cb.total
 
 
 # --------------------------------------------------------------------------- edge cases

@@ -181,3 +181,21 @@ def test_step_api_validates_like_the_reference():
         wa, wb = O.aggregation_weights(a, sys_, [3, 1]), kz.aggregation_weights(b, sys_, [3, 1])
         np.testing.assert_array_equal(wa.phi, wb.phi)
         np.testing.assert_array_equal(wa.rows, wb.rows)
+
+
+def test_subarray_channel_view_validates_leakage():
+    """SubarrayChannel.from_channel (assembly.py:29-48) raises for a user nonzero outside its subarrays."""
+    import oracle as O
+    from helpers import load, oracle_channel_from_mask
+    z = load("ref_lockstep.npz")
+    chan = oracle_channel_from_mask(z["h"], z["vr_mask"], z["n_subarrays"])
+    sub = kz.SubarrayChannel.from_channel(chan)
+    assert len(sub.blocks) == int(z["n_subarrays"]) and sub.n_users == chan.h.shape[1]
+    h = chan.h.copy()
+    k0 = next(k for k in range(h.shape[1]) if len(chan.vrs[k].visible_subarrays) < int(z["n_subarrays"]))
+    s_off = next(s for s in range(int(z["n_subarrays"])) if s not in chan.vrs[k0].visible_subarrays)
+    m = h.shape[0] // int(z["n_subarrays"])
+    h[s_off * m, k0] = 1.0
+    leaky = O.ChannelMatrix(h=h, vrs=chan.vrs, cfg=chan.cfg)
+    with pytest.raises(ValueError):
+        kz.SubarrayChannel.from_channel(leaky)
