@@ -473,9 +473,21 @@ def run_precoding(scheme: str, sys, reference, epsilon: float = 1e-6, max_iters:
         flops_measured=setup + flops_rhs + asm, noop_steps=int(res.noop_steps[0].sum()))
 
 
+def _stored_resid(res: BatchResult, c: int) -> np.ndarray:
+    """The stored row residuals the scheme left for rhs c of system 0 (SolverState.resid): the R block of the
+    complex128 solve workspace (csrc/kz_solve_generic.cuh gen_layout: M [B*K][Nt], Q [B*K][K], R [B*K][K],
+    each 256-byte aligned)."""
+    import torch
+    k, nt = res.dev.n_users, res.dev.n_antennas
+    al = lambda x: (x + 255) & ~255  # noqa: E731
+    off = al(k * nt * 16) + al(k * k * 16) + c * k * 16
+    raw = res.workspace[off:off + k * 16]
+    return raw.view(torch.complex128).cpu().numpy().copy()
+
+
 def _state_from(res: BatchResult, c: int) -> SolverState:
     m = res.iterates()[0, c].cpu().numpy()
-    return SolverState(rhs=c, col=m, coef=res.v[0, :, c].cpu().numpy(), resid=np.zeros(res.dev.n_users, complex),
+    return SolverState(rhs=c, col=m, coef=res.v[0, :, c].cpu().numpy(), resid=_stored_resid(res, c),
                        counter=FlopCounter(int(res.flops[0, c])), iters=int(res.iters[0, c]),
                        noop_steps=int(res.noop_steps[0, c]))
 

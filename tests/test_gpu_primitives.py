@@ -124,3 +124,18 @@ def test_ahk_step_noops_and_forms():
         assert O.ahk_step(a, sys_, wa, use_vr=use_vr)
         assert kz.ahk_step(b, sys_, wb, use_vr=use_vr)
         same_state(b, a)
+
+
+@pytest.mark.parametrize("scheme", O.SCHEMES)
+def test_solve_returns_the_reference_state(scheme):
+    """solve() returns SolverState like the reference (solvers.py:460-507): col, coef, the stored residuals
+    the scheme left (stale where the scheme does not refresh), iters, noop steps, flop total."""
+    kz = _kz()
+    sys_ = ref_system()
+    vref = O.auxiliary_matrix(sys_.channel, sys_.reg)
+    for mode in ("residual", "oracle"):
+        kw = dict(epsilon=1e-8) if mode == "residual" else dict(epsilon=1e-6, reference=vref[:, 2])
+        a, ta = O.solve(scheme, sys_, 2, O.StoppingRule(mode=mode, **kw), rng=np.random.default_rng(4))
+        b, tb = kz.solve(scheme, sys_, 2, kz.StoppingRule(mode=mode, **kw), rng=np.random.default_rng(4))
+        assert ta.n_iters == tb.n_iters and ta.converged == tb.converged
+        same_state(b, a)
