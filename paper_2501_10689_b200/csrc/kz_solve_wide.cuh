@@ -727,9 +727,11 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         __syncthreads();
         KZ_PHASE();
         tmem::wait_st();
+        KZ_PHASE();  // [timing] TMEM store drain
         float f0[16], f1[16];
         tmem::ld16(my_tmem, f0);  // the parked iterate streams in while the step lengths are formed
         tmem::ld16(my_tmem + 16, f1);
+        KZ_PHASE();  // [timing] TMEM load issue
         // step lengths of this thread's two rhs (fixed-order pairwise sums => identical in every thread)
         auto gamma_of = [&](int rr, bool& step) -> T {
           step = false;
@@ -753,6 +755,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
         };
         bool st0, st1;
         const T gm0 = gamma_of(g, st0), gm1 = gamma_of(g + 16, st1);
+        KZ_PHASE();  // [timing] step lengths
         {
           tmem::wait_ld();
 #pragma unroll
@@ -771,6 +774,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             m1[k + 8] = st1 ? cfma(gm1, m1[k + 8], o1) : o1;
           }
         }
+        KZ_PHASE();  // [timing] iterate reload + update
         // q += gamma phi over the aggregated rows (threads over (row, rhs))
         {  // rhs of entry e is e % G == lane = g + 16 a (nthr is a multiple of 32): this thread's own step
           const bool stq = a ? st1 : st0;
@@ -782,6 +786,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
               Qs[xs(i, lane)] = cfma(gq, Phi[xs(i, lane)], Qs[xs(i, lane)]);
             }
         }
+        KZ_PHASE();  // [timing] coefficient update
         // bookkeeping once per rhs (warp 0: lane = rhs slot)
         if (w == 0 && g0 + lane < K && !donev[lane]) {
           const bool st = a ? st1 : st0;
