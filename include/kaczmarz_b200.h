@@ -158,6 +158,10 @@ typedef struct kz_out {
    per-rhs scratch).  The workspace doubles as the resumable solver state. */
 size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop);
 
+/* Byte offset in that workspace of the stored row residuals (SolverState.resid, solvers.py:112-136) after a
+   complex128 KZ_STOP_RESIDUAL / KZ_STOP_ORACLE solve: [B*K rhs][K] complex of prob->dtype, rhs-major. */
+size_t kz_solve_resid_offset(const kz_problem* prob);
+
 /* Run scheme over every (system, rhs).  resume = 0 initialises the state
    (SolverState.initial, solvers.py:129-136); resume = 1 continues from the
    workspace (next host-stream chunk). */

@@ -103,7 +103,7 @@ def lib():
 
 EXPORTS = (
     "kz_abi_version", "kz_last_error", "kz_last_launch_count",
-    "kz_solve_workspace_bytes", "kz_solve",
+    "kz_solve_workspace_bytes", "kz_solve_resid_offset", "kz_solve",
     "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue",
     "kz_channel_synth", "kz_partition_counts", "kz_partition_fill",
     "kz_residual_refresh", "kz_project_rows", "kz_ahk_step",
@@ -116,6 +116,8 @@ def _declare(lb):
     lb.kz_last_launch_count.restype = C.c_int32
     lb.kz_solve_workspace_bytes.restype = C.c_size_t
     lb.kz_solve_workspace_bytes.argtypes = [C.POINTER(KzProblem), C.POINTER(KzStop)]
+    lb.kz_solve_resid_offset.restype = C.c_size_t
+    lb.kz_solve_resid_offset.argtypes = [C.POINTER(KzProblem)]
     lb.kz_solve.restype = C.c_int
     lb.kz_solve.argtypes = [C.POINTER(KzProblem), C.c_int32, C.POINTER(KzStop), C.POINTER(KzRng),
                             C.POINTER(KzOut), P, C.c_size_t, C.c_int32, P]

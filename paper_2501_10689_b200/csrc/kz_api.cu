@@ -68,6 +68,11 @@ size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop) {
   return gen + ls_extra_ws(*prob);
 }
 
+size_t kz_solve_resid_offset(const kz_problem* prob) {
+  if (!prob) return 0;
+  return gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).R;
+}
+
 int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng, kz_out* out,
              void* workspace, size_t workspace_bytes, int32_t resume, void* stream) {
   g_launches = 0;

@@ -474,15 +474,12 @@ def run_precoding(scheme: str, sys, reference, epsilon: float = 1e-6, max_iters:
 
 
 def _stored_resid(res: BatchResult, c: int) -> np.ndarray:
-    """The stored row residuals the scheme left for rhs c of system 0 (SolverState.resid): the R block of the
-    complex128 solve workspace (csrc/kz_solve_generic.cuh gen_layout: M [B*K][Nt], Q [B*K][K], R [B*K][K],
-    each 256-byte aligned)."""
+    """The stored row residuals the scheme left for rhs c of system 0 (SolverState.resid), read from the
+    complex128 solve workspace at kz_solve_resid_offset."""
     import torch
-    k, nt = res.dev.n_users, res.dev.n_antennas
-    al = lambda x: (x + 255) & ~255  # noqa: E731
-    off = al(k * nt * 16) + al(k * k * 16) + c * k * 16
-    raw = res.workspace[off:off + k * 16]
-    return raw.view(torch.complex128).cpu().numpy().copy()
+    k = res.dev.n_users
+    off = int(_lib.lib().kz_solve_resid_offset(C.byref(res.dev.problem))) + c * k * 16
+    return res.workspace[off:off + k * 16].view(torch.complex128).cpu().numpy().copy()
 
 
 def _state_from(res: BatchResult, c: int) -> SolverState:
