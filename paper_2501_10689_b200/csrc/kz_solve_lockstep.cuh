@@ -273,50 +273,78 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   auto ant = [&](int k) { return (w << 5) + (k / V) * (A * V) + a * V + (k % V); };
   auto rowp = [&](int i) -> const T* { return Hs + rowB[i] + (rowS[i] & 1) - rowS[i]; };
 
-  // partial h_i^H m over this thread's antennas of chunk w (row overlaps the chunk)
-  auto partial = [&](int i, bool uniform_row) -> T {
+  // this thread's share of h_i^H m over chunk w (row overlaps the chunk), before the a-lane reduction.
+  // Straight-line (predicated rather than branching on full / partial chunks) so that several rows' partials
+  // interleave; the skipped elements and the even/odd accumulator split keep the arithmetic of one row as before.
+  auto partial_local = [&](int i) -> T {
     const int s = rowS[i], e = s + rowL[i];
-    const int lo = max(s, w << 5), hi = min(e, (w << 5) + 32);
     const T* hp = rowp(i);
     T acc0 = czero<T>(), acc1 = czero<T>();
-    if (lo == (w << 5) && hi == (w << 5) + 32) {
+    if constexpr (V == 2) {
+      const bool full = s <= (w << 5) && e >= (w << 5) + 32;
+      if (full) {
 #pragma unroll
-      for (int k = 0; k < NPT; k += V) {
-        int n = ant(k);
-        if constexpr (V == 2) {
+        for (int k = 0; k < NPT; k += V) {
+          const int n = ant(k);
           float4 hv = *reinterpret_cast<const float4*>(hp + n);
           acc0 = cfma_conj(T{(Rl)hv.x, (Rl)hv.y}, m[k], acc0);
           acc1 = cfma_conj(T{(Rl)hv.z, (Rl)hv.w}, m[k + 1], acc1);
-        } else {
-          if (k & 1) acc1 = cfma_conj(hp[n], m[k], acc1);
-          else acc0 = cfma_conj(hp[n], m[k], acc0);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NPT; ++k) {
+          const int n = ant(k);
+          if (n >= s && n < e) {
+            if (k & 1) acc1 = cfma_conj(hp[n], m[k], acc1);
+            else acc0 = cfma_conj(hp[n], m[k], acc0);
+          }
         }
       }
     } else {
 #pragma unroll
       for (int k = 0; k < NPT; ++k) {
-        int n = ant(k);
-        if (n >= lo && n < hi) {
-          if (k & 1) acc1 = cfma_conj(hp[n], m[k], acc1);
-          else acc0 = cfma_conj(hp[n], m[k], acc0);
+        const int n = ant(k);
+        const bool in = n >= s && n < e;
+        const T h = in ? hp[n] : czero<T>();
+        if (in) {
+          if (k & 1) acc1 = cfma_conj(h, m[k], acc1);
+          else acc0 = cfma_conj(h, m[k], acc0);
         }
       }
     }
-    (void)uniform_row;
-    T acc = cadd(acc0, acc1);
+    return cadd(acc0, acc1);
+  };
+  auto reduce_a = [&](T& acc) {
 #pragma unroll
     for (int off = G; off < 32; off <<= 1) {
       acc.x += __shfl_xor_sync(FULL, acc.x, off);
       acc.y += __shfl_xor_sync(FULL, acc.y, off);
     }
-    return acc;
   };
-  // refresh partials for the rows listed for this chunk -> P[i][w - c0_i][g]
+  // refresh partials for the rows listed for this chunk -> P[i][w - c0_i][g]; four rows in flight
   auto refresh_partials = [&](const int* lptr, const int* lst) {
-    for (int q = lptr[w]; q < lptr[w + 1]; ++q) {
-      int i = lst[q];
-      T v = partial(i, true);
+    auto put = [&](int i, T v) {
       if (a == 0) Ps[((size_t)i * p.S + (w - c0[i])) * G + g] = v;
+    };
+    int q = lptr[w];
+    const int q1 = lptr[w + 1];
+    for (; q + 3 < q1; q += 4) {
+      const int i0 = lst[q], i1 = lst[q + 1], i2 = lst[q + 2], i3 = lst[q + 3];
+      T v0 = partial_local(i0), v1 = partial_local(i1), v2 = partial_local(i2), v3 = partial_local(i3);
+      reduce_a(v0);
+      reduce_a(v1);
+      reduce_a(v2);
+      reduce_a(v3);
+      put(i0, v0);
+      put(i1, v1);
+      put(i2, v2);
+      put(i3, v3);
+    }
+    for (; q < q1; ++q) {
+      const int i = lst[q];
+      T v = partial_local(i);
+      reduce_a(v);
+      put(i, v);
     }
   };
   // finalise residuals of `rows` (n of them) from the slot partials
