@@ -530,28 +530,32 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     // y over this thread's antennas, rows in ascending order
 #pragma unroll
     for (int k = 0; k < NPT; ++k) y[k] = czero<T>();
-    for (int q = cp[w]; q < cp[w + 1]; ++q) {
-      int i = cl[q];
+    // ascending rows; predicated straight-line code (no full / partial branch) so the next row's loads
+    // issue under this row's arithmetic -- per element the same operations in the same order
+    auto acc_row = [&](int i) {
       const T ph = Phi[xs(i, g)];
       const int s = rowS[i], e = s + rowL[i];
       const T* hp = rowp(i);
-      if (s <= (w << 5) && e >= (w << 5) + 32) {
 #pragma unroll
-        for (int k = 0; k < NPT; ++k) {
-          int n = ant(k);
-          if constexpr (EXACT) y[k] = cadd(y[k], cmul(ph, hp[n]));
-          else y[k] = cfma(ph, hp[n], y[k]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < NPT; ++k) {
-          int n = ant(k);
-          if (n >= s && n < e) {
-            if constexpr (EXACT) y[k] = cadd(y[k], cmul(ph, hp[n]));
-            else y[k] = cfma(ph, hp[n], y[k]);
-          }
+      for (int k = 0; k < NPT; ++k) {
+        const int n = ant(k);
+        const bool in = n >= s && n < e;
+        const T h = in ? hp[n] : czero<T>();
+        if (in) {
+          if constexpr (EXACT) y[k] = cadd(y[k], cmul(ph, h));
+          else y[k] = cfma(ph, h, y[k]);
         }
       }
+    };
+    {
+      int q = cp[w];
+      const int q1 = cp[w + 1];
+      for (; q + 1 < q1; q += 2) {
+        const int i0 = cl[q], i1 = cl[q + 1];
+        acc_row(i0);
+        acc_row(i1);
+      }
+      if (q < q1) acc_row(cl[q]);
     }
     double sy = 0.0;
 #pragma unroll
