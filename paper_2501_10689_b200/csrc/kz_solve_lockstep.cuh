@@ -59,7 +59,7 @@ struct LsArgs {
 // ------------------------------------------------------------------ smem plan
 struct LsPlan {
   int K, W, G, S, hcap, cs, KW;
-  size_t rowS, rowL, rowB, c0, c1, en, cost, cmask, clist_ptr, clist, olist, nlist, ocl_ptr, ocl, ncl_ptr, ncl,
+  size_t rowS, rowL, rowB, rvo, c0, c1, en, cost, cmask, clist_ptr, clist, olist, nlist, ocl_ptr, ocl, ncl_ptr, ncl,
       H, P, Q, R, Dp, scr, sel, gam, num, sp, nz, done, iters, noop, flops, prev, pool, poolcnt, misc, total;
 };
 
@@ -72,6 +72,7 @@ __host__ __device__ inline LsPlan ls_plan(int K, int W, int G, int S, int hcap, 
   p.rowS = o; o = a16(o + 4 * K);
   p.rowL = o; o = a16(o + 4 * K);
   p.rowB = o; o = a16(o + 4 * K);
+  p.rvo = o; o = a16(o + 8 * (size_t)K);
   p.c0 = o; o = a16(o + 4 * K);
   p.c1 = o; o = a16(o + 4 * K);
   p.en = o; o = a16(o + 8 * K);
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   int* rowS = (int*)(sm + pl.rowS);
   int* rowL = (int*)(sm + pl.rowL);
   int* rowB = (int*)(sm + pl.rowB);
+  long long* rvo = (long long*)(sm + pl.rvo);  // heff offset of row i (row_val_ptr)
   int* c0 = (int*)(sm + pl.c0);
   int* c1 = (int*)(sm + pl.c1);
   double* en = (double*)(sm + pl.en);
@@ -171,72 +173,98 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   KZ_TSTART
 
   // ---------------------------------------------------------------- setup
+  // (all parallel: no single-thread loops over rows / chunks, no load latency per row)
   for (int i = tid; i < K; i += nthr) {
     size_t r = (size_t)b * K + i;
     int sg = p.P.row_seg_ptr[r];
     int s = p.P.seg_start[sg], L = p.P.seg_len[sg];
     rowS[i] = s;
     rowL[i] = L;
+    rvo[i] = p.P.row_val_ptr[r];
     c0[i] = s >> 5;
     c1[i] = (s + L - 1) >> 5;
     en[i] = p.P.row_energy[r];
   }
-  __syncthreads(); KZ_PHASE();
-  if (tid == 0) {  // antenna-aligned row bases (even), VR partition lists
-    int base = 0;
-    for (int i = 0; i < K; ++i) {
-      rowB[i] = base;
-      base += (rowL[i] + 3) & ~1;
-    }
-    misc[0] = base;
-    int no = 0, nn = 0;
-    if (p.P.orth_ptr) {
-      int o0 = p.P.orth_ptr[b], o1 = p.P.orth_ptr[b + 1];
-      for (int q = o0; q < o1; ++q) olist[no++] = p.P.orth_idx[q];
-      int n0 = p.P.non_ptr[b], n1 = p.P.non_ptr[b + 1];
-      for (int q = n0; q < n1; ++q) nlist[nn++] = p.P.non_idx[q];
-    }
-    misc[1] = no;
-    misc[2] = nn;
+  int nO = 0, nN = 0;
+  if (p.P.orth_ptr) {
+    const int o0 = p.P.orth_ptr[b], n0 = p.P.non_ptr[b];
+    nO = p.P.orth_ptr[b + 1] - o0;
+    nN = p.P.non_ptr[b + 1] - n0;
+    for (int q = tid; q < nO; q += nthr) olist[q] = p.P.orth_idx[o0 + q];
+    for (int q = tid; q < nN; q += nthr) nlist[q] = p.P.non_idx[n0 + q];
   }
   __syncthreads(); KZ_PHASE();
-  const int nO = misc[1], nN = misc[2];
-  // per-chunk row lists (ascending rows): all rows, O rows, N rows
-  if (tid == 0) {
-    int q = 0, qo = 0, qn = 0;
-    for (int ww = 0; ww < W; ++ww) {
-      clist_ptr[ww] = q;
-      ocl_ptr[ww] = qo;
-      ncl_ptr[ww] = qn;
-      for (int i = 0; i < K; ++i)
-        if (c0[i] <= ww && ww <= c1[i]) clist[q++] = i;
-      for (int k = 0; k < nO; ++k) {
-        int i = olist[k];
-        if (c0[i] <= ww && ww <= c1[i]) ocl[qo++] = i;
+  if (w == 0) {  // antenna-aligned row bases (even): exclusive prefix of (L + 3) & ~1 by one warp
+    int carry = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int i = base + lane;
+      const int v = i < K ? ((rowL[i] + 3) & ~1) : 0;
+      int sc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += t2;
       }
-      for (int k = 0; k < nN; ++k) {
-        int i = nlist[k];
-        if (c0[i] <= ww && ww <= c1[i]) ncl[qn++] = i;
-      }
+      if (i < K) rowB[i] = carry + sc - v;
+      carry += __shfl_sync(FULL, sc, 31);
     }
-    clist_ptr[W] = q;
-    ocl_ptr[W] = qo;
-    ncl_ptr[W] = qn;
+    if (lane == 0) misc[0] = carry;
   }
-  // H rows -> shared memory, element for antenna n of row i at Hs[rowB + (s&1) + n - s]
-  for (int i = 0; i < K; ++i) {
-    size_t r = (size_t)b * K + i;
-    const T* src = heff + p.P.row_val_ptr[r];
-    T* dst = Hs + rowB[i] + (rowS[i] & 1);
-    int L = rowL[i];
-    for (int j = tid; j < L; j += nthr) dst[j] = src[j];
+  // per-chunk row lists (ascending rows): warp ww counts and compacts its chunk's rows with ballots
+  auto chunk_list = [&](int* ptr, int* out, const int* src, int n) {  // src = NULL: rows 0..n-1
+    for (int ww = w; ww < W; ww += nthr >> 5) {
+      int cnt = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int k = base + lane;
+        const int i = k < n ? (src ? src[k] : k) : 0;
+        cnt += __popc(__ballot_sync(FULL, k < n && c0[i] <= ww && ww <= c1[i]));
+      }
+      if (lane == 0) ptr[ww + 1] = cnt;
+    }
+    __syncthreads();
     if (tid == 0) {
-      if (rowS[i] & 1) Hs[rowB[i]] = czero<T>();
-      int end = rowB[i] + (rowS[i] & 1) + L;
-      int lim = rowB[i] + ((L + 3) & ~1);
-      for (int e = end; e < lim; ++e) Hs[e] = czero<T>();
+      ptr[0] = 0;
+      for (int ww = 0; ww < W; ++ww) ptr[ww + 1] += ptr[ww];
+    }
+    __syncthreads();
+    for (int ww = w; ww < W; ww += nthr >> 5) {
+      int q = ptr[ww];
+      for (int base = 0; base < n; base += 32) {
+        const int k = base + lane;
+        const int i = k < n ? (src ? src[k] : k) : 0;
+        const bool ov = k < n && c0[i] <= ww && ww <= c1[i];
+        const unsigned bal = __ballot_sync(FULL, ov);
+        if (ov) out[q + __popc(bal & ((1u << lane) - 1))] = i;
+        q += __popc(bal);
+      }
+    }
+  };
+  chunk_list(clist_ptr, clist, nullptr, K);
+  chunk_list(ocl_ptr, ocl, olist, nO);
+  chunk_list(ncl_ptr, ncl, nlist, nN);
+  __syncthreads();
+  // H rows -> shared memory, element for antenna n of row i at Hs[rowB + (s&1) + n - s]: asynchronous copies,
+  // all rows in flight; the even-alignment pad entries are zeroed by one thread per row
+  for (int i = 0; i < K; ++i) {
+    const T* src = heff + rvo[i];
+    T* dst = Hs + rowB[i] + (rowS[i] & 1);
+    const int L = rowL[i];
+    for (int j = tid; j < L; j += nthr) {
+      if constexpr (sizeof(T) == 16) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + j) : "memory");
+      } else {
+        cp_async8(dst + j, src + j, true);
+      }
     }
   }
+  for (int i = tid; i < K; i += nthr) {
+    if (rowS[i] & 1) Hs[rowB[i]] = czero<T>();
+    const int end = rowB[i] + (rowS[i] & 1) + rowL[i];
+    const int lim = rowB[i] + ((rowL[i] + 3) & ~1);
+    for (int e = end; e < lim; ++e) Hs[e] = czero<T>();
+  }
+  cp_async_wait_all();
   if constexpr (SCH == KZ_VR_OGRK) {
     for (int i = tid; i < K; i += nthr) {
       size_t r = (size_t)b * K + i;
