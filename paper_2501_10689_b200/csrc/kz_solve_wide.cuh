@@ -328,10 +328,23 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
     const int ns = c1[i] - c0[i];
-    for (int s = 0; s <= ns; ++s) {
-      T v = pp[(size_t)s * G];
-      dx += v.x;
-      dy += v.y;
+    if (SCH != KZ_VR_OAHK && SL <= 8) {  // every slot load issued at once (predicated), then the sums in slot
+                                          // order (vr-oahk: register pressure, measured slower)
+      T v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v[s] = s <= ns ? pp[(size_t)s * G] : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s <= ns) {
+          dx += v[s].x;
+          dy += v[s].y;
+        }
+    } else {
+      for (int s = 0; s <= ns; ++s) {
+        T v = pp[(size_t)s * G];
+        dx += v.x;
+        dy += v.y;
+      }
     }
     T q = Qs[xs(i, gg)];
     const int c = g0 + gg;
@@ -420,6 +433,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           if (SCH != KZ_GK && act) u = draw_u(gg);  // independent of the residuals: issue early
           float wsum = 0.f;
           if (act)
+#pragma unroll 4
             for (int i = hl; i < K; i += 16) {
               bool upd = true;
               if constexpr (SCH == KZ_VR_OGRK) {
@@ -431,6 +445,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
               wsum += r.x * r.x + r.y * r.y;
             }
           __syncwarp();
+          KZ_PHASE();  // [timing] residuals of this rhs' rows
           int isel = -1;
           long long f;
           if constexpr (SCH == KZ_GK) {
@@ -503,6 +518,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
             }
             if (tot > 0.f && isel < 0) isel = lastnz;
           }
+          KZ_PHASE();  // [timing] row pick
           if (hl == 0 && act) {
             if (isel < 0) {
               donev[gg] = 1;
@@ -638,6 +654,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
           float nx = 0.f, ny = 0.f, sp = 0.f;
           bool nz = false;
           if (act)
+#pragma unroll(SCH == KZ_VR_OAHK ? 1 : 4)
             for (int i = hl; i < K; i += 16) {
               if (which && inset[i] != which) continue;
               const T r = resid(i, gg);
