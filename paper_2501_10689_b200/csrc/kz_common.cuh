@@ -20,14 +20,19 @@
 // iteration), [10] wall ns, [11] smid, [12..43] per-warp cycles from iteration start to the end of
 // the warp's refresh (KZ_WSTAMP), summed over iterations.
 #define KZ_TSTART __shared__ volatile int kz_dummy; long long kz_t_last = clock64(); long long kz_ph[12] = {0}; \
+  long long kz_sm[8] = {0}; const long long kz_s0 = kz_t_last; \
   int kz_pi = 0; long long kz_w0 = 0, kz_wacc = 0; \
   unsigned long long kz_g0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(kz_g0));
 #define KZ_PHASE() do { (void)kz_dummy; if (threadIdx.x == 0) { long long n_ = clock64(); \
   kz_ph[kz_pi < 9 ? kz_pi : 9] += n_ - kz_t_last; kz_t_last = n_; } ++kz_pi; } while (0)
 #define KZ_ITER() (kz_pi = 1, kz_w0 = clock64())
+// setup checkpoint k (< 8): cycles since kernel start on thread 0, dumped to slots [36 + k] (kernels with at
+// most 24 warps, whose per-warp slots stop below 36)
+#define KZ_SETUP_MARK(k) do { if (threadIdx.x == 0) kz_sm[(k) & 7] = clock64() - kz_s0; } while (0)
 #define KZ_WSTAMP() (kz_wacc += clock64() - kz_w0)
 #define KZ_TDUMP(ptr) do { if ((ptr)) { long long* o_ = (ptr) + (size_t)blockIdx.x * 44; \
-  if ((threadIdx.x & 31) == 0) o_[12 + (threadIdx.x >> 5)] = kz_wacc; \
+  if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 24) o_[12 + (threadIdx.x >> 5)] = kz_wacc; \
+  if (threadIdx.x == 0 && blockDim.x <= 768) for (int q_ = 0; q_ < 8; ++q_) o_[36 + q_] = kz_sm[q_]; \
   if (threadIdx.x == 0) { unsigned long long g1_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1_)); \
   kz_ph[10] = (long long)(g1_ - kz_g0); unsigned smid_; asm("mov.u32 %0, %%smid;" : "=r"(smid_)); kz_ph[11] = smid_; \
   for (int q_ = 0; q_ < 12; ++q_) o_[q_] = kz_ph[q_]; } } } while (0)
@@ -35,6 +40,7 @@
 #define KZ_TSTART
 #define KZ_PHASE() do {} while (0)
 #define KZ_ITER() ((void)0)
+#define KZ_SETUP_MARK(k) do {} while (0)
 #define KZ_WSTAMP() ((void)0)
 #define KZ_TDUMP(ptr) do {} while (0)
 #endif

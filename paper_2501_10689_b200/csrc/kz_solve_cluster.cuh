@@ -95,7 +95,7 @@ __device__ __forceinline__ float2 ld_remote(const float2* p, int rank) {
 struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
   size_t rowS, rowL, rvo, c0, c1, en, ien, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
-      Ro, Fo, IN, Phl, dloc, dlst, dcnt, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
+      Ro, Fo, IN, Phl, dloc, dlst, dcnt, blk, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
       misc, total;
 };
 
@@ -144,6 +144,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.dloc = o; o = al(o + 4 * (size_t)p.KO * CL);
   p.dlst = o; o = al(o + 4 * (size_t)p.KO * CL);
   p.dcnt = o; o = al(o + 4 * (size_t)p.KO);
+  p.blk = o; o = al(o + 8 * (size_t)((K + 31) / 32));  // setup: per 32-row block (local rows, pieces)
   p.AG4 = o; o = al(o + (agg ? 16 * (size_t)CL * G : 0));
   p.GAMv = o; o = al(o + 8 * G);
   p.stepv = o; o = al(o + 4 * G);
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   // (ascending CTAs; the phi push is one precomputed address per destination)
   uint32_t* dlst = (uint32_t*)(sm + pl.dlst);
   int* dcnt = (int*)(sm + pl.dcnt);
+  int* blk = (int*)(sm + pl.blk);
   float4* AG4 = (float4*)(sm + pl.AG4);
   T* GAMv = (T*)(sm + pl.GAMv);
   int* stepv = (int*)(sm + pl.stepv);
@@ -294,114 +296,176 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     ien[i] = (float)(1.0 / p.P.row_energy[r]);
     inset[i] = 0;
   }
+  if (AGG && p.P.orth_ptr && tid == 0) {  // partition ranges read alongside the rows (one latency round)
+    misc[8] = p.P.orth_ptr[b];
+    misc[9] = p.P.orth_ptr[b + 1];
+    misc[10] = p.P.non_ptr[b];
+    misc[11] = p.P.non_ptr[b + 1];
+  }
   __syncthreads();
+  KZ_SETUP_MARK(0);
   if (AGG && p.P.orth_ptr) {
-    for (int q = p.P.orth_ptr[b] + tid; q < p.P.orth_ptr[b + 1]; q += nthr) inset[p.P.orth_idx[q]] = 1;
-    for (int q = p.P.non_ptr[b] + tid; q < p.P.non_ptr[b + 1]; q += nthr) inset[p.P.non_idx[q]] = 2;
+    for (int q = misc[8] + tid; q < misc[9]; q += nthr) inset[p.P.orth_idx[q]] = 1;
+    for (int q = misc[10] + tid; q < misc[11]; q += nthr) inset[p.P.non_idx[q]] = 2;
   }
-  // rows touching this slice, ascending (warp 0 compacts with ballots)
-  if (w == 0) {
-    int n = 0, hcar = 0;
-    for (int base = 0; base < K; base += 32) {
-      const int i = base + lane;
-      int l0 = W, l1 = -1;  // local warps whose chunks lie in [c0_i, c1_i] (contiguous: chunk_of is increasing)
-      if (i < K)
-        for (int ww = 0; ww < W; ++ww) {
-          const int ch = chunk_of(ww);
-          if (ch >= c0[i] && ch <= c1[i] && ch < nch) {
-            l0 = min(l0, ww);
-            l1 = ww;
-          }
+  // rows touching this slice, ascending: 32-row blocks spread over the warps, two ballot passes around a
+  // block-level prefix (local row index and H piece offset of every row)
+  const int nblk32 = (K + 31) / 32;
+  auto row_span = [&](int i, int& l0, int& l1) {  // local warps whose chunks lie in [c0_i, c1_i] (contiguous)
+    l0 = W;
+    l1 = -1;
+    if (i < K)
+      for (int ww = 0; ww < W; ++ww) {
+        const int ch = chunk_of(ww);
+        if (ch >= c0[i] && ch <= c1[i] && ch < nch) {
+          l0 = min(l0, ww);
+          l1 = ww;
         }
-      const bool ov = l0 <= l1;
-      const unsigned bal = __ballot_sync(FULL, ov);
-      const int np = ov ? l1 - l0 + 1 : 0;
-      int sc = np;
+      }
+  };
+  for (int bk = w; bk < nblk32; bk += W) {
+    int l0, l1;
+    row_span(bk * 32 + lane, l0, l1);
+    const bool ov = l0 <= l1;
+    int np = ov ? l1 - l0 + 1 : 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t2 = __shfl_up_sync(FULL, sc, o);
-        if (lane >= o) sc += t2;
-      }
-      const int idx = n + __popc(bal & ((1u << lane) - 1));
-      if (i < K) loc[i] = ov ? idx : -1;
-      if (ov && idx < pl.nlcap) {
-        lrow[idx] = i;
-        lh[idx] = (hcar + sc - np) * CH;
-        lcc[idx] = l0 | (l1 << 8);
-      }
-      n += __popc(bal);
-      hcar += __shfl_sync(FULL, sc, 31);
-    }
+    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(FULL, np, o);
+    const int cnt = __popc(__ballot_sync(FULL, ov));
     if (lane == 0) {
-      misc[1] = n;
-      misc[2] = hcar;
+      blk[2 * bk] = cnt;
+      blk[2 * bk + 1] = np;
     }
   }
   __syncthreads();
+  for (int bk = w; bk < nblk32; bk += W) {
+    int n = 0, hcar = 0;
+    for (int q = 0; q < bk; ++q) {
+      n += blk[2 * q];
+      hcar += blk[2 * q + 1];
+    }
+    const int i = bk * 32 + lane;
+    int l0, l1;
+    row_span(i, l0, l1);
+    const bool ov = l0 <= l1;
+    const unsigned bal = __ballot_sync(FULL, ov);
+    const int np = ov ? l1 - l0 + 1 : 0;
+    int sc = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t2 = __shfl_up_sync(FULL, sc, o);
+      if (lane >= o) sc += t2;
+    }
+    const int idx = n + __popc(bal & ((1u << lane) - 1));
+    if (i < K) loc[i] = ov ? idx : -1;
+    if (ov && idx < pl.nlcap) {
+      lrow[idx] = i;
+      lh[idx] = (hcar + sc - np) * CH;
+      lcc[idx] = l0 | (l1 << 8);
+    }
+  }
+  if (tid == 0) {
+    int n = 0, hcar = 0;
+    for (int q = 0; q < nblk32; ++q) {
+      n += blk[2 * q];
+      hcar += blk[2 * q + 1];
+    }
+    misc[1] = n;
+    misc[2] = hcar;
+  }
+  __syncthreads();
+  KZ_SETUP_MARK(1);
   const int NL = misc[1], npairs = misc[2];
   if (npairs > p.pcap || NL > pl.nlcap) __trap();  // layout hint violated: fail loudly
-  // row pieces -> shared memory, zero padded to whole chunks: one warp per (local row, piece), lanes over
-  // the 32 antennas of the piece (coalesced 256 B), all issued as asynchronous copies (no load latency per
-  // piece; the row offsets come from shared memory, so no dependent global load either)
-  {
-    int n = 0;  // this warp's current local row, advanced by W pieces at a time
-    for (int q = w; q < npairs; q += W) {
-      while (n < NL - 1 && lh[n + 1] <= q * CH) ++n;
-      const int pc = q - (lh[n] >> 5);
-      const int i = lrow[n];
-      const int ant = chunk_of((lcc[n] & 0xFF) + pc) * CH + lane;
-      const int s = rowS[i];
-      const bool in = ant >= s && ant < s + rowL[i];
-      cp_async8(Hs + q * CH + lane, heff + rvo[i] + (in ? ant - s : 0), in);
+  // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
+  // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
+  // no dependent global load, no load latency per piece)
+  for (int n = w; n < NL; n += W) {
+    const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
+    const int s = rowS[i], L = rowL[i];
+    const T* src = heff + rvo[i];
+    for (int pc = 0; pc <= l1 - l0; ++pc) {
+      const int ant = chunk_of(l0 + pc) * CH + lane;
+      const bool in = ant >= s && ant < s + L;
+      cp_async8(Hs + h0 + pc * CH + lane, src + (in ? ant - s : 0), in);
     }
-    cp_async_wait_all();
   }
-  // per-chunk piece lists (ascending rows)
-  auto build_list = [&](int* ptr, int2* out, int which, int base0) {
-    int cnt = 0;
+  KZ_SETUP_MARK(2);
+  cp_async_wait_all();
+  KZ_SETUP_MARK(3);
+  // per-chunk piece lists (ascending rows): all rows (lst) and, for vr-oahk, the O rows then the N rows
+  // (olst / nlst share one array); one counting pass and one fill pass for all of them
+  const bool want_all = SCH != KZ_VR_OAHK || residual;
+  constexpr bool want_on = SCH == KZ_VR_OAHK;
+  auto entry = [&](int n, int l0) {
+    const int i = lrow[n], o = i / KO, il = i - o * KO;
+    const int slot = chunk_of(w) - c0[i];
+    return make_int2((lh[n] + (w - l0) * CH) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
+  };
+  {
+    int ca = 0, co = 0, cn = 0;
     for (int base = 0; base < NL; base += 32) {
       const int n = base + lane;
       bool ov = false;
+      int set = 0;
       if (n < NL) {
         const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
-        ov = l0 <= w && w <= l1 && (which == 0 || inset[lrow[n]] == which);
+        ov = l0 <= w && w <= l1;
+        set = inset[lrow[n]];
       }
-      cnt += __popc(__ballot_sync(FULL, ov));
+      ca += __popc(__ballot_sync(FULL, ov));
+      co += __popc(__ballot_sync(FULL, ov && set == 1));
+      cn += __popc(__ballot_sync(FULL, ov && set == 2));
     }
-    if (lane == 0) ptr[w + 1] = cnt;
-    __syncthreads();
-    if (tid == 0) {
-      ptr[0] = base0;
-      for (int ww = 0; ww < W; ++ww) ptr[ww + 1] += ptr[ww];
+    if (lane == 0) {
+      if (want_all) lptr[w + 1] = ca;
+      if (want_on) {
+        optr[w + 1] = co;
+        nptr[w + 1] = cn;
+      }
     }
-    __syncthreads();
-    int q = ptr[w];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (want_all) {
+      lptr[0] = 0;
+      for (int ww = 0; ww < W; ++ww) lptr[ww + 1] += lptr[ww];
+    }
+    if (want_on) {
+      optr[0] = 0;
+      for (int ww = 0; ww < W; ++ww) optr[ww + 1] += optr[ww];
+      nptr[0] = optr[W];
+      for (int ww = 0; ww < W; ++ww) nptr[ww + 1] += nptr[ww];
+    }
+  }
+  __syncthreads();
+  {
+    int qa = want_all ? lptr[w] : 0, qo = want_on ? optr[w] : 0, qn = want_on ? nptr[w] : 0;
     for (int base = 0; base < NL; base += 32) {
       const int n = base + lane;
       bool ov = false;
-      int l0 = 0;
+      int set = 0, l0 = 0;
       if (n < NL) {
         l0 = lcc[n] & 0xFF;
         const int l1 = lcc[n] >> 8;
-        ov = l0 <= w && w <= l1 && (which == 0 || inset[lrow[n]] == which);
+        ov = l0 <= w && w <= l1;
+        set = inset[lrow[n]];
       }
-      const unsigned bal = __ballot_sync(FULL, ov);
+      const unsigned ba = __ballot_sync(FULL, ov);
+      const unsigned bo = __ballot_sync(FULL, ov && set == 1);
+      const unsigned bn = __ballot_sync(FULL, ov && set == 2);
+      const unsigned below = (1u << lane) - 1;
       if (ov) {
-        const int i = lrow[n], o = i / KO, il = i - o * KO;
-        const int slot = chunk_of(w) - c0[i];
-        out[q + __popc(bal & ((1u << lane) - 1))] =
-            make_int2((lh[n] + (w - l0) * CH) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
+        const int2 e = entry(n, l0);
+        if (want_all) lst[qa + __popc(ba & below)] = e;
+        if (want_on && set == 1) olst[qo + __popc(bo & below)] = e;
+        if (want_on && set == 2) nlst[qn + __popc(bn & below)] = e;
       }
-      q += __popc(bal);
+      qa += __popc(ba);
+      qo += __popc(bo);
+      qn += __popc(bn);
     }
-  };
-  __syncthreads();
-  if (SCH != KZ_VR_OAHK || residual) build_list(lptr, lst, 0, 0);
-  if (SCH == KZ_VR_OAHK) {
-    build_list(optr, olst, 1, 0);
-    __syncthreads();
-    build_list(nptr, nlst, 2, optr[W]);
   }
+  KZ_SETUP_MARK(4);
   if constexpr (SCH == KZ_VR_OGRK) {
     // owner: bitmask of X_i for its rows (coupling is symmetric: i in X_j <=> j in X_i, vrgraph.py:60-82);
     // every CTA: the refresh cost of each X_j (flop charge)
@@ -453,7 +517,9 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     }
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
+  KZ_SETUP_MARK(5);
   cluster_sync();  // every CTA of the cluster is resident and initialised before any DSMEM traffic
+  KZ_SETUP_MARK(6);
   for (int e = tid; e < nown * CL; e += nthr) {  // owner: where each CTA keeps its piece of an owned row
     const int il = e / CL, d = e % CL, i = o_lo + il;
     dloc[e] = d == c ? loc[i] : ld_remote(loc + i, d);
@@ -466,6 +532,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
     dcnt[il] = n;
   }
   __syncthreads();
+  KZ_SETUP_MARK(7);
   KZ_PHASE();
 
   const int a = lane / LPA, g = lane % LPA;

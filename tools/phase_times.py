@@ -77,6 +77,10 @@ if wst.max() > 0:
     print("  per-warp refresh end (cyc/iter, mean over CTAs):", " ".join(f"{x:.0f}" for x in wst.mean(axis=0)))
     print(f"  slowest warp per CTA: mean {wst.max(axis=1).mean():.0f}  fastest: {wst.min(axis=1).mean():.0f}")
 print(f"  setup {ph[:, 0].mean():.0f} cyc ({ph[:, 0].mean() / tot.mean() * 100:.1f}%)")
+marks = raw[:, 36:44]
+if marks.max() > 0:  # KZ_SETUP_MARK checkpoints (cycles since kernel start, thread 0), as increments
+    m = marks.mean(axis=0)
+    print("  setup checkpoints (cyc since start, mean over CTAs):", " ".join(f"{x:.0f}" for x in m))
 for q, v in enumerate(per_it, start=1):
     if v > 0:
         print(f"  phase {q}: {v:8.0f} cyc/iter ({v * a.iters / tot.mean() * 100:5.1f}%)")
