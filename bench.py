@@ -346,6 +346,19 @@ def main():
     fp32_peak, fp32_src = measured_fp32_peak()
     reg3_peak = measured_fp32_reg3_peak()
     smem_peak = measured_smem_peak()
+    smem_ncu = None  # shared-memory bytes the dominant launch moves, from ncu counters (profiles/r01_ncu_smem.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_smem.json")) as fh:
+            rec = json.load(fh).get(dom)
+        if rec and a.dtype == "c64" and cfg.name == "cfg2":
+            sb = rec["shared_bytes_per_iteration"] * iters * B / rec["B"]
+            smem_ncu = {"bytes_per_launch": sb, "achieved_GBps": sb / (avg[dom] / 1e3) / 1e9, "peak_GBps": smem_peak,
+                        "frac": sb / (avg[dom] / 1e3) / 1e9 / smem_peak if smem_peak else None,
+                        "ncu_pct_of_peak_sustained": rec["pct_of_peak_sustained_elapsed"],
+                        "source": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum x 128 B of the ncu --set full capture "
+                                  f"({rec['capture']}, B={rec['B']}, T={rec['T']}), scaled to this launch's T and B"}
+    except (OSError, ValueError, KeyError):
+        pass
     t_dom = avg[dom] / 1e3
     tflops = 8.0 * elems_dom / t_dom / 1e12
     bytes_dom = csize * elems_dom
@@ -453,6 +466,7 @@ def main():
                                                             "per SMSP vs 0.97 for the immediate form"}
                                             if reg3_peak else None),
                          "smem_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": smem_peak},
+                         "smem_ncu": smem_ncu,
                          "hbm_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": hbm_peak,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,

@@ -157,6 +157,29 @@ def main():
         with open(os.path.join(prof, f"{a.tag}_launches_summary.txt"), "w") as fh:
             fh.write("\n".join(lines) + "\n")
         subprocess.run(["cp", lpath, os.path.join(prof, f"{a.tag}_launches.csv")])
+    # shared-memory traffic measured by ncu for the wide-kernel captures (cfg2, B=1024, T=50): the bench's
+    # roofline.smem_ncu scales it to its own T (bytes are per iteration; setup is <1%)
+    smem = {}
+    for sc, rep_name in (("vr-oahk", "full_vroahk"), ("grk", "full_wide_grk"), ("ahk", "full_wide_ahk")):
+        rep = os.path.join(a.dir, rep_name + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        if len(rows) < 3:
+            continue
+        m = dict(zip(rows[0], rows[2]))
+        wf = float(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", ""))
+        smem[sc] = {"capture": rep_name, "B": 1024, "T": 50,
+                    "shared_wavefronts": wf, "shared_bytes": wf * 128.0,
+                    "shared_bytes_per_iteration": wf * 128.0 / 50,
+                    "excessive_wavefronts": float(m.get("derived__memory_l1_wavefronts_shared_excessive", "0").replace(",", "")),
+                    "pct_of_peak_sustained_elapsed": float(
+                        m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]),
+                    "duration_ms": float(m["gpu__time_duration.sum"].replace(",", ""))}
+    if smem:
+        with open(os.path.join(prof, f"{a.tag}_ncu_smem.json"), "w") as fh:
+            json.dump(smem, fh, indent=1)
     # full-set captures: key metrics, stall samples by straight-line SASS block, hottest source lines
     for rep_name, title, ksub, out in FULL_SETS:
         rep = os.path.join(a.dir, rep_name + ".ncu-rep")
