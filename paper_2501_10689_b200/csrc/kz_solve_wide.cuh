@@ -29,6 +29,7 @@ namespace wide {
 
 constexpr int G = 32;
 constexpr int CH = 32;  // chunk = antennas per warp
+constexpr int HSKEW = 6;  // spare H elements per row for the bank skew of the row bases
 // [row][rhs] arrays (P slots, Q, R) are XOR-swizzled on the rhs index so that
 // both access directions (lanes over rhs: refresh / projection; lanes over
 // rows: finalise / selection) are bank-conflict free.
@@ -165,14 +166,16 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
     int carry = 0;
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
-      int v = i < K ? (c1[i] - c0[i] + 1) * CH : 0;
+      // each row gets HSKEW spare elements and starts 2 (i & 3) elements into its allocation: the rows a warp
+      // projects (one per lane, chunk-aligned otherwise) then fall on four different 16-byte bank groups
+      int v = i < K ? (c1[i] - c0[i] + 1) * CH + HSKEW : 0;
       int sc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         int t2 = __shfl_up_sync(FULL, sc, o);
         if (lane >= o) sc += t2;
       }
-      if (i < K) hoff[i] = carry + sc - v;
+      if (i < K) hoff[i] = carry + sc - v + 2 * (i & 3);
       carry += __shfl_sync(FULL, sc, 31);
     }
   }
@@ -917,7 +920,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
 inline size_t wide_smem_bytes(const kz_problem& P, int* S_out, int* hcap_out) {
   const int K = P.n_users;
   const int S = (P.max_support + wide::CH - 2) / wide::CH + 1;  // chunks a row can touch
-  const int hcap = K * S * wide::CH;
+  const int hcap = K * (S * wide::CH + wide::HSKEW);
   *S_out = S;
   *hcap_out = hcap;
   return wide::plan(K, P.n_antennas, S, hcap).total;
