@@ -789,8 +789,13 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
       for (int pair = w; pair < G / 2; pair += W) {
         const int gg = pair + hf * (G / 2);
         bool act = !donev[gg];
-        float nrm2 = 0.f;
-        for (int d = 0; d < CL; ++d) nrm2 += SPP[d * G + gg];
+        // the draw is independent of the sums: issue it first (counter-based Philox / a stream read, consumed
+        // only if a row is drawn)
+        const double u_draw = (SCH != KZ_GK && act) ? draw_u(gg) : 0.0;
+        // ||r||^2 of the state after the last step: butterfly over the CTAs' partials (same order in every CTA)
+        float nrm2 = hl < CL ? SPP[hl * G + gg] : 0.f;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) nrm2 += __shfl_xor_sync(FULL, nrm2, o);
         bool stopped = false;
         if (act && hl == 0) stopped = stop_test(gg, nrm2);
         stopped = __shfl_sync(FULL, stopped, 16 * hf);
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
           }
           const float tot = __shfl_sync(FULL, incl, 16 * hf + 15);
           const bool draw = act && tot > 0.f;  // tot == 0: None, no draw consumed (solvers.py:235-236)
-          const float tau = draw ? (float)draw_u(gg) * tot : 0.f;
+          const float tau = draw ? (float)u_draw * tot : 0.f;
           const unsigned hit = (__ballot_sync(FULL, draw && v > 0.f && incl > tau) & hmask) >> (16 * hf);
           const unsigned nzb = (__ballot_sync(FULL, draw && v > 0.f) & hmask) >> (16 * hf);
           if (draw) cstar = hit ? __ffs(hit) - 1 : 31 - __clz(nzb);
