@@ -106,14 +106,28 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
   int it = 0;
   if (active) {
     const size_t rid = (size_t)b * K + c;
+    // draws in batches of 32: lane l evaluates (or loads) the draw of iteration it0 + l once, iteration it takes
+    // it with a shuffle -- the same stream values, one Philox evaluation / one coalesced load per 32 iterations
+    double ubuf = 0.0;
+    int ibuf = 0;
+    auto refill = [&](int it0) {
+      const int d = it0 + lane;
+      if (p.R.kind == KZ_RNG_HOST_INDEX) {
+        if (d < p.T) ibuf = p.R.indices[rid * p.R.stream_len + d];
+      } else if (p.R.kind == KZ_RNG_PHILOX) {
+        ubuf = philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+      } else if (d < p.T) {
+        ubuf = p.R.uniforms[rid * p.R.stream_len + d];
+      }
+    };
     for (it = 0; it < p.T; ++it) {
+      if ((it & 31) == 0) refill(it);
       // ---- draw (solvers.py:218-230)
       int i;
       if (p.R.kind == KZ_RNG_HOST_INDEX) {
-        i = p.R.indices[rid * p.R.stream_len + it];
+        i = __shfl_sync(FULL, ibuf, it & 31);
       } else if (SCH == KZ_URK) {
-        const double u = p.R.kind == KZ_RNG_PHILOX ? philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)it)
-                                                   : p.R.uniforms[rid * p.R.stream_len + it];
+        const double u = __shfl_sync(FULL, ubuf, it & 31);
         i = (int)(u * K);
         i = i >= K ? K - 1 : i;
       } else {  // energy-weighted pick without replacement from the epoch pool (warp-parallel scan)
@@ -122,8 +136,7 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
           poolcnt = K;
           __syncwarp();
         }
-        const double u = p.R.kind == KZ_RNG_PHILOX ? philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)it)
-                                                   : p.R.uniforms[rid * p.R.stream_len + it];
+        const double u = __shfl_sync(FULL, ubuf, it & 31);
         double tot = 0.0;
         for (int j = lane; j < K; j += 32)
           if ((pool[j >> 5] >> (j & 31)) & 1u) tot += en[j];
