@@ -109,6 +109,9 @@ typedef struct kz_problem {
 } kz_problem;
 
 #define KZ_PROBLEM_CONTIGUOUS 1
+/* kz_epilogue only: the workspace already holds G0 = H^H H of this problem from an earlier kz_epilogue call
+   on the same workspace (the Gram-form path; H is the same, so several V of one batch share it) */
+#define KZ_PROBLEM_GRAM_CACHED 2
 
 typedef struct kz_stop {
   int32_t mode;         /* kz_stop_mode */

@@ -19,6 +19,7 @@ KZ_ERR_WORKSPACE = -4
 
 SCHEME_IDS = {"urk": 0, "swor-erk": 1, "gk": 2, "grk": 3, "vr-ogrk": 4, "ahk": 5, "vr-oahk": 6}
 KZ_C128, KZ_C64 = 0, 1
+KZ_PROBLEM_CONTIGUOUS, KZ_PROBLEM_GRAM_CACHED = 1, 2  # kz_problem.flags
 STOP_LOCKSTEP, STOP_RESIDUAL, STOP_ORACLE = 0, 1, 2
 RNG_NONE, RNG_HOST_UNIFORM, RNG_HOST_INDEX, RNG_PHILOX = 0, 1, 2, 3
 

@@ -21,7 +21,11 @@ from .batch import DeviceBatch, HostBatch
 
 
 def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = False, snr_linear=None,
-             want_f: bool = False, stream=None) -> dict:
+             want_f: bool = False, stream=None, workspace=None, gram_cached: bool = False) -> dict:
+    """F / NMSE / sum-rate of the solutions v [B][K][K] (kz_epilogue).  `workspace` (uint8 device tensor, e.g.
+    the "workspace" of an earlier result) is reused when large enough; with gram_cached=True it must hold the
+    Gram G0 = H^H H of this batch from an earlier Gram-form call on the same workspace (several V of one batch,
+    one stream), which is then not recomputed.  The result's "workspace" can be passed back."""
     import torch
     lb = _lib.lib()
     b, k, nt = dev.n_systems, dev.n_users, dev.n_antennas
@@ -47,13 +51,23 @@ def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = Fa
     # the Gram-form epilogue (contiguous VRs, K >= 96, F not stored) always needs its G0 / G0 V workspace
     gram_form = dev.host.contiguous and k >= int(os.environ.get("KZ_EPILOGUE_GRAM_KMIN", 32)) and not want_f
     need = lb.kz_epilogue_workspace_bytes(C.byref(dev.problem)) if (rates or gram_form) else 0
-    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
+    if workspace is not None and workspace.numel() >= need:
+        ws = workspace
+    else:
+        if gram_cached:
+            raise ValueError("gram_cached needs the workspace of an earlier Gram-form epilogue of this batch")
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
+    prob = dev.problem
+    if gram_cached and gram_form:
+        prob = type(dev.problem).from_buffer_copy(dev.problem)
+        prob.flags |= _lib.KZ_PROBLEM_GRAM_CACHED
     s = stream if stream is not None else torch.cuda.current_stream()
     P = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    _lib.check(lb.kz_epilogue(C.byref(dev.problem), v.data_ptr(), P(f), P(v_ref), P(beta_ref), P(snr),
+    _lib.check(lb.kz_epilogue(C.byref(prob), v.data_ptr(), P(f), P(v_ref), P(beta_ref), P(snr),
                               beta.data_ptr(), P(nm), P(r), P(sr), ws.data_ptr(), ws.numel(),
                               C.c_void_p(s.cuda_stream)))
-    return {"f": f, "beta": beta, "nmse": nm, "rates": r, "sum_rate": sr, "launches": lb.kz_last_launch_count()}
+    return {"f": f, "beta": beta, "nmse": nm, "rates": r, "sum_rate": sr, "launches": lb.kz_last_launch_count(),
+            "workspace": ws, "gram_form": gram_form}
 
 
 @dataclass(frozen=True)

@@ -690,8 +690,9 @@ __global__ void __launch_bounds__(EPG_THREADS, 1) kz_epilogue_gram_kernel(
   const TV* V = v + (size_t)b * K * K;
   const double2* Vr = v_ref ? (const double2*)v_ref + (size_t)b * K * K : nullptr;
 
-  // G0 = H^H H, both triangles (one warp per pair, lanes over the overlap)
-  {
+  // G0 = H^H H, both triangles (one warp per pair, lanes over the overlap); kept from an earlier call on the
+  // same workspace when the caller says so (KZ_PROBLEM_GRAM_CACHED)
+  if (!(P.flags & KZ_PROBLEM_GRAM_CACHED)) {
     const TH* hv = (const TH*)P.heff;
     const int npair = K * (K + 1) / 2;
     for (int e = tid >> 5; e < npair; e += nw) {

@@ -563,3 +563,24 @@ def test_bench_workload_c64_vs_c128_same_draws(scheme):
         np.testing.assert_allclose(n64[above], n128[above], rtol=1e-3)
     assert np.all(n64[~above] <= 1e-6), n64[~above].max()
     np.testing.assert_allclose(o64["sum_rate"].cpu().numpy(), o128["sum_rate"].cpu().numpy(), rtol=1e-3)
+
+
+def test_epilogue_gram_cache_is_exact():
+    """kz_epilogue with KZ_PROBLEM_GRAM_CACHED (G0 from an earlier call on the same workspace) returns bitwise
+    the same beta / NMSE / rates as recomputing G0 (the bench's five epilogues of one step share it)."""
+    import torch
+    kz = _kz()
+    ch = kz.generate(kz.CONFIGS["cfg2"], range(8))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    rz = kz.rzf_batched(dev)
+    r1 = kz.solve_batch(dev, "ahk", mode="lockstep", max_iters=20)
+    r2 = kz.solve_batch(dev, "grk", mode="lockstep", max_iters=20, rng=("philox", 3))
+    e1 = kz.epilogue(dev, r1.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
+    assert e1["gram_form"]
+    fresh = kz.epilogue(dev, r2.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
+    cached = kz.epilogue(dev, r2.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, workspace=e1["workspace"],
+                         gram_cached=True)
+    for key in ("beta", "nmse", "rates", "sum_rate"):
+        assert torch.equal(fresh[key], cached[key]), key
+    with pytest.raises(ValueError):
+        kz.epilogue(dev, r2.v, rates=True, gram_cached=True)
