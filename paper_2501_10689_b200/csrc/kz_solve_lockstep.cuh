@@ -956,6 +956,11 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
       rc = ls_dispatch<float2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);
     }
   } else {
+    rc = chunked ? 0 : rkwarp_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
+    if (rc != 0) {
+      if (rc == 1) *launches = 2;
+      return rc;
+    }
     size_t smem = ls_smem_bytes<double2>(P, &Sl, &hcap);
     if ((int)smem > maxsm) return 0;
     rc = ls_dispatch<double2>(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, s);

@@ -1,4 +1,4 @@
-// Warp-per-rhs kernel for the one-row-per-iteration schemes (urk, swor-erk) in complex64, fixed T,
+// Warp-per-rhs kernel for the one-row-per-iteration schemes (urk, swor-erk) in complex64 or complex128, fixed T,
 // contiguous VRs (solvers.py:382-389 with rk_step, solvers.py:173-188).
 //
 // An RK iteration touches one row (|Gamma_i| antennas) per rhs, so the wide kernel's CTA-wide barriers
@@ -22,8 +22,8 @@ struct Plan {
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
 
-// nw warps (rhs) per CTA, hcap packed H elements
-__host__ __device__ inline Plan plan(int K, int Nt, int nw, int hcap) {
+// nw warps (rhs) per CTA, hcap packed H elements, cs bytes per complex (8: complex64, 16: complex128)
+__host__ __device__ inline Plan plan(int K, int Nt, int nw, int hcap, int cs = 8) {
   Plan p;
   const int KW = (K + 31) / 32;
   size_t o = 0;
@@ -31,27 +31,29 @@ __host__ __device__ inline Plan plan(int K, int Nt, int nw, int hcap) {
   p.rowL = o; o = al(o + 4 * (size_t)K);
   p.hoff = o; o = al(o + 4 * (size_t)K);
   p.en = o; o = al(o + 8 * (size_t)K);
-  p.M = o; o = al(o + 8 * (size_t)nw * Nt);
-  p.Q = o; o = al(o + 8 * (size_t)nw * K);
+  p.M = o; o = al(o + (size_t)cs * nw * Nt);
+  p.Q = o; o = al(o + (size_t)cs * nw * K);
   p.pool = o; o = al(o + 4 * (size_t)nw * KW);
-  o = al(o + 8 * (size_t)hcap);  // H last
+  o = al(o + (size_t)cs * hcap);  // H last
   p.total = o;
   return p;
 }
 
 }  // namespace rkw
 
-template <int SCH>
+// T = float2 (throughput) or double2 (oracle mode: numpy's complex scalar x array products)
+template <int SCH, class T>
 __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
   using namespace rkw;
-  using T = float2;
+  using Rl = typename Cx<T>::real;
+  constexpr bool EXACT = sizeof(T) == 16;
   extern __shared__ __align__(16) unsigned char sm[];
   const int K = p.P.n_users, Nt = p.P.n_antennas;
   const int ngroups = (K + nw - 1) / nw;
   const int b = blockIdx.x / ngroups, c0g = (blockIdx.x % ngroups) * nw;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int KW = (K + 31) / 32;
-  const Plan pl = plan(K, Nt, nw, p.hcap);
+  const Plan pl = plan(K, Nt, nw, p.hcap, (int)sizeof(T));
   int* rowS = (int*)(sm + pl.rowS);
   int* rowL = (int*)(sm + pl.rowL);
   int* hoff = (int*)(sm + pl.hoff);
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
   T* Qs = (T*)(sm + pl.Q) + (size_t)w * K;
   uint32_t* pool = (uint32_t*)(sm + pl.pool) + (size_t)w * KW;
   T* Hs = (T*)(sm + pl.pool + al(4 * (size_t)nw * KW));
-  const float regf = (float)p.P.reg[b];
+  const Rl regf = (Rl)p.P.reg[b];
 
   for (int i = tid; i < K; i += nthr) {
     const size_t r = (size_t)b * K + i;
@@ -90,12 +92,19 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
     const T* heff = (const T*)p.P.heff;
     for (int i = w; i < K; i += nthr >> 5) {
       const T* src = heff + p.P.row_val_ptr[(size_t)b * K + i];
-      for (int e = lane; e < rowL[i]; e += 32) cp_async8(Hs + hoff[i] + e, src + e, true);  // no wait per row
+      for (int e = lane; e < rowL[i]; e += 32) {  // no wait per row
+        if constexpr (EXACT) {
+          const uint32_t d = (uint32_t)__cvta_generic_to_shared(Hs + hoff[i] + e);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + e) : "memory");
+        } else {
+          cp_async8(Hs + hoff[i] + e, src + e, true);
+        }
+      }
     }
     cp_async_wait_all();
   }
-  for (int n = lane; n < Nt; n += 32) Ms[n] = make_float2(0.f, 0.f);
-  for (int i = lane; i < K; i += 32) Qs[i] = make_float2(0.f, 0.f);
+  for (int n = lane; n < Nt; n += 32) Ms[n] = czero<T>();
+  for (int i = lane; i < K; i += 32) Qs[i] = czero<T>();
   for (int q = lane; q < KW; q += 32) pool[q] = 0;
   int poolcnt = 0;
   __syncthreads();
@@ -170,28 +179,32 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
       // ---- refresh of row i (solvers.py:159-170) and rk_step (solvers.py:173-188)
       const int s = rowS[i], L = rowL[i];
       const T* h = Hs + hoff[i];
-      float dx = 0.f, dy = 0.f;
+      Rl dx = 0, dy = 0;
       for (int e = lane; e < L; e += 32) {
         const T hv = h[e], mv = Ms[s + e];
-        dx = fmaf(hv.x, mv.x, dx); dx = fmaf(hv.y, mv.y, dx);
-        dy = fmaf(hv.x, mv.y, dy); dy = fmaf(-hv.y, mv.x, dy);
+        dx = fma(hv.x, mv.x, dx); dx = fma(hv.y, mv.y, dx);
+        dy = fma(hv.x, mv.y, dy); dy = fma(-hv.y, mv.x, dy);
       }
       dx = warp_sum(dx);
       dy = warp_sum(dy);
       const T q = Qs[i];
-      const float tg = i == c ? 1.f : 0.f;
-      const T r = make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
-      const float e = (float)en[i];
-      const T gm = make_float2(r.x / e, r.y / e);
+      const Rl tg = i == c ? (Rl)1 : (Rl)0;
+      const T r = Cx<T>::make((tg - dx) - q.x * regf, ((Rl)0 - dy) - q.y * regf);
+      const Rl e = (Rl)en[i];
+      const T gm = Cx<T>::make(r.x / e, r.y / e);
       for (int e2 = lane; e2 < L; e2 += 32) {
         const T hv = h[e2];
         T mv = Ms[s + e2];
-        mv.x = fmaf(gm.x, hv.x, mv.x); mv.x = fmaf(-gm.y, hv.y, mv.x);
-        mv.y = fmaf(gm.x, hv.y, mv.y); mv.y = fmaf(gm.y, hv.x, mv.y);
+        if constexpr (EXACT) {  // col[idx] += gamma * eff_rows[i] (numpy scalar x array, then add)
+          mv = cadd(mv, cmul(gm, hv));
+        } else {
+          mv.x = fmaf(gm.x, hv.x, mv.x); mv.x = fmaf(-gm.y, hv.y, mv.x);
+          mv.y = fmaf(gm.x, hv.y, mv.y); mv.y = fmaf(gm.y, hv.x, mv.y);
+        }
         Ms[s + e2] = mv;
       }
       if (lane == 0) {
-        Qs[i] = make_float2(q.x + gm.x, q.y + gm.y);
+        Qs[i] = Cx<T>::make(q.x + gm.x, q.y + gm.y);
         if (p.O.rows && it < p.O.rows_cap) p.O.rows[rid * p.O.rows_cap + it] = i;
       }
       flops += 2 * (8LL * Nt + 4);
@@ -222,15 +235,16 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
 inline int rkwarp_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
                            int32_t* tstop, int maxsm, cudaStream_t s) {
   if (scheme != KZ_URK && scheme != KZ_SWOR_ERK) return 0;
-  if (P.dtype != KZ_C64 || !(P.flags & KZ_PROBLEM_CONTIGUOUS)) return 0;
+  if (!(P.flags & KZ_PROBLEM_CONTIGUOUS)) return 0;
   static const bool off = getenv("KZ_DISABLE_RKWARP") != nullptr;  // A/B switch
   if (off) return 0;
   const int K = P.n_users, Nt = P.n_antennas;
   const int hcap = K * P.max_support;
   int nw = K < 32 ? K : 32;
   size_t smem = 0;
+  const int cs = P.dtype == KZ_C128 ? 16 : 8;
   for (; nw >= 1; nw = nw > 8 ? nw - 8 : nw - 1) {
-    smem = rkw::plan(K, Nt, nw, hcap).total;
+    smem = rkw::plan(K, Nt, nw, hcap, cs).total;
     if (smem <= (size_t)maxsm) break;
   }
   if (nw < 1) return 0;
@@ -245,7 +259,9 @@ inline int rkwarp_dispatch(const kz_problem& P, int scheme, const kz_rng& R, con
   a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
   a.tstop = tstop;
   const int groups = (K + nw - 1) / nw;
-  auto kern = scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK> : kz_rkwarp_kernel<KZ_SWOR_ERK>;
+  auto kern = P.dtype == KZ_C128
+                  ? (scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK, double2> : kz_rkwarp_kernel<KZ_SWOR_ERK, double2>)
+                  : (scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK, float2> : kz_rkwarp_kernel<KZ_SWOR_ERK, float2>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
   kern<<<P.n_systems * groups, 32 * nw, smem, s>>>(a, nw);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
