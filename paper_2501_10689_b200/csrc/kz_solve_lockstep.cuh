@@ -578,12 +578,14 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
     {
       int q = cp[w];
       const int q1 = cp[w + 1];
-      for (; q + 1 < q1; q += 2) {
-        const int i0 = cl[q], i1 = cl[q + 1];
+      for (; q + 3 < q1; q += 4) {
+        const int i0 = cl[q], i1 = cl[q + 1], i2 = cl[q + 2], i3 = cl[q + 3];
         acc_row(i0);
         acc_row(i1);
+        acc_row(i2);
+        acc_row(i3);
       }
-      if (q < q1) acc_row(cl[q]);
+      for (; q < q1; ++q) acc_row(cl[q]);
     }
     double sy = 0.0;
 #pragma unroll
