@@ -139,3 +139,23 @@ def test_solve_returns_the_reference_state(scheme):
         b, tb = kz.solve(scheme, sys_, 2, kz.StoppingRule(mode=mode, **kw), rng=np.random.default_rng(4))
         assert ta.n_iters == tb.n_iters and ta.converged == tb.converged
         same_state(b, a)
+
+
+def test_integration_md_flow():
+    """The INTEGRATION.md drop-in flow end to end (oracle channel objects stand in for kaczprec's)."""
+    kz = _kz()
+    cfg = O.ArrayConfig(256, 100e9, 16)
+    chan, reg = O.power_control(O.random_channel(cfg, 16, 5, 0.35, np.random.default_rng(0)), 0.0)
+    sys_ = kz.AugmentedSystem.from_channel(chan, reg)
+    ref = kz.rzf_precoder(chan, reg)
+    run = kz.run_precoding("vr-oahk", sys_, ref, epsilon=1e-6)
+    assert run.converged and run.nmse_trace[-1] < 1e-6
+    st, tr = kz.solve("gk", sys_, 0, kz.StoppingRule(mode="residual", epsilon=1e-8))
+    assert tr.converged
+    V = kz.solve_all("grk", sys_, kz.StoppingRule(mode="residual", epsilon=1e-8), rng=np.random.default_rng(7))
+    f = kz.assemble_vr(kz.SubarrayChannel.from_channel(chan), V).f
+    assert kz.nmse(f, ref.f) < 1e-6
+    r = kz.InstanceRun("vr-oahk", sys_, rhs=0, rng=None)
+    for _ in range(10):
+        r.step()
+    assert r.state.iters == 10
