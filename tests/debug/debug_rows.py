@@ -3,8 +3,8 @@ solve_all residual mode on one realization of a config; print the CDF margin."""
 import os
 import sys
 
-sys.path[:0] = [os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests")]
+_ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # test-side debugging aid
+sys.path[:0] = [_ROOT, os.path.join(_ROOT, "tests")]
 import numpy as np  # noqa: E402
 
 import oracle as O  # noqa: E402
