@@ -1,15 +1,21 @@
-"""Benchmark of the batched Kaczmarz precoding hot path (BASELINE.json configs[1] = cfg2).
+"""Benchmark of the batched Kaczmarz precoding hot path.
 
-One step = one full pass of the cfg2 workload over this rank's realizations:
-the direct RZF reference (K2), then for each of the five cfg2 schemes
-(urk, grk, vr-ogrk, ahk, vr-oahk) a fixed-T (T=200) lockstep solve of every
-(system, rhs) pair (K1) followed by the fused epilogue (K3: F = beta H V,
-NMSE vs RZF, Eq. (7) sum-rate).  Inputs are seeded synthetic channels of the
-cfg2 model (there is no dataset); realizations are sharded across ranks
-(weak scaling, no data-path collective; the per-system NMSE / sum-rate
-statistics are gathered at the end).
+Headline (BASELINE.json configs[1] = cfg2, the config the metric is quoted on): one step = one full pass of the
+cfg2 workload over this rank's realizations: the direct RZF reference (K2), then for each of the five cfg2
+schemes (urk, grk, vr-ogrk, ahk, vr-oahk) a fixed-T (T=200) lockstep solve of every (system, rhs) pair (K1)
+followed by the fused epilogue (K3: F = beta H V, NMSE vs RZF, Eq. (7) sum-rate).  Inputs are seeded synthetic
+channels of the cfg model (there is no dataset); realizations are sharded across ranks (weak scaling, no
+data-path collective; the per-system NMSE / sum-rate statistics are gathered at the end).
+
+Sub-records on the N=1 line (rank 0, one GPU), each with its own warm-up, device-timed steps, clocks, roofline
+and end-to-end figure:
+  complex128_oracle_mode  the same cfg2 step with the exact-arithmetic (oracle-mode) kernels
+  configs.cfg3            BASELINE configs[2]: Nt=1024, K=128, VR ~ U[128,512], VR-OAHK T=200, B=4096, c64
+  configs.cfg4            BASELINE configs[3]: Nt=4096, K=256, VR=512, GRK + VR-OAHK to residual 1e-4
+                          (solve_all semantics), B=16384 (the largest single-GPU config), c64
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py --config cfg4 --scaling strong     (torchrun: 16384 realizations split over the ranks)
 
 Prints one JSON line on rank 0.
 """
@@ -31,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Kaczmarz precoder solves/s"
 UNIT = "precoders/s"
+NOMINAL_FP32_TFLOPS = 2 * 148 * 128 * 1.965e9 / 1e12  # 148 SMs x 128 FP32 lanes x 2 flops x max SM clock
 
 
 def parse():
@@ -40,13 +47,18 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--batch", type=int, default=0, help="realizations per rank (default: the config's)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch (default: the config's B) realizations per rank; strong: the config's B "
+                         "split over the ranks")
+    ap.add_argument("--batch", type=int, default=0, help="realizations per rank (weak) or in total (strong)")
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--schemes", default="")
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 oracle-mode step")
+    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 oracle-mode record")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg3 / cfg4 records")
+    ap.add_argument("--config-steps", type=int, default=1, help="timed steps of the cfg3 / cfg4 records")
     return ap.parse_args()
 
 
@@ -146,72 +158,328 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# --------------------------------------------------------------------------- algorithmic bytes
+# --------------------------------------------------------------------------- algorithmic work
 
-def h_elems_per_launch(host, scheme, iters):
-    """H_eff elements the algorithm streams per rhs-iteration
-    (sum over R_t of |Gamma_i| plus the projected row), summed over every
-    (system, rhs) of one launch of T iterations.  Bytes = elems * sizeof(complex);
-    real flops = 8 * elems (one complex MAC per streamed element)."""
-    sup = host.support_sizes().astype(np.float64)        # (B, K)
+def elems_per_rhs_iter(sup, scheme, coupled=None):
+    """H_eff elements the algorithm streams per rhs-iteration, per system (B,): the refreshed rows R_t plus the
+    projected row; real flops = 8 x elements (one complex MAC each), bytes = c x elements.
+    sup: (B, K) support sizes; coupled: (ptr, idx) of the VR-OGRK coupled sets."""
+    sup = sup.astype(np.float64)
     b, k = sup.shape
-    tot_rows = sup.sum(axis=1)                            # sum_i |Gamma_i| per system
+    tot_rows = sup.sum(axis=1)
     mean_row = sup.mean(axis=1)
     if scheme in ("grk", "gk"):
-        per = tot_rows + mean_row
-    elif scheme in ("urk", "swor-erk"):
-        per = 2 * mean_row
-    elif scheme == "vr-ogrk":
+        return tot_rows + mean_row
+    if scheme in ("urk", "swor-erk"):
+        return 2 * mean_row
+    if scheme == "vr-ogrk":
+        ptr, idx = coupled
         xs = np.zeros(b)
         for s in range(b):
-            cp = host.coupled_ptr[s * k:(s + 1) * k + 1]
-            idx = host.coupled_idx
+            cp = ptr[s * k:(s + 1) * k + 1]
             xs[s] = np.mean([sup[s, idx[cp[i]:cp[i + 1]]].sum() for i in range(k)])
-        per = xs + mean_row
-    else:  # ahk, vr-oahk: refresh + aggregation over every row
-        per = 2 * tot_rows
-    return float(iters * k * per.sum())
+        return xs + mean_row
+    return 2 * tot_rows  # ahk, vr-oahk: refresh + aggregation over every row
 
 
-MICRO = os.path.join(ROOT, "profiles", "r01_microbench.json")
+MICRO = os.path.join(ROOT, "profiles", "r02_microbench.json")
 
 
-def measured_fp32_peak():
-    """FP32 FFMA peak (TFLOP/s) from tools/microbench.cu as committed under profiles/."""
+def _micro(probe, key):
     try:
         with open(MICRO) as fh:
             for line in fh:
                 d = json.loads(line)
-                if d.get("probe") == "FFMA":
-                    return float(d["chip_TFLOPs_fp32"]), "measured (tools/microbench.cu, profiles/r01_microbench.json)"
-    except (OSError, ValueError):
-        pass
-    return 2 * 148 * 128 * 1.965e9 / 1e12, "nominal 148 SM x 128 FFMA/clk x 1.965 GHz"
-
-
-def measured_fp32_reg3_peak():
-    """FP32 FFMA rate when every FMA reads three registers (the kernels' form), tools/fma_forms.cu."""
-    try:
-        with open(MICRO) as fh:
-            for line in fh:
-                d = json.loads(line)
-                if d.get("probe") == "FFMA reg3":
-                    return float(d["chip_TFLOPs_fp32"])
+                if d.get("probe") == probe:
+                    return d
     except (OSError, ValueError):
         pass
     return None
 
 
-def measured_smem_peak():
+def fp32_peak():
+    """Roofline denominator: the nominal FP32 FMA peak at the maximum SM clock (148 SMs x 128 lanes x 2 flops
+    x 1.965 GHz = 74.4 TFLOP/s); the measured FFMA rates (tools/microbench.cu, with their clocks) are views."""
+    return NOMINAL_FP32_TFLOPS, "nominal: 148 SM x 128 FP32 lanes x 2 flops x 1.965 GHz (max SM clock)"
+
+
+def measured_views():
+    out = {}
+    for probe in ("FFMA imm", "FFMA reg3", "LDS.128"):
+        d = _micro(probe, None)
+        if d:
+            out[probe] = {k: d[k] for k in d if k != "probe"}
+    return out or None
+
+
+def peaks_json():
     try:
-        with open(MICRO) as fh:
-            for line in fh:
-                d = json.loads(line)
-                if d.get("probe") == "LDS.128 distinct":
-                    return float(d["chip_TBps"]) * 1e3
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
     except (OSError, ValueError):
-        pass
-    return 148 * 128 * 1.965e9 / 1e9
+        return {}
+
+
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+# --------------------------------------------------------------------------- workloads
+
+class Workload:
+    """One config's step on this rank's systems: inputs resident in HBM, per step RZF + per scheme (solve +
+    epilogue), chunked over `chunk` systems (bounded per-call outputs / workspaces)."""
+
+    def __init__(self, cfg, schemes, dtype, lo, hi, dev_id, chunk=0, device_inputs=False):
+        import paper_2501_10689_b200 as kz
+        self.kz, self.cfg, self.schemes, self.dtype = kz, cfg, schemes, dtype
+        self.lo, self.hi, self.B = lo, hi, hi - lo
+        self.dev_id = dev_id
+        self.tol = cfg.extra.get("residual_tol")
+        self.iters = cfg.n_iters
+        seeds = range(lo, hi)
+        if device_inputs:  # SURVEY §8(f) f1/f2: drops -> channel entries + VR partition on the device
+            self.host = None
+            self.dev = kz.DeviceBatch.from_drops(kz.generate_drops(cfg, seeds), dtype=dtype, device=dev_id)
+        else:
+            self.host = kz.HostBatch.from_contiguous(kz.generate(cfg, seeds))
+            self.dev = self.host.to_device(dtype, device=dev_id)
+        self.chunk = chunk if 0 < chunk < self.B else self.B
+        self.sup = (self.dev.t["seg_len"].cpu().numpy().reshape(self.B, cfg.n_users))
+        self.ws = {}
+
+    def coupled(self):
+        if self.host is not None:
+            return self.host.coupled_ptr, self.host.coupled_idx
+        return self.dev.t["coupled_ptr"].cpu().numpy(), self.dev.t["coupled_idx"].cpu().numpy()
+
+    def rng(self, sc, seed):
+        return ("philox", seed) if sc in self.kz.STOCHASTIC_SCHEMES else None
+
+    def step(self, dev, seed, events=None, collect=None, out_host=None, copy_stream=None, stream=None):
+        """One step over `dev` (this workload's batch or an uploaded copy).  events[sc] gets the (start, end) of
+        the scheme's solve launches; collect[sc] the per-system (V, NMSE, sum-rate, iters) of the last chunk
+        set; out_host: pinned host buffers the results are copied into on copy_stream."""
+        import torch
+        kz = self.kz
+        launches = 0
+        k = self.cfg.n_users
+        for lo in range(0, self.B, self.chunk):
+            hi = min(self.B, lo + self.chunk)
+            sub = dev.view(lo, hi) if (lo, hi) != (0, self.B) else dev
+            rz = kz.rzf_batched(sub)
+            launches += rz["launches"]
+            ews, gram = None, False  # the epilogues of a chunk share H, so the Gram G0 is formed once
+            for sc in self.schemes:
+                e0, e1 = _events()
+                e0.record(stream)
+                if self.tol:
+                    res = kz.solve_batch(sub, sc, mode="residual", epsilon=self.tol, max_iters=10_000 * k,
+                                         rng=self.rng(sc, seed), workspace=self.ws.get(sc),
+                                         system_base=self.lo + lo)
+                else:
+                    res = kz.solve_batch(sub, sc, mode="lockstep", max_iters=self.iters, rng=self.rng(sc, seed),
+                                         workspace=self.ws.get(sc), system_base=self.lo + lo)
+                e1.record(stream)
+                self.ws[sc] = res.workspace
+                ep = kz.epilogue(sub, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, workspace=ews,
+                                 gram_cached=gram)
+                ews, gram = ep["workspace"], ep["gram_form"]
+                launches += res.launches + ep["launches"]
+                if events is not None:
+                    events.setdefault(sc, []).append((e0, e1))
+                if collect is not None:
+                    c = collect.setdefault(sc, {"nmse": [], "sum_rate": [], "iters": []})
+                    c["nmse"].append(ep["nmse"])
+                    c["sum_rate"].append(ep["sum_rate"])
+                    c["iters"].append(res.iters)
+                if out_host is not None:
+                    done_ev = torch.cuda.Event()
+                    done_ev.record(stream)
+                    copy_stream.wait_event(done_ev)
+                    with torch.cuda.stream(copy_stream):
+                        for src, dst in zip((res.v, ep["nmse"], ep["sum_rate"]), out_host[sc]):
+                            src.record_stream(copy_stream)
+                            dst[lo:hi].copy_(src, non_blocking=True)
+        return launches
+
+    def out_buffers(self):
+        import torch
+        k = self.cfg.n_users
+        cdt = torch.complex128 if self.dtype == "c128" else torch.complex64
+        return {sc: (torch.empty((self.B, k, k), dtype=cdt).pin_memory(),
+                     torch.empty(self.B, dtype=torch.float64).pin_memory(),
+                     torch.empty(self.B, dtype=torch.float64).pin_memory()) for sc in self.schemes}
+
+    def elems(self, sc, iters_tensor=None):
+        """Algorithmic H elements of one solve launch (all systems)."""
+        per = elems_per_rhs_iter(self.sup, sc, self.coupled() if sc == "vr-ogrk" else None)  # (B,)
+        if iters_tensor is None:
+            return float(per.sum() * self.cfg.n_users * self.iters)
+        it = iters_tensor.double().sum(dim=1).cpu().numpy()  # rhs-iterations per system
+        return float((per * it).sum())
+
+
+def timed_steps(wl, steps, warmup, seed0, flush, world, stream, dist):
+    """Warm-up, then `steps` device-timed steps (barrier + synchronize on both sides, L2 flushed between
+    steps outside the events).  Returns (step ms list, per-scheme events, launches, clocks)."""
+    import torch
+    for w in range(warmup):
+        wl.step(wl.dev, seed0 + w, stream=stream)
+    torch.cuda.synchronize()
+    per_scheme, launches, step_ms = {}, 0, []
+    with ClockSampler(wl.dev_id.index or 0) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for s in range(steps):
+            flush.fill_(s & 0xFF)  # L2 flush (256 MiB write), outside the timed events
+            e0, e1 = _events()
+            e0.record(stream)
+            launches += wl.step(wl.dev, seed0 + 1000 + s, events=per_scheme, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    return step_ms, per_scheme, launches, clk.summary()
+
+
+def e2e_run(wl, n_steps, seed0, stream, dev_id, warm_compute=True):
+    """End to end through the public API: pinned host inputs in, per-system V / NMSE / sum-rate out.  Every step
+    uploads its inputs (kz.DeviceBatch from pinned host tensors, on an upload stream one step ahead, as a serving
+    loop would) and reads each scheme's results back into pinned host buffers on a copy stream; the timed region
+    spans all n steps (first upload to last read-back) and is divided by n."""
+    import torch
+    kz = wl.kz
+    pinned = {name: t.cpu().pin_memory() for name, t in wl.dev.t.items() if name in kz.DeviceBatch.FIELDS
+              or name == "snr_linear"}
+    copy_stream = torch.cuda.Stream(device=dev_id)
+    up_stream = torch.cuda.Stream(device=dev_id)
+    outs = wl.out_buffers()
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    d2h = sum(sum(t.numel() * t.element_size() for t in o) for o in outs.values())
+    host = wl.dev.host
+
+    def upload():
+        with torch.cuda.stream(up_stream):
+            d = kz.DeviceBatch(host, wl.dtype, device=dev_id, pinned=pinned)
+            ev = torch.cuda.Event()
+            ev.record(up_stream)
+        for t in d.t.values():
+            t.record_stream(stream)  # consumed on the compute stream
+        return d, ev
+
+    def run_step(d, ev, s):
+        stream.wait_event(ev)
+        wl.step(d, seed0 + s, out_host=outs, copy_stream=copy_stream, stream=stream)
+
+    if warm_compute:
+        run_step(*upload(), 0)  # untimed warm-up (allocator, pinned staging, streams)
+    else:  # the kernels ran already (device-timed steps): warm only the upload allocations
+        d, _ = upload()
+        torch.cuda.synchronize()
+        del d
+    stream.wait_stream(copy_stream)
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    with ClockSampler(dev_id.index or 0) as clk:
+        e0.record(stream)
+        up_stream.wait_stream(stream)  # the first upload starts inside the timed region
+        nxt = upload()
+        for s in range(1, n_steps + 1):
+            cur = nxt
+            if s < n_steps:
+                nxt = upload()  # next step's inputs stream in while this step computes
+            run_step(cur[0], cur[1], s)
+            del cur
+        stream.wait_stream(copy_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n_steps
+    return {"ms_per_step": ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_steps,
+            "clocks": clk.summary()}
+
+
+def roofline(wl, per_scheme, iters_by_scheme=None):
+    """Dominant launch (largest mean solve time) against the FP32 FMA peak: achieved = algorithmic flops
+    (8 x H elements the algorithm streams) / mean launch time (CUDA events on the launch stream)."""
+    avg = {sc: float(np.mean([a.elapsed_time(b) for a, b in ev])) for sc, ev in per_scheme.items()}
+    dom = max(avg, key=avg.get)
+    n_launch_per_step = max(1, -(-wl.B // wl.chunk))
+    it = iters_by_scheme.get(dom) if iters_by_scheme else None
+    el = wl.elems(dom, it) / n_launch_per_step  # per launch (chunks are equal-sized but the last)
+    t = avg[dom] / 1e3
+    tflops = 8.0 * el / t / 1e12
+    peak, src = fp32_peak()
+    csize = 16 if wl.dtype == "c128" else 8
+    return dom, avg, {"kernel": f"kz_solve[{dom}]", "bound": "fp32-fma", "achieved": tflops, "peak": peak,
+                      "unit": "TFLOP/s", "frac": tflops / peak, "peak_source": src,
+                      "algorithmic_flops_per_launch": 8.0 * el, "launch_ms": avg[dom],
+                      "smem_view": {"algorithmic_GBps": csize * el / t / 1e9},
+                      "hbm_view": {"algorithmic_GBps": csize * el / t / 1e9,
+                                   "peak_GBps": float(peaks_json().get("hbm_gbs", 6550.7)),
+                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+
+
+def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2e=True, chunk=4096):
+    """A BASELINE config other than the headline at its stated size on this GPU (N=1 sub-record)."""
+    import torch
+    import paper_2501_10689_b200 as kz
+    cfg = kz.CONFIGS[name]
+    t0 = time.perf_counter()
+    wl = Workload(cfg, list(cfg.schemes), dtype, 0, cfg.n_systems, dev_id, chunk=chunk, device_inputs=True)
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t0
+    # warm-up on one chunk (kernel / allocator init), then full device-timed steps
+    warm = Workload.__new__(Workload)
+    warm.__dict__.update(wl.__dict__)
+    warm.B = min(wl.B, wl.chunk)
+    for w in range(max(1, warmup)):
+        warm.step(wl.dev.view(0, warm.B), 11 + w, stream=stream)
+    torch.cuda.synchronize()
+    per_scheme, step_ms, collect = {}, [], {}
+    with ClockSampler(dev_id.index or 0) as clk:
+        for s in range(steps):
+            flush.fill_(s & 0xFF)
+            e0, e1 = _events()
+            e0.record(stream)
+            wl.step(wl.dev, 2000 + s, events=per_scheme, collect=collect if s == steps - 1 else None, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    iters = {sc: torch.cat(c["iters"]) for sc, c in collect.items()}
+    dom, avg, roof = roofline(wl, {sc: ev for sc, ev in per_scheme.items()}, iters)
+    # per-launch mean over the chunks: report per-step totals per scheme
+    per_step_solve = {sc: float(np.sum([a.elapsed_time(b) for a, b in ev])) / steps for sc, ev in per_scheme.items()}
+    ms = float(np.mean(step_ms))
+    rec = {"workload": (f"{name}: Nt={cfg.n_antennas} K={cfg.n_users} VR={cfg.vr_len[0]}"
+                        f"{'' if cfg.vr_len[0] == cfg.vr_len[1] else '-' + str(cfg.vr_len[1])}, "
+                        f"{','.join(cfg.schemes)} x {wl.B} realizations, "
+                        + (f"residual tolerance {wl.tol} (solve_all semantics)" if wl.tol else f"T={cfg.n_iters}")
+                        + ", RZF + solve + F/NMSE/sum-rate epilogue"),
+           "value": len(cfg.schemes) * wl.B / (ms / 1e3), "unit": UNIT, "dtype": "complex64" if dtype == "c64"
+           else "complex128", "steps": steps, "warmup": f"{max(1, warmup)} step(s) on the first {warm.B} systems",
+           "ms_per_step": ms, "chunk_systems": wl.chunk, "solve_ms_per_step": per_step_solve,
+           "mean_iters_per_rhs": {sc: float(t.double().mean()) for sc, t in iters.items()},
+           "median_nmse": {sc: float(torch.cat(c["nmse"]).median()) for sc, c in collect.items()},
+           "mean_sum_rate": {sc: float(torch.cat(c["sum_rate"]).mean()) for sc, c in collect.items()},
+           "rhs_iterations_per_s": float(sum(float(t.double().sum()) for t in iters.values()) / (ms / 1e3)),
+           "roofline": roof, "clocks": clk.summary(), "inputs": "seeded drops -> kz_channel_synth / kz_partition "
+           f"on the device ({prep_s:.1f} s incl. host drop draws); L2: inputs larger than L2 (+256 MiB flush)"}
+    if do_e2e:
+        try:
+            e = e2e_run(wl, 1, 3000, stream, dev_id, warm_compute=False)
+            e["value"] = len(cfg.schemes) * wl.B / (e["ms_per_step"] / 1e3)
+            e["unit"] = UNIT
+            rec["e2e"] = e
+        except RuntimeError as exc:  # pinned host memory for the whole input set not available
+            rec["e2e"] = {"unavailable": str(exc)[:200]}
+    del wl
+    torch.cuda.empty_cache()
+    return rec
 
 
 # --------------------------------------------------------------------------- main
@@ -225,11 +493,18 @@ def main():
     cfg = CONFIGS[a.config]
     schemes = [s for s in a.schemes.split(",") if s] or list(cfg.schemes)
     iters = a.iters or cfg.n_iters
-    B = a.batch or cfg.n_systems
+    if a.iters:
+        cfg = type(cfg)(**{**cfg.__dict__, "n_iters": a.iters})
+    tol = cfg.extra.get("residual_tol")
+    if a.scaling == "strong":
+        n_total = a.batch or cfg.n_systems
+    else:
+        n_total = (a.batch or cfg.n_systems) * world
     workload = (f"{a.config}: Nt={cfg.n_antennas} K={cfg.n_users} VR={cfg.vr_len[0]}"
                 f"{'' if cfg.vr_len[0] == cfg.vr_len[1] else '-' + str(cfg.vr_len[1])}, "
-                f"{len(schemes)} schemes ({','.join(schemes)}) x {B} realizations/rank, T={iters}, "
-                "RZF + solve + F/NMSE/sum-rate epilogue")
+                f"{len(schemes)} schemes ({','.join(schemes)}) x {n_total} realizations"
+                f"{'' if a.scaling == 'strong' else f' ({n_total // world}/rank)'}, "
+                + (f"residual tolerance {tol}" if tol else f"T={iters}") + ", RZF + solve + F/NMSE/sum-rate epilogue")
 
     if a.impl == "reference":
         if rank != 0:
@@ -240,19 +515,20 @@ def main():
         val = per_step / t
         line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": a.gpus,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+                "scaling": a.scaling, "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
                 "config": {"workload": workload, "sample_per_step": f"{r} realizations x {len(schemes)} schemes",
                            "parallelism": f"process pool x{min(cores, per_step)}"},
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, per_step), "kind": "port",
                                  "sample": f"{r} realizations x {len(schemes)} schemes per step, T={iters}, "
-                                           "oracle/ numpy port of kaczprec (reference not installable on the box)"},
+                                           "oracle/ numpy port of kaczprec (the reference is pure Python and is "
+                                           "not on the GPU box; the port is pinned bitwise to it)"},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
     # CPU baseline before any CUDA initialisation (fork-safe), rank 0 at N=1 only
     cpu_baseline = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and not tol:
         cores = host_cores()
         walls, per_step, r = cpu_reference_steps(a.config, schemes, iters, 1, 0, cores)
         cpu_baseline = {"value": per_step / walls[0], "unit": UNIT, "cores": min(cores, per_step), "kind": "port",
@@ -262,246 +538,108 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2501_10689_b200 as kz
-    from paper_2501_10689_b200 import _lib
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev_id = torch.device("cuda", local)
-    lo, hi = kz.shard_range(B * world, rank, world)  # weak scaling: B realizations per rank
-    seeds = range(lo, hi)
-    ch = kz.generate(cfg, seeds)
-    host = kz.HostBatch.from_contiguous(ch)
-    dev = host.to_device(a.dtype, device=dev_id)
-    csize = 16 if a.dtype == "c128" else 8
+    lo, hi = kz.shard_range(n_total, rank, world)  # contiguous block of realizations per rank
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev_id)
-    ws = torch.empty(_lib.lib().kz_solve_workspace_bytes(
-        __import__("ctypes").byref(dev.problem), None), dtype=torch.uint8, device=dev_id)
+    big = cfg.n_antennas > 512
+    wl = Workload(cfg, schemes, a.dtype, lo, hi, dev_id, chunk=4096 if big else 0, device_inputs=big)
+    B = wl.B
 
-    def step(d, seed, per_scheme_ms=None, collect=None):
-        n_launch = 0
-        rz = kz.rzf_batched(d)
-        n_launch += rz["launches"]
-        ews, gram = None, False  # the five epilogues of a step share H, so the Gram G0 is formed once
-        for sc in schemes:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            res = kz.solve_batch(d, sc, mode="lockstep", max_iters=iters,
-                                 rng=("philox", seed * 7919 + 17) if sc in kz.STOCHASTIC_SCHEMES else None,
-                                 workspace=ws)
-            e1.record(stream)
-            ep = kz.epilogue(d, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, workspace=ews,
-                             gram_cached=gram)
-            ews, gram = ep["workspace"], ep["gram_form"]
-            n_launch += res.launches + ep["launches"]
-            if per_scheme_ms is not None:
-                per_scheme_ms.setdefault(sc, []).append((e0, e1))
-            if collect is not None:
-                collect[sc] = (res.v, ep["nmse"], ep["sum_rate"])
-        return n_launch
-
-    for w in range(a.warmup):
-        step(dev, w)
-    torch.cuda.synchronize()
-
-    per_scheme = {}
-    launches = 0
-    step_ms = []
-    with ClockSampler(local) as clk:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for s in range(a.steps):
-            flush.fill_(s & 0xFF)  # L2 flush (256 MiB write), outside the timed events
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            launches += step(dev, 1000 + s, per_scheme)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    step_ms, per_scheme, launches, clocks = timed_steps(wl, a.steps, a.warmup, 0, flush, world, stream, dist)
     t_rank = float(np.sum(step_ms)) / 1e3
     t = torch.tensor([t_rank], dtype=torch.float64, device=dev_id)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     ms_per_step = 1e3 * t_max / a.steps
-    precoders = len(schemes) * B * world * a.steps
+    precoders = len(schemes) * n_total * a.steps
     value = precoders / t_max
-    rhs_iters = len(schemes) * B * world * cfg.n_users * iters * a.steps / t_max
 
-    # dominant kernel: the scheme solve with the largest launch time
-    avg = {sc: float(np.mean([x.elapsed_time(y) for x, y in ev])) for sc, ev in per_scheme.items()}
-    dom = max(avg, key=avg.get)
-    elems_dom = h_elems_per_launch(host, dom, iters)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    fp32_peak, fp32_src = measured_fp32_peak()
-    reg3_peak = measured_fp32_reg3_peak()
-    smem_peak = measured_smem_peak()
-    smem_ncu = None  # shared-memory bytes the dominant launch moves, from ncu counters (profiles/r01_ncu_smem.json)
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_smem.json")) as fh:
-            rec = json.load(fh).get(dom)
-        if rec and a.dtype == "c64" and cfg.name == "cfg2":
-            sb = rec["shared_bytes_per_iteration"] * iters * B / rec["B"]
-            smem_ncu = {"bytes_per_launch": sb, "achieved_GBps": sb / (avg[dom] / 1e3) / 1e9, "peak_GBps": smem_peak,
-                        "frac": sb / (avg[dom] / 1e3) / 1e9 / smem_peak if smem_peak else None,
-                        "ncu_pct_of_peak_sustained": rec["pct_of_peak_sustained_elapsed"],
-                        "source": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum x 128 B of the ncu --set full capture "
-                                  f"({rec['capture']}, B={rec['B']}, T={rec['T']}), scaled to this launch's T and B"}
-    except (OSError, ValueError, KeyError):
-        pass
-    t_dom = avg[dom] / 1e3
-    tflops = 8.0 * elems_dom / t_dom / 1e12
-    bytes_dom = csize * elems_dom
+    # statistics of one more step: the final gather of per-system NMSE / sum-rate / iterations (the only
+    # cross-GPU step)
+    col = {}
+    wl.step(wl.dev, 99, collect=col, stream=stream)
+    stats, iters_dom = {}, {}
+    for sc in schemes:
+        c = {k: torch.cat(v) for k, v in col[sc].items()}
+        iters_dom[sc] = c["iters"]
+        g = kz.gather_stats({"nmse": c["nmse"], "sum_rate": c["sum_rate"],
+                             "iters": c["iters"].double().mean(dim=1)}, n_total)
+        stats[sc] = {"median_nmse": float(g["nmse"].median()), "mean_sum_rate": float(g["sum_rate"].mean()),
+                     "mean_iters_per_rhs": float(g["iters"].mean()), "systems": int(g["nmse"].numel())}
+    rhs_iters = sum(float(iters_dom[sc].double().sum()) for sc in schemes) * world * a.steps / t_max
+    dom, avg, roof = roofline(wl, per_scheme, iters_dom if tol else None)
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(dom)
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{a.config}/{dom}")
     except (OSError, ValueError):
         pass
-    # end to end through the public API: pinned host inputs in, per-system results out.
-    # Every step copies its inputs H2D (kz.DeviceBatch from pinned host tensors), runs RZF + 5 x (solve +
-    # epilogue) and reads each scheme's V, NMSE and sum-rate back into pinned host buffers.  As a serving loop
-    # would, the upload of step s+1 runs on an upload stream while step s computes, and the D2H of scheme k
-    # overlaps the solve of scheme k+1 on a copy stream; the timed region spans all n steps (first upload to
-    # last read-back) and is divided by n.
+    roof["traffic"] = traffic
+    roof["measured_views"] = measured_views()
+    roof["note"] = ("H_eff is on-chip (shared memory, or a thread-block cluster's shared memory for Nt > 512) and "
+                    "each streamed h element feeds 2 rhs in registers (8 FFMA per complex element), so the launch "
+                    "is CUDA-core FP32-FMA bound (SURVEY 8(d): report the FMA roofline); flops = 8 x the H_eff "
+                    "elements the algorithm streams per rhs-iteration")
+
     e2e = None
     if not a.no_e2e:
-        pinned = kz.pin_host(host, a.dtype)
-        copy_stream = torch.cuda.Stream(device=dev_id)
-        up_stream = torch.cuda.Stream(device=dev_id)
-        outs_h = {sc: (torch.empty((B, cfg.n_users, cfg.n_users), dtype=dev.complex_dtype).pin_memory(),
-                       torch.empty(B, dtype=torch.float64).pin_memory(),
-                       torch.empty(B, dtype=torch.float64).pin_memory()) for sc in schemes}
-        h2d = sum(t.numel() * t.element_size() for t in pinned.values())
-        d2h = sum(sum(t.numel() * t.element_size() for t in o) for o in outs_h.values())
-
-        def upload():
-            with torch.cuda.stream(up_stream):
-                d = kz.DeviceBatch(host, a.dtype, device=dev_id, pinned=pinned)
-                ev = torch.cuda.Event()
-                ev.record(up_stream)
-            for t in d.t.values():
-                t.record_stream(stream)  # consumed on the compute stream
-            return d, ev
-
-        def e2e_step(d, ev, s):
-            stream.wait_event(ev)
-            rz = kz.rzf_batched(d)
-            ews, gram = None, False
-            for sc in schemes:
-                res = kz.solve_batch(d, sc, mode="lockstep", max_iters=iters,
-                                     rng=("philox", s * 104729 + 5) if sc in kz.STOCHASTIC_SCHEMES else None,
-                                     workspace=ws)
-                ep = kz.epilogue(d, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, workspace=ews,
-                                 gram_cached=gram)
-                ews, gram = ep["workspace"], ep["gram_form"]
-                done_ev = torch.cuda.Event()
-                done_ev.record(stream)
-                copy_stream.wait_event(done_ev)
-                with torch.cuda.stream(copy_stream):
-                    for src, dst in zip((res.v, ep["nmse"], ep["sum_rate"]), outs_h[sc]):
-                        src.record_stream(copy_stream)
-                        dst.copy_(src, non_blocking=True)
-
-        e2e_step(*upload(), 0)  # untimed warm-up (allocator, pinned staging, streams)
-        stream.wait_stream(copy_stream)
-        torch.cuda.synchronize()
-        n_e2e = max(1, min(a.steps, 5))
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk_e2e:
-            e0.record(stream)
-            up_stream.wait_stream(stream)  # the first upload starts inside the timed region
-            nxt = upload()
-            for s in range(1, n_e2e + 1):
-                cur = nxt
-                if s < n_e2e:
-                    nxt = upload()  # next step's inputs stream in while this step computes
-                e2e_step(cur[0], cur[1], s)
-                del cur
-            stream.wait_stream(copy_stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64, device=dev_id)
+        e = e2e_run(wl, max(1, min(a.steps, 5)), 5000, stream, dev_id)
+        te = torch.tensor([e["ms_per_step"]], dtype=torch.float64, device=dev_id)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": len(schemes) * B * world / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": float(te.item()),
-               "steps": n_e2e, "clocks": clk_e2e.summary(),
+        e["ms_per_step"] = float(te.item())
+        e2e = {"value": len(schemes) * n_total / (e["ms_per_step"] / 1e3), "unit": UNIT, **e,
                "path": "kz.DeviceBatch(pinned, upload stream, one step ahead) -> rzf_batched -> solve_batch + "
                        "epilogue per scheme -> V/NMSE/sum-rate to pinned host (copy stream)"}
 
-    # final gather of per-system statistics (the only cross-GPU step)
-    col = {}
-    step(dev, 99, collect=col)
-    stats = {}
-    for sc in schemes:
-        g = kz.gather_stats({"nmse": col[sc][1], "sum_rate": col[sc][2]}, B * world)
-        stats[sc] = {"median_nmse": float(g["nmse"].median()), "mean_sum_rate": float(g["sum_rate"].mean()),
-                     "systems": int(g["nmse"].numel())}
-
-    # the same step in complex128 oracle mode (BASELINE cfg2 quotes both modes): one warm + one timed step
-    c128 = None
-    if not a.no_c128 and a.dtype == "c64":
-        dev128 = host.to_device("c128", device=dev_id)
-        step(dev128, 7)
-        torch.cuda.synchronize()
-        ev128 = {}
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step(dev128, 8, ev128)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t128 = e0.elapsed_time(e1)
-        c128 = {"value": len(schemes) * B * world / (t128 / 1e3), "unit": UNIT, "ms_per_step": t128,
-                "dtype": "complex128",
-                "per_scheme_launch_ms": {sc: ev[0][0].elapsed_time(ev[0][1]) for sc, ev in ev128.items()},
-                "note": "one timed step, same workload; the exact-arithmetic kernels of the oracle-mode parity tests"}
-        del dev128
+    # N=1 sub-records (rank 0, one GPU): the complex128 oracle mode of the same step, and cfg3 / cfg4
+    c128 = configs = None
+    if world == 1 and a.config == "cfg2" and a.dtype == "c64":
+        if not a.no_c128:
+            wl128 = Workload(cfg, schemes, "c128", lo, hi, dev_id)
+            ms128, ev128, _, clk128 = timed_steps(wl128, a.steps, a.warmup, 7, flush, 1, stream, dist)
+            e = None
+            if not a.no_e2e:
+                e = e2e_run(wl128, max(1, min(a.steps, 3)), 6000, stream, dev_id)
+                e["value"] = len(schemes) * B / (e["ms_per_step"] / 1e3)
+                e["unit"] = UNIT
+            c128 = {"value": len(schemes) * B / (float(np.mean(ms128)) / 1e3), "unit": UNIT,
+                    "ms_per_step": float(np.mean(ms128)), "steps": a.steps, "warmup": a.warmup,
+                    "dtype": "complex128",
+                    "per_scheme_launch_ms": {sc: float(np.mean([x.elapsed_time(y) for x, y in ev]))
+                                             for sc, ev in ev128.items()},
+                    "clocks": clk128, "e2e": e,
+                    "note": "the same cfg2 step with the exact-arithmetic kernels of the oracle-mode parity tests "
+                            "(complex128, numpy-faithful selection; like-for-like with the complex128 CPU arm)"}
+            del wl128
+            torch.cuda.empty_cache()
+        if not a.no_configs:
+            configs = {}
+            for name in ("cfg3", "cfg4"):
+                configs[name] = config_record(name, dev_id, stream, flush, a.config_steps, 1,
+                                              do_e2e=not a.no_e2e)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "complex64" if a.dtype == "c64" else "complex128",
             "data": "synthetic (seeded cfg model: LoS spherical wavefront, contiguous VR, unit-norm columns)",
-            "config": {"workload": workload, "global_batch": B * world, "realizations_per_rank": B,
+            "config": {"workload": workload, "global_batch": n_total, "realizations_per_rank": B,
                        "l2": "flushed between timed steps (256 MiB write outside the events)",
-                       "rng": "on-device Philox4x32-10 row draws", "parallelism": f"realizations sharded x{world}"},
+                       "rng": "on-device Philox4x32-10 row draws keyed by (seed, global system, rhs, draw)",
+                       "parallelism": f"realizations sharded x{world} ({a.scaling} scaling)"},
             "rhs_iterations_per_s": rhs_iters,
             "per_scheme_launch_ms": avg,
-            "roofline": {"kernel": f"kz_solve[{dom}]", "bound": "fp32-fma", "achieved": tflops,
-                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": tflops / fp32_peak, "traffic": traffic,
-                         "algorithmic_flops_per_launch": 8.0 * elems_dom, "peak_source": fp32_src,
-                         "note": "H_eff is shared-memory resident and each streamed h element is reused by "
-                                 "2 rhs in registers (8 FFMA per complex element), so the launch is CUDA-core "
-                                 "FMA bound (SURVEY 8(d): report the FMA roofline); flops = 8 x streamed H_eff "
-                                 "elements per rhs-iteration",
-                         "ffma_3reg_view": ({"peak_TFLOPs": reg3_peak, "frac": tflops / reg3_peak,
-                                             "peak_source": "tools/fma_forms.cu (profiles/r01_microbench.json): "
-                                                            "FFMA with three register operands issues at 0.81/clk "
-                                                            "per SMSP vs 0.97 for the immediate form"}
-                                            if reg3_peak else None),
-                         "smem_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": smem_peak},
-                         "smem_ncu": smem_ncu,
-                         "hbm_view": {"algorithmic_GBps": bytes_dom / t_dom / 1e9, "peak_GBps": hbm_peak,
-                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
+            "roofline": roof,
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "stats": stats, "complex128_oracle_mode": c128,
+            "clocks": clocks, "stats": stats, "complex128_oracle_mode": c128, "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 5
+#define KZ_ABI_VERSION 6
 
 /* status codes */
 #define KZ_OK 0
@@ -63,7 +63,7 @@ enum kz_rng_kind {
   KZ_RNG_NONE = 0,           /* deterministic schemes (gk, ahk, vr-oahk) */
   KZ_RNG_HOST_UNIFORM = 1,   /* u[b][rhs][s] fp64: one Generator.random() per greedy-weighted pick */
   KZ_RNG_HOST_INDEX = 2,     /* idx[b][rhs][s] int32: host-evaluated uniform / energy-swor picks */
-  KZ_RNG_PHILOX = 3          /* on-device Philox4x32-10 keyed by (seed, b, rhs, draw) */
+  KZ_RNG_PHILOX = 3          /* on-device Philox4x32-10 keyed by (seed, system_base + b, rhs, draw) */
 };
 
 /*
@@ -131,6 +131,10 @@ typedef struct kz_rng {
   const double* uniforms;/* HOST_UNIFORM: [B][K][stream_len] */
   const int32_t* indices;/* HOST_INDEX:   [B][K][stream_len] */
   uint64_t seed;         /* PHILOX key */
+  int64_t system_base;   /* PHILOX: global index of system 0 of this batch.  The draws of a system are keyed by
+                            its global index, so a realization's row stream does not depend on how the
+                            realizations are chunked or sharded across ranks (the reference's worker-count
+                            invariance, pkg/README.md:68-70, tests/test_experiments.py:139-146) */
 } kz_rng;
 
 typedef struct kz_out {
@@ -157,9 +161,17 @@ typedef struct kz_out {
   void* iterates;           /* optional [B][K rhs][Nt] complex (dtype): final iterate m (SolverState.col) */
 } kz_out;
 
-/* Bytes of device workspace kz_solve needs for this problem (iterates M, residuals,
-   per-rhs scratch).  The workspace doubles as the resumable solver state. */
+/* Bytes of device workspace that is enough for any kz_solve call on this problem (the global-memory kernel's
+   iterates M, residuals and per-rhs scratch; the workspace doubles as its resumable solver state). */
 size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop);
+
+/* Bytes the kz_solve(prob, scheme, stop, rng, out, resume = 0) call would need for the kernel it dispatches to:
+   the on-chip kernels (contiguous supports, fixed T or per-rhs residual tolerance) keep every iterate in
+   registers / shared memory / TMEM and need only B*K int32 of stop bookkeeping, so a batch as large as
+   BASELINE cfg4 (B = 16384, K = 256, Nt = 4096) runs in one call; the global-memory kernel needs
+   kz_solve_workspace_bytes.  Decides without launching (device attributes of the current device). */
+size_t kz_solve_workspace_bytes_for(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng,
+                                    const kz_out* out);
 
 /* Byte offset in that workspace of the stored row residuals (SolverState.resid, solvers.py:112-136) after a
    complex128 KZ_STOP_RESIDUAL / KZ_STOP_ORACLE solve: [B*K rhs][K] complex of prob->dtype, rhs-major. */
@@ -192,6 +204,9 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
    (NULL = no rates); beta_out [B], nmse_out [B], rates_out [B][K], sum_rate_out [B]
    each may be NULL. */
 size_t kz_epilogue_workspace_bytes(const kz_problem* prob);
+/* 1 if kz_epilogue on this problem takes the Gram form (contiguous VRs, K >= 32, F not stored: every output is a
+   quadratic form in G0 = H^H H, which the workspace then holds and KZ_PROBLEM_GRAM_CACHED may reuse), else 0 */
+int32_t kz_epilogue_uses_gram(const kz_problem* prob, int32_t want_f);
 int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double* v_ref, const double* beta_ref,
                 const double* snr_linear, double* beta_out, double* nmse_out, double* rates_out,
                 double* sum_rate_out, void* workspace, size_t workspace_bytes, void* stream);

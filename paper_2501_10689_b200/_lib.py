@@ -11,6 +11,8 @@ import os
 
 from .build import lib_path
 
+ABI_VERSION = 6  # include/kaczmarz_b200.h KZ_ABI_VERSION: the struct layouts below follow it
+
 KZ_OK = 0
 KZ_ERR_INVALID = -1
 KZ_ERR_CUDA = -2
@@ -49,7 +51,7 @@ class KzStop(C.Structure):
 class KzRng(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("stream_len", C.c_int32), ("stream_base", C.c_int64),
-        ("uniforms", P), ("indices", P), ("seed", C.c_uint64),
+        ("uniforms", P), ("indices", P), ("seed", C.c_uint64), ("system_base", C.c_int64),
     ]
 
 
@@ -98,14 +100,17 @@ def lib():
     except OSError as exc:
         raise ExtensionMissingError(f"cannot load {LIB_PATH}: {exc}") from exc
     _declare(lb)
+    if lb.kz_abi_version() != ABI_VERSION:
+        raise ExtensionMissingError(f"{LIB_PATH} has ABI {lb.kz_abi_version()}, this binding expects {ABI_VERSION}; "
+                                    "rebuild it with `python -m paper_2501_10689_b200.build`")
     _LIB = lb
     return lb
 
 
 EXPORTS = (
     "kz_abi_version", "kz_last_error", "kz_last_launch_count",
-    "kz_solve_workspace_bytes", "kz_solve_resid_offset", "kz_solve",
-    "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue",
+    "kz_solve_workspace_bytes", "kz_solve_workspace_bytes_for", "kz_solve_resid_offset", "kz_solve",
+    "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue_uses_gram", "kz_epilogue",
     "kz_channel_synth", "kz_partition_counts", "kz_partition_fill",
     "kz_residual_refresh", "kz_project_rows", "kz_ahk_step",
 )
@@ -117,6 +122,9 @@ def _declare(lb):
     lb.kz_last_launch_count.restype = C.c_int32
     lb.kz_solve_workspace_bytes.restype = C.c_size_t
     lb.kz_solve_workspace_bytes.argtypes = [C.POINTER(KzProblem), C.POINTER(KzStop)]
+    lb.kz_solve_workspace_bytes_for.restype = C.c_size_t
+    lb.kz_solve_workspace_bytes_for.argtypes = [C.POINTER(KzProblem), C.c_int32, C.POINTER(KzStop),
+                                                C.POINTER(KzRng), C.POINTER(KzOut)]
     lb.kz_solve_resid_offset.restype = C.c_size_t
     lb.kz_solve_resid_offset.argtypes = [C.POINTER(KzProblem)]
     lb.kz_solve.restype = C.c_int
@@ -128,6 +136,8 @@ def _declare(lb):
     lb.kz_rzf.argtypes = [C.POINTER(KzProblem), P, P, P, P, P, C.c_size_t, P]
     lb.kz_epilogue_workspace_bytes.restype = C.c_size_t
     lb.kz_epilogue_workspace_bytes.argtypes = [C.POINTER(KzProblem)]
+    lb.kz_epilogue_uses_gram.restype = C.c_int32
+    lb.kz_epilogue_uses_gram.argtypes = [C.POINTER(KzProblem), C.c_int32]
     lb.kz_epilogue.restype = C.c_int
     lb.kz_epilogue.argtypes = [C.POINTER(KzProblem), P, P, P, P, P, P, P, P, P, P, C.c_size_t, P]
     lb.kz_channel_synth.restype = C.c_int

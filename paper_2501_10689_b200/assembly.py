@@ -12,8 +12,6 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
-import os
-
 import numpy as np
 
 from . import _lib
@@ -48,14 +46,16 @@ def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = Fa
         keep.append(snr)
     r = torch.zeros((b, k), dtype=torch.float64, device=d) if rates else None
     sr = torch.zeros(b, dtype=torch.float64, device=d) if rates else None
-    # the Gram-form epilogue (contiguous VRs, K >= 96, F not stored) always needs its G0 / G0 V workspace
-    gram_form = dev.host.contiguous and k >= int(os.environ.get("KZ_EPILOGUE_GRAM_KMIN", 32)) and not want_f
+    # the library decides the form (kz_epilogue_uses_gram); the Gram form always needs its G0 / G0 V workspace
+    gram_form = bool(lb.kz_epilogue_uses_gram(C.byref(dev.problem), 1 if want_f else 0))
     need = lb.kz_epilogue_workspace_bytes(C.byref(dev.problem)) if (rates or gram_form) else 0
+    # a workspace holding G0 is stamped with the batch it was formed for; gram_cached accepts only that batch
+    stamp = (dev.problem.heff, dev.problem.row_val_ptr, b, k, nt, id(dev))
+    if gram_cached and (workspace is None or getattr(workspace, "_kz_gram_of", None) != stamp):
+        raise ValueError("gram_cached needs the workspace of an earlier Gram-form epilogue of this batch")
     if workspace is not None and workspace.numel() >= need:
         ws = workspace
     else:
-        if gram_cached:
-            raise ValueError("gram_cached needs the workspace of an earlier Gram-form epilogue of this batch")
         ws = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
     prob = dev.problem
     if gram_cached and gram_form:
@@ -66,6 +66,7 @@ def epilogue(dev: DeviceBatch, v, *, v_ref=None, beta_ref=None, rates: bool = Fa
     _lib.check(lb.kz_epilogue(C.byref(prob), v.data_ptr(), P(f), P(v_ref), P(beta_ref), P(snr),
                               beta.data_ptr(), P(nm), P(r), P(sr), ws.data_ptr(), ws.numel(),
                               C.c_void_p(s.cuda_stream)))
+    ws._kz_gram_of = stamp if gram_form else None
     return {"f": f, "beta": beta, "nmse": nm, "rates": r, "sum_rate": sr, "launches": lb.kz_last_launch_count(),
             "workspace": ws, "gram_form": gram_form}
 

@@ -243,6 +243,18 @@ class HostBatch:
             "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size"))
 
 
+class _HostView:
+    """Shape / hint stand-in for the HostBatch of a DeviceBatch.view (the packed host arrays stay the parent's)."""
+
+    def __init__(self, parent, n_systems: int):
+        self.parent = parent
+        self.n_systems = n_systems
+        self.n_users, self.n_antennas, self.contiguous = parent.n_users, parent.n_antennas, parent.contiguous
+
+    def layout_hints(self) -> dict:
+        return self.parent.layout_hints()
+
+
 def pin_host(host: HostBatch, dtype: str = "c128", pin: bool = True) -> dict:
     """Host tensors of a batch (page-locked when `pin`), heff already in the compute dtype."""
     import torch
@@ -359,6 +371,30 @@ class DeviceBatch:
         obj = cls.__new__(cls)
         obj.host, obj.dtype, obj.device, obj.t = host, dtype, dev, t
         obj._drop_keep = (wl, r0, th, ccnt, ocnt, inset)
+        obj.problem = obj._make_problem(t)
+        return obj
+
+    # CSR pointer fields indexed by row (b*K + i) / by system; their VALUES are absolute offsets into the value
+    # arrays, so a contiguous range of systems is the same value arrays behind offset pointer arrays
+    _PER_ROW = ("row_seg_ptr", "row_val_ptr", "row_energy", "coupled_ptr")
+    _PER_SYSTEM = ("reg", "orth_ptr", "non_ptr", "non_union_size", "snr_linear")
+
+    def view(self, lo: int, hi: int) -> "DeviceBatch":
+        """Systems [lo, hi) of this batch without copying: the kz_problem's per-row / per-system arrays start at
+        row lo*K / system lo, the packed values are shared (layout hints are the whole batch's upper bounds)."""
+        if not 0 <= lo <= hi <= self.n_systems:
+            raise ValueError(f"system range [{lo}, {hi}) outside [0, {self.n_systems})")
+        k = self.n_users
+        t = dict(self.t)
+        for name in self._PER_ROW:
+            t[name] = self.t[name][lo * k:]
+        for name in self._PER_SYSTEM:
+            if name in self.t:
+                t[name] = self.t[name][lo:hi] if name == "snr_linear" else self.t[name][lo:]
+        obj = DeviceBatch.__new__(DeviceBatch)
+        obj.host = _HostView(self.host, hi - lo)
+        obj.dtype, obj.device, obj.t = self.dtype, self.device, t
+        obj.parent = self
         obj.problem = obj._make_problem(t)
         return obj
 

@@ -65,7 +65,23 @@ size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop) {
   (void)stop;
   if (!prob) return 0;
   size_t gen = gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).total;
-  return gen + ls_extra_ws(*prob);
+  return gen > ls_extra_ws(*prob) ? gen : ls_extra_ws(*prob);
+}
+
+size_t kz_solve_workspace_bytes_for(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng,
+                                    const kz_out* out) {
+  if (!prob || !stop || !rng || !out) return 0;
+  if (prob->n_systems == 0) return 0;
+  // ask the fast-path dispatchers which kernel kz_solve(resume = 0) would take, without launching anything
+  int32_t dummy = 0;
+  g_dry_launch = true;
+  int fast = lockstep_try_launch(*prob, scheme, *stop, *rng, *out, 0, nullptr, ~size_t(0), nullptr, &dummy);
+  if (fast != 1)
+    fast = cluster_try_launch(*prob, scheme, *stop, *rng, *out, 0, nullptr, ~size_t(0), nullptr, &dummy);
+  g_dry_launch = false;
+  cudaGetLastError();  // eligibility probes (attributes, occupancy) leave no sticky error behind
+  if (fast == 1) return ls_extra_ws(*prob);  // the on-chip kernels keep only the stop iterations in HBM
+  return gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).total;
 }
 
 size_t kz_solve_resid_offset(const kz_problem* prob) {
@@ -110,9 +126,7 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
     return fail(KZ_ERR_INVALID, "vr-oahk needs the orthogonal / non-orthogonal partition");
   if (!out->v) return fail(KZ_ERR_INVALID, "out->v must be non-null");
   if (prob->n_systems == 0) return KZ_OK;
-  size_t need = kz_solve_workspace_bytes(prob, stop);
-  if (!workspace || workspace_bytes < need)
-    return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+  if (!workspace) workspace_bytes = 0;
 
   cudaStream_t s = (cudaStream_t)stream;
   const int K = prob->n_users;
@@ -127,6 +141,10 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
   if (fast == 1) return cuda_check("kz_solve(cluster)");
   if (fast < 0) return fail(KZ_ERR_CUDA, "cluster launch failed");
 
+  // generic kernel: the per-rhs state (iterates, residuals, counters) lives in the workspace
+  const size_t need = gen_layout(prob->n_systems, K, prob->n_antennas, prob->dtype).total;
+  if (!workspace || workspace_bytes < need)
+    return fail(KZ_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
   const int nw = GEN_WARPS;
   size_t cs = prob->dtype == KZ_C128 ? 16 : 8;
   size_t smem = (size_t)nw * 2 * K * sizeof(double) + (size_t)nw * K * cs;
@@ -193,6 +211,10 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
 static bool epilogue_gram_path(const kz_problem* prob) {
   static const int kmin = getenv("KZ_EPILOGUE_GRAM_KMIN") ? atoi(getenv("KZ_EPILOGUE_GRAM_KMIN")) : 32;
   return (prob->flags & KZ_PROBLEM_CONTIGUOUS) && prob->n_users >= kmin && getenv("KZ_EPILOGUE_ANTENNA") == nullptr;
+}
+
+int32_t kz_epilogue_uses_gram(const kz_problem* prob, int32_t want_f) {
+  return prob && epilogue_gram_path(prob) && !want_f ? 1 : 0;
 }
 
 size_t kz_epilogue_workspace_bytes(const kz_problem* prob) {

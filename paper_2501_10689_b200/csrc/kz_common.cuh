@@ -49,6 +49,10 @@ namespace kz {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// host side: set by kz_solve_workspace_bytes_for while it asks the dispatchers which kernel a call would take;
+// every launch function returns 1 ("would launch") right before its kernel launch when it is set
+inline thread_local bool g_dry_launch = false;
+
 template <class T> struct Cx;
 template <> struct Cx<float2> {
   using real = float;

@@ -584,7 +584,9 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_contig_kernel(
   const double beta = 1.0 / sqrt(s1);
   if (beta_out && threadIdx.x == 0) beta_out[b] = beta;
   // pass 2: F = beta H V (stored), NMSE against beta_ref H V_ref
-  T* F = f_out ? f_out + (size_t)b * Nt * K : fws + (size_t)b * Nt * K;
+  // F is stored only where it is read: the caller's f_out, else the workspace when pass 3 needs it (the ABI
+  // asks for no workspace when neither F nor rates are requested)
+  T* F = f_out ? f_out + (size_t)b * Nt * K : (snr_linear ? fws + (size_t)b * Nt * K : nullptr);
   const double br = Vr ? beta_ref[b] : 0.0;
   double e2 = 0.0, r2 = 0.0;
   for (int n = warp; n < Nt; n += nw) {
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_epilogue_contig_kernel(
       }
       if (c < K) {
         const double ox = beta * fr, oy = beta * fi;
-        F[(size_t)n * K + c] = from_d2<T>(make_double2(ox, oy));
+        if (F) F[(size_t)n * K + c] = from_d2<T>(make_double2(ox, oy));
         if (Vr) {
           const double dx = br * gr - ox, dy = br * gi - oy;
           e2 += dx * dx + dy * dy;

@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   };
   auto draw_u = [&](int gg) -> double {
     const int cc = g0 + gg, d = itv[gg];
-    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)cc, (uint64_t)d);
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)cc, (uint64_t)d);
     return p.R.uniforms[((size_t)b * K + cc) * p.R.stream_len + d];
   };
   // residual-mode stopping test of the state after step itv (solvers.py:480-503); returns true if the rhs stops
@@ -1223,6 +1223,7 @@ inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStre
     cudaGetLastError();
     return 0;
   }
+  if (g_dry_launch) return 1;
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   if (a.mode == KZ_STOP_LOCKSTEP)
     kz_lockstep_finalize<<<(a.P.n_systems + 127) / 128, 128, 0, s>>>(a.tstop, groups, a.P.n_systems, a.O.n_outer,
@@ -1246,8 +1247,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   if (stochastic && R.kind != KZ_RNG_PHILOX &&
       !(lockstep && R.kind == KZ_RNG_HOST_UNIFORM && R.stream_base == 0 && R.stream_len >= S.max_iters))
     return 0;
-  GenLayout L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
-  if (ws_bytes < L.total + ls_extra_ws(P)) return 0;
+  if (ws_bytes < ls_extra_ws(P)) return 0;  // tstop only: the per-rhs state lives on chip
   int dev = 0, maxsm = 0, smsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1296,7 +1296,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.nblk = CL > 1 ? nb : 1;  // must match the layout hint (HostBatch.slice_pairs / batch.cluster_blocks)
   a.pcap = cands[pick].pcap;
   a.rcap = cands[pick].rcap;
-  a.tstop = (int32_t*)(ws + L.total);
+  a.tstop = (int32_t*)ws;
   int rc = 0;
   if (GG == 32) {
     switch (scheme) {

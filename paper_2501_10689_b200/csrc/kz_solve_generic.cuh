@@ -101,7 +101,7 @@ template <class T> struct Gen {
   }
   __device__ __forceinline__ double uniform(int b, int c) const {
     int64_t d = draws(b, c);
-    if (G.kind == KZ_RNG_PHILOX) return philox_uniform(G.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+    if (G.kind == KZ_RNG_PHILOX) return philox_uniform(G.seed, (uint32_t)(b + G.system_base), (uint32_t)c, (uint64_t)d);
     return G.uniforms[rid(b, c) * G.stream_len + (d - G.stream_base)];
   }
   __device__ __forceinline__ int index_draw(int b, int c) const {

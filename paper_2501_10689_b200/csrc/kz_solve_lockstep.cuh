@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   auto draw_u = [&](int gg) -> double {
     int c = g0 + gg;
     int d = itv[gg];
-    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)c, (uint64_t)d);
     return p.R.uniforms[((size_t)b * K + c) * p.R.stream_len + d];
   };
   auto log_row = [&](int gg, int it, int i) {
@@ -890,6 +890,7 @@ inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int 
   if (cudaFuncSetAttribute(kz_lockstep_kernel<T, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
+  if (g_dry_launch) return 1;
   kz_lockstep_kernel<T, SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);
@@ -940,9 +941,8 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
       (R.stream_base != 0 || R.stream_len < S.max_iters))
     return 0;
   if (scheme == KZ_SWOR_ERK && R.kind == KZ_RNG_PHILOX && P.n_users > 1024) return 0;
-  GenLayout L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
-  if (ws_bytes < L.total + ls_extra_ws(P)) return 0;
-  int32_t* tstop = (int32_t*)(ws + L.total);
+  if (ws_bytes < ls_extra_ws(P)) return 0;  // tstop only: the per-rhs state lives on chip
+  int32_t* tstop = (int32_t*)ws;
   int Sl, hcap;
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);

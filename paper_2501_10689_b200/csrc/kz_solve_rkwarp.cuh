@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(1024, 1) kz_rkwarp_kernel(LsArgs p, int nw) {
       if (p.R.kind == KZ_RNG_HOST_INDEX) {
         if (d < p.T) ibuf = p.R.indices[rid * p.R.stream_len + d];
       } else if (p.R.kind == KZ_RNG_PHILOX) {
-        ubuf = philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+        ubuf = philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)c, (uint64_t)d);
       } else if (d < p.T) {
         ubuf = p.R.uniforms[rid * p.R.stream_len + d];
       }
@@ -263,6 +263,7 @@ inline int rkwarp_dispatch(const kz_problem& P, int scheme, const kz_rng& R, con
                   ? (scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK, double2> : kz_rkwarp_kernel<KZ_SWOR_ERK, double2>)
                   : (scheme == KZ_URK ? kz_rkwarp_kernel<KZ_URK, float2> : kz_rkwarp_kernel<KZ_SWOR_ERK, float2>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  if (g_dry_launch) return 1;
   kern<<<P.n_systems * groups, 32 * nw, smem, s>>>(a, nw);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(LsArgs p) {
   };
   auto draw_u = [&](int gg) -> double {
     int c = g0 + gg, d = itv[gg];
-    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)b, (uint32_t)c, (uint64_t)d);
+    if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)c, (uint64_t)d);
     return p.R.uniforms[((size_t)b * K + c) * p.R.stream_len + d];
   };
   auto take_step = [&](int gg, int i, T r, long long f) {
@@ -943,6 +943,7 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
   if (cudaFuncSetAttribute(kz_wide_kernel<SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
+  if (g_dry_launch) return 1;
   kz_wide_kernel<SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);

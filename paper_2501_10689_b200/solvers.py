@@ -277,11 +277,13 @@ def _stream_ptr(stream):
 def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_iters: int, epsilon: float = 0.0,
                 check_every: int = 1, f_ref=None, v_ref=None, rng=None, rows_cap: int = 0, trace_cap: int = 0,
                 rhs_mask=None, chunk: int | None = None, stream=None, workspace=None,
-                want_iterates: bool = False) -> BatchResult:
+                want_iterates: bool = False, system_base: int = 0) -> BatchResult:
     """Run `scheme` on every (system, rhs) of `dev` with one kz_solve launch.
 
     mode: "lockstep" (run_precoding), "residual" / "oracle" (solve / solve_all).
     rng : None, ("philox", seed), or a HostStreams.
+    system_base: global index of system 0 of `dev` (Philox draws are keyed by the global system index, so a
+    realization's rows do not depend on how the batch is chunked or sharded).
     """
     import torch
     scheme = canonical_scheme(scheme)
@@ -351,11 +353,6 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
         out.flops_trace = res.flops_trace.data_ptr()
         out.n_checks = res.n_checks.data_ptr()
 
-    need = lb.kz_solve_workspace_bytes(C.byref(dev.problem), C.byref(stop))
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
-    res.workspace = workspace
-
     rg = _lib.KzRng()
     host = isinstance(rng, HostStreams)
     if rng is None:
@@ -368,6 +365,7 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
             raise ValueError(f"unknown rng spec {rng!r}")
         rg.kind = _lib.RNG_PHILOX
         rg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        rg.system_base = int(system_base)
     if host and scheme not in STOCHASTIC_SCHEMES:
         host = False
         rg.kind = _lib.RNG_NONE
@@ -388,6 +386,14 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
                 rg.uniforms = arr.data_ptr()
             else:
                 rg.indices = arr.data_ptr()
+        if not resume:
+            # size the workspace for the kernel this call dispatches to (the on-chip kernels need only the stop
+            # bookkeeping; the global-memory kernel holds every iterate)
+            need = lb.kz_solve_workspace_bytes_for(C.byref(dev.problem), _lib.SCHEME_IDS[scheme], C.byref(stop),
+                                                   C.byref(rg), C.byref(out))
+            if workspace is None or workspace.numel() < need:
+                workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=d)
+            res.workspace = workspace
         _lib.check(lb.kz_solve(C.byref(dev.problem), _lib.SCHEME_IDS[scheme], C.byref(stop), C.byref(rg),
                                C.byref(out), workspace.data_ptr(), workspace.numel(), resume, sp))
         launches += lb.kz_last_launch_count()
@@ -563,15 +569,47 @@ def solve_all(scheme: str, sys, stop: StoppingRule, rng: np.random.Generator | N
 
 def run_precoding_batched(scheme: str, dev: DeviceBatch, *, max_iters: int, rng=None, epsilon: float = 0.0,
                           f_ref=None, v_ref=None, beta_ref=None, rates: bool = True, want_f: bool = False,
-                          rows_cap: int = 0, stream=None, workspace=None) -> dict:
+                          rows_cap: int = 0, stream=None, workspace=None, chunk_systems: int = 0,
+                          system_base: int = 0) -> dict:
     """Fixed-T (epsilon = 0) or NMSE-stopped lockstep precoding of every system in `dev`,
-    followed by the fused epilogue (F = beta H V, NMSE vs beta_ref H V_ref, Eq. (7) rates)."""
+    followed by the fused epilogue (F = beta H V, NMSE vs beta_ref H V_ref, Eq. (7) rates).
+
+    chunk_systems > 0 runs the batch as consecutive views of that many systems (bounded per-call workspaces
+    and outputs; Philox draws keyed by the global system index, so the results equal the one-call run).
+    system_base: global index of system 0 of `dev` (sharded callers)."""
+    import torch
     from .assembly import epilogue
-    res = solve_batch(dev, scheme, mode="lockstep", max_iters=max_iters, epsilon=epsilon, f_ref=f_ref, rng=rng,
-                      rows_cap=rows_cap, stream=stream, workspace=workspace)
-    ep = epilogue(dev, res.v, v_ref=v_ref, beta_ref=beta_ref, rates=rates, want_f=want_f, stream=stream)
-    out = {"solve": res, **ep}
-    out["launches"] = res.launches + ep["launches"]
+    b = dev.n_systems
+    if chunk_systems <= 0 or chunk_systems >= b:
+        res = solve_batch(dev, scheme, mode="lockstep", max_iters=max_iters, epsilon=epsilon, f_ref=f_ref, rng=rng,
+                          rows_cap=rows_cap, stream=stream, workspace=workspace, system_base=system_base)
+        ep = epilogue(dev, res.v, v_ref=v_ref, beta_ref=beta_ref, rates=rates, want_f=want_f, stream=stream)
+        out = {"solve": res, **ep, "v": res.v}
+        out["launches"] = res.launches + ep["launches"]
+        return out
+    if isinstance(rng, HostStreams):
+        raise ValueError("chunk_systems needs on-device draws (rng=('philox', seed)) or a deterministic scheme")
+    sl = lambda a, lo, hi: None if a is None else a[lo:hi]  # noqa: E731
+    parts, eps_, launches = [], [], 0
+    for lo in range(0, b, chunk_systems):
+        hi = min(b, lo + chunk_systems)
+        sub = dev.view(lo, hi)
+        res = solve_batch(sub, scheme, mode="lockstep", max_iters=max_iters, epsilon=epsilon,
+                          f_ref=sl(f_ref, lo, hi), rng=rng, rows_cap=rows_cap, stream=stream, workspace=workspace,
+                          system_base=system_base + lo)
+        workspace = res.workspace
+        ep = epilogue(sub, res.v, v_ref=sl(v_ref, lo, hi), beta_ref=sl(beta_ref, lo, hi), rates=rates,
+                      want_f=want_f, stream=stream)
+        parts.append(res)
+        eps_.append(ep)
+        launches += res.launches + ep["launches"]
+    cat = lambda xs: None if xs[0] is None else torch.cat(xs)  # noqa: E731
+    res = BatchResult(scheme=parts[0].scheme, dev=dev, **{f: cat([getattr(p, f) for p in parts]) for f in (
+        "v", "iters", "converged", "done", "noop_steps", "flops", "n_outer", "sys_converged", "rows")})
+    res.launches = launches
+    out = {"solve": res, "v": res.v, "launches": launches, "workspace": None, "gram_form": eps_[0]["gram_form"]}
+    for key in ("f", "beta", "nmse", "rates", "sum_rate"):
+        out[key] = cat([e[key] for e in eps_])
     return out
 
 

@@ -19,6 +19,10 @@ Fixtures
   ref_cfg1.npz       BASELINE cfg1-shaped inputs (contiguous VRs, lambda/(4 pi r) LoS,
                      unit columns, xi=K/SNR), 3 realizations, GRK T=50 + RZF + rates
   ref_cfg2.npz       BASELINE cfg2-shaped, 1 realization, the 5 cfg2 schemes, T=200
+  ref_cfg2_philox.npz  BASELINE cfg2-shaped, realizations 0-1, urk / grk / vr-ogrk at T=200 with the row draws
+                     of the throughput mode: the reference's rng is oracle.philox.PhiloxGenerator(seed, b),
+                     whose spawned children serve the device's Philox4x32-10 draws (pins the draw shim and the
+                     device keying against the real reference)
   kaczplot_convergence.npz   per-iteration nmse/resid/flops of the reference's own
                      golden CSV pkg/kaczplot/tests/data/convergence.csv
 """
@@ -207,6 +211,29 @@ def config_fixture(name, seeds, schemes, iters, fname):
     np.savez_compressed(os.path.join(HERE, fname), **out)
 
 
+PHILOX_SEED = 2024
+
+
+def philox_fixture(seeds, schemes, iters, fname):
+    from oracle.philox import PhiloxGenerator
+    cfgd = CONFIGS["cfg2"]
+    ch = generate(cfgd, seeds)
+    out = {"seeds": np.asarray(seeds), "n_iters": iters, "philox_seed": PHILOX_SEED}
+    for b, seed in enumerate(seeds):
+        chan = contiguous_reference(ch, b)
+        reg = float(ch.reg[b])
+        sys_ = kaczprec.AugmentedSystem.from_channel(chan, reg)
+        ref = kaczprec.rzf_precoder(chan, reg)
+        for sc in schemes:
+            run, rows = run_logged(sc, sys_, ref, 0.0, PhiloxGenerator(PHILOX_SEED, int(seed)), max_iters=iters)
+            out[f"{b}/{sc}/v"] = run.v
+            out[f"{b}/{sc}/rows"] = pad_rows(rows, iters)
+            out[f"{b}/{sc}/nmse"] = run.nmse_trace[-1]
+            _, out[f"{b}/{sc}/sum_rate"] = kaczprec.spectral_efficiency(chan.h, run.precoder.f,
+                                                                        float(ch.snr_linear[b]))
+    np.savez_compressed(os.path.join(HERE, fname), **out)
+
+
 def kaczplot_fixture():
     path = "/root/reference/pkg/kaczplot/tests/data/convergence.csv"
     with open(path) as fh:
@@ -226,12 +253,21 @@ def kaczplot_fixture():
 
 
 if __name__ == "__main__":
-    lockstep_fixture()
-    fixed_t_fixture()
-    solve_fixture()
-    config_fixture("cfg1", [0, 1, 2], ["grk"], 50, "ref_cfg1.npz")
-    config_fixture("cfg2", [0], ["urk", "grk", "vr-ogrk", "ahk", "vr-oahk"], 200, "ref_cfg2.npz")
-    kaczplot_fixture()
+    only = set(sys.argv[1:])
+    if not only or "lockstep" in only:
+        lockstep_fixture()
+    if not only or "fixed_t" in only:
+        fixed_t_fixture()
+    if not only or "solve" in only:
+        solve_fixture()
+    if not only or "cfg1" in only:  # BASELINE cfg1: all 100 seeded realizations
+        config_fixture("cfg1", list(range(100)), ["grk"], 50, "ref_cfg1.npz")
+    if not only or "cfg2" in only:
+        config_fixture("cfg2", [0], ["urk", "grk", "vr-ogrk", "ahk", "vr-oahk"], 200, "ref_cfg2.npz")
+    if not only or "philox" in only:
+        philox_fixture([0, 1], ["urk", "grk", "vr-ogrk"], 200, "ref_cfg2_philox.npz")
+    if not only or "kaczplot" in only:
+        kaczplot_fixture()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -34,3 +34,69 @@ def contiguous_from_fixture(z):
     from paper_2501_10689_b200.channel import ContiguousChannels
     return ContiguousChannels(int(z["n_antennas"]), int(z["start"].shape[1]), z["start"], z["length"], z["heff"],
                               z["row_val_ptr"], z["reg"], z["snr_linear"])
+
+
+def oracle_cfg2_philox_task(args):
+    """One cfg2 realization through the oracle port fed the device's Philox draws (worker of a spawn pool:
+    regenerates its own channel).  Returns rows (K, T) int16 (-1 padded), V, NMSE vs RZF and the Eq. (7)
+    sum-rate, for the scheme."""
+    system, scheme, seed, iters = args
+    from threadpoolctl import threadpool_limits
+    from oracle.philox import PhiloxGenerator
+    from paper_2501_10689_b200.channel import generate
+    with threadpool_limits(1):
+        ch = generate("cfg2", [system])
+        chan = oracle_channel_contiguous(ch, 0)
+        reg = float(ch.reg[0])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        rng = PhiloxGenerator(seed, system) if scheme in ("urk", "swor-erk", "grk", "vr-ogrk") else None
+        run = O.run_precoding(scheme, sys_, ref, epsilon=0.0, max_iters=iters, rng=rng, traces=False)
+        rows = np.full((ch.n_users, iters), -1, dtype=np.int16)
+        for c, r in enumerate(run.rows):
+            rows[c, :len(r)] = r
+        f = O.assemble_dense(chan, run.v).f
+        _, sr = O.spectral_efficiency(chan.h, f, float(ch.snr_linear[0]))
+        return {"system": system, "scheme": scheme, "rows": rows, "v": run.v, "nmse": O.nmse(f, ref.f),
+                "sum_rate": sr}
+
+
+def spawn_pool_map(fn, tasks, max_workers=None):
+    """Map fn over tasks on a spawn-context process pool (safe after CUDA initialisation: the workers never
+    touch the GPU), one task at a time per worker, order preserved."""
+    import multiprocessing as mp
+    n = max_workers or min(len(tasks), len(os.sched_getaffinity(0)))
+    with mp.get_context("spawn").Pool(processes=max(1, n)) as pool:
+        return pool.map(fn, tasks, chunksize=1)
+
+
+def oracle_solve_columns_task(args):
+    """Per-rhs `solve` (residual mode) of columns `cols` of realization `system` of a named config, the
+    stochastic schemes fed the device's Philox draws (spawn-pool worker).  Returns (cols, V columns, iters)."""
+    cfg_name, system, scheme, cols, seed, eps = args
+    from threadpoolctl import threadpool_limits
+    from oracle.philox import PhiloxGenerator
+    from paper_2501_10689_b200.channel import generate
+    with threadpool_limits(1):
+        ch = generate(cfg_name, [system])
+        chan = oracle_channel_contiguous(ch, 0)
+        sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[0]))
+        kids = PhiloxGenerator(seed, system).spawn(ch.n_users)
+        vcols, iters = [], []
+        for c in cols:
+            st, tr = O.solve(scheme, sys_, c, O.StoppingRule(mode="residual", epsilon=eps), rng=kids[c])
+            vcols.append(st.coef)
+            iters.append(tr.n_iters)
+        return cols, np.stack(vcols, axis=1), iters
+
+
+C64_REL = 1e-3      # north_star: complex64 NMSE / sum-rate within 1e-3 relative
+C64_FLOOR = 1e-6    # SURVEY.md §9.7: the complex64 NMSE floor (~5e-8 measured on cfg2) sits below this
+
+
+def c64_nmse_ok(n64, n128):
+    """SURVEY.md §9.7 complex64 NMSE criterion, elementwise: within 1e-3 relative of the complex128 NMSE where
+    that is above 1e-5; below it (within a few decades of the fp32 floor, where fp32 rounding of F alone moves
+    the NMSE by ~1e-8) the two agree to 1e-6 absolute (for a c128 NMSE at 1e-15 this is NMSE_64 <= 1e-6)."""
+    n64, n128 = np.asarray(n64, dtype=np.float64), np.asarray(n128, dtype=np.float64)
+    return np.where(n128 >= 1e-5, np.abs(n64 - n128) <= C64_REL * n128, np.abs(n64 - n128) <= C64_FLOOR)

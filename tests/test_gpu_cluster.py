@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import oracle_channel_contiguous
+from helpers import c64_nmse_ok, oracle_channel_contiguous, oracle_solve_columns_task, spawn_pool_map
 
 pytestmark = pytest.mark.gpu
 
@@ -146,7 +146,9 @@ def test_cluster_residual_tolerance(cfg, nsys):
             v = res.v[b].cpu().numpy().astype(np.complex128)
             r = np.eye(k) - gram @ v
             rn = np.linalg.norm(r, axis=0)
-            assert rn.max() <= 2 * eps, (scheme, rn.max())
+            # the fp32 stopping test sees the refreshed fp32 residuals; recomputed in float64 from the rounded
+            # V they agree to fp32 rounding of V (|dr| ~ cond * 6e-8 * ||V||, << 1% of eps here)
+            assert rn.max() <= 1.01 * eps, (scheme, rn.max())
             if scheme == "vr-oahk" and b == 0:
                 chan = oracle_channel_contiguous(ch, b)
                 sys_ = O.AugmentedSystem.from_channel(chan, reg)
@@ -185,9 +187,7 @@ def test_cluster_cfg5_ahk_nmse_vs_rzf():
         out = kz.run_precoding_batched(sc, dev64, max_iters=T, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
         ref = kz.run_precoding_batched(sc, dev128, max_iters=T, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
         got, want = out["nmse"].cpu().numpy(), ref["nmse"].cpu().numpy()
-        above = want >= 1e-5  # relative criterion above the fp32 floor, else NMSE_64 <= 1e-6
-        np.testing.assert_allclose(got[above], want[above], rtol=1e-3)
-        assert np.all(got[~above] <= 1e-6), got
+        assert np.all(c64_nmse_ok(got, want)), (got, want)
         np.testing.assert_allclose(out["sum_rate"].cpu().numpy(), ref["sum_rate"].cpu().numpy(), rtol=1e-3)
 
 
@@ -215,7 +215,7 @@ def test_cluster_residual_check_every_and_partial_slices(scheme):
         reg = float(ch.reg[b])
         v = res.v[b].cpu().numpy().astype(np.complex128)
         rn = np.linalg.norm(np.eye(k) - (h.conj().T @ h + reg * np.eye(k)) @ v, axis=0)
-        assert rn.max() <= 2 * eps, (scheme, rn.max())
+        assert rn.max() <= 1.01 * eps, (scheme, rn.max())
         if scheme in ("gk", "ahk", "vr-oahk") and b == 0:
             chan = oracle_channel_contiguous(ch, b)
             sys_ = O.AugmentedSystem.from_channel(chan, reg)
@@ -242,3 +242,43 @@ def test_cluster_gk_lockstep_rows_log_and_noop_free():
         rows = res.rows[b].cpu().numpy()
         same = np.mean([np.array_equal(rows[c], run.rows[c]) for c in range(ch.n_users)])
         assert same >= 0.9, same
+
+
+@pytest.mark.parametrize("scheme", ["grk", "vr-oahk"])
+def test_cfg4_c64_nmse_and_rate_vs_oracle(scheme):
+    """BASELINE cfg4 at its stated size per system (Nt=4096, K=256, VR=512, residual tolerance 1e-4, solve_all
+    semantics, solvers.py:460-537) in complex64 against the complex128 oracle on the same realization, GRK fed the
+    device's Philox draws (oracle/philox.py): NMSE vs RZF and the Eq. (7) sum-rate within 1e-3 relative (the
+    north_star's complex64 criterion; the runs stop on the residual, far above the fp32 floor), every rhs
+    converged, and for the deterministic VR-OAHK the per-rhs iteration counts equal to the oracle's for at least
+    90% of the rhs (+-1: an fp32 residual norm sitting on the threshold)."""
+    kz = _kz()
+    eps, seed, k = 1e-4, 4242, 256
+    ch = kz.generate("cfg4", [0])
+    dev64 = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    dev128 = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    rz = kz.rzf_batched(dev128)
+    rng = ("philox", seed) if scheme == "grk" else None
+    res = kz.solve_batch(dev64, scheme, mode="residual", epsilon=eps, max_iters=10000 * k, rng=rng)
+    assert bool(res.converged.all())
+    ep = kz.epilogue(dev64, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True)
+    tasks = [("cfg4", 0, scheme, list(range(c, min(k, c + 8))), seed, eps) for c in range(0, k, 8)]
+    v_or = np.zeros((k, k), dtype=np.complex128)
+    it_or = np.zeros(k, dtype=np.int64)
+    for cols, vc, its in spawn_pool_map(oracle_solve_columns_task, tasks):
+        v_or[:, cols] = vc
+        it_or[cols] = its
+    chan = oracle_channel_contiguous(ch, 0)
+    reg = float(ch.reg[0])
+    ref = O.rzf_precoder(chan, reg)
+    f_or = O.assemble_dense(chan, v_or).f
+    n128 = O.nmse(f_or, ref.f)
+    _, s128 = O.spectral_efficiency(chan.h, f_or, float(ch.snr_linear[0]))
+    n64, s64 = float(ep["nmse"][0]), float(ep["sum_rate"][0])
+    its = res.iters[0].cpu().numpy()
+    print(f"cfg4 {scheme}: nmse c64 {n64:.6e} oracle {n128:.6e}; sum-rate {s64:.9f} vs {s128:.9f}; "
+          f"iters equal {np.mean(its == it_or):.3f}, max |diff| {np.abs(its - it_or).max()}")
+    assert s64 == pytest.approx(s128, rel=1e-3)
+    assert n64 == pytest.approx(n128, rel=1e-3)
+    if scheme == "vr-oahk":  # deterministic: the fp32 run stops where the oracle does
+        assert np.abs(its - it_or).max() <= 1 and np.mean(its == it_or) >= 0.9

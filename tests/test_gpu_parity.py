@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import contiguous_from_fixture, load, oracle_channel_contiguous, oracle_channel_from_mask
+from helpers import c64_nmse_ok, contiguous_from_fixture, load, oracle_channel_contiguous, oracle_channel_from_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -187,10 +187,7 @@ def test_config_parity_c128(name):
 
 def _c64_ok(n64, n128, s64, s128):
     assert s64 == pytest.approx(s128, rel=REL_C64)
-    if n128 >= 1e-5:
-        assert n64 == pytest.approx(n128, rel=REL_C64)
-    else:
-        assert n64 <= 1e-6
+    assert c64_nmse_ok(n64, n128), (n64, n128)
 
 
 @pytest.mark.parametrize("name", ["ref_cfg1.npz", "ref_cfg2.npz"])
@@ -419,7 +416,16 @@ def test_register_resident_path_all_schemes(scheme, dtype):
             assert int(res.noop_steps[b].sum()) == run.noop_steps
             np.testing.assert_array_equal(res.iters[b].cpu().numpy(), run.iters)
         else:
-            assert rel(v, run.v) <= 1e-3 or scheme in ("grk", "vr-ogrk", "gk")
+            if scheme in ("grk", "vr-ogrk", "gk"):
+                # greedy picks may break fp32 near-ties differently, so V is judged through the north_star's
+                # complex64 criterion: NMSE vs RZF and sum-rate against the complex128 oracle
+                ep = kz.epilogue(dev.view(b, b + 1), res.v[b:b + 1], v_ref=O.auxiliary_matrix(chan, sys_.reg)[None],
+                                 beta_ref=[ref.norm_factor], rates=True)
+                f_run = O.assemble_dense(chan, run.v).f
+                _, s128 = O.spectral_efficiency(chan.h, f_run, float(ch.snr_linear[b]))
+                _c64_ok(float(ep["nmse"][0]), O.nmse(f_run, ref.f), float(ep["sum_rate"][0]), s128)
+            else:
+                assert rel(v, run.v) <= 1e-3
             if scheme in ("urk", "swor-erk"):  # host index streams: rows and flop counters exact in c64 too
                 assert_rows(res.rows, run.rows, b)
                 setup = 4 * ch.n_antennas * k
@@ -558,10 +564,7 @@ def test_bench_workload_c64_vs_c128_same_draws(scheme):
     o128 = kz.run_precoding_batched(scheme, d128, max_iters=200, rng=rng, v_ref=rz["v"], beta_ref=rz["beta"],
                                     rates=True)
     n64, n128 = o64["nmse"].cpu().numpy(), o128["nmse"].cpu().numpy()
-    above = n128 >= 1e-5
-    if scheme == "urk" or above.any():
-        np.testing.assert_allclose(n64[above], n128[above], rtol=1e-3)
-    assert np.all(n64[~above] <= 1e-6), n64[~above].max()
+    assert np.all(c64_nmse_ok(n64, n128)), (n64, n128)
     np.testing.assert_allclose(o64["sum_rate"].cpu().numpy(), o128["sum_rate"].cpu().numpy(), rtol=1e-3)
 
 

@@ -159,3 +159,71 @@ def test_kaczplot_golden_csv():
             big = want_n > 1e-9
             np.testing.assert_allclose(np.asarray(run.nmse_trace)[big], want_n[big], rtol=1e-9)
             np.testing.assert_allclose(run.resid_trace, z[f"{sc}/{seed}/resid"], rtol=1e-8, atol=1e-14)
+
+
+# --------------------------------------------------------------------------- throughput-mode draws (oracle/philox.py)
+
+def test_philox_known_answers():
+    """Philox4x32-10 known-answer vectors of its publication (Salmon et al., SC'11: zero, all-ones and pi-digit
+    counter/key pairs) for the numpy restatement of the device's draw generator."""
+    from oracle.philox import philox4x32_10
+    cases = [((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+             ((0xFFFFFFFF,) * 4, (0xFFFFFFFF, 0xFFFFFFFF), (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+             ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+              (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
+    for ctr, key, want in cases:
+        got = philox4x32_10(np.array([ctr], dtype=np.uint32), key[0], key[1])[0]
+        assert [int(x) for x in got] == list(want)
+
+
+def test_philox_uniform_keying_and_range():
+    from oracle.philox import philox_uniform
+    u = philox_uniform(2024, np.arange(64)[:, None], 3, np.arange(200)[None, :])
+    assert u.shape == (64, 200) and np.all((u >= 0) & (u < 1))
+    assert abs(u.mean() - 0.5) < 0.01
+    # one (system, rhs, draw) evaluated alone equals its entry in the broadcast evaluation
+    assert philox_uniform(2024, 17, 3, 123) == u[17, 123]
+    assert philox_uniform(2025, 17, 3, 123) != u[17, 123]
+
+
+def test_philox_choice_is_numpy_generator_choice():
+    """The shim's choice(n, p) is numpy Generator.choice's own algorithm on the stream's next uniform
+    (cumsum, normalise by the last entry, searchsorted right): checked against numpy itself with twin PCG64
+    generators over random weight vectors."""
+    from oracle.philox import PhiloxStream
+    rs = np.random.default_rng(5)
+    for trial in range(300):
+        k = int(rs.integers(1, 200))
+        w = rs.random(k) ** 4
+        if trial % 7 == 0:
+            w[rs.integers(k)] = 0.0
+        p = w / w.sum()
+        g1, g2 = np.random.default_rng(trial), np.random.default_rng(trial)
+        want = int(g1.choice(k, p=p))
+        s = PhiloxStream(0, 0, 0)
+        s._next = lambda g=g2: float(g.random())  # feed the twin generator's uniform
+        assert s.choice(k, p=p) == want
+
+
+def test_philox_fixture_reference_bitwise():
+    """The oracle port fed the device's Philox draws (PhiloxGenerator) reproduces the REAL reference run with the
+    same draws (tests/golden/ref_cfg2_philox.npz, cfg2 realizations 0-1, urk / grk / vr-ogrk, T = 200): row
+    sequences and V bitwise."""
+    from oracle.philox import PhiloxGenerator
+    z = load("ref_cfg2_philox.npz")
+    from paper_2501_10689_b200.channel import generate
+    seeds = [int(s) for s in z["seeds"]]
+    ch = generate("cfg2", seeds)
+    T = int(z["n_iters"])
+    for b, seed in enumerate(seeds):
+        chan = oracle_channel_contiguous(ch, b)
+        reg = float(ch.reg[b])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        for sc in ("urk", "grk", "vr-ogrk"):
+            run = O.run_precoding(sc, sys_, ref, epsilon=0.0, max_iters=T,
+                                  rng=PhiloxGenerator(int(z["philox_seed"]), seed), traces=False)
+            np.testing.assert_array_equal(run.v, z[f"{b}/{sc}/v"])
+            rows = z[f"{b}/{sc}/rows"]
+            for c in range(ch.n_users):
+                np.testing.assert_array_equal(run.rows[c], rows[c, :len(run.rows[c])])
