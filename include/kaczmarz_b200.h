@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 6
+#define KZ_ABI_VERSION 7
 
 /* status codes */
 #define KZ_OK 0
@@ -46,8 +46,12 @@ extern "C" {
 #define KZ_ERR_WORKSPACE (-4) /* workspace too small */
 #define KZ_ERR_UNSUPPORTED (-5)
 
-/* schemes, in the order of SCHEMES (solvers.py:39) */
-enum kz_scheme { KZ_URK = 0, KZ_SWOR_ERK = 1, KZ_GK = 2, KZ_GRK = 3, KZ_VR_OGRK = 4, KZ_AHK = 5, KZ_VR_OAHK = 6 };
+/* schemes, in the order of SCHEMES (solvers.py:39), then the extension the BASELINE cfg3 asks for */
+enum kz_scheme { KZ_URK = 0, KZ_SWOR_ERK = 1, KZ_GK = 2, KZ_GRK = 3, KZ_VR_OGRK = 4, KZ_AHK = 5, KZ_VR_OAHK = 6,
+                 /* grouped VR-OAHK (no reference counterpart; CPU restatement oracle/grouped.py): per iteration an
+                    exact block step on each orthogonal group O_1..O_g, then the non-orthogonal rows aggregated in
+                    consecutive blocks of at most kz_problem.agg_cap rows.  g = 1 and agg_cap >= |N| is vr-oahk. */
+                 KZ_VR_OAHK_G = 7 };
 enum kz_dtype { KZ_C128 = 0, KZ_C64 = 1 };
 
 /* stopping drivers */
@@ -106,6 +110,14 @@ typedef struct kz_problem {
      min(K, pairs)) */
   int32_t slice_rows_128;
   int32_t slice_rows_256;
+  /* KZ_VR_OAHK_G only: the orthogonal rows of system b (orth_idx[orth_ptr[b] .. orth_ptr[b+1])) form the groups
+     [ogrp_ptr[j], ogrp_ptr[j+1]) for j in [ogrp_sys[b], ogrp_sys[b+1]) (absolute offsets into orth_idx, each group
+     ascending and pairwise VR-disjoint); the non-orthogonal rows are aggregated in consecutive blocks of at most
+     agg_cap rows */
+  const int32_t* ogrp_sys;      /* [B+1] */
+  const int32_t* ogrp_ptr;      /* [total groups + 1] */
+  int32_t agg_cap;
+  int32_t _pad0;
 } kz_problem;
 
 #define KZ_PROBLEM_CONTIGUOUS 1

@@ -15,6 +15,7 @@ from .metrics import CADD, CMUL, nmse, spectral_efficiency
 from .rzf import Precoder, apply_auxiliary, auxiliary_matrix, mrc_precoder, rzf_batched, rzf_precoder
 from .solvers import (
     SCHEMES,
+    EXTENDED_SCHEMES,
     AggregationWeights,
     InstanceRun,
     SelectionStrategy,
@@ -50,7 +51,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AugmentedSystem", "BatchResult", "CADD", "CMUL", "CONFIGS", "ContiguousChannels", "DeviceBatch", "Drops",
     "FlopCounter", "HostBatch", "HostStreams", "NearFieldConfig", "Precoder", "PrecodingRun", "RunTrace",
-    "SCHEMES", "STOCHASTIC_SCHEMES", "SolverState", "StoppingRule", "UserPartition", "VR_SCHEMES",
+    "SCHEMES", "EXTENDED_SCHEMES", "STOCHASTIC_SCHEMES", "SolverState", "StoppingRule", "UserPartition", "VR_SCHEMES",
     "apply_auxiliary", "assemble_dense", "assemble_vr", "auxiliary_matrix", "build_partition",
     "canonical_scheme", "display_scheme", "epilogue", "generate", "generate_drops", "mrc_precoder", "nmse", "pin_host", "rzf_batched",
     "rzf_precoder", "run_precoding", "run_precoding_batched", "solve", "solve_all", "solve_batch",

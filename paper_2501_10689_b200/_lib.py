@@ -11,7 +11,7 @@ import os
 
 from .build import lib_path
 
-ABI_VERSION = 6  # include/kaczmarz_b200.h KZ_ABI_VERSION: the struct layouts below follow it
+ABI_VERSION = 7  # include/kaczmarz_b200.h KZ_ABI_VERSION: the struct layouts below follow it
 
 KZ_OK = 0
 KZ_ERR_INVALID = -1
@@ -19,7 +19,7 @@ KZ_ERR_CUDA = -2
 KZ_ERR_NOT_PD = -3
 KZ_ERR_WORKSPACE = -4
 
-SCHEME_IDS = {"urk": 0, "swor-erk": 1, "gk": 2, "grk": 3, "vr-ogrk": 4, "ahk": 5, "vr-oahk": 6}
+SCHEME_IDS = {"urk": 0, "swor-erk": 1, "gk": 2, "grk": 3, "vr-ogrk": 4, "ahk": 5, "vr-oahk": 6, "vr-oahk-g": 7}
 KZ_C128, KZ_C64 = 0, 1
 KZ_PROBLEM_CONTIGUOUS, KZ_PROBLEM_GRAM_CACHED = 1, 2  # kz_problem.flags
 STOP_LOCKSTEP, STOP_RESIDUAL, STOP_ORACLE = 0, 1, 2
@@ -38,6 +38,7 @@ class KzProblem(C.Structure):
         ("max_support", C.c_int32), ("flags", C.c_int32),
         ("slice_pairs_128", C.c_int32), ("slice_pairs_256", C.c_int32),
         ("slice_rows_128", C.c_int32), ("slice_rows_256", C.c_int32),
+        ("ogrp_sys", P), ("ogrp_ptr", P), ("agg_cap", C.c_int32), ("_pad0", C.c_int32),
     ]
 
 

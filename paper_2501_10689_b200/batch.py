@@ -25,7 +25,7 @@ import os
 import numpy as np
 
 from . import _lib
-from .vrgraph import greedy_mis, overlap_from_intervals, overlap_from_segments
+from .vrgraph import greedy_mis, grouped_mis, overlap_from_intervals, overlap_from_segments
 
 
 def _union_size_intervals(start, length):
@@ -72,11 +72,25 @@ class HostBatch:
     non_union_size: np.ndarray
     contiguous: bool
     snr_linear: np.ndarray | None = None
+    # orthogonal groups (grouped VR-OAHK, kz_problem.ogrp_*): system b's groups are [ogrp_ptr[j], ogrp_ptr[j+1])
+    # for j in [ogrp_sys[b], ogrp_sys[b+1]) (absolute offsets into orth_idx); None = one group per system
+    ogrp_sys: np.ndarray | None = None
+    ogrp_ptr: np.ndarray | None = None
+    orth_groups: int = 1      # groups built per system (1: the reference's single orthogonal set)
+    agg_cap: int = 0          # hyperplanes per aggregated step of vr-oahk-g (0: all non-orthogonal rows)
+
+    def __post_init__(self):
+        if self.ogrp_sys is None:  # one group per system: the reference's orthogonal set
+            self.ogrp_sys = np.arange(self.n_systems + 1, dtype=np.int32)
+            self.ogrp_ptr = np.asarray(self.orth_ptr, dtype=np.int32).copy()
 
     # ------------------------------------------------------------ builders
     @classmethod
-    def from_contiguous(cls, ch, partition: bool = True) -> "HostBatch":
-        """From `channel.ContiguousChannels` (one segment per user)."""
+    def from_contiguous(cls, ch, partition: bool = True, orth_groups: int = 1, agg_cap: int = 0) -> "HostBatch":
+        """From `channel.ContiguousChannels` (one segment per user).  orth_groups > 1 builds the orthogonal row
+        groups of the grouped VR-OAHK variant (vrgraph.grouped_mis; the orthogonal set then holds every group and
+        is NOT one mutually orthogonal set, so plain vr-oahk refuses such a batch); agg_cap = hyperplanes per
+        aggregated step of vr-oahk-g (0 = all non-orthogonal rows at once)."""
         b, k = ch.start.shape
         rows = b * k
         lens = ch.length.reshape(-1).astype(np.int64)
@@ -87,10 +101,15 @@ class HostBatch:
                           for r in range(rows)])
         energy = e + np.repeat(ch.reg, k)
         cp, ci, op, oi, np_, ni, nu = [0], [], [0], [], [0], [], []
+        gs, gp = [0], [0]
         if partition:
             for s in range(b):
                 adj = overlap_from_intervals(ch.start[s], ch.length[s])
-                orth = greedy_mis(adj)
+                groups = grouped_mis(adj, orth_groups) if orth_groups > 1 else [greedy_mis(adj)]
+                orth = np.concatenate(groups)
+                for g in groups:
+                    gp.append(gp[-1] + len(g))
+                gs.append(len(gp) - 1)
                 in_o = np.zeros(k, dtype=bool)
                 in_o[orth] = True
                 non = np.flatnonzero(~in_o)
@@ -108,11 +127,13 @@ class HostBatch:
             op = [0] * (b + 1)
             np_ = [0] * (b + 1)
             nu = [0] * b
+            gs, gp = list(range(b + 1)), [0] * (b + 1)
         i32 = lambda a: np.asarray(a, dtype=np.int32)  # noqa: E731
         return cls(b, k, ch.n_antennas, np.arange(rows + 1, dtype=np.int32), i32(ch.start.reshape(-1)),
                    i32(ch.length.reshape(-1)), ch.row_val_ptr.astype(np.int64), ch.heff.astype(np.complex128),
                    energy, np.asarray(ch.reg, dtype=np.float64), i32(cp), i32(ci), i32(op), i32(oi), i32(np_),
-                   i32(ni), i32(nu), True, np.asarray(ch.snr_linear, dtype=np.float64))
+                   i32(ni), i32(nu), True, np.asarray(ch.snr_linear, dtype=np.float64), i32(gs), i32(gp),
+                   max(1, orth_groups), int(agg_cap))
 
     @classmethod
     def from_systems(cls, systems, snr_linear=None) -> "HostBatch":
@@ -175,6 +196,14 @@ class HostBatch:
                 off += a[-1]
             return np.concatenate(out)
 
+        if any(p.orth_groups != parts[0].orth_groups or p.agg_cap != parts[0].agg_cap for p in parts):
+            raise ValueError("batches to concatenate must share orth_groups and agg_cap")
+        gsys, gptr, goff, ooff = [np.zeros(1, dtype=np.int32)], [np.zeros(1, dtype=np.int32)], 0, 0
+        for p in parts:
+            gsys.append(p.ogrp_sys[1:] + goff)
+            gptr.append(p.ogrp_ptr[1:] - p.ogrp_ptr[0] + ooff)
+            goff += int(p.ogrp_sys[-1])
+            ooff += int(p.orth_ptr[-1])
         return cls(sum(p.n_systems for p in parts), k, nt, cat_ptr("row_seg_ptr"),
                    np.concatenate([p.seg_start for p in parts]), np.concatenate([p.seg_len for p in parts]),
                    cat_ptr("row_val_ptr"), np.concatenate([p.heff for p in parts]),
@@ -183,7 +212,9 @@ class HostBatch:
                    cat_ptr("orth_ptr"), np.concatenate([p.orth_idx for p in parts]),
                    cat_ptr("non_ptr"), np.concatenate([p.non_idx for p in parts]),
                    np.concatenate([p.non_union_size for p in parts]), all(p.contiguous for p in parts),
-                   None if any(p.snr_linear is None for p in parts) else np.concatenate([p.snr_linear for p in parts]))
+                   None if any(p.snr_linear is None for p in parts) else np.concatenate([p.snr_linear for p in parts]),
+                   np.concatenate(gsys).astype(np.int32), np.concatenate(gptr).astype(np.int32),
+                   parts[0].orth_groups, parts[0].agg_cap)
 
     # ------------------------------------------------------------ accessors
     def support_sizes(self) -> np.ndarray:
@@ -250,6 +281,7 @@ class _HostView:
         self.parent = parent
         self.n_systems = n_systems
         self.n_users, self.n_antennas, self.contiguous = parent.n_users, parent.n_antennas, parent.contiguous
+        self.orth_groups, self.agg_cap = parent.orth_groups, parent.agg_cap
 
     def layout_hints(self) -> dict:
         return self.parent.layout_hints()
@@ -272,7 +304,7 @@ class DeviceBatch:
     """Device-resident copy of a HostBatch plus the KzProblem that points at it."""
 
     FIELDS = ("row_seg_ptr", "seg_start", "seg_len", "row_val_ptr", "heff", "row_energy", "reg", "coupled_ptr",
-              "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size")
+              "coupled_idx", "orth_ptr", "orth_idx", "non_ptr", "non_idx", "non_union_size", "ogrp_sys", "ogrp_ptr")
 
     def __init__(self, host: HostBatch, dtype: str = "c128", device=None, pinned=None):
         """Upload `host`.  `pinned` may be the dict returned by `pin_host(host, dtype)`:
@@ -306,6 +338,7 @@ class DeviceBatch:
         p.slice_pairs_256 = hints["slice_pairs_256"]
         p.slice_rows_128 = hints["slice_rows_128"]
         p.slice_rows_256 = hints["slice_rows_256"]
+        p.agg_cap = self.host.agg_cap if self.host.agg_cap > 0 else self.host.n_users
         return p
 
     @classmethod
@@ -360,6 +393,8 @@ class DeviceBatch:
         with torch.cuda.stream(s):
             t["coupled_ptr"] = torch.cat([z, torch.cumsum(ccnt, 0, dtype=torch.int32)])
             t["orth_ptr"] = torch.cat([z, torch.cumsum(ocnt, 0, dtype=torch.int32)])
+            t["ogrp_sys"] = torch.arange(b + 1, dtype=torch.int32, device=dev)  # one orthogonal group per system
+            t["ogrp_ptr"] = t["orth_ptr"]
             t["non_ptr"] = torch.cat([z, torch.cumsum(k - ocnt, 0, dtype=torch.int32)])
             n_c, n_o = int(t["coupled_ptr"][-1]), int(t["orth_ptr"][-1])  # sizes: one small device->host read
         t["coupled_idx"] = torch.empty(max(n_c, 1), dtype=torch.int32, device=dev)
@@ -377,7 +412,7 @@ class DeviceBatch:
     # CSR pointer fields indexed by row (b*K + i) / by system; their VALUES are absolute offsets into the value
     # arrays, so a contiguous range of systems is the same value arrays behind offset pointer arrays
     _PER_ROW = ("row_seg_ptr", "row_val_ptr", "row_energy", "coupled_ptr")
-    _PER_SYSTEM = ("reg", "orth_ptr", "non_ptr", "non_union_size", "snr_linear")
+    _PER_SYSTEM = ("reg", "orth_ptr", "non_ptr", "non_union_size", "snr_linear", "ogrp_sys")
 
     def view(self, lo: int, hi: int) -> "DeviceBatch":
         """Systems [lo, hi) of this batch without copying: the kz_problem's per-row / per-system arrays start at

@@ -94,7 +94,7 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
   g_launches = 0;
   int st = check_problem(prob);
   if (st) return st;
-  if (scheme < KZ_URK || scheme > KZ_VR_OAHK) return fail(KZ_ERR_INVALID, "unknown scheme %d", (int)scheme);
+  if (scheme < KZ_URK || scheme > KZ_VR_OAHK_G) return fail(KZ_ERR_INVALID, "unknown scheme %d", (int)scheme);
   if (!stop || !rng || !out) return fail(KZ_ERR_INVALID, "null stop/rng/out");
   if (stop->mode < KZ_STOP_LOCKSTEP || stop->mode > KZ_STOP_ORACLE)
     return fail(KZ_ERR_INVALID, "unknown stopping mode %d", (int)stop->mode);
@@ -124,6 +124,10 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
     return fail(KZ_ERR_INVALID, "vr-ogrk needs the coupled sets");
   if ((scheme == KZ_VR_OAHK) && (!prob->orth_ptr || !prob->non_ptr || !prob->non_union_size))
     return fail(KZ_ERR_INVALID, "vr-oahk needs the orthogonal / non-orthogonal partition");
+  if (scheme == KZ_VR_OAHK_G && (!prob->orth_ptr || !prob->non_ptr || !prob->ogrp_sys || !prob->ogrp_ptr))
+    return fail(KZ_ERR_INVALID, "vr-oahk-g needs the orthogonal groups and the non-orthogonal rows");
+  if (scheme == KZ_VR_OAHK_G && prob->agg_cap < 1)
+    return fail(KZ_ERR_INVALID, "vr-oahk-g needs agg_cap >= 1 (got %d)", (int)prob->agg_cap);
   if (!out->v) return fail(KZ_ERR_INVALID, "out->v must be non-null");
   if (prob->n_systems == 0) return KZ_OK;
   if (!workspace) workspace_bytes = 0;

@@ -275,6 +275,28 @@ template <class T> struct Gen {
     if (O.rows && it < O.rows_cap) O.rows[rid(b, c) * O.rows_cap + it] = i;
   }
 
+  // |union of the supports of `rows`| (the span ahk_step charges, solvers.py:279-286): antennas marked in the
+  // warp's y scratch, counted, cleared (ahk() zeroes y again before aggregating)
+  __device__ int union_size(int b, const int32_t* rows, int nrows, int warp, int lane) const {
+    T* y = Y(b, warp);
+    const int nt = Nt();
+    for (int n = lane; n < nt; n += 32) y[n] = czero<T>();
+    __syncwarp();
+    for (int k = 0; k < nrows; ++k) {
+      size_t rr = rid(b, rows[k]);
+      for (int s = P.row_seg_ptr[rr]; s < P.row_seg_ptr[rr + 1]; ++s) {
+        const int st = P.seg_start[s], ln = P.seg_len[s];
+        for (int j = lane; j < ln; j += 32) y[st + j] = Cx<T>::make(1, 0);
+      }
+      __syncwarp();
+    }
+    int cnt = 0;
+    for (int n = lane; n < nt; n += 32) cnt += y[n].x != 0 ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    __syncwarp();
+    return cnt;
+  }
+
   // aggregated step over `rows` (solvers.py:257-309); dense==true mirrors use_vr=False.
   // phi is warp scratch [K].  Returns false on a no-op.
   __device__ bool ahk(int b, int c, const int32_t* rows, int nrows, bool dense, int span_size, T* phi,
@@ -445,6 +467,29 @@ template <class T> struct Gen {
           const int32_t* nrows = P.non_idx + n0;
           f += refresh_rows_vr(b, c, nrows, n1 - n0, lane);
           bool ok = ahk(b, c, nrows, n1 - n0, false, P.non_union_size[b], phi, warp, lane, f);
+          if (!ok && lane == 0) noop(b, c) += 1;
+        }
+        it += 1;
+        break;
+      }
+      case KZ_VR_OAHK_G: {  // oracle/grouped.py GroupedRun.step
+        for (int gi = P.ogrp_sys[b]; gi < P.ogrp_sys[b + 1]; ++gi) {
+          const int o0 = P.ogrp_ptr[gi], o1 = P.ogrp_ptr[gi + 1];
+          const int32_t* orows = P.orth_idx + o0;
+          f += refresh_rows_vr(b, c, orows, o1 - o0, lane);
+          for (int kk = 0; kk < o1 - o0; ++kk) {  // one group: disjoint supports, order-independent
+            const int i = orows[kk];
+            rk_project(b, c, i, lane);
+            f += 2 + 8 * (int64_t)support(b, i) + 2;
+          }
+        }
+        const int n0 = P.non_ptr[b], n1 = P.non_ptr[b + 1], cap = P.agg_cap;
+        for (int s0 = n0; s0 < n1; s0 += cap) {  // consecutive ascending blocks of at most agg_cap rows
+          const int nb = min(cap, n1 - s0);
+          const int32_t* brows = P.non_idx + s0;
+          f += refresh_rows_vr(b, c, brows, nb, lane);
+          const int span = union_size(b, brows, nb, warp, lane);
+          bool ok = ahk(b, c, brows, nb, false, span, phi, warp, lane, f);
           if (!ok && lane == 0) noop(b, c) += 1;
         }
         it += 1;

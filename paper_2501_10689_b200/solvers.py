@@ -34,16 +34,19 @@ from .metrics import CADD, CMUL
 from .vrgraph import UserPartition, build_partition
 
 SCHEMES = ("urk", "swor-erk", "gk", "grk", "vr-ogrk", "ahk", "vr-oahk")
+# batched-API extension (BASELINE cfg3; no reference counterpart, CPU restatement in oracle/grouped.py): VR-OAHK with
+# several orthogonal row groups and at most HostBatch.agg_cap hyperplanes per aggregated step
+EXTENDED_SCHEMES = ("vr-oahk-g",)
 STOCHASTIC_SCHEMES = frozenset({"urk", "swor-erk", "grk", "vr-ogrk"})
-VR_SCHEMES = frozenset({"vr-ogrk", "vr-oahk"})
+VR_SCHEMES = frozenset({"vr-ogrk", "vr-oahk", "vr-oahk-g"})
 _UNIFORM_SCHEMES = frozenset({"grk", "vr-ogrk"})
 
 
-def canonical_scheme(name: str) -> str:
-    """solvers.py:48-52."""
+def canonical_scheme(name: str, extended: bool = False) -> str:
+    """solvers.py:48-52 (extended=True also accepts EXTENDED_SCHEMES, for the batched entry points)."""
     low = name.strip().lower()
-    if low not in SCHEMES:
-        raise ValueError(f"unknown scheme {name!r}; expected one of {SCHEMES}")
+    if low not in SCHEMES and not (extended and low in EXTENDED_SCHEMES):
+        raise ValueError(f"unknown scheme {name!r}; expected one of {SCHEMES + (EXTENDED_SCHEMES if extended else ())}")
     return low
 
 
@@ -286,7 +289,10 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
     realization's rows do not depend on how the batch is chunked or sharded).
     """
     import torch
-    scheme = canonical_scheme(scheme)
+    scheme = canonical_scheme(scheme, extended=True)
+    if scheme == "vr-oahk" and getattr(dev.host, "orth_groups", 1) > 1:
+        raise ValueError("this batch holds several orthogonal groups (orth_groups > 1): run vr-oahk-g on it, or "
+                         "build the batch with orth_groups=1 for vr-oahk")
     lb = _lib.lib()
     b, k = dev.n_systems, dev.n_users
     d = dev.device

@@ -74,6 +74,22 @@ def greedy_mis(adj: np.ndarray) -> np.ndarray:
     return np.asarray(sorted(chosen), dtype=np.int64)
 
 
+def grouped_mis(adj: np.ndarray, n_groups: int) -> list:
+    """Orthogonal row groups for the grouped VR-OAHK variant (BASELINE cfg3): O_1 = greedy_mis(adj), O_g = the same
+    greedy on the subgraph induced by the rows not yet grouped (lowest original index on ties, since the induced
+    subgraph keeps the ascending order).  Each group is pairwise VR-disjoint.  Returns ascending index arrays."""
+    k = adj.shape[0]
+    rem = np.arange(k)
+    groups = []
+    for _ in range(max(1, n_groups)):
+        if rem.size == 0:
+            break
+        loc = greedy_mis(adj[np.ix_(rem, rem)])
+        groups.append(rem[loc])
+        rem = np.setdiff1d(rem, rem[loc])
+    return groups
+
+
 def partition_from_adjacency(adj: np.ndarray) -> UserPartition:
     k = adj.shape[0]
     orth = greedy_mis(adj)

@@ -199,3 +199,21 @@ def test_subarray_channel_view_validates_leakage():
     leaky = O.ChannelMatrix(h=h, vrs=chan.vrs, cfg=chan.cfg)
     with pytest.raises(ValueError):
         kz.SubarrayChannel.from_channel(leaky)
+
+
+def test_grouped_orthogonal_groups_match_oracle_restatement():
+    """HostBatch(orth_groups=g) packs the groups of oracle/grouped.py grouped_partition (vectorised intervals vs
+    set intersections) and one-group batches keep the reference's single orthogonal set."""
+    from oracle.grouped import grouped_partition
+    from helpers import oracle_channel_contiguous
+    ch = kz.generate("cfg3", range(4))
+    hb = kz.HostBatch.from_contiguous(ch, orth_groups=3, agg_cap=8)
+    h1 = kz.HostBatch.from_contiguous(ch)
+    assert hb.agg_cap == 8 and hb.orth_groups == 3
+    for b in range(4):
+        groups, non = grouped_partition(oracle_channel_contiguous(ch, b).vrs, 3)
+        got = [tuple(hb.orth_idx[hb.ogrp_ptr[j]:hb.ogrp_ptr[j + 1]]) for j in range(hb.ogrp_sys[b], hb.ogrp_sys[b + 1])]
+        assert got == [tuple(g) for g in groups]
+        assert tuple(hb.non_idx[hb.non_ptr[b]:hb.non_ptr[b + 1]]) == tuple(non)
+        assert list(h1.ogrp_sys[b:b + 2]) == [b, b + 1]
+        assert tuple(h1.orth_idx[h1.ogrp_ptr[b]:h1.ogrp_ptr[b + 1]]) == tuple(groups[0])

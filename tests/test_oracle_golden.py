@@ -227,3 +227,65 @@ def test_philox_fixture_reference_bitwise():
             rows = z[f"{b}/{sc}/rows"]
             for c in range(ch.n_users):
                 np.testing.assert_array_equal(run.rows[c], rows[c, :len(run.rows[c])])
+
+
+# --------------------------------------------------------------------------- grouped VR-OAHK (oracle/grouped.py)
+
+def test_grouped_restatement_limit_is_reference_vr_oahk():
+    """One orthogonal group and an aggregation cap >= |N| is the reference's vr-oahk: bitwise equal to the REAL
+    reference's fixed-T runs (tests/golden/ref_fixed_t.npz, Bernoulli-subarray drops, T = 15) -- V and flop
+    counts -- so the restatement is anchored to the reference path it extends."""
+    from oracle.grouped import run_precoding_grouped
+    z = load("ref_fixed_t.npz")
+    for seed in range(4):
+        chan = oracle_channel_from_mask(z[f"{seed}/h"], z[f"{seed}/vr_mask"], 4)
+        reg = float(z[f"{seed}/reg"])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        run = run_precoding_grouped(sys_, O.rzf_precoder(chan, reg), 1, sys_.n_users, 15)
+        np.testing.assert_array_equal(run.v, z[f"{seed}/vr-oahk/v"])
+        assert run.flops_measured == int(z[f"{seed}/vr-oahk/flops_measured"])
+
+
+def test_grouped_partition_properties():
+    """Groups are pairwise VR-disjoint (mutually orthogonal rows), disjoint from each other and from N, cover
+    every row; group 1 is the reference's maximal independent set; each group's block step solves its rows
+    exactly (Theorem 4: their residuals vanish right after the step)."""
+    from oracle.grouped import GroupedRun, grouped_partition
+    from paper_2501_10689_b200.channel import generate
+    ch = generate("cfg3", [3])
+    chan = oracle_channel_contiguous(ch, 0)
+    sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[0]))
+    groups, non = grouped_partition(chan.vrs, 4)
+    assert tuple(groups[0]) == sys_.partition.orthogonal_sorted
+    seen = set()
+    for g in groups:
+        for a in g:
+            for b in g:
+                if a < b:
+                    assert not (chan.vrs[a].visible_subarrays & chan.vrs[b].visible_subarrays)
+        assert not (seen & set(g))
+        seen |= set(g)
+    assert seen | set(non) == set(range(sys_.n_users)) and not (seen & set(non))
+    assert list(non) == sorted(non)
+    run = GroupedRun(sys_, 5, groups, non, 8)
+    st = run.state
+    for g in groups:
+        O.residual_refresh(st, sys_, rows=np.asarray(g), use_vr=True)
+        O.orthogonal_block_step(st, sys_, np.asarray(g), use_vr=True)
+        O.residual_refresh(st, sys_, rows=np.asarray(g), use_vr=True)
+        assert np.max(np.abs(st.resid[list(g)])) <= 1e-13
+
+
+def test_grouped_aggregation_cap_blocks():
+    """agg_cap splits N into consecutive ascending blocks; every setting contracts the error towards RZF."""
+    from oracle.grouped import run_precoding_grouped
+    from paper_2501_10689_b200.channel import generate
+    ch = generate("cfg3", [1])
+    chan = oracle_channel_contiguous(ch, 0)
+    reg = float(ch.reg[0])
+    sys_ = O.AugmentedSystem.from_channel(chan, reg)
+    ref = O.rzf_precoder(chan, reg)
+    for ng, cap in ((1, 8), (4, 8), (2, 3)):
+        e1 = run_precoding_grouped(sys_, ref, ng, cap, 1).nmse_trace[-1]
+        e3 = run_precoding_grouped(sys_, ref, ng, cap, 3).nmse_trace[-1]
+        assert e3 < e1 < 1.0, (ng, cap, e1, e3)

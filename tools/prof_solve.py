@@ -21,10 +21,12 @@ ap.add_argument("--batch", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--residual", type=float, default=0.0, help="residual tolerance (solve_all semantics); 0: fixed T")
+ap.add_argument("--groups", type=int, default=1, help="orthogonal groups per system (vr-oahk-g)")
+ap.add_argument("--cap", type=int, default=0, help="hyperplanes per aggregated step (vr-oahk-g; 0: all)")
 a = ap.parse_args()
 cfg = kz.CONFIGS[a.config]
 ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
-dev = kz.HostBatch.from_contiguous(ch).to_device(a.dtype)
+dev = kz.HostBatch.from_contiguous(ch, orth_groups=a.groups, agg_cap=a.cap).to_device(a.dtype)
 rng = ("philox", 7) if a.scheme in kz.STOCHASTIC_SCHEMES else None
 times = []
 for r in range(a.reps):
