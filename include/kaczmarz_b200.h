@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KZ_ABI_VERSION 7
+#define KZ_ABI_VERSION 8
 
 /* status codes */
 #define KZ_OK 0
@@ -118,6 +118,11 @@ typedef struct kz_problem {
   const int32_t* ogrp_ptr;      /* [total groups + 1] */
   int32_t agg_cap;
   int32_t _pad0;
+  /* element range [val_lo, val_hi) of heff the batch's rows occupy (= row_val_ptr[0], row_val_ptr[B*K] for dense
+     packing).  When known (val_hi > val_lo) the complex64 on-chip kernels stage H_eff into shared memory with TMA
+     tensor copies over that range; 0, 0 = unknown (asynchronous-copy staging) */
+  int64_t val_lo;
+  int64_t val_hi;
 } kz_problem;
 
 #define KZ_PROBLEM_CONTIGUOUS 1

@@ -11,7 +11,7 @@ import os
 
 from .build import lib_path
 
-ABI_VERSION = 7  # include/kaczmarz_b200.h KZ_ABI_VERSION: the struct layouts below follow it
+ABI_VERSION = 8  # include/kaczmarz_b200.h KZ_ABI_VERSION: the struct layouts below follow it
 
 KZ_OK = 0
 KZ_ERR_INVALID = -1
@@ -39,6 +39,7 @@ class KzProblem(C.Structure):
         ("slice_pairs_128", C.c_int32), ("slice_pairs_256", C.c_int32),
         ("slice_rows_128", C.c_int32), ("slice_rows_256", C.c_int32),
         ("ogrp_sys", P), ("ogrp_ptr", P), ("agg_cap", C.c_int32), ("_pad0", C.c_int32),
+        ("val_lo", C.c_int64), ("val_hi", C.c_int64),
     ]
 
 

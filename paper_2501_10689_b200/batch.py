@@ -217,6 +217,12 @@ class HostBatch:
                    parts[0].orth_groups, parts[0].agg_cap)
 
     # ------------------------------------------------------------ accessors
+    def val_range(self) -> tuple:
+        """heff element range [lo, hi) of this batch's rows (kz_problem.val_lo / val_hi)."""
+        if self.row_val_ptr.size == 0:
+            return 0, 0
+        return int(self.row_val_ptr[0]), int(self.row_val_ptr[-1])
+
     def support_sizes(self) -> np.ndarray:
         return np.diff(self.row_val_ptr).reshape(self.n_systems, self.n_users)
 
@@ -277,14 +283,21 @@ class HostBatch:
 class _HostView:
     """Shape / hint stand-in for the HostBatch of a DeviceBatch.view (the packed host arrays stay the parent's)."""
 
-    def __init__(self, parent, n_systems: int):
+    def __init__(self, parent, n_systems: int, row0: int):
+        while isinstance(parent, _HostView):  # a view of a view: rows relative to the root batch
+            parent = parent.parent
         self.parent = parent
         self.n_systems = n_systems
+        self.row0 = row0  # first row of the view in the root batch
         self.n_users, self.n_antennas, self.contiguous = parent.n_users, parent.n_antennas, parent.contiguous
         self.orth_groups, self.agg_cap = parent.orth_groups, parent.agg_cap
 
     def layout_hints(self) -> dict:
         return self.parent.layout_hints()
+
+    def val_range(self) -> tuple:
+        k, lo = self.n_users, self.row0 // self.n_users
+        return int(self.parent.row_val_ptr[self.row0]), int(self.parent.row_val_ptr[(lo + self.n_systems) * k])
 
 
 def pin_host(host: HostBatch, dtype: str = "c128", pin: bool = True) -> dict:
@@ -339,6 +352,7 @@ class DeviceBatch:
         p.slice_rows_128 = hints["slice_rows_128"]
         p.slice_rows_256 = hints["slice_rows_256"]
         p.agg_cap = self.host.agg_cap if self.host.agg_cap > 0 else self.host.n_users
+        p.val_lo, p.val_hi = self.host.val_range()  # heff element range of the rows (TMA staging bounds)
         return p
 
     @classmethod
@@ -427,7 +441,7 @@ class DeviceBatch:
             if name in self.t:
                 t[name] = self.t[name][lo:hi] if name == "snr_linear" else self.t[name][lo:]
         obj = DeviceBatch.__new__(DeviceBatch)
-        obj.host = _HostView(self.host, hi - lo)
+        obj.host = _HostView(self.host, hi - lo, getattr(self.host, "row0", 0) + lo * k)
         obj.dtype, obj.device, obj.t = self.dtype, self.device, t
         obj.parent = self
         obj.problem = obj._make_problem(t)

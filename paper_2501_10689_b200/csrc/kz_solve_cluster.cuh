@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "kz_common.cuh"
+#include "kz_tma.cuh"
 #include "kz_solve_generic.cuh"
 
 // timing build: close a phase before each cluster barrier so the barrier wait is its own phase
@@ -96,7 +97,7 @@ struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
   size_t rowS, rowL, rvo, c0, c1, en, ien, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, blk, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
-      misc, total;
+      misc, mbar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -166,6 +167,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nchk = o; o = al(o + 4 * G);
   p.flops = o; o = al(o + 8 * G);
   p.misc = o; o = al(o + 64);
+  p.mbar = o; o = al(o + 8);
   p.total = o;
   return p;
 }
@@ -173,6 +175,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
 }  // namespace clu
 
 struct CluArgs {
+  HeffTma tma;  // TMA staging of the row pieces (kz_tma.cuh); tma.ok = 0: asynchronous-copy staging
   kz_problem P;
   kz_rng R;
   kz_out O;
@@ -191,7 +194,7 @@ struct CluArgs {
 // rhs g, g + 16 on 16 antennas, the wide kernel's mapping: twice the FMAs per loaded element set and per
 // piece overhead, when the larger inbox fits)
 template <int SCH, int GG>
-__global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
+__global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constant__ CluArgs p) {
   using namespace clu;
   constexpr int G = GG;
   constexpr int NA = G == 16 ? 4 : 2;  // a-lanes sharing a (row, chunk) piece
@@ -379,18 +382,47 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(CluArgs p) {
   // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
   // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
   // no dependent global load, no load latency per piece)
-  for (int n = w; n < NL; n += W) {
-    const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
-    const int s = rowS[i], L = rowL[i];
-    const T* src = heff + rvo[i];
-    for (int pc = 0; pc <= l1 - l0; ++pc) {
-      const int ant = chunk_of(l0 + pc) * CH + lane;
-      const bool in = ant >= s && ant < s + L;
-      cp_async8(Hs + h0 + pc * CH + lane, src + (in ? ant - s : 0), in);
+  if (p.tma.ok) {
+    // TMA: one 1-D tensor copy per (row, chunk) piece, lanes over the pieces of a local row; the mbarrier
+    // expects every issuing thread's bytes before its single arrival (thread 0, after a barrier)
+    uint64_t* mbar = (uint64_t*)(sm + pl.mbar);
+    if (tid == 0) tma::mbar_init(mbar, 1);
+    __syncthreads();
+    for (int n = w; n < NL; n += W) {
+      const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
+      const long long x0 = rvo[i] - rowS[i] - p.tma.base;  // map coordinate of antenna 0 of row i
+      for (int pc = lane; pc <= l1 - l0; pc += 32) {
+        tma::mbar_expect(mbar, tma::PIECE_BYTES);
+        tma::load_piece(Hs + h0 + pc * CH, &p.tma.map, (int)(x0 + chunk_of(l0 + pc) * CH), mbar);
+      }
     }
+    __syncthreads();
+    if (tid == 0) tma::mbar_arrive(mbar);
+    KZ_SETUP_MARK(2);
+    tma::mbar_wait(mbar, 0);
+    // zero the antennas of the first / last piece outside the support (the copies pulled the neighbours' data)
+    for (int n = w; n < NL; n += W) {
+      const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
+      const int s = rowS[i], L = rowL[i];
+      for (int pc = 0; pc <= l1 - l0; pc += max(1, l1 - l0)) {
+        const int ant = chunk_of(l0 + pc) * CH + lane;
+        if (ant < s || ant >= s + L) Hs[h0 + pc * CH + lane] = make_float2(0.f, 0.f);
+      }
+    }
+  } else {
+    for (int n = w; n < NL; n += W) {
+      const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
+      const int s = rowS[i], L = rowL[i];
+      const T* src = heff + rvo[i];
+      for (int pc = 0; pc <= l1 - l0; ++pc) {
+        const int ant = chunk_of(l0 + pc) * CH + lane;
+        const bool in = ant >= s && ant < s + L;
+        cp_async8(Hs + h0 + pc * CH + lane, src + (in ? ant - s : 0), in);
+      }
+    }
+    KZ_SETUP_MARK(2);
+    cp_async_wait_all();
   }
-  KZ_SETUP_MARK(2);
-  cp_async_wait_all();
   KZ_SETUP_MARK(3);
   // per-chunk piece lists (ascending rows): all rows (lst) and, for vr-oahk, the O rows then the N rows
   // (olst / nlst share one array); one counting pass and one fill pass for all of them
@@ -1283,6 +1315,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   const int W = cands[pick].W, CL = cands[pick].CL, GG = cands[pick].G;
   const size_t smem = cands[pick].smem;
   CluArgs a;
+  heff_tma_encode(P, &a.tma);
   a.P = P;
   a.R = R;
   a.O = O;

@@ -45,7 +45,7 @@ def test_python_binding_lists_the_exports(libpath):
     from paper_2501_10689_b200 import _lib
     assert set(_lib.EXPORTS) == set(declared_functions())
     lb = _lib.lib()
-    assert lb.kz_abi_version() == _lib.ABI_VERSION == 7
+    assert lb.kz_abi_version() == _lib.ABI_VERSION == 8
 
 
 def test_library_is_sm100a(libpath):
