@@ -231,7 +231,7 @@ class Workload:
     """One config's step on this rank's systems: inputs resident in HBM, per step RZF + per scheme (solve +
     epilogue), chunked over `chunk` systems (bounded per-call outputs / workspaces)."""
 
-    def __init__(self, cfg, schemes, dtype, lo, hi, dev_id, chunk=0, device_inputs=False):
+    def __init__(self, cfg, schemes, dtype, lo, hi, dev_id, chunk=0, device_inputs=False, orth_groups=1, agg_cap=0):
         import paper_2501_10689_b200 as kz
         self.kz, self.cfg, self.schemes, self.dtype = kz, cfg, schemes, dtype
         self.lo, self.hi, self.B = lo, hi, hi - lo
@@ -243,11 +243,12 @@ class Workload:
             self.host = None
             self.dev = kz.DeviceBatch.from_drops(kz.generate_drops(cfg, seeds), dtype=dtype, device=dev_id)
         else:
-            self.host = kz.HostBatch.from_contiguous(kz.generate(cfg, seeds))
+            self.host = kz.HostBatch.from_contiguous(kz.generate(cfg, seeds), orth_groups=orth_groups, agg_cap=agg_cap)
             self.dev = self.host.to_device(dtype, device=dev_id)
         self.chunk = chunk if 0 < chunk < self.B else self.B
         self.sup = (self.dev.t["seg_len"].cpu().numpy().reshape(self.B, cfg.n_users))
         self.ws = {}
+        self.tma = {}  # per scheme: H_eff staged by TMA tensor copies in the last solve (kz_last_tma_staging)
 
     def coupled(self):
         if self.host is not None:
@@ -283,6 +284,7 @@ class Workload:
                                          workspace=self.ws.get(sc), system_base=self.lo + lo)
                 e1.record(stream)
                 self.ws[sc] = res.workspace
+                self.tma[sc] = res.tma_staging
                 ep = kz.epilogue(sub, res.v, v_ref=rz["v"], beta_ref=rz["beta"], rates=True, workspace=ews,
                                  gram_cached=gram)
                 ews, gram = ep["workspace"], ep["gram_form"]
@@ -424,13 +426,18 @@ def roofline(wl, per_scheme, iters_by_scheme=None):
                                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
 
 
-def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2e=True, chunk=4096):
+def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2e=True, chunk=4096, n_systems=0,
+                  schemes=None, orth_groups=1, agg_cap=0):
     """A BASELINE config other than the headline at its stated size on this GPU (N=1 sub-record)."""
     import torch
     import paper_2501_10689_b200 as kz
     cfg = kz.CONFIGS[name]
+    schemes = list(schemes or cfg.schemes)
+    B = n_systems or cfg.n_systems
     t0 = time.perf_counter()
-    wl = Workload(cfg, list(cfg.schemes), dtype, 0, cfg.n_systems, dev_id, chunk=chunk, device_inputs=True)
+    grouped = orth_groups > 1 or agg_cap > 0
+    wl = Workload(cfg, schemes, dtype, 0, B, dev_id, chunk=chunk, device_inputs=not grouped,
+                  orth_groups=orth_groups, agg_cap=agg_cap)
     torch.cuda.synchronize()
     prep_s = time.perf_counter() - t0
     # warm-up on one chunk (kernel / allocator init), then full device-timed steps
@@ -446,7 +453,8 @@ def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2
             flush.fill_(s & 0xFF)
             e0, e1 = _events()
             e0.record(stream)
-            wl.step(wl.dev, 2000 + s, events=per_scheme, collect=collect if s == steps - 1 else None, stream=stream)
+            n_launch = wl.step(wl.dev, 2000 + s, events=per_scheme, collect=collect if s == steps - 1 else None,
+                               stream=stream)
             e1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -457,22 +465,27 @@ def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2
     ms = float(np.mean(step_ms))
     rec = {"workload": (f"{name}: Nt={cfg.n_antennas} K={cfg.n_users} VR={cfg.vr_len[0]}"
                         f"{'' if cfg.vr_len[0] == cfg.vr_len[1] else '-' + str(cfg.vr_len[1])}, "
-                        f"{','.join(cfg.schemes)} x {wl.B} realizations, "
+                        f"{','.join(schemes)} x {wl.B} realizations, "
+                        + (f"{orth_groups} orthogonal groups, <= {agg_cap} hyperplanes per aggregated step, "
+                           if grouped else "")
                         + (f"residual tolerance {wl.tol} (solve_all semantics)" if wl.tol else f"T={cfg.n_iters}")
                         + ", RZF + solve + F/NMSE/sum-rate epilogue"),
-           "value": len(cfg.schemes) * wl.B / (ms / 1e3), "unit": UNIT, "dtype": "complex64" if dtype == "c64"
+           "value": len(schemes) * wl.B / (ms / 1e3), "unit": UNIT, "dtype": "complex64" if dtype == "c64"
            else "complex128", "steps": steps, "warmup": f"{max(1, warmup)} step(s) on the first {warm.B} systems",
            "ms_per_step": ms, "chunk_systems": wl.chunk, "solve_ms_per_step": per_step_solve,
            "mean_iters_per_rhs": {sc: float(t.double().mean()) for sc, t in iters.items()},
            "median_nmse": {sc: float(torch.cat(c["nmse"]).median()) for sc, c in collect.items()},
            "mean_sum_rate": {sc: float(torch.cat(c["sum_rate"]).mean()) for sc, c in collect.items()},
            "rhs_iterations_per_s": float(sum(float(t.double().sum()) for t in iters.values()) / (ms / 1e3)),
-           "roofline": roof, "clocks": clk.summary(), "inputs": "seeded drops -> kz_channel_synth / kz_partition "
-           f"on the device ({prep_s:.1f} s incl. host drop draws); L2: inputs larger than L2 (+256 MiB flush)"}
+           "roofline": roof, "clocks": clk.summary(),
+           "inputs": ("host packing (HostBatch.from_contiguous with the orthogonal groups)" if grouped else
+                      "seeded drops -> kz_channel_synth / kz_partition on the device")
+           + f" ({prep_s:.1f} s); L2 flushed between steps (256 MiB write)",
+           "gpu_launches_per_step": n_launch, "tma_staging": dict(wl.tma)}
     if do_e2e:
         try:
             e = e2e_run(wl, 1, 3000, stream, dev_id, warm_compute=False)
-            e["value"] = len(cfg.schemes) * wl.B / (e["ms_per_step"] / 1e3)
+            e["value"] = len(schemes) * wl.B / (e["ms_per_step"] / 1e3)
             e["unit"] = UNIT
             rec["e2e"] = e
         except RuntimeError as exc:  # pinned host memory for the whole input set not available
@@ -624,6 +637,12 @@ def main():
             for name in ("cfg3", "cfg4"):
                 configs[name] = config_record(name, dev_id, stream, flush, a.config_steps, 1,
                                               do_e2e=not a.no_e2e)
+            # BASELINE cfg3's own variant (orthogonal row groups + at most 8 hyperplanes per aggregated step;
+            # no reference counterpart, CPU restatement oracle/grouped.py) on the global-memory kernel, at a
+            # reduced batch (its many sequential sub-steps per iteration run there, ~12x the cluster kernel)
+            configs["cfg3_grouped"] = config_record("cfg3", dev_id, stream, flush, a.config_steps, 1,
+                                                    do_e2e=not a.no_e2e, n_systems=256, schemes=["vr-oahk-g"],
+                                                    orth_groups=4, agg_cap=8)
 
     if rank == 0:
         line = {
@@ -637,6 +656,7 @@ def main():
                        "parallelism": f"realizations sharded x{world} ({a.scaling} scaling)"},
             "rhs_iterations_per_s": rhs_iters,
             "per_scheme_launch_ms": avg,
+            "tma_staging": dict(wl.tma),
             "roofline": roof,
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "stats": stats, "complex128_oracle_mode": c128, "configs": configs,

@@ -287,6 +287,9 @@ int kz_ahk_step(const kz_problem* prob, int32_t system, void* col, void* coef, c
 /* Number of kernels the last kz_* call on this thread launched (benchmark
    bookkeeping for the gpu_launches count). */
 int32_t kz_last_launch_count(void);
+/* 1 if the last kz_solve on this thread staged H_eff into shared memory with TMA tensor copies (complex64
+   on-chip kernels with kz_problem.val_lo/val_hi set), else 0 (evidence for the staging path) */
+int32_t kz_last_tma_staging(void);
 
 const char* kz_last_error(void);
 int32_t kz_abi_version(void);

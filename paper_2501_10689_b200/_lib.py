@@ -110,7 +110,7 @@ def lib():
 
 
 EXPORTS = (
-    "kz_abi_version", "kz_last_error", "kz_last_launch_count",
+    "kz_abi_version", "kz_last_error", "kz_last_launch_count", "kz_last_tma_staging",
     "kz_solve_workspace_bytes", "kz_solve_workspace_bytes_for", "kz_solve_resid_offset", "kz_solve",
     "kz_rzf_workspace_bytes", "kz_rzf", "kz_epilogue_workspace_bytes", "kz_epilogue_uses_gram", "kz_epilogue",
     "kz_channel_synth", "kz_partition_counts", "kz_partition_fill",
@@ -122,6 +122,7 @@ def _declare(lb):
     lb.kz_abi_version.restype = C.c_int32
     lb.kz_last_error.restype = C.c_char_p
     lb.kz_last_launch_count.restype = C.c_int32
+    lb.kz_last_tma_staging.restype = C.c_int32
     lb.kz_solve_workspace_bytes.restype = C.c_size_t
     lb.kz_solve_workspace_bytes.argtypes = [C.POINTER(KzProblem), C.POINTER(KzStop)]
     lb.kz_solve_workspace_bytes_for.restype = C.c_size_t

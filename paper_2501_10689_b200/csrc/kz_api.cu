@@ -60,6 +60,7 @@ extern "C" {
 int32_t kz_abi_version(void) { return KZ_ABI_VERSION; }
 const char* kz_last_error(void) { return g_err.c_str(); }
 int32_t kz_last_launch_count(void) { return g_launches; }
+int32_t kz_last_tma_staging(void) { return g_last_tma; }
 
 size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop) {
   (void)stop;
@@ -92,6 +93,7 @@ size_t kz_solve_resid_offset(const kz_problem* prob) {
 int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng, kz_out* out,
              void* workspace, size_t workspace_bytes, int32_t resume, void* stream) {
   g_launches = 0;
+  g_last_tma = 0;
   int st = check_problem(prob);
   if (st) return st;
   if (scheme < KZ_URK || scheme > KZ_VR_OAHK_G) return fail(KZ_ERR_INVALID, "unknown scheme %d", (int)scheme);

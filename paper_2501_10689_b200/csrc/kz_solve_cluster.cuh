@@ -1256,6 +1256,7 @@ inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStre
     return 0;
   }
   if (g_dry_launch) return 1;
+  note_tma(a.tma);
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   if (a.mode == KZ_STOP_LOCKSTEP)
     kz_lockstep_finalize<<<(a.P.n_systems + 127) / 128, 128, 0, s>>>(a.tstop, groups, a.P.n_systems, a.O.n_outer,

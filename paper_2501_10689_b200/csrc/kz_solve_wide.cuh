@@ -970,6 +970,7 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
       cudaSuccess)
     return -1;
   if (g_dry_launch) return 1;
+  note_tma(a.tma);
   kz_wide_kernel<SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);

@@ -23,6 +23,9 @@
 
 namespace kz {
 
+// host: whether the last launch on this thread staged H_eff with TMA (kz_last_tma_staging)
+inline thread_local int g_last_tma = 0;
+
 struct HeffTma {
   CUtensorMap map;  // 64-byte aligned (CUtensorMap's own alignment)
   long long base;   // heff element that coordinate 0 addresses
@@ -66,6 +69,9 @@ inline void heff_tma_encode(const kz_problem& P, HeffTma* t) {
   t->base = base;
   t->ok = 1;
 }
+
+// host: called by the launchers right before a kernel launch
+inline void note_tma(const HeffTma& t) { g_last_tma = t.ok; }
 
 namespace tma {
 

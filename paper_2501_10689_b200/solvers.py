@@ -261,6 +261,7 @@ class BatchResult:
     n_checks: object = None
     workspace: object = None
     launches: int = 0
+    tma_staging: bool = False  # H_eff staged into shared memory by TMA tensor copies (kz_last_tma_staging)
 
     m: object = None          # (B, K rhs, Nt) final iterates when requested
 
@@ -403,6 +404,7 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
         _lib.check(lb.kz_solve(C.byref(dev.problem), _lib.SCHEME_IDS[scheme], C.byref(stop), C.byref(rg),
                                C.byref(out), workspace.data_ptr(), workspace.numel(), resume, sp))
         launches += lb.kz_last_launch_count()
+        res.tma_staging = bool(lb.kz_last_tma_staging())
         if not host:
             break
         pz = paused.cpu().numpy().astype(bool)

@@ -158,3 +158,24 @@ def test_run_precoding_batched_chunks_equal_unsplit():
                                  chunk_systems=7)
     for key in ("v", "nmse", "sum_rate", "beta"):
         assert torch.equal(a[key], b[key]), key
+
+
+def test_tma_staging_is_the_default_path():
+    """The complex64 on-chip kernels stage H_eff with TMA tensor copies (kz_last_tma_staging) and give the same
+    bits as the asynchronous-copy staging on a copy of the problem without the value range."""
+    import torch
+    kz = _kz()
+    ch = kz.generate("cfg2", range(6))
+    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
+    a = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20)
+    assert a.tma_staging
+    dev.problem.val_lo, dev.problem.val_hi = 0, 0  # unknown range: the non-TMA staging
+    b = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=20)
+    assert not b.tma_staging and torch.equal(a.v, b.v)
+    big = kz.generate(kz.NearFieldConfig("t_tma", 1024, 40, (96, 400)), range(2))
+    dv = kz.HostBatch.from_contiguous(big).to_device("c64")
+    c = kz.solve_batch(dv, "grk", mode="lockstep", max_iters=10, rng=("philox", 1))
+    assert c.tma_staging  # cluster kernel
+    dv.problem.val_lo, dv.problem.val_hi = 0, 0
+    d = kz.solve_batch(dv, "grk", mode="lockstep", max_iters=10, rng=("philox", 1))
+    assert torch.equal(c.v, d.v)
