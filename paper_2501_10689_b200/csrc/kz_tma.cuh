@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -57,15 +58,21 @@ inline void heff_tma_encode(const kz_problem& P, HeffTma* t) {
   if (n + 64 >= (1LL << 31)) return;  // coordinates are signed 32-bit
   void* addr = (char*)P.heff + base * 8;
   if (((uintptr_t)addr & 15) != 0) return;
+  static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
   auto fn = tma_encode_fn();
-  if (!fn) return;
+  if (!fn) {
+    if (verbose) fprintf(stderr, "[kz tma] cuTensorMapEncodeTiled entry point unavailable\n");
+    return;
+  }
   cuuint64_t dim[1] = {(cuuint64_t)n};
+  cuuint64_t stride[1] = {(cuuint64_t)n * 8};
   cuuint32_t box[1] = {32};
   cuuint32_t es[1] = {1};
-  if (fn(&t->map, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, addr, dim, nullptr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return;
+  const CUresult r = fn(&t->map, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, addr, dim, stride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (verbose) fprintf(stderr, "[kz tma] encode n=%lld base=%lld -> %d\n", n, base, (int)r);
+  if (r != CUDA_SUCCESS) return;
   t->base = base;
   t->ok = 1;
 }
