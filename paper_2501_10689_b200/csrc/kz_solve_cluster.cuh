@@ -136,6 +136,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
   p.olst = o; o = al(o + (oahk ? 8 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
   p.nlst = p.olst;
+  o = (o + 127) & ~size_t(127);  // tensor-copy destinations are 128-byte aligned (pieces are 256 B)
   p.H = o; o = al(o + 8 * (size_t)pcap * CH);
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Ro = o; o = al(o + (greedy ? 8 * (size_t)p.KO * G : 0));
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
   constexpr bool GREEDY = SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK;
 
-  extern __shared__ __align__(16) unsigned char sm[];
+  extern __shared__ __align__(128) unsigned char sm[];
   const int K = p.P.n_users, Nt = p.P.n_antennas;
   const int CL = (int)cluster_ctas(), c = (int)cta_rank();
   const int ngroups = (K + G - 1) / G;
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
   // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
   // no dependent global load, no load latency per piece)
-  if (p.tma.ok) {
+  if (p.tma.ok && (tma::saddr(Hs) & 127) == 0) {
     // TMA: one 1-D tensor copy per (row, chunk) piece, lanes over the pieces of a local row; the mbarrier
     // expects every issuing thread's bytes before its single arrival (thread 0, after a barrier)
     uint64_t* mbar = (uint64_t*)(sm + pl.mbar);

@@ -38,7 +38,7 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 struct Plan {
   int K, W, SL, hcap;
   size_t rowS, rowL, c0, c1, hoff, en, inv_en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
-      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, total;
+      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -86,7 +86,6 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.pool = o; o = al(o + 4 * (size_t)G * KW);
   p.poolcnt = o; o = al(o + 4 * G);
   p.misc = o; o = al(o + 32);
-  p.mbar = o; o = al(o + 8);
   p.total = o;
   return p;
 }
@@ -232,32 +231,8 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     if (w == 0) tmem::alloc(misc, 256);
     tmem::fence_before();
   }
-  // rows -> shared memory, zero padded to whole chunks
-  if (p.tma.ok) {
-    // TMA (kz_tma.cuh): one 1-D tensor copy per (row, chunk) piece, warps over rows, lanes over its pieces; the
-    // mbarrier expects every issuing thread's bytes before thread 0's single arrival (after a barrier)
-    uint64_t* mbar = (uint64_t*)(sm + pl.mbar);
-    if (tid == 0) tma::mbar_init(mbar, 1);
-    __syncthreads();
-    for (int i = w; i < K; i += W) {
-      const long long x0 = p.P.row_val_ptr[(size_t)b * K + i] - rowS[i] - p.tma.base;  // coordinate of antenna 0
-      for (int pc = lane; pc <= c1[i] - c0[i]; pc += 32) {
-        tma::mbar_expect(mbar, tma::PIECE_BYTES);
-        tma::load_piece(Hs + hoff[i] + pc * CH, &p.tma.map, (int)(x0 + (c0[i] + pc) * CH), mbar);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) tma::mbar_arrive(mbar);
-    tma::mbar_wait(mbar, 0);
-    // zero the first / last piece's antennas outside the support (the copies pulled the neighbouring rows')
-    for (int i = w; i < K; i += W) {
-      const int np = c1[i] - c0[i];
-      for (int pc = 0; pc <= np; pc += max(1, np)) {
-        const int ant = (c0[i] + pc) * CH + lane;
-        if (ant < rowS[i] || ant >= rowS[i] + rowL[i]) Hs[hoff[i] + pc * CH + lane] = make_float2(0.f, 0.f);
-      }
-    }
-  } else {  // flat parallel copy
+  // rows -> shared memory, zero padded to whole chunks (flat parallel copy)
+  {
     const int total = hoff[K - 1] + (c1[K - 1] - c0[K - 1] + 1) * CH;
     for (int e = tid; e < total; e += nthr) {
       // row of element e: last i with hoff[i] <= e (binary search)
@@ -964,7 +939,9 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
   a.ws = ws;
   a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
   a.tstop = tstop;
-  heff_tma_encode(P, &a.tma);
+  // no TMA here: the rows' bank-skewed shared-memory bases (2 (i & 3) elements, for the projection gathers) are
+  // 16-byte aligned, tensor copies need 128-byte aligned destinations; setup staging is ~1% of a launch
+  a.tma.ok = 0;
   const int groups = (P.n_users + wide::G - 1) / wide::G;
   if (cudaFuncSetAttribute(kz_wide_kernel<SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
