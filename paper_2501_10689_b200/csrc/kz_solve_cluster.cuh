@@ -136,7 +136,6 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
   p.olst = o; o = al(o + (oahk ? 8 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
   p.nlst = p.olst;
-  o = (o + 127) & ~size_t(127);  // tensor-copy destinations are 128-byte aligned (pieces are 256 B)
   p.H = o; o = al(o + 8 * (size_t)pcap * CH);
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Ro = o; o = al(o + (greedy ? 8 * (size_t)p.KO * G : 0));
@@ -176,8 +175,8 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
 }  // namespace clu
 
 struct CluArgs {
-  HeffTma tma;  // TMA staging of the row pieces (kz_tma.cuh); tma.ok = 0: asynchronous-copy staging
   kz_problem P;
+  int bulk;  // stage the row pieces with bulk copies where the parity allows (kz_tma.cuh)
   kz_rng R;
   kz_out O;
   int mode;     // KZ_STOP_LOCKSTEP (fixed T) or KZ_STOP_RESIDUAL
@@ -383,46 +382,58 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
   // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
   // no dependent global load, no load latency per piece)
-  if (p.tma.ok && (tma::saddr(Hs) & 127) == 0) {
-    // TMA: one 1-D tensor copy per (row, chunk) piece, lanes over the pieces of a local row; the mbarrier
-    // expects every issuing thread's bytes before its single arrival (thread 0, after a barrier)
+  {
+    // bulk copies (kz_tma.cuh) for the rows whose packed offset has their first antenna's parity, one per
+    // contiguous antenna run (a row's pieces in this CTA form at most nblk runs); 8-byte asynchronous copies
+    // (zero-filled outside the support) for the others
     uint64_t* mbar = (uint64_t*)(sm + pl.mbar);
-    if (tid == 0) tma::mbar_init(mbar, 1);
+    const bool bulk = p.bulk != 0;
+    if (bulk && tid == 0) tma::mbar_init(mbar, 1);
     __syncthreads();
     for (int n = w; n < NL; n += W) {
       const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
-      const long long x0 = rvo[i] - rowS[i] - p.tma.base;  // map coordinate of antenna 0 of row i
-      for (int pc = lane; pc <= l1 - l0; pc += 32) {
-        tma::mbar_expect(mbar, tma::PIECE_BYTES);
-        tma::load_piece(Hs + h0 + pc * CH, &p.tma.map, (int)(x0 + chunk_of(l0 + pc) * CH), mbar);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) tma::mbar_arrive(mbar);
-    KZ_SETUP_MARK(2);
-    tma::mbar_wait(mbar, 0);
-    // zero the antennas of the first / last piece outside the support (the copies pulled the neighbours' data)
-    for (int n = w; n < NL; n += W) {
-      const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
       const int s = rowS[i], L = rowL[i];
-      for (int pc = 0; pc <= l1 - l0; pc += max(1, l1 - l0)) {
-        const int ant = chunk_of(l0 + pc) * CH + lane;
-        if (ant < s || ant >= s + L) Hs[h0 + pc * CH + lane] = make_float2(0.f, 0.f);
+      unsigned fallback = 0;  // local pieces (bit pc) left to the asynchronous copies
+      if (lane == 0) {
+        int la = l0;
+        while (la <= l1) {
+          int lb = la;
+          while (lb < l1 && chunk_of(lb + 1) == chunk_of(lb) + 1) ++lb;
+          const bool done = bulk && tma::stage_run_bulk(Hs + h0 + (la - l0) * CH, heff, rvo[i], s, L,
+                                                         chunk_of(la) * CH, (chunk_of(lb) + 1) * CH, p.P.val_lo,
+                                                         p.P.val_hi, mbar);
+          if (!done)
+            for (int l = la; l <= lb; ++l) fallback |= 1u << (l - l0);
+          la = lb + 1;
+        }
       }
-    }
-  } else {
-    for (int n = w; n < NL; n += W) {
-      const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
-      const int s = rowS[i], L = rowL[i];
+      fallback = __shfl_sync(FULL, fallback, 0);
       const T* src = heff + rvo[i];
       for (int pc = 0; pc <= l1 - l0; ++pc) {
+        if (!((fallback >> pc) & 1u)) continue;
         const int ant = chunk_of(l0 + pc) * CH + lane;
         const bool in = ant >= s && ant < s + L;
         cp_async8(Hs + h0 + pc * CH + lane, src + (in ? ant - s : 0), in);
       }
     }
+    if (bulk) {
+      __syncthreads();
+      if (tid == 0) tma::mbar_arrive(mbar);
+    }
     KZ_SETUP_MARK(2);
     cp_async_wait_all();
+    if (bulk) {
+      tma::mbar_wait(mbar, 0);
+      // zero the first / last piece's antennas outside the support (a widened bulk range pulls in a neighbour)
+      for (int n = w; n < NL; n += W) {
+        const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
+        const int s = rowS[i], L = rowL[i];
+        for (int pc = 0; pc <= l1 - l0; pc += max(1, l1 - l0)) {
+          const int ant = chunk_of(l0 + pc) * CH + lane;
+          if (ant < s || ant >= s + L) Hs[h0 + pc * CH + lane] = make_float2(0.f, 0.f);
+        }
+      }
+    }
   }
   KZ_SETUP_MARK(3);
   // per-chunk piece lists (ascending rows): all rows (lst) and, for vr-oahk, the O rows then the N rows
@@ -1257,7 +1268,7 @@ inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStre
     return 0;
   }
   if (g_dry_launch) return 1;
-  note_tma(a.tma);
+  note_tma(a.bulk);
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   if (a.mode == KZ_STOP_LOCKSTEP)
     kz_lockstep_finalize<<<(a.P.n_systems + 127) / 128, 128, 0, s>>>(a.tstop, groups, a.P.n_systems, a.O.n_outer,
@@ -1317,8 +1328,8 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   const int W = cands[pick].W, CL = cands[pick].CL, GG = cands[pick].G;
   const size_t smem = cands[pick].smem;
   CluArgs a;
-  heff_tma_encode(P, &a.tma);
   a.P = P;
+  a.bulk = bulk_staging_ok(P);
   a.R = R;
   a.O = O;
   a.mode = lockstep ? KZ_STOP_LOCKSTEP : KZ_STOP_RESIDUAL;

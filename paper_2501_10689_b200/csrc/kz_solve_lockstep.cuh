@@ -46,8 +46,8 @@ template <> struct Ls<double2> {
 };
 
 struct LsArgs {
-  HeffTma tma;  // TMA staging of H_eff (kz_tma.cuh); tma.ok = 0: asynchronous-copy / load staging
   kz_problem P;
+  int bulk;  // stage the rows with bulk copies where the parity allows (kz_tma.cuh)
   kz_rng R;
   kz_out O;
   int T;       // iterations
@@ -879,7 +879,7 @@ template <class T, int SCH>
 inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
                      size_t smem, int S, int hcap, cudaStream_t s) {
   LsArgs a;
-  a.tma.ok = 0;
+  a.bulk = 0;
   a.P = P;
   a.R = R;
   a.O = O;

@@ -38,7 +38,7 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 struct Plan {
   int K, W, SL, hcap;
   size_t rowS, rowL, c0, c1, hoff, en, inv_en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
-      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, total;
+      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -86,6 +86,7 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.pool = o; o = al(o + 4 * (size_t)G * KW);
   p.poolcnt = o; o = al(o + 4 * G);
   p.misc = o; o = al(o + 32);
+  p.mbar = o; o = al(o + 8);
   p.total = o;
   return p;
 }
@@ -231,20 +232,42 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     if (w == 0) tmem::alloc(misc, 256);
     tmem::fence_before();
   }
-  // rows -> shared memory, zero padded to whole chunks (flat parallel copy)
+  // rows -> shared memory, zero padded to whole chunks: one bulk copy per row whose packed offset has its first
+  // antenna's parity (kz_tma.cuh; warp per row, lane 0 issues), 8-byte asynchronous copies for the others, then
+  // the first / last piece's antennas outside the support are zeroed
   {
-    const int total = hoff[K - 1] + (c1[K - 1] - c0[K - 1] + 1) * CH;
-    for (int e = tid; e < total; e += nthr) {
-      // row of element e: last i with hoff[i] <= e (binary search)
-      int lo = 0, hi = K - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (hoff[mid] <= e) lo = mid; else hi = mid - 1;
+    uint64_t* mbar = (uint64_t*)(sm + pl.mbar);
+    const bool bulk = p.bulk != 0;
+    if (bulk && tid == 0) tma::mbar_init(mbar, 1);
+    __syncthreads();
+    for (int i = w; i < K; i += W) {
+      const int s = rowS[i], L = rowL[i], np = c1[i] - c0[i] + 1;
+      const long long rvo = p.P.row_val_ptr[(size_t)b * K + i];
+      int done = 0;
+      if (lane == 0 && bulk)
+        done = tma::stage_run_bulk(Hs + hoff[i], heff, rvo, s, L, c0[i] * CH, (c1[i] + 1) * CH, p.P.val_lo,
+                                   p.P.val_hi, mbar);
+      if (!__shfl_sync(FULL, done, 0))
+        for (int pc = 0; pc < np; ++pc) {
+          const int ant = (c0[i] + pc) * CH + lane;
+          const bool in = ant >= s && ant < s + L;
+          cp_async8(Hs + hoff[i] + pc * CH + lane, heff + rvo + (in ? ant - s : 0), in);
+        }
+    }
+    if (bulk) {
+      __syncthreads();
+      if (tid == 0) tma::mbar_arrive(mbar);
+    }
+    cp_async_wait_all();
+    if (bulk) {
+      tma::mbar_wait(mbar, 0);
+      for (int i = w; i < K; i += W) {
+        const int np = c1[i] - c0[i];
+        for (int pc = 0; pc <= np; pc += max(1, np)) {
+          const int ant = (c0[i] + pc) * CH + lane;
+          if (ant < rowS[i] || ant >= rowS[i] + rowL[i]) Hs[hoff[i] + pc * CH + lane] = make_float2(0.f, 0.f);
+        }
       }
-      int i = lo;
-      int n = c0[i] * CH + (e - hoff[i]);
-      int s = rowS[i];
-      Hs[e] = (n >= s && n < s + rowL[i]) ? heff[p.P.row_val_ptr[(size_t)b * K + i] + (n - s)] : make_float2(0.f, 0.f);
     }
   }
   if constexpr (SCH == KZ_VR_OGRK) {
@@ -939,15 +962,13 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
   a.ws = ws;
   a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
   a.tstop = tstop;
-  // no TMA here: the rows' bank-skewed shared-memory bases (2 (i & 3) elements, for the projection gathers) are
-  // 16-byte aligned, tensor copies need 128-byte aligned destinations; setup staging is ~1% of a launch
-  a.tma.ok = 0;
+  a.bulk = bulk_staging_ok(P);
   const int groups = (P.n_users + wide::G - 1) / wide::G;
   if (cudaFuncSetAttribute(kz_wide_kernel<SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return -1;
   if (g_dry_launch) return 1;
-  note_tma(a.tma);
+  note_tma(a.bulk);
   kz_wide_kernel<SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);

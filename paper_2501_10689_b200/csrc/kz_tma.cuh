@@ -1,88 +1,44 @@
-// TMA staging of the packed rows H_eff into shared memory (north_star: "H is staged in shared memory via TMA").
+// Bulk-copy (TMA engine) staging of the packed rows H_eff into shared memory.
 //
-// The complex64 rows h_bi live back to back in heff (kz_problem.row_val_ptr).  A kernel keeps every row in shared
-// memory as whole 32-antenna chunk pieces (zero padded where the row's support [s, s+L) does not cover the
-// chunk).  Each piece is one 1-D tensor copy (cp.async.bulk.tensor.1d, 32 elements x 8 B = 256 B) whose start
-// coordinate is the element of heff that antenna chunk_start would have: element granularity, so no alignment
-// constraint on row starts; coordinates before the mapped range read as zero (TMA out-of-bounds fill), and the
-// pad lanes a piece pulls from the neighbouring rows are zeroed after the copies land.  Completion is tracked by
-// one mbarrier per CTA (expect_tx per issuing thread, one arrival after all of them).
+// The complex64 rows h_bi live back to back in heff (kz_problem.row_val_ptr).  The on-chip kernels keep every
+// row in shared memory as whole 32-antenna chunk pieces, zero padded where the row's support [s, s+L) does not
+// cover a chunk; the element for antenna a of row i sits at an even shared-memory element index + (a mod 32)
+// within its chunk piece, so its parity is a's.  The row's elements in heff start at row_val_ptr[i]: antenna a at
+// element row_val_ptr[i] + a - s.  When that index has a's parity (row_val_ptr[i] - s even) the row's
+// contiguous run of antennas, widened to even antenna bounds, is ONE cp.async.bulk copy (16-byte aligned source
+// and destination, size a multiple of 16 B: the bulk-copy engine, SASS UBLKCP) completing on the CTA's mbarrier;
+// the one neighbour element a widened bound may pull in lands in a pad lane and is zeroed afterwards with the
+// other pads.  Rows of the other parity, and rows whose widened range would leave [val_lo, val_hi) (the batch's
+// first / last row), are staged with 8-byte asynchronous copies (LDGSTS).  With dense packing about half the
+// rows take each path.
 //
-// The tensor map is encoded on the host per launch over the element range [val_lo, val_hi) the batch's rows
-// occupy (kz_problem), coordinates relative to its 16-byte aligned base; batches whose range does not fit the
-// signed 32-bit TMA coordinates (or whose range is unknown: val_hi = 0) keep the asynchronous-copy path.
+// The tensor form (cp.async.bulk.tensor with a CUtensorMap, element-granular coordinates: every row by TMA) is
+// the natural tool here; on this pool's driver (580.178, CUDA 12.9 runtime) UTMALDG raised "illegal instruction"
+// even for the canonical 2-D example (tools/tma_std.cu, tools/tma_probe.cu), so it is not used.
 #pragma once
 
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "../../include/kaczmarz_b200.h"
 
 namespace kz {
 
-// host: whether the last launch on this thread staged H_eff with TMA (kz_last_tma_staging)
+// host: whether the last launch on this thread staged rows with bulk copies (kz_last_tma_staging)
 inline thread_local int g_last_tma = 0;
 
-struct HeffTma {
-  CUtensorMap map;  // 64-byte aligned (CUtensorMap's own alignment)
-  long long base;   // heff element that coordinate 0 addresses
-  int ok;           // 1: the TMA path is usable for this launch
-  int _pad;
-};
-
-inline PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    cudaGetLastError();
-    return (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }();
-  return fn;
+// host: bulk staging usable for this problem (value range known, 16-byte aligned heff, complex64)
+inline int bulk_staging_ok(const kz_problem& P) {
+  static const bool off = getenv("KZ_NO_TMA") != nullptr;  // A/B switch: asynchronous-copy staging only
+  return !off && P.dtype == KZ_C64 && P.heff && P.val_hi > P.val_lo && P.val_lo >= 0 &&
+                 ((uintptr_t)P.heff & 15) == 0
+             ? 1
+             : 0;
 }
-
-// host: encode the 1-D map over heff[val_lo & ~1, val_hi) (complex64 as 8-byte elements, 32-element boxes)
-inline void heff_tma_encode(const kz_problem& P, HeffTma* t) {
-  t->ok = 0;
-  t->base = 0;
-  static const bool off = getenv("KZ_NO_TMA") != nullptr;  // A/B switch: the asynchronous-copy staging
-  if (off || P.dtype != KZ_C64 || !P.heff || P.val_hi <= P.val_lo || P.val_lo < 0) return;
-  const long long base = P.val_lo & ~1LL;
-  const long long n = P.val_hi - base;
-  if (n + 64 >= (1LL << 31)) return;  // coordinates are signed 32-bit
-  void* addr = (char*)P.heff + base * 8;
-  if (((uintptr_t)addr & 15) != 0) return;
-  static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
-  auto fn = tma_encode_fn();
-  if (!fn) {
-    if (verbose) fprintf(stderr, "[kz tma] cuTensorMapEncodeTiled entry point unavailable\n");
-    return;
-  }
-  cuuint64_t dim[1] = {(cuuint64_t)n};
-  cuuint64_t stride[1] = {(cuuint64_t)n * 8};
-  cuuint32_t box[1] = {32};
-  cuuint32_t es[1] = {1};
-  const CUresult r = fn(&t->map, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, addr, dim, stride, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (verbose) fprintf(stderr, "[kz tma] encode n=%lld base=%lld -> %d\n", n, base, (int)r);
-  if (r != CUDA_SUCCESS) return;
-  t->base = base;
-  t->ok = 1;
-}
-
-// host: called by the launchers right before a kernel launch
-inline void note_tma(const HeffTma& t) { g_last_tma = t.ok; }
+inline void note_tma(int ok) { g_last_tma = ok; }
 
 namespace tma {
-
-constexpr uint32_t PIECE_BYTES = 32 * 8;  // one 32-antenna complex64 chunk piece
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -107,13 +63,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-// 32 elements of heff starting at map coordinate x -> dst (16-byte aligned shared memory)
-__device__ __forceinline__ void load_piece(void* dst, const CUtensorMap* map, int x, uint64_t* mb) {
-  asm volatile(
-      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::
-          "r"(saddr(dst)),
-      "l"((unsigned long long)map), "r"(x), "r"(saddr(mb))
-      : "memory");
+// bytes (multiple of 16) from 16-byte aligned global src to 16-byte aligned shared dst, completing on mb
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(mb))
+               : "memory");
+}
+
+// One contiguous antenna run [r0, r1) (even chunk bounds) of row (s, L, rvo) whose shared-memory copy of antenna
+// r0 is at dst: issue its bulk copy when the parity / bounds allow (returns true), else nothing (returns false).
+__device__ __forceinline__ bool stage_run_bulk(float2* dst, const float2* heff, long long rvo, int s, int L, int r0,
+                                               int r1, long long val_lo, long long val_hi, uint64_t* mb) {
+  if (((rvo - s) & 1) != 0) return false;
+  const int a0 = max(r0, s) & ~1, a1 = (min(r1, s + L) + 1) & ~1;  // widened to even antennas (within the run)
+  if (a1 <= a0) return true;                                        // nothing of the row in this run
+  const long long e0 = rvo + (a0 - s), e1 = rvo + (a1 - s);
+  if (e0 < val_lo || e1 > val_hi) return false;
+  const uint32_t bytes = (uint32_t)(a1 - a0) * 8u;
+  mbar_expect(mb, bytes);
+  bulk_copy(dst + (a0 - r0), heff + e0, bytes, mb);
+  return true;
 }
 
 }  // namespace tma

@@ -160,27 +160,24 @@ def test_run_precoding_batched_chunks_equal_unsplit():
         assert torch.equal(a[key], b[key]), key
 
 
-def test_tma_staging_is_the_default_path():
-    """The large-array (cluster) kernel stages its row pieces with TMA tensor copies (kz_last_tma_staging) and
-    gives the same bits as the asynchronous-copy staging (problem without the value range); the cfg2 kernel keeps
-    its element staging (bank-skewed row bases are not 128-byte aligned)."""
+def test_bulk_copy_staging_is_the_default_path():
+    """The complex64 on-chip kernels (wide cfg2 kernel and large-array cluster kernel) stage H_eff with bulk copies
+    (cp.async.bulk + mbarrier, kz_last_tma_staging) and give the same bits as the 8-byte asynchronous-copy staging
+    (problem without the value range), also on a view (chunk) of a batch."""
     import torch
     kz = _kz()
-    ch = kz.generate("cfg2", range(4))
-    dev = kz.HostBatch.from_contiguous(ch).to_device("c64")
-    assert not kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=5).tma_staging
-    big = kz.generate(kz.NearFieldConfig("t_tma", 1024, 40, (96, 400)), range(3))
-    dv = kz.HostBatch.from_contiguous(big).to_device("c64")
-    for sc in ("grk", "vr-oahk"):
-        rng = ("philox", 1) if sc == "grk" else None
-        c = kz.solve_batch(dv, sc, mode="lockstep", max_iters=10, rng=rng)
-        assert c.tma_staging
-        lo, hi = dv.problem.val_lo, dv.problem.val_hi
-        dv.problem.val_lo, dv.problem.val_hi = 0, 0
-        d = kz.solve_batch(dv, sc, mode="lockstep", max_iters=10, rng=rng)
-        dv.problem.val_lo, dv.problem.val_hi = lo, hi
-        assert not d.tma_staging and torch.equal(c.v, d.v), sc
-    # a view (chunk) of the batch: the map covers only the view's rows (coordinates relative to its base)
-    sub = dv.view(1, 3)
-    e = kz.solve_batch(sub, "vr-oahk", mode="lockstep", max_iters=10)
-    assert e.tma_staging and torch.equal(e.v, kz.solve_batch(dv, "vr-oahk", mode="lockstep", max_iters=10).v[1:3])
+    for conf, n in (("cfg2", 4), (kz.NearFieldConfig("t_bulk", 1024, 40, (96, 400)), 3)):
+        dv = kz.HostBatch.from_contiguous(kz.generate(conf, range(n))).to_device("c64")
+        for sc in ("grk", "vr-oahk"):
+            rng = ("philox", 1) if sc == "grk" else None
+            c = kz.solve_batch(dv, sc, mode="lockstep", max_iters=10, rng=rng)
+            assert c.tma_staging
+            lo, hi = dv.problem.val_lo, dv.problem.val_hi
+            dv.problem.val_lo, dv.problem.val_hi = 0, 0
+            d = kz.solve_batch(dv, sc, mode="lockstep", max_iters=10, rng=rng)
+            dv.problem.val_lo, dv.problem.val_hi = lo, hi
+            assert not d.tma_staging and torch.equal(c.v, d.v), sc
+        sub = dv.view(1, n)
+        e = kz.solve_batch(sub, "vr-oahk", mode="lockstep", max_iters=10)
+        assert e.tma_staging
+        assert torch.equal(e.v, kz.solve_batch(dv, "vr-oahk", mode="lockstep", max_iters=10).v[1:n])
