@@ -393,21 +393,25 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
     for (int n = w; n < NL; n += W) {
       const int i = lrow[n], l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8, h0 = lh[n];
       const int s = rowS[i], L = rowL[i];
-      unsigned fallback = 0;  // local pieces (bit pc) left to the asynchronous copies
-      if (lane == 0) {
-        int la = l0;
-        while (la <= l1) {
-          int lb = la;
-          while (lb < l1 && chunk_of(lb + 1) == chunk_of(lb) + 1) ++lb;
-          const bool done = bulk && tma::stage_run_bulk(Hs + h0 + (la - l0) * CH, heff, rvo[i], s, L,
-                                                         chunk_of(la) * CH, (chunk_of(lb) + 1) * CH, p.P.val_lo,
-                                                         p.P.val_hi, mbar);
-          if (!done)
-            for (int l = la; l <= lb; ++l) fallback |= 1u << (l - l0);
-          la = lb + 1;
+      // the row's local pieces split into runs at the slice-block boundaries (multiples of Bc local chunks);
+      // within a block the chunks are consecutive, so a run is one contiguous antenna range: lane j, run j
+      unsigned fallback = ~0u;  // local pieces (bit pc) left to the asynchronous copies
+      if (bulk) {
+        bool done = true;
+        const int j = l0 / Bc + lane;
+        if (j <= l1 / Bc) {
+          const int la = max(l0, j * Bc), lb = min(l1, j * Bc + Bc - 1);
+          done = tma::stage_run_bulk(Hs + h0 + (la - l0) * CH, heff, rvo[i], s, L, chunk_of(la) * CH,
+                                     (chunk_of(lb) + 1) * CH, p.P.val_lo, p.P.val_hi, mbar);
         }
+        const unsigned fb = __ballot_sync(FULL, !done);  // runs that fell back
+        fallback = 0;
+        for (int jj = 0; jj <= l1 / Bc - l0 / Bc; ++jj)
+          if ((fb >> jj) & 1u) {
+            const int jb = l0 / Bc + jj, la = max(l0, jb * Bc), lb = min(l1, jb * Bc + Bc - 1);
+            fallback |= ((lb - la + 1 >= 32) ? ~0u : ((1u << (lb - la + 1)) - 1u)) << (la - l0);
+          }
       }
-      fallback = __shfl_sync(FULL, fallback, 0);
       const T* src = heff + rvo[i];
       for (int pc = 0; pc <= l1 - l0; ++pc) {
         if (!((fallback >> pc) & 1u)) continue;
