@@ -23,12 +23,21 @@
 #include "kz_solve_generic.cuh"
 #include "kz_tmem.cuh"
 
+// per-scheme switches (bit = kz_scheme), measured with same-box A/B runs (tools/ab3.sh)
+#ifndef KZ_WIDE_HALF_MASK
+#define KZ_WIDE_HALF_MASK ((1 << KZ_GK) | (1 << KZ_GRK) | (1 << KZ_VR_OGRK) | (1 << KZ_VR_OAHK))
+#endif
+#ifndef KZ_WIDE_PARW_MASK
+#define KZ_WIDE_PARW_MASK (1 << KZ_VR_OAHK)
+#endif
+
 namespace kz {
 
 namespace wide {
 
 constexpr int G = 32;
 constexpr int CH = 32;  // chunk = antennas per warp
+template <int A, int B> struct JRange { static constexpr int lo = A, hi = B; };
 constexpr int HSKEW = 6;  // spare H elements per row for the bank skew of the row bases
 // [row][rhs] arrays (P slots, Q, R) are XOR-swizzled on the rhs index so that
 // both access directions (lanes over rhs: refresh / projection; lanes over
@@ -38,7 +47,7 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 struct Plan {
   int K, W, SL, hcap;
   size_t rowS, rowL, c0, c1, hoff, en, inv_en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
-      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, total;
+      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, WP, lspl, ospl, nspl, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -87,6 +96,16 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.poolcnt = o; o = al(o + 4 * G);
   p.misc = o; o = al(o + 32);
   p.mbar = o; o = al(o + 8);
+  p.lspl = o; o = al(o + 8 * (size_t)p.W);
+  p.ospl = o; o = al(o + 8 * (size_t)p.W);
+  p.nspl = o; o = al(o + 8 * (size_t)p.W);
+  // per-warp weight partials of the aggregation schemes ([warp][rhs]: num float2, ||phi||^2, nonzero flag); they
+  // live in R (unused by AHK / VR-OAHK) when it is large enough
+  if ((size_t)K * G * 8 >= (size_t)p.W * G * 16) {
+    p.WP = p.R;
+  } else {
+    p.WP = o; o = al(o + 16 * (size_t)p.W * G);
+  }
   p.total = o;
   return p;
 }
@@ -99,6 +118,10 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   using T = float2;
   constexpr bool PER_LANE_ROW = SCH == KZ_URK || SCH == KZ_SWOR_ERK;
   constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
+  // measured per scheme (same-box A/B, tools/ab3.sh): half pieces in their own list segments, and the aggregation
+  // weights formed by the whole CTA (PAR_W) instead of one half-warp per rhs
+  constexpr bool HALF = (KZ_WIDE_HALF_MASK >> SCH) & 1;
+  constexpr bool PAR_W = AGG && ((KZ_WIDE_PARW_MASK >> SCH) & 1);
 
   extern __shared__ __align__(16) unsigned char sm[];
   const int K = p.P.n_users, Nt = p.P.n_antennas;
@@ -188,15 +211,25 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     for (int q = p.P.non_ptr[b] + tid; q < p.P.non_ptr[b + 1]; q += nthr) inset[p.P.non_idx[q]] = 2;
   }
   __syncthreads();
-  // per-chunk row lists (all rows / O / N), ascending rows: warp w compacts with ballots.
-  // entry = (h element offset of this chunk | row << 20,
-  //          P offset of (row, slot) | (row & 15) | half-chunk mask << 28)
-  auto build_list = [&](int* ptr, int2* out, int which) {
-    int n = 0;
+  // per-chunk row lists (all rows / O / N): warp w compacts with ballots, in three segments of ascending rows --
+  // the pieces whose support covers both 16-antenna halves of the chunk, then those touching only the first half,
+  // then only the second half (spl[2 w], spl[2 w + 1]: segment starts): a half piece needs half the loads and FMAs
+  // (the other half of the chunk is zero padding), and a row of L = 128 at a random start has one of its 4-5 pieces
+  // in that case.  entry = (h element offset of this chunk | row << 20,
+  //                          P offset of (row, slot) | (row & 15) | half-chunk mask << 28)
+  auto build_list = [&](int* ptr, int* spl, int2* out, int which) {
+    auto half_mask = [&](int i) {  // which 16-antenna halves of this chunk the row's support touches
+      const int lo = rowS[i] - w * CH, hi = rowS[i] + rowL[i] - w * CH;
+      return (lo < 16 && hi > 0 ? 1 : 0) | (lo < 32 && hi > 16 ? 2 : 0);
+    };
+    int n = 0, nf = 0, nl = 0;
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
       bool ov = i < K && c0[i] <= w && w <= c1[i] && (which == 0 || inset[i] == which);
+      const int hm = ov ? half_mask(i) : 0;
       n += __popc(__ballot_sync(FULL, ov));
+      nf += __popc(__ballot_sync(FULL, ov && (hm == 3 || !HALF)));
+      nl += __popc(__ballot_sync(FULL, ov && hm == 1 && HALF));
     }
     if (lane == 0) ptr[w + 1] = n;
     __syncthreads();
@@ -205,27 +238,36 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       for (int ww = 0; ww < W; ++ww) ptr[ww + 1] += ptr[ww];
     }
     __syncthreads();
-    n = ptr[w];
+    int q[3] = {ptr[w], ptr[w] + nf, ptr[w] + nf + nl};
+    if (lane == 0) {
+      spl[2 * w] = q[1];
+      spl[2 * w + 1] = q[2];
+    }
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
       bool ov = i < K && c0[i] <= w && w <= c1[i] && (which == 0 || inset[i] == which);
-      unsigned bal = __ballot_sync(FULL, ov);
-      if (ov) {
-        int slot = w - c0[i];
-        // which 16-antenna halves of this chunk the row's support touches (the rest is zero padding)
-        const int lo = rowS[i] - w * CH, hi = rowS[i] + rowL[i] - w * CH;
-        const int hm = (lo < 16 && hi > 0 ? 1 : 0) | (lo < 32 && hi > 16 ? 2 : 0);
-        out[n + __popc(bal & ((1u << lane) - 1))] =
-            make_int2((hoff[i] + slot * CH) | (i << 20), (i * SL + slot) * G | (i & 15) | (hm << 28));
+      const int hm = ov ? half_mask(i) : 0;
+      const int seg = (hm == 3 || !HALF) ? 0 : (hm == 1 ? 1 : 2);
+#pragma unroll
+      for (int sg = 0; sg < 3; ++sg) {
+        const unsigned bal = __ballot_sync(FULL, ov && seg == sg);
+        if (ov && seg == sg) {
+          const int slot = w - c0[i];
+          out[q[sg] + __popc(bal & ((1u << lane) - 1))] =
+              make_int2((hoff[i] + slot * CH) | (i << 20), (i * SL + slot) * G | (i & 15) | (hm << 28));
+        }
+        q[sg] += __popc(bal);
       }
-      n += __popc(bal);
     }
   };
   __syncthreads();  // hoff ready
-  if (SCH != KZ_VR_OAHK) build_list(lptr, lst, 0);
+  int* lspl = (int*)(sm + pl.lspl);
+  int* ospl = (int*)(sm + pl.ospl);
+  int* nspl = (int*)(sm + pl.nspl);
+  if (SCH != KZ_VR_OAHK) build_list(lptr, lspl, lst, 0);
   if (SCH == KZ_VR_OAHK) {
-    build_list(optr, olst, 1);
-    build_list(nptr, nlst, 2);
+    build_list(optr, ospl, olst, 1);
+    build_list(nptr, nspl, nlst, 2);
   }
   // TMEM: 4 warps per 32-lane subpartition x 64 columns (2 rhs x 16 complex antennas) each
   if constexpr (AGG) {
@@ -318,18 +360,20 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   T m0[E], m1[E];  // rhs g and g + 16
 #pragma unroll
   for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
-  const int l0 = lptr[w], l1 = lptr[w + 1];
   const float4* H4 = reinterpret_cast<const float4*>(Hs);
   // antenna of element k of this thread within the chunk: 4*(k/2) + 2a + (k&1)
 
   // conj(h) . m for both rhs over the chunk; returns this lane's rhs partial after
   // the a-lane exchange (lane a keeps rhs g + 16a)
-  auto dot_chunk = [&](int h0) -> T {
+  // j range [J0, J1) of the thread's 8 float4 pairs: <0, 8> = the whole chunk, <0, 4> / <4, 8> = the first /
+  // second 16 antennas (a half piece: the rest of the chunk is zero padding, skipping it is exact)
+  auto dot_part = [&](auto jr, int h0) -> T {
+    constexpr int J0 = decltype(jr)::lo, J1 = decltype(jr)::hi;
     const float4* hp = H4 + ((h0 + 2 * a) >> 1);
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
     {
 #pragma unroll
-      for (int j = 0; j < E / 2; ++j) {
+      for (int j = J0; j < J1; ++j) {
         float4 h = hp[2 * j];
         const int k = 2 * j;
         x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
@@ -350,6 +394,44 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   };
   // P element of list entry e for this lane's rhs
   auto pslot = [&](int ey) { return (ey & 0x0FFFFFE0) + ((g + 16 * a) ^ (ey & 15)); };
+  // partials of the list entries [q, q1) -> P, NF pieces in flight (1, 2 or 4)
+  auto refresh_seg = [&](auto jr, auto nf, const int2* L, int q, const int q1) {
+    constexpr int NF = decltype(nf)::value;
+    if constexpr (NF >= 4) {
+      for (; q + 3 < q1; q += 4) {
+        const int2 e0 = L[q], e1 = L[q + 1], e2 = L[q + 2], e3 = L[q + 3];
+        const T v0 = dot_part(jr, e0.x & 0xFFFFF);
+        const T v1 = dot_part(jr, e1.x & 0xFFFFF);
+        const T v2 = dot_part(jr, e2.x & 0xFFFFF);
+        const T v3 = dot_part(jr, e3.x & 0xFFFFF);
+        Ps[pslot(e0.y)] = v0;
+        Ps[pslot(e1.y)] = v1;
+        Ps[pslot(e2.y)] = v2;
+        Ps[pslot(e3.y)] = v3;
+      }
+    }
+    for (; q + 1 < q1; q += 2) {
+      const int2 e0 = L[q], e1 = L[q + 1];
+      const T v0 = dot_part(jr, e0.x & 0xFFFFF);
+      const T v1 = dot_part(jr, e1.x & 0xFFFFF);
+      Ps[pslot(e0.y)] = v0;
+      Ps[pslot(e1.y)] = v1;
+    }
+    if (q < q1) {
+      const int2 e0 = L[q];
+      Ps[pslot(e0.y)] = dot_part(jr, e0.x & 0xFFFFF);
+    }
+  };
+  // refresh partials of warp w's pieces of a list: whole-chunk pieces (four in flight; vr-oahk two: its larger
+  // live state would spill), then the first-half and second-half pieces (two in flight)
+  auto refresh_list = [&](const int* ptr, const int* spl, const int2* L) {
+    using NF = std::integral_constant<int, SCH == KZ_VR_OAHK ? 2 : 4>;
+    refresh_seg(JRange<0, 8>{}, NF{}, L, ptr[w], spl[2 * w]);
+    if constexpr (HALF) {
+      refresh_seg(JRange<0, 4>{}, std::integral_constant<int, 2>{}, L, spl[2 * w], spl[2 * w + 1]);
+      refresh_seg(JRange<4, 8>{}, std::integral_constant<int, 2>{}, L, spl[2 * w + 1], ptr[w + 1]);
+    }
+  };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
@@ -421,30 +503,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   for (t = 1; t <= p.T; ++t) {
     KZ_ITER();
     if constexpr (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK) {
-      // refresh every row overlapping this chunk, up to four rows in flight
-      int q = l0;
-      for (; q + 3 < l1; q += 4) {
-        const int2 e0 = lst[q], e1 = lst[q + 1], e2 = lst[q + 2], e3 = lst[q + 3];
-        const T v0 = dot_chunk(e0.x & 0xFFFFF);
-        const T v1 = dot_chunk(e1.x & 0xFFFFF);
-        const T v2 = dot_chunk(e2.x & 0xFFFFF);
-        const T v3 = dot_chunk(e3.x & 0xFFFFF);
-        Ps[pslot(e0.y)] = v0;
-        Ps[pslot(e1.y)] = v1;
-        Ps[pslot(e2.y)] = v2;
-        Ps[pslot(e3.y)] = v3;
-      }
-      for (; q + 1 < l1; q += 2) {
-        int2 e0 = lst[q], e1 = lst[q + 1];
-        T v0 = dot_chunk(e0.x & 0xFFFFF);
-        T v1 = dot_chunk(e1.x & 0xFFFFF);
-        Ps[pslot(e0.y)] = v0;
-        Ps[pslot(e1.y)] = v1;
-      }
-      if (q < l1) {
-        int2 e0 = lst[q];
-        Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF);
-      }
+      refresh_list(lptr, lspl, lst);  // every row overlapping this chunk
       KZ_WSTAMP();
       __syncthreads();
       KZ_PHASE();
@@ -642,36 +701,56 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       project(m1, sel[g + 16], gam[g + 16]);
       __syncthreads();  // sel/gam are rewritten by the next draw
     } else {  // AHK / VR-OAHK (solvers.py:407-421)
-      // refresh partials of the rows in list (ptr, L) -> P
-      auto refresh_list = [&](const int* ptr, const int2* L) {
-        int q = ptr[w];
-        const int q1 = ptr[w + 1];
-        // up to four rows in flight (vr-oahk keeps two: its larger live state would spill)
-        for (; SCH != KZ_VR_OAHK && q + 3 < q1; q += 4) {
-          const int2 e0 = L[q], e1 = L[q + 1], e2 = L[q + 2], e3 = L[q + 3];
-          const T v0 = dot_chunk(e0.x & 0xFFFFF);
-          const T v1 = dot_chunk(e1.x & 0xFFFFF);
-          const T v2 = dot_chunk(e2.x & 0xFFFFF);
-          const T v3 = dot_chunk(e3.x & 0xFFFFF);
-          Ps[pslot(e0.y)] = v0;
-          Ps[pslot(e1.y)] = v1;
-          Ps[pslot(e2.y)] = v2;
-          Ps[pslot(e3.y)] = v3;
+      // residuals -> weights phi = r/e, num = vdot(phi, r), ||phi||^2 (solvers.py:248-254, 274) with the whole
+      // CTA: thread (w, lane) takes rows w, w + W, ... of rhs lane and leaves its partial sums in WP[w][lane];
+      // warp 0 reduces them per rhs in warp order (reduce_weights) once the partials are visible
+      float2* WPn = (float2*)(sm + pl.WP);
+      float* WPs = (float*)(sm + pl.WP + 8 * (size_t)W * G);
+      int* WPz = (int*)(sm + pl.WP + 12 * (size_t)W * G);
+      auto weights = [&](int which) {
+        const int gg = lane;
+        float nx = 0.f, ny = 0.f, sp = 0.f;
+        bool nz = false;
+        if (g0 + gg < K && !donev[gg])
+#pragma unroll(SCH == KZ_VR_OAHK ? 1 : 4)
+          for (int i = w; i < K; i += W) {
+            if (which && inset[i] != which) continue;
+            const T r = resid(i, gg);
+            const float ie = inv_en[i];
+            const T ph = make_float2(r.x * ie, r.y * ie);
+            Phi[xs(i, gg)] = ph;
+            nz |= (ph.x != 0.f || ph.y != 0.f);
+            nx = fmaf(ph.x, r.x, nx); nx = fmaf(ph.y, r.y, nx);
+            ny = fmaf(ph.x, r.y, ny); ny = fmaf(-ph.y, r.x, ny);
+            sp = fmaf(ph.x, ph.x, sp); sp = fmaf(ph.y, ph.y, sp);
+          }
+        WPn[w * G + gg] = make_float2(nx, ny);
+        WPs[w * G + gg] = sp;
+        WPz[w * G + gg] = nz ? 1 : 0;
+      };
+      auto reduce_weights = [&](int nrows) {  // warp 0, lane = rhs slot
+        if (w != 0) return;
+        const int gg = lane;
+        float nx = 0.f, ny = 0.f, sp = 0.f;
+        int anz = 0;
+        for (int ww = 0; ww < W; ++ww) {
+          const float2 n2 = WPn[ww * G + gg];
+          nx += n2.x;
+          ny += n2.y;
+          sp += WPs[ww * G + gg];
+          anz |= WPz[ww * G + gg];
         }
-        for (; q + 1 < q1; q += 2) {
-          int2 e0 = L[q], e1 = L[q + 1];
-          T v0 = dot_chunk(e0.x & 0xFFFFF);
-          T v1 = dot_chunk(e1.x & 0xFFFFF);
-          Ps[pslot(e0.y)] = v0;
-          Ps[pslot(e1.y)] = v1;
-        }
-        if (q < q1) {
-          int2 e0 = L[q];
-          Ps[pslot(e0.y)] = dot_chunk(e0.x & 0xFFFFF);
+        if (g0 + gg < K && !donev[gg]) {
+          numv[gg] = make_float2(nx, ny);
+          spv[gg] = sp;
+          nzv[gg] = (anz && nrows > 0) ? 1 : 0;
+          flv[gg] += 2LL * nrows;
+        } else {
+          nzv[gg] = 0;
         }
       };
-      // residuals -> weights phi = r/e, num = vdot(phi, r), ||phi||^2 (warp per rhs; solvers.py:248-254, 274)
-      auto weights = [&](int which, int nrows) {
+      // the same with one half-warp per rhs (lanes over rows, shuffle reductions): the AHK form
+      auto weights_rhs = [&](int which, int nrows) {
         const int hf = lane >> 4, hl = lane & 15;  // one half-warp per rhs, lanes over rows
         const unsigned hmask = 0xFFFFu << (16 * hf);
         for (int pair = w; pair < G / 2; pair += W) {
@@ -713,8 +792,9 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       };
       // aggregated projection (solvers.py:257-309): m parked in TMEM while y = sum phi h
       // (ascending rows) occupies the registers
-      auto aggregate = [&](const int* ptr, const int2* L, int nrows, int span, bool dense, bool mark_done,
+      auto aggregate = [&](const int* ptr, const int* spl, const int2* L, int nrows, int span, bool dense, bool mark_done,
                            long long ycost) {
+        if constexpr (PAR_W) reduce_weights(nrows);
         {
           float f0[16], f1[16];
 #pragma unroll
@@ -734,12 +814,13 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         }
 #pragma unroll
         for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);  // registers now hold y
-        auto agg_entry = [&](int2 e) {
+        auto agg_entry = [&](auto jr, int2 e) {  // y += phi_i h_i on the entry's j range
+          constexpr int J0 = decltype(jr)::lo, J1 = decltype(jr)::hi;
           const int i = e.x >> 20;
           const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
           const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
 #pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
+          for (int j = J0; j < J1; ++j) {
             float4 h = hp[2 * j];
             const int k = 2 * j;
             m0[k] = cfma(p0, make_float2(h.x, h.y), m0[k]);
@@ -748,14 +829,19 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
             m1[k + 1] = cfma(p1, make_float2(h.z, h.w), m1[k + 1]);
           }
         };
-        int q = ptr[w];
-        const int q1 = ptr[w + 1];
-        for (; q + 1 < q1; q += 2) {  // two entries per trip: the next entry's loads overlap this one's FMAs
-          const int2 ea = L[q], eb = L[q + 1];
-          agg_entry(ea);
-          agg_entry(eb);
+        auto agg_seg = [&](auto jr, int q, const int q1) {
+          for (; q + 1 < q1; q += 2) {  // two entries per trip: the next entry's loads overlap this one's FMAs
+            const int2 ea = L[q], eb = L[q + 1];
+            agg_entry(jr, ea);
+            agg_entry(jr, eb);
+          }
+          if (q < q1) agg_entry(jr, L[q]);
+        };
+        agg_seg(JRange<0, 8>{}, ptr[w], spl[2 * w]);
+        if constexpr (HALF) {
+          agg_seg(JRange<0, 4>{}, spl[2 * w], spl[2 * w + 1]);
+          agg_seg(JRange<4, 8>{}, spl[2 * w + 1], ptr[w + 1]);
         }
-        if (q < q1) agg_entry(L[q]);
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
@@ -853,17 +939,17 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       };
 
       if constexpr (SCH == KZ_AHK) {
-        refresh_list(lptr, lst);
+        refresh_list(lptr, lspl, lst);
         if (tid < G && g0 + tid < K && !donev[tid]) flv[tid] += dense_refresh;
         __syncthreads();
         KZ_PHASE();
-        weights(0, K);
+        if constexpr (PAR_W) weights(0); else weights_rhs(0, K);
         __syncthreads();
         KZ_PHASE();
-        aggregate(lptr, lst, K, Nt, true, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
+        aggregate(lptr, lspl, lst, K, Nt, true, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
       } else {
         // exact block projection on the orthogonal group O (solvers.py:312-332)
-        refresh_list(optr, olst);
+        refresh_list(optr, ospl, olst);
         __syncthreads();
         KZ_PHASE();
         for (int e = tid; e < K * G; e += nthr) {
@@ -884,13 +970,13 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           project(m1, i, Phi[xs(i, g + 16)]);
         }
         if (nN > 0) {
-          refresh_list(nptr, nlst);
+          refresh_list(nptr, nspl, nlst);
           __syncthreads();
           KZ_PHASE();
-          weights(2, nN);
+          if constexpr (PAR_W) weights(2); else weights_rhs(2, nN);
           __syncthreads();
           KZ_PHASE();
-          aggregate(nptr, nlst, nN, unionN, false, false, costN);
+          aggregate(nptr, nspl, nlst, nN, unionN, false, false, costN);
         }
         if (tid < G && g0 + tid < K) itv[tid] += 1;
       }
@@ -978,7 +1064,7 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
 // 1 launched, 0 not eligible / not a single-row scheme, -1 failure
 inline int wide_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
                          int32_t* tstop, int maxsm, cudaStream_t s) {
-  if (P.dtype != KZ_C64 || P.n_antennas % wide::CH != 0 || P.n_users < 17) return 0;
+  if (P.dtype != KZ_C64 || P.n_antennas % wide::CH != 0 || P.n_users < 17 || P.n_users > 128) return 0;
   int S, hcap;
   size_t smem = wide_smem_bytes(P, &S, &hcap);
   if ((int)smem > maxsm) return 0;
