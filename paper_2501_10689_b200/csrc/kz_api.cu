@@ -77,11 +77,15 @@ size_t kz_solve_workspace_bytes_for(const kz_problem* prob, int32_t scheme, cons
   int32_t dummy = 0;
   g_dry_launch = true;
   int fast = lockstep_try_launch(*prob, scheme, *stop, *rng, *out, 0, nullptr, ~size_t(0), nullptr, &dummy);
-  if (fast != 1)
+  bool clu = false;
+  if (fast != 1) {
     fast = cluster_try_launch(*prob, scheme, *stop, *rng, *out, 0, nullptr, ~size_t(0), nullptr, &dummy);
+    clu = fast == 1;
+  }
   g_dry_launch = false;
   cudaGetLastError();  // eligibility probes (attributes, occupancy) leave no sticky error behind
-  if (fast == 1) return ls_extra_ws(*prob);  // the on-chip kernels keep only the stop iterations in HBM
+  // the on-chip kernels keep only the stop iterations in HBM (the streamed cluster variant also its padded H_eff)
+  if (fast == 1) return clu ? g_cluster_dry_ws : ls_extra_ws(*prob);
   return gen_layout(prob->n_systems, prob->n_users, prob->n_antennas, prob->dtype).total;
 }
 

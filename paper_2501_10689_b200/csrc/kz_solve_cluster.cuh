@@ -102,7 +102,8 @@ struct Plan {
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap, int G, int rcap) {
+__host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, int pcap, int G, int rcap,
+                                      bool streamed = false) {
   Plan p;
   p.K = K;
   p.W = W;
@@ -136,7 +137,7 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
   p.olst = o; o = al(o + (oahk ? 8 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
   p.nlst = p.olst;
-  p.H = o; o = al(o + 8 * (size_t)pcap * CH);
+  p.H = o; o = al(o + (streamed ? 0 : 8 * (size_t)pcap * CH));  // streamed: H from the padded global copy
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Ro = o; o = al(o + (greedy ? 8 * (size_t)p.KO * G : 0));
   p.Fo = o; o = al(o + (agg ? 8 * (size_t)p.KO * G : 0));
@@ -188,13 +189,34 @@ struct CluArgs {
   int pcap;     // (row, chunk) pairs reserved per CTA
   int rcap;     // local rows reserved per CTA (0: min(K, pcap))
   int32_t* tstop;
+  const float2* hpad;  // streamed variant: H_eff padded to whole chunks, row r of system b at (b K + r) NS CH
 };
+
+// prepares CluArgs::hpad for the streamed variant: row r's chunk pieces c0_r .. c0_r + NS - 1, zero outside the
+// support (one warp per row; coalesced 256-byte pieces)
+__global__ void __launch_bounds__(256) kz_hpad_kernel(const kz_problem P, int NS, float2* hpad) {
+  const long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= (long long)P.n_systems * P.n_users) return;
+  const int sg = P.row_seg_ptr[r];
+  const int s = P.seg_start[sg], L = P.seg_len[sg];
+  const int c0 = s / 32;
+  const float2* src = (const float2*)P.heff + P.row_val_ptr[r];
+  float2* dst = hpad + r * NS * 32;
+  for (int pc = 0; pc < NS; ++pc) {
+    const int ant = (c0 + pc) * 32 + lane;
+    dst[pc * 32 + lane] = (ant >= s && ant < s + L) ? src[ant - s] : make_float2(0.f, 0.f);
+  }
+}
 
 // GG = rhs per cluster: 16 (lane (a, g), a = lane >> 3: rhs g, g + 8 on 8 antennas) or 32 (a = lane >> 4:
 // rhs g, g + 16 on 16 antennas, the wide kernel's mapping: twice the FMAs per loaded element set and per
 // piece overhead, when the larger inbox fits)
-template <int SCH, int GG>
-__global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constant__ CluArgs p) {
+// ST (streamed): H_eff is read from the padded global copy CluArgs::hpad through L1 / L2 instead of being staged
+// into shared memory, so two CTAs (of different clusters) share an SM: one cluster's barrier waits and latency-bound
+// phases overlap the other's FMA-bound refresh
+template <int SCH, int GG, bool ST = false>
+__global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __grid_constant__ CluArgs p) {
   using namespace clu;
   constexpr int G = GG;
   constexpr int NA = G == 16 ? 4 : 2;  // a-lanes sharing a (row, chunk) piece
@@ -213,7 +235,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   const int b = cid / ngroups, grp = cid % ngroups, g0 = grp * G;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int W = nthr >> 5;
-  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap, G, p.rcap);
+  const Plan pl = plan(SCH, K, W, CL, p.NS, p.pcap, G, p.rcap, ST);
   const int KO = pl.KO, NS = pl.NS, KW = (K + 31) / 32;
   // block-interleaved slices: CTA c owns nblk blocks of Bc = W / nblk chunks, block j at chunk
   // (j CL + c) Bc, so every CTA samples the whole array and the VR-coverage ramps at the array edges no
@@ -382,7 +404,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
   // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
   // no dependent global load, no load latency per piece)
-  {
+  if constexpr (!ST) {
     // bulk copies (kz_tma.cuh) for the rows whose packed offset has their first antenna's parity, one per
     // contiguous antenna run (a row's pieces in this CTA form at most nblk runs); 8-byte asynchronous copies
     // (zero-filled outside the support) for the others
@@ -444,10 +466,18 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   // (olst / nlst share one array); one counting pass and one fill pass for all of them
   const bool want_all = SCH != KZ_VR_OAHK || residual;
   constexpr bool want_on = SCH == KZ_VR_OAHK;
+  // H element offset of local row n's piece on local warp ww (l0: the row's first local warp)
+  auto hoff_of = [&](int n, int ww, int l0) -> int {
+    if constexpr (ST) {
+      const int i = lrow[n];
+      return (i * NS + chunk_of(ww) - c0[i]) * CH;
+    }
+    return lh[n] + (ww - l0) * CH;
+  };
   auto entry = [&](int n, int l0) {
     const int i = lrow[n], o = i / KO, il = i - o * KO;
     const int slot = chunk_of(w) - c0[i];
-    return make_int2((lh[n] + (w - l0) * CH) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
+    return make_int2(hoff_of(n, w, l0) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
   };
   {
     int ca = 0, co = 0, cn = 0;
@@ -589,7 +619,13 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   T m0[E], m1[E];  // rhs g and g + LPA
 #pragma unroll
   for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);
-  const float4* H4 = reinterpret_cast<const float4*>(Hs);
+  const float4* H4 = ST ? reinterpret_cast<const float4*>(p.hpad + (size_t)b * K * NS * CH)
+                        : reinterpret_cast<const float4*>(Hs);
+  // streamed: read-only global loads (L1-cached, the slice's pieces are re-read every iteration)
+  auto ldh = [](const float4* q) -> float4 {
+    if constexpr (ST) return __ldg(q);
+    return *q;
+  };
 
   // conj(h) . m over this warp's chunk for both rhs, reduced over the a-lanes; lane < G ends with rhs lane
   auto dot16 = [&](int h0) -> T {
@@ -597,7 +633,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
 #pragma unroll
     for (int j = 0; j < E / 2; ++j) {
-      const float4 h = hp[NA * j];
+      const float4 h = ldh(hp + NA * j);
       const int k = 2 * j;
       x0 = fmaf(h.x, m0[k].x, x0); x0 = fmaf(h.y, m0[k].y, x0);
       y0 = fmaf(h.x, m0[k].y, y0); y0 = fmaf(-h.y, m0[k].x, y0);
@@ -724,10 +760,10 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
   auto project = [&](T (&mr)[E], int n, T gm) {  // m += gm h on this warp's chunk of local row n
     const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
     if (w < l0 || w > l1) return;
-    const float4* hp = H4 + ((lh[n] + (w - l0) * CH) >> 1) + a;
+    const float4* hp = H4 + (hoff_of(n, w, l0) >> 1) + a;
 #pragma unroll
     for (int j = 0; j < E / 2; ++j) {
-      const float4 h = hp[NA * j];
+      const float4 h = ldh(hp + NA * j);
       const int k = 2 * j;
       mr[k].x = fmaf(gm.x, h.x, mr[k].x); mr[k].x = fmaf(-gm.y, h.y, mr[k].x);
       mr[k].y = fmaf(gm.x, h.y, mr[k].y); mr[k].y = fmaf(gm.y, h.x, mr[k].y);
@@ -1057,7 +1093,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
           const float4* hp1 = H4 + ((e1 & 0xFFFFF) >> 1) + a;
 #pragma unroll
           for (int j = 0; j < E / 2; ++j) {
-            const float4 h0 = hp0[NA * j], h1 = hp1[NA * j];
+            const float4 h0 = ldh(hp0 + NA * j), h1 = ldh(hp1 + NA * j);
             const int k = 2 * j;
             y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
             y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
@@ -1075,7 +1111,7 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
 #pragma unroll
           for (int j = 0; j < E / 2; ++j) {
-            const float4 h0 = hp0[NA * j];
+            const float4 h0 = ldh(hp0 + NA * j);
             const int k = 2 * j;
             y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
             y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
@@ -1231,19 +1267,26 @@ __global__ void __launch_bounds__(256, 1) kz_cluster_kernel(const __grid_constan
 
 // ------------------------------------------------------------------ host side
 inline size_t cluster_smem_bytes(const kz_problem& P, int scheme, int W, int G, int* CL, int* NS, int* pcap,
-                                 int* rcap) {
+                                 int* rcap, bool streamed = false) {
   const int nch = P.n_antennas / clu::CH;
   *CL = (nch + W - 1) / W;
   *NS = (P.max_support + clu::CH - 2) / clu::CH + 1;  // inbox slots: chunks a row can touch
   *pcap = W == 4 ? P.slice_pairs_128 : (W == 8 ? P.slice_pairs_256 : 0);
   *rcap = W == 4 ? P.slice_rows_128 : (W == 8 ? P.slice_rows_256 : 0);
   if (*pcap <= 0) return ~size_t(0);
-  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap, G, *rcap).total;
+  return clu::plan(scheme, P.n_users, W, *CL, *NS, *pcap, G, *rcap, streamed).total;
 }
 
-template <int SCH, int GG>
+// bytes of the streamed variant's padded H_eff copy (CluArgs::hpad), placed after the tstop block of the workspace
+inline size_t cluster_hpad_offset(const kz_problem& P) { return kz_align(ls_extra_ws(P)); }
+inline size_t cluster_hpad_bytes(const kz_problem& P, int NS) {
+  return (size_t)P.n_systems * P.n_users * NS * clu::CH * sizeof(float2);
+}
+inline size_t g_cluster_dry_ws = 0;  // workspace the dispatched cluster variant needs (dry launches)
+
+template <int SCH, int GG, bool ST>
 inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStream_t s) {
-  auto kern = kz_cluster_kernel<SCH, GG>;
+  auto kern = kz_cluster_kernel<SCH, GG, ST>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
   if (CL > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
@@ -1272,7 +1315,11 @@ inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStre
     return 0;
   }
   if (g_dry_launch) return 1;
-  note_tma(a.bulk);
+  note_tma(ST ? 0 : a.bulk);
+  if (ST) {
+    const long long rows = (long long)a.P.n_systems * a.P.n_users;
+    kz_hpad_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(a.P, a.NS, const_cast<float2*>(a.hpad));
+  }
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   if (a.mode == KZ_STOP_LOCKSTEP)
     kz_lockstep_finalize<<<(a.P.n_systems + 127) / 128, 128, 0, s>>>(a.tstop, groups, a.P.n_systems, a.O.n_outer,
@@ -1305,18 +1352,34 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   // they fit); clusters stay within 16 CTAs
   // candidates in order of preference: 32 rhs x 256-antenna CTAs, 16 rhs x 256, 16 rhs x 128 (two CTAs per
   // SM when they fit), 16 rhs x 128; clusters stay within 16 CTAs
-  struct Cand { int G, W, CL, NS, pcap, rcap; size_t smem; bool two_per_sm; };
-  Cand cands[5] = {{32, 8}, {16, 8}, {16, 4}, {16, 4}, {32, 4}};
+  struct Cand { int G, W, CL, NS, pcap, rcap; size_t smem; bool two_per_sm, st; };
+  // streamed (ST) candidates first when enabled: H_eff read through L1 / L2, two CTAs per SM; they need the padded
+  // copy in the workspace (kz_solve_workspace_bytes_for reports it), 20-bit piece offsets and, for the aggregation
+  // schemes, 16 rhs (m and y of 32 rhs do not fit the 128 registers of two CTAs per SM)
+  const bool agg_scheme = scheme == KZ_AHK || scheme == KZ_VR_OAHK;
+  Cand cands[7] = {{32, 8, 0, 0, 0, 0, 0, true, true}, {16, 8, 0, 0, 0, 0, 0, true, true},
+                   {32, 8}, {16, 8}, {16, 4}, {16, 4}, {32, 4}};
   const size_t two = (size_t)(smsm / 2 - 1024);
-  for (int k = 0; k < 5; ++k) {
+  // KZ_CLUSTER_STREAM: 0 never, 1 (default) where it measured faster, 2 whenever eligible.  Measured same-box
+  // (tools/ab_stream.sh, profiles/r02_ab_cluster_stream.log): the aggregation schemes in residual mode (cfg4
+  // vr-oahk: ~2.4 iterations per rhs, so staging H_eff into shared memory was a large part of the launch) -16%;
+  // cfg4 grk -1%; the fixed-T cfg3 / cfg5 aggregation runs +12..28% (H_eff re-read from L2 every iteration)
+  static const int env_stream = getenv("KZ_CLUSTER_STREAM") ? atoi(getenv("KZ_CLUSTER_STREAM")) : 1;
+  const bool want_stream = env_stream == 2 || (env_stream == 1 && resid && agg_scheme);
+  for (int k = 0; k < 7; ++k) {
     Cand& cd = cands[k];
-    cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap, &cd.rcap);
-    cd.two_per_sm = k == 2;
+    cd.smem = cluster_smem_bytes(P, scheme, cd.W, cd.G, &cd.CL, &cd.NS, &cd.pcap, &cd.rcap, cd.st);
+    if (k == 4) cd.two_per_sm = true;
+    if (cd.st) {
+      const bool ok = want_stream && !(agg_scheme && cd.G == 32) && (long long)P.n_users * cd.NS * clu::CH < (1 << 20) &&
+                      ws_bytes >= cluster_hpad_offset(P) + cluster_hpad_bytes(P, cd.NS);
+      if (!ok) cd.smem = ~size_t(0);
+    }
   }
   static const int forced_w = getenv("KZ_CLUSTER_W") ? atoi(getenv("KZ_CLUSTER_W")) : 0;
   static const int forced_g = getenv("KZ_CLUSTER_G") ? atoi(getenv("KZ_CLUSTER_G")) : 0;
   int pick = -1;
-  for (int k = 0; k < 5 && pick < 0; ++k) {
+  for (int k = 0; k < 7 && pick < 0; ++k) {
     const Cand& cd = cands[k];
     if ((forced_w && cd.W != forced_w) || (forced_g && cd.G != forced_g)) continue;
     if (cd.CL > 16 || cd.smem > (cd.two_per_sm ? two : (size_t)maxsm)) continue;
@@ -1324,13 +1387,15 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   }
   static const bool verbose = getenv("KZ_VERBOSE") != nullptr;
   if (verbose)
-    for (int k = 0; k < 5; ++k)
-      fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: G %d W %d CL %d pairs %d smem %zu%s\n", scheme,
-              P.n_users, P.n_antennas, cands[k].G, cands[k].W, cands[k].CL, cands[k].pcap,
-              cands[k].smem == ~size_t(0) ? 0 : cands[k].smem, k == pick ? "  <- picked" : "");
+    for (int k = 0; k < 7; ++k)
+      fprintf(stderr, "[kz cluster] scheme %d K %d Nt %d: G %d W %d CL %d%s pairs %d smem %zu%s\n", scheme,
+              P.n_users, P.n_antennas, cands[k].G, cands[k].W, cands[k].CL, cands[k].st ? " streamed" : "",
+              cands[k].pcap, cands[k].smem == ~size_t(0) ? 0 : cands[k].smem, k == pick ? "  <- picked" : "");
   if (pick < 0) return 0;
   const int W = cands[pick].W, CL = cands[pick].CL, GG = cands[pick].G;
+  const bool ST = cands[pick].st;
   const size_t smem = cands[pick].smem;
+  g_cluster_dry_ws = ST ? cluster_hpad_offset(P) + cluster_hpad_bytes(P, cands[pick].NS) : ls_extra_ws(P);
   CluArgs a;
   a.P = P;
   a.bulk = bulk_staging_ok(P);
@@ -1347,25 +1412,42 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.pcap = cands[pick].pcap;
   a.rcap = cands[pick].rcap;
   a.tstop = (int32_t*)ws;
+  a.hpad = ST && ws ? (const float2*)(ws + cluster_hpad_offset(P)) : nullptr;
   int rc = 0;
-  if (GG == 32) {
+  if (ST) {
+    if (GG == 32) {
+      switch (scheme) {
+        case KZ_GK: rc = cluster_launch<KZ_GK, 32, true>(a, W, CL, smem, s); break;
+        case KZ_GRK: rc = cluster_launch<KZ_GRK, 32, true>(a, W, CL, smem, s); break;
+        case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 32, true>(a, W, CL, smem, s); break;
+      }
+    } else {
+      switch (scheme) {
+        case KZ_GK: rc = cluster_launch<KZ_GK, 16, true>(a, W, CL, smem, s); break;
+        case KZ_GRK: rc = cluster_launch<KZ_GRK, 16, true>(a, W, CL, smem, s); break;
+        case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 16, true>(a, W, CL, smem, s); break;
+        case KZ_AHK: rc = cluster_launch<KZ_AHK, 16, true>(a, W, CL, smem, s); break;
+        case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 16, true>(a, W, CL, smem, s); break;
+      }
+    }
+  } else if (GG == 32) {
     switch (scheme) {
-      case KZ_GK: rc = cluster_launch<KZ_GK, 32>(a, W, CL, smem, s); break;
-      case KZ_GRK: rc = cluster_launch<KZ_GRK, 32>(a, W, CL, smem, s); break;
-      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 32>(a, W, CL, smem, s); break;
-      case KZ_AHK: rc = cluster_launch<KZ_AHK, 32>(a, W, CL, smem, s); break;
-      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 32>(a, W, CL, smem, s); break;
+      case KZ_GK: rc = cluster_launch<KZ_GK, 32, false>(a, W, CL, smem, s); break;
+      case KZ_GRK: rc = cluster_launch<KZ_GRK, 32, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 32, false>(a, W, CL, smem, s); break;
+      case KZ_AHK: rc = cluster_launch<KZ_AHK, 32, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 32, false>(a, W, CL, smem, s); break;
     }
   } else {
     switch (scheme) {
-      case KZ_GK: rc = cluster_launch<KZ_GK, 16>(a, W, CL, smem, s); break;
-      case KZ_GRK: rc = cluster_launch<KZ_GRK, 16>(a, W, CL, smem, s); break;
-      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 16>(a, W, CL, smem, s); break;
-      case KZ_AHK: rc = cluster_launch<KZ_AHK, 16>(a, W, CL, smem, s); break;
-      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 16>(a, W, CL, smem, s); break;
+      case KZ_GK: rc = cluster_launch<KZ_GK, 16, false>(a, W, CL, smem, s); break;
+      case KZ_GRK: rc = cluster_launch<KZ_GRK, 16, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 16, false>(a, W, CL, smem, s); break;
+      case KZ_AHK: rc = cluster_launch<KZ_AHK, 16, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 16, false>(a, W, CL, smem, s); break;
     }
   }
-  if (rc == 1) *launches = lockstep ? 2 : 1;
+  if (rc == 1) *launches = (lockstep ? 2 : 1) + (ST ? 1 : 0);
   return rc;
 }
 
