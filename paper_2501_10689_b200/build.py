@@ -17,7 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libkaczmarz_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 # variant "timing": per-phase clock64 accounting in the lockstep kernels (-DKZ_TIMING)
-VARIANTS = {"": [], "timing": ["-DKZ_TIMING"]}
+# variant "checked": bounds checks on every on-chip index the kernels compute (-DKZ_CHECKED, kz_common.cuh)
+VARIANTS = {"": [], "timing": ["-DKZ_TIMING"], "checked": ["-DKZ_CHECKED"]}
 
 
 def lib_path(variant: str = "") -> str:
@@ -77,5 +78,5 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
 
 
 if __name__ == "__main__":
-    var = "timing" if "--timing" in sys.argv else ""
+    var = "timing" if "--timing" in sys.argv else ("checked" if "--checked" in sys.argv else "")
     print(build(force="--force" in sys.argv, verbose=True, variant=var))

@@ -45,6 +45,24 @@
 #define KZ_TDUMP(ptr) do {} while (0)
 #endif
 
+// Bounds-checked build variant `checked` (-DKZ_CHECKED, python -m paper_2501_10689_b200.build --checked): the
+// shared-memory, cluster-shared-memory (DSMEM), TMEM and piece-list indices the on-chip kernels compute are checked
+// against their allocations; a violation prints the site and traps.  It stands in for compute-sanitizer memcheck,
+// which is closed on this GPU pool (tools/sanitize_cases.py runs every kernel under it).
+#ifdef KZ_CHECKED
+#include <cstdio>
+#define KZ_CHECK(cond, what)                                                                                        \
+  do {                                                                                                            \
+    if (!(cond)) {                                                                                                \
+      printf("[kz checked] %s:%d: %s violated (block %d thread %d)\n", __FILE__, __LINE__, what, (int)blockIdx.x,  \
+             (int)threadIdx.x);                                                                                   \
+      __trap();                                                                                                   \
+    }                                                                                                             \
+  } while (0)
+#else
+#define KZ_CHECK(cond, what) do {} while (0)
+#endif
+
 namespace kz {
 
 constexpr unsigned FULL = 0xffffffffu;

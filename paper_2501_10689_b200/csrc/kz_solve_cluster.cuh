@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   KZ_SETUP_MARK(1);
   const int NL = misc[1], npairs = misc[2];
   if (npairs > p.pcap || NL > pl.nlcap) __trap();  // layout hint violated: fail loudly
+  KZ_CHECK(!ST || (long long)K * NS * CH < (1 << 20), "cluster: streamed piece offsets fit 20 bits");
   // row pieces -> shared memory, zero padded to whole chunks: one warp per local row, lanes over the 32
   // antennas of each piece (coalesced 256 B), all issued as asynchronous copies (offsets from shared memory:
   // no dependent global load, no load latency per piece)
@@ -477,6 +478,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   auto entry = [&](int n, int l0) {
     const int i = lrow[n], o = i / KO, il = i - o * KO;
     const int slot = chunk_of(w) - c0[i];
+    KZ_CHECK(slot >= 0 && slot < NS && o < CL, "cluster: piece slot / owner");
     return make_int2(hoff_of(n, w, l0) | (n << 20), ((il * NS + slot) * G) | ((il & 15) << 20) | (o << 24));
   };
   {
@@ -628,7 +630,9 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   };
 
   // conj(h) . m over this warp's chunk for both rhs, reduced over the a-lanes; lane < G ends with rhs lane
+  const int hcap_el = ST ? K * NS * CH : pl.pcap * CH;  // elements of H_eff the kernel may read
   auto dot16 = [&](int h0) -> T {
+    KZ_CHECK(h0 >= 0 && (h0 & 1) == 0 && h0 + CH <= hcap_el, "cluster: refresh piece inside H");
     const float4* hp = H4 + (h0 >> 1) + a;
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
 #pragma unroll
@@ -661,6 +665,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     if (lane < G) {
       T* dst = INs + (e.y & 0xFFFFF) + (lane ^ ((e.y >> 20) & 15));
       const int o = e.y >> 24;
+      KZ_CHECK(o < CL && (e.y & 0xFFFFF) + G <= KO * NS * G, "cluster: inbox slot (DSMEM) index");
       if (o == c) *dst = v; else st_remote(dst, o, v);
     }
   };
@@ -709,6 +714,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   };
   auto push_phi = [&](int il, int gg, T v) {
     const int nd = dcnt[il];
+    KZ_CHECK(il >= 0 && il < KO && nd <= CL && gg < G, "cluster: phi destinations");
     const uint32_t* da = dlst + il * CL;
     const uint32_t off = 8u * (uint32_t)gg;
 #pragma unroll 4
@@ -760,6 +766,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   auto project = [&](T (&mr)[E], int n, T gm) {  // m += gm h on this warp's chunk of local row n
     const int l0 = lcc[n] & 0xFF, l1 = lcc[n] >> 8;
     if (w < l0 || w > l1) return;
+    KZ_CHECK(n >= 0 && n < pl.nlcap && hoff_of(n, w, l0) + CH <= hcap_el, "cluster: projected piece inside H");
     const float4* hp = H4 + (hoff_of(n, w, l0) >> 1) + a;
 #pragma unroll
     for (int j = 0; j < E / 2; ++j) {
@@ -1087,6 +1094,8 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
         const int q1 = ptr[w + 1];
         for (; q + 1 < q1; q += 2) {  // two pieces in flight
           const int e0 = L[q].x, e1 = L[q + 1].x, n0 = e0 >> 20, n1 = e1 >> 20;
+          KZ_CHECK(n0 < pl.nlcap && n1 < pl.nlcap && (e0 & 0xFFFFF) + CH <= hcap_el && (e1 & 0xFFFFF) + CH <= hcap_el,
+                   "cluster: aggregated pieces inside H / Phl");
           const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
           const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + LPA];
           const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   int* lspl = (int*)(sm + pl.lspl);
   int* ospl = (int*)(sm + pl.ospl);
   int* nspl = (int*)(sm + pl.nspl);
+  KZ_CHECK(tid >= K || hoff[tid] + (c1[tid] - c0[tid] + 1) * CH <= pl.hcap, "wide: row layout inside H");
   if (SCH != KZ_VR_OAHK) build_list(lptr, lspl, lst, 0);
   if (SCH == KZ_VR_OAHK) {
     build_list(optr, ospl, olst, 1);
@@ -342,6 +343,10 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   }
   __syncthreads();
   KZ_PHASE();
+  KZ_CHECK(SCH == KZ_VR_OAHK || lptr[W] <= K * SL, "wide: piece list capacity");
+  KZ_CHECK(SCH != KZ_VR_OAHK || (optr[W] <= K * SL && nptr[W] <= K * SL), "wide: O / N piece list capacity");
+  KZ_CHECK(!AGG || W <= 16, "wide: TMEM columns (4 warps x 64 per lane quarter)");
+  KZ_CHECK(!AGG || pl.WP != pl.R || (size_t)W * G * 16 <= (size_t)K * G * 8, "wide: weight partials inside R");
   uint32_t my_tmem = 0;
   if constexpr (AGG) {
     tmem::fence_after();
@@ -369,6 +374,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   // second 16 antennas (a half piece: the rest of the chunk is zero padding, skipping it is exact)
   auto dot_part = [&](auto jr, int h0) -> T {
     constexpr int J0 = decltype(jr)::lo, J1 = decltype(jr)::hi;
+    KZ_CHECK(h0 >= 0 && (h0 & 1) == 0 && h0 + CH <= pl.hcap, "wide: refresh piece inside H");
     const float4* hp = H4 + ((h0 + 2 * a) >> 1);
     float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f, u0 = 0.f, v0 = 0.f, u1 = 0.f, v1 = 0.f;
     {
@@ -393,7 +399,11 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     return a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
   };
   // P element of list entry e for this lane's rhs
-  auto pslot = [&](int ey) { return (ey & 0x0FFFFFE0) + ((g + 16 * a) ^ (ey & 15)); };
+  auto pslot = [&](int ey) {
+    const int o = (ey & 0x0FFFFFE0) + ((g + 16 * a) ^ (ey & 15));
+    KZ_CHECK(o >= 0 && o < K * SL * G, "wide: P slot index");
+    return o;
+  };
   // partials of the list entries [q, q1) -> P, NF pieces in flight (1, 2 or 4)
   auto refresh_seg = [&](auto jr, auto nf, const int2* L, int q, const int q1) {
     constexpr int NF = decltype(nf)::value;
@@ -433,6 +443,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     }
   };
   auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
+    KZ_CHECK(i >= 0 && i < K && gg >= 0 && gg < G && c1[i] - c0[i] < SL, "wide: residual row / slots");
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
     const int ns = c1[i] - c0[i];
@@ -485,6 +496,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   // m_r += gm h_i on this thread's antennas of the chunk (rows zero padded => whole chunk)
   auto project = [&](T (&mr)[E], int i, T gm) {
     if (i < 0 || w < c0[i] || w > c1[i]) return;
+    KZ_CHECK(i < K && hoff[i] + (w - c0[i] + 1) * CH <= pl.hcap, "wide: projected piece inside H");
     const float4* hp = H4 + ((hoff[i] + (w - c0[i]) * CH + 2 * a) >> 1);
 #pragma unroll
     for (int j = 0; j < E / 2; ++j) {
@@ -817,6 +829,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         auto agg_entry = [&](auto jr, int2 e) {  // y += phi_i h_i on the entry's j range
           constexpr int J0 = decltype(jr)::lo, J1 = decltype(jr)::hi;
           const int i = e.x >> 20;
+          KZ_CHECK(i < K && (e.x & 0xFFFFF) + CH <= pl.hcap, "wide: aggregated piece inside H");
           const T p0 = Phi[xs(i, g)], p1 = Phi[xs(i, g + 16)];
           const float4* hp = H4 + (((e.x & 0xFFFFF) + 2 * a) >> 1);
 #pragma unroll
