@@ -97,7 +97,7 @@ struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
   size_t rowS, rowL, rvo, c0, c1, en, ien, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, blk, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
-      misc, mbar, total;
+      misc, mbar, sptr, setn, setc, setspan, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -114,8 +114,8 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nlcap = K < pcap ? K : pcap;
   if (rcap > 0 && rcap < p.nlcap) p.nlcap = rcap;
   const int KW = (K + 31) / 32;
-  const bool ogrk = scheme == KZ_VR_OGRK, oahk = scheme == KZ_VR_OAHK;
-  const bool agg = scheme == KZ_AHK || oahk, greedy = !agg;  // arrays only one family touches are sized 0
+  const bool ogrk = scheme == KZ_VR_OGRK, oahk = scheme == KZ_VR_OAHK, gog = scheme == KZ_VR_OAHK_G;
+  const bool agg = scheme == KZ_AHK || oahk || gog, greedy = !agg;  // arrays only one family touches are sized 0
   size_t o = 0;
   p.rowS = o; o = al(o + 4 * K);
   p.rowL = o; o = al(o + 4 * K);
@@ -169,6 +169,12 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.flops = o; o = al(o + 8 * G);
   p.misc = o; o = al(o + 64);
   p.mbar = o; o = al(o + 8);
+  // grouped vr-oahk: per-warp list offsets of every row set (orthogonal groups, then aggregation blocks; at most K
+  // sets) and per-set row count, sum of 8 |Gamma_i| and support union (flop charges)
+  p.sptr = o; o = al(o + (gog ? 4 * (size_t)W * (K + 1) : 0));
+  p.setn = o; o = al(o + (gog ? 4 * (size_t)K : 0));
+  p.setc = o; o = al(o + (gog ? 8 * (size_t)K : 0));
+  p.setspan = o; o = al(o + (gog ? 4 * (size_t)K : 0));
   p.total = o;
   return p;
 }
@@ -224,8 +230,9 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   constexpr int E = CH / NA;           // antennas per thread per chunk
   auto xo = [](int il, int gg) { return clu::xo<G>(il, gg); };
   using T = float2;
-  constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK;
+  constexpr bool AGG = SCH == KZ_AHK || SCH == KZ_VR_OAHK || SCH == KZ_VR_OAHK_G;
   constexpr bool GREEDY = SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_VR_OGRK;
+  constexpr bool GRP = SCH == KZ_VR_OAHK_G;  // grouped vr-oahk (oracle/grouped.py): row sets in order
 
   extern __shared__ __align__(128) unsigned char sm[];
   const int K = p.P.n_users, Nt = p.P.n_antennas;
@@ -322,6 +329,10 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     inset[i] = 0;
   }
   if (AGG && p.P.orth_ptr && tid == 0) {  // partition ranges read alongside the rows (one latency round)
+    if (GRP) {
+      misc[12] = p.P.ogrp_sys[b];
+      misc[13] = p.P.ogrp_sys[b + 1];
+    }
     misc[8] = p.P.orth_ptr[b];
     misc[9] = p.P.orth_ptr[b + 1];
     misc[10] = p.P.non_ptr[b];
@@ -329,7 +340,14 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   }
   __syncthreads();
   KZ_SETUP_MARK(0);
-  if (AGG && p.P.orth_ptr) {
+  if (GRP) {  // set ids: 1 + group index for the orthogonal groups, then one per block of agg_cap N rows
+    const int g0s = misc[12], ngs = misc[13] - misc[12], cap = p.P.agg_cap > 0 ? p.P.agg_cap : K;
+    for (int gi = 0; gi < ngs; ++gi)
+      for (int q = p.P.ogrp_ptr[g0s + gi] + tid; q < p.P.ogrp_ptr[g0s + gi + 1]; q += nthr)
+        inset[p.P.orth_idx[q]] = (uint8_t)(1 + gi);
+    for (int q = misc[10] + tid; q < misc[11]; q += nthr) inset[p.P.non_idx[q]] = (uint8_t)(1 + ngs + (q - misc[10]) / cap);
+    if (tid == 0) misc[14] = ngs + (misc[11] - misc[10] + cap - 1) / cap;
+  } else if (AGG && p.P.orth_ptr) {
     for (int q = misc[8] + tid; q < misc[9]; q += nthr) inset[p.P.orth_idx[q]] = 1;
     for (int q = misc[10] + tid; q < misc[11]; q += nthr) inset[p.P.non_idx[q]] = 2;
   }
@@ -465,7 +483,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   KZ_SETUP_MARK(3);
   // per-chunk piece lists (ascending rows): all rows (lst) and, for vr-oahk, the O rows then the N rows
   // (olst / nlst share one array); one counting pass and one fill pass for all of them
-  const bool want_all = SCH != KZ_VR_OAHK || residual;
+  const bool want_all = (SCH != KZ_VR_OAHK && !GRP) || residual;
   constexpr bool want_on = SCH == KZ_VR_OAHK;
   // H element offset of local row n's piece on local warp ww (l0: the row's first local warp)
   auto hoff_of = [&](int n, int ww, int l0) -> int {
@@ -543,6 +561,68 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
       qa += __popc(ba);
       qo += __popc(bo);
       qn += __popc(bn);
+    }
+  }
+  int* sptr = (int*)(sm + pl.sptr);
+  int* setn = (int*)(sm + pl.setn);
+  long long* setc = (long long*)(sm + pl.setc);
+  int* setspan = (int*)(sm + pl.setspan);
+  const int nset = GRP ? misc[14] : 0, ngs = GRP ? misc[13] - misc[12] : 0;
+  if constexpr (GRP) {
+    if (nset > K || nset > 254) __trap();  // set ids are uint8 and the tables hold K sets
+    // one list per warp, ordered by set (one ballot pass per set), sptr[w (K+1) + s] = start of set s + 1
+    int tot = 0;
+    for (int base = 0; base < NL; base += 32) {
+      const int n = base + lane;
+      const bool ov = n < NL && (lcc[n] & 0xFF) <= w && w <= (lcc[n] >> 8);
+      tot += __popc(__ballot_sync(FULL, ov));
+    }
+    if (lane == 0) lptr[w + 1] = tot;
+    __syncthreads();
+    if (tid == 0) {
+      lptr[0] = 0;
+      for (int ww = 0; ww < W; ++ww) lptr[ww + 1] += lptr[ww];
+    }
+    __syncthreads();
+    int q = lptr[w];
+    for (int st = 1; st <= nset; ++st) {
+      if (lane == 0) sptr[w * (K + 1) + st - 1] = q;
+      for (int base = 0; base < NL; base += 32) {
+        const int n = base + lane;
+        const int l0 = n < NL ? (lcc[n] & 0xFF) : 0;
+        const bool ov = n < NL && l0 <= w && w <= (lcc[n] >> 8) && inset[lrow[n]] == st;
+        const unsigned bal = __ballot_sync(FULL, ov);
+        if (ov) lst[q + __popc(bal & ((1u << lane) - 1))] = entry(n, l0);
+        q += __popc(bal);
+      }
+    }
+    if (lane == 0) sptr[w * (K + 1) + nset] = q;
+    KZ_CHECK(q == lptr[w + 1], "cluster grouped: every piece in one set");
+    // per set (warp per set): rows, sum of 8 |Gamma_i| and the union of the supports (coverage bitmap, lane = word)
+    for (int st = w; st < nset; st += W) {
+      int n = 0, cnt = 0;
+      long long c8 = 0;
+      for (int w0 = 0; w0 < Nt / 32; w0 += 32) {
+        const int wd = w0 + lane;
+        uint32_t bits = 0;
+        for (int i = 0; i < K; ++i) {
+          if (inset[i] != st + 1) continue;
+          if (w0 == 0) {
+            n += 1;
+            c8 += 8LL * rowL[i];
+          }
+          const int lo = max(rowS[i], 32 * wd), hi = min(rowS[i] + rowL[i], 32 * wd + 32);
+          if (lo < hi) bits |= (hi - lo == 32 ? ~0u : ((1u << (hi - lo)) - 1u)) << (lo - 32 * wd);
+        }
+        if (wd < Nt / 32) cnt += __popc(bits);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+      if (lane == 0) {
+        setn[st] = n;
+        setc[st] = c8;
+        setspan[st] = cnt;
+      }
     }
   }
   KZ_SETUP_MARK(4);
@@ -669,9 +749,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
       if (o == c) *dst = v; else st_remote(dst, o, v);
     }
   };
-  auto refresh = [&](const int* ptr, const int2* L) {
-    int q = ptr[w];
-    const int q1 = ptr[w + 1];
+  auto refresh_range = [&](int q, const int q1, const int2* L) {
     for (; q + 3 < q1; q += 4) {  // four pieces in flight
       const int2 e0 = L[q], e1 = L[q + 1], e2 = L[q + 2], e3 = L[q + 3];
       const T v0 = dot16(e0.x & 0xFFFFF);
@@ -692,6 +770,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     }
     if (q < q1) deliver(L[q], dot16(L[q].x & 0xFFFFF));
   };
+  auto refresh = [&](const int* ptr, const int2* L) { refresh_range(ptr[w], ptr[w + 1], L); };
   // owner: residual of owned row il for rhs gg from the slice sums (fixed slice order)
   auto oresid = [&](int il, int gg, bool dense) -> T {
     const int i = o_lo + il;
@@ -809,6 +888,148 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     if (SCH == KZ_GK) return dense_refresh + 4LL * K;
     if (SCH == KZ_GRK) return dense_refresh + 4LL * K + 2;
     return (prevv[gg] >= 0 ? cost[prevv[gg]] : 0) + 4LL * K + 2;
+  };
+  // aggregated projection over the list entries [q0, q1) (solvers.py:257-309): y = sum_i phi_i h_i (ascending
+  // rows), den = ||y||^2 + xi ||phi||^2 from fixed-order reductions over warps and CTAs, then m += gamma y and the
+  // owners' q += gamma phi over their rows of set qset (0: every row); nrows / ycost / span: the ahk_step charges
+  auto agg_step = [&](int q0, const int q1, const int2* L, int nrows, long long ycost, int span, int qset) {
+      T y0[E], y1[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
+      int q = q0;
+      for (; q + 1 < q1; q += 2) {  // two pieces in flight
+        const int e0 = L[q].x, e1 = L[q + 1].x, n0 = e0 >> 20, n1 = e1 >> 20;
+        KZ_CHECK(n0 < pl.nlcap && n1 < pl.nlcap && (e0 & 0xFFFFF) + CH <= hcap_el && (e1 & 0xFFFFF) + CH <= hcap_el,
+                 "cluster: aggregated pieces inside H / Phl");
+        const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
+        const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + LPA];
+        const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
+        const float4* hp1 = H4 + ((e1 & 0xFFFFF) >> 1) + a;
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+          const float4 h0 = ldh(hp0 + NA * j), h1 = ldh(hp1 + NA * j);
+          const int k = 2 * j;
+          y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
+          y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
+          y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
+          y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
+          y0[k] = cfma(p10, make_float2(h1.x, h1.y), y0[k]);
+          y0[k + 1] = cfma(p10, make_float2(h1.z, h1.w), y0[k + 1]);
+          y1[k] = cfma(p11, make_float2(h1.x, h1.y), y1[k]);
+          y1[k + 1] = cfma(p11, make_float2(h1.z, h1.w), y1[k + 1]);
+        }
+      }
+      if (q < q1) {
+        const int e0 = L[q].x, n0 = e0 >> 20;
+        const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
+        const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+          const float4 h0 = ldh(hp0 + NA * j);
+          const int k = 2 * j;
+          y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
+          y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
+          y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
+          y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
+        }
+      }
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        s0 = fmaf(y0[k].x, y0[k].x, fmaf(y0[k].y, y0[k].y, s0));
+        s1 = fmaf(y1[k].x, y1[k].x, fmaf(y1[k].y, y1[k].y, s1));
+      }
+#pragma unroll
+      for (int o = LPA; o < 32; o <<= 1) {
+        s0 += __shfl_xor_sync(FULL, s0, o);
+        s1 += __shfl_xor_sync(FULL, s1, o);
+      }
+      if (a == 0) {
+        Dp[w * G + g] = s0;
+        Dp[w * G + g + LPA] = s1;
+      }
+      __syncthreads();
+      if (tid < G) {
+        float dy = 0.f;
+        for (int ww = 0; ww < W; ++ww) dy += Dp[ww * G + tid];
+        for (int d = 0; d < CL; ++d) {
+          float* dst = DY + c * G + tid;
+          if (d == c) *dst = dy; else st_remote(dst, d, dy);
+        }
+      }
+      cluster_sync();
+      KZ_PHASE();
+      // step length per rhs (identical in every CTA: fixed-order sums of the pushed partials)
+      if (tid < G) {
+        const int gg = tid;
+        bool live = livev[gg];
+        if (SCH == KZ_AHK) {
+          live = false;
+          if (!donev[gg]) {
+            float n2 = 0.f;
+            for (int d = 0; d < CL; ++d) n2 += AG4[d * G + gg].w;
+            if (!stop_test(gg, n2)) {
+              live = true;
+              flv[gg] += dense_refresh + 2LL * K;
+            }
+          }
+          livev[gg] = live;
+        }
+        stepv[gg] = 0;
+        if (live) {
+          float nx = 0.f, ny = 0.f, sp = 0.f, den = 0.f;
+          int nz = 0;
+          for (int d = 0; d < CL; ++d) {
+            const float4 v = AG4[d * G + gg];
+            nx += v.x; ny += v.y; sp += v.z; nz |= NZP[d * G + gg];
+            den += DY[d * G + gg];
+          }
+          den = fmaf(regf, sp, den);
+          const int n = nrows;
+          if (SCH != KZ_AHK) flv[gg] += 2LL * nrows;  // aggregation_weights charge
+          bool step = false;
+          if (nz && n > 0) {
+            long long f = 6LL * n + 2LL * max(n - 1, 0) + ycost + 4LL * span + 3LL * n + 2;
+            if (den != 0.f) {
+              step = true;
+              f += 2 + 8LL * span + 8LL * n;
+              GAMv[gg] = make_float2(nx / den, ny / den);
+            }
+            flv[gg] += f;
+          }
+          if (step) {
+            stepv[gg] = 1;
+            if (SCH == KZ_AHK) itv[gg] += 1;
+          } else {
+            noopv[gg] += 1;
+            if (SCH == KZ_AHK) {  // ahk_step returned False: InstanceRun.done (solvers.py:407-413)
+              donev[gg] = 1;
+              sdone[gg] = 1;
+              if (residual) {
+                nchk[gg] += 1;
+                convv[gg] = 1;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (stepv[g]) {
+        const T gm = GAMv[g];
+#pragma unroll
+        for (int k = 0; k < E; ++k) m0[k] = cfma(gm, y0[k], m0[k]);
+      }
+      if (stepv[g + LPA]) {
+        const T gm = GAMv[g + LPA];
+#pragma unroll
+        for (int k = 0; k < E; ++k) m1[k] = cfma(gm, y1[k], m1[k]);
+      }
+      // owner: q += gamma phi over its aggregated rows
+      for (int e = tid; e < nown * G; e += nthr) {
+        const int il = e / G, gg = e % G;
+        if (!stepv[gg] || (qset > 0 && inset[o_lo + il] != qset)) continue;
+        Qo[xo(il, gg)] = cfma(GAMv[gg], Fo[xo(il, gg)], Qo[xo(il, gg)]);
+      }
   };
   int t;
   for (t = 1;; ++t) {
@@ -1013,6 +1234,49 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
       owner_weights(0, false);
       cluster_sync();
       KZ_PHASE();
+    } else if constexpr (GRP) {  // grouped VR-OAHK (oracle/grouped.py GroupedRun.step), fixed T
+      for (int gg = tid; gg < G; gg += nthr) livev[gg] = !donev[gg];
+      __syncthreads();
+      const int* sp = sptr + w * (K + 1);
+      for (int st = 1; st <= nset; ++st) {
+        refresh_range(sp[st - 1], sp[st], lst);
+        cluster_sync();
+        if (st <= ngs) {  // orthogonal group: exact block projection (solvers.py:312-332)
+          for (int pair = w; pair < G / 2; pair += W) {
+            const int gg = pair + hf * (G / 2);
+            if (livev[gg])
+              for (int il = hl; il < nown; il += 16) {
+                const int i = o_lo + il;
+                if (inset[i] != st) continue;
+                const T r = oresid(il, gg, false);
+                const T gm = make_float2(r.x * ien[i], r.y * ien[i]);
+                Fo[xo(il, gg)] = gm;
+                push_phi(il, gg, gm);
+              }
+          }
+          cluster_sync();
+          for (int e = tid; e < nown * G; e += nthr) {
+            const int il = e / G, gg = e % G;
+            if (inset[o_lo + il] != st || !livev[gg]) continue;
+            const T gm = Fo[xo(il, gg)], q = Qo[xo(il, gg)];
+            Qo[xo(il, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
+          }
+          const bool l0v = livev[g], l1v = livev[g + LPA];
+          for (int q = sp[st - 1]; q < sp[st]; ++q) {
+            const int n = lst[q].x >> 20;
+            if (l0v) project(m0, n, Phl[n * G + g]);
+            if (l1v) project(m1, n, Phl[n * G + g + LPA]);
+          }
+          if (tid < G && livev[tid]) flv[tid] += 2 * (setc[st - 1] + 4LL * setn[st - 1]);
+        } else {  // block of <= agg_cap rows: refresh, weights, aggregated step (solvers.py:417-421, 248-309)
+          if (tid < G && livev[tid]) flv[tid] += setc[st - 1] + 4LL * setn[st - 1];
+          owner_weights(st, true);
+          cluster_sync();
+          agg_step(sp[st - 1], sp[st], lst, setn[st - 1], setc[st - 1], setspan[st - 1], st);
+        }
+        __syncthreads();
+      }
+      if (tid < G && livev[tid]) itv[tid] += 1;
     } else {  // VR-OAHK (solvers.py:414-421)
       // orthogonal group O: exact block projection (solvers.py:312-332); residual mode refreshes every row
       if (residual) refresh(lptr, lst); else refresh(optr, olst);
@@ -1081,153 +1345,11 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
         KZ_PHASE();
       }
     }
-    if constexpr (AGG) {
-      // aggregated projection (solvers.py:257-309): y = sum_i phi_i h_i over the rows (ascending),
-      // den = ||y||^2 + xi ||phi||^2 from fixed-order reductions over warps and CTAs
-      if (SCH == KZ_AHK || nN > 0) {
-        const int* ptr = SCH == KZ_AHK ? lptr : nptr;
-        const int2* L = SCH == KZ_AHK ? lst : nlst;
-        T y0[E], y1[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k) y0[k] = y1[k] = make_float2(0.f, 0.f);
-        int q = ptr[w];
-        const int q1 = ptr[w + 1];
-        for (; q + 1 < q1; q += 2) {  // two pieces in flight
-          const int e0 = L[q].x, e1 = L[q + 1].x, n0 = e0 >> 20, n1 = e1 >> 20;
-          KZ_CHECK(n0 < pl.nlcap && n1 < pl.nlcap && (e0 & 0xFFFFF) + CH <= hcap_el && (e1 & 0xFFFFF) + CH <= hcap_el,
-                   "cluster: aggregated pieces inside H / Phl");
-          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
-          const T p10 = Phl[n1 * G + g], p11 = Phl[n1 * G + g + LPA];
-          const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
-          const float4* hp1 = H4 + ((e1 & 0xFFFFF) >> 1) + a;
-#pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
-            const float4 h0 = ldh(hp0 + NA * j), h1 = ldh(hp1 + NA * j);
-            const int k = 2 * j;
-            y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
-            y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
-            y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
-            y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
-            y0[k] = cfma(p10, make_float2(h1.x, h1.y), y0[k]);
-            y0[k + 1] = cfma(p10, make_float2(h1.z, h1.w), y0[k + 1]);
-            y1[k] = cfma(p11, make_float2(h1.x, h1.y), y1[k]);
-            y1[k + 1] = cfma(p11, make_float2(h1.z, h1.w), y1[k + 1]);
-          }
-        }
-        if (q < q1) {
-          const int e0 = L[q].x, n0 = e0 >> 20;
-          const T p00 = Phl[n0 * G + g], p01 = Phl[n0 * G + g + LPA];
-          const float4* hp0 = H4 + ((e0 & 0xFFFFF) >> 1) + a;
-#pragma unroll
-          for (int j = 0; j < E / 2; ++j) {
-            const float4 h0 = ldh(hp0 + NA * j);
-            const int k = 2 * j;
-            y0[k] = cfma(p00, make_float2(h0.x, h0.y), y0[k]);
-            y0[k + 1] = cfma(p00, make_float2(h0.z, h0.w), y0[k + 1]);
-            y1[k] = cfma(p01, make_float2(h0.x, h0.y), y1[k]);
-            y1[k + 1] = cfma(p01, make_float2(h0.z, h0.w), y1[k + 1]);
-          }
-        }
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-          s0 = fmaf(y0[k].x, y0[k].x, fmaf(y0[k].y, y0[k].y, s0));
-          s1 = fmaf(y1[k].x, y1[k].x, fmaf(y1[k].y, y1[k].y, s1));
-        }
-#pragma unroll
-        for (int o = LPA; o < 32; o <<= 1) {
-          s0 += __shfl_xor_sync(FULL, s0, o);
-          s1 += __shfl_xor_sync(FULL, s1, o);
-        }
-        if (a == 0) {
-          Dp[w * G + g] = s0;
-          Dp[w * G + g + LPA] = s1;
-        }
-        __syncthreads();
-        if (tid < G) {
-          float dy = 0.f;
-          for (int ww = 0; ww < W; ++ww) dy += Dp[ww * G + tid];
-          for (int d = 0; d < CL; ++d) {
-            float* dst = DY + c * G + tid;
-            if (d == c) *dst = dy; else st_remote(dst, d, dy);
-          }
-        }
-        cluster_sync();
-        KZ_PHASE();
-        // step length per rhs (identical in every CTA: fixed-order sums of the pushed partials)
-        if (tid < G) {
-          const int gg = tid;
-          bool live = livev[gg];
-          if (SCH == KZ_AHK) {
-            live = false;
-            if (!donev[gg]) {
-              float n2 = 0.f;
-              for (int d = 0; d < CL; ++d) n2 += AG4[d * G + gg].w;
-              if (!stop_test(gg, n2)) {
-                live = true;
-                flv[gg] += dense_refresh + 2LL * K;
-              }
-            }
-            livev[gg] = live;
-          }
-          stepv[gg] = 0;
-          if (live) {
-            float nx = 0.f, ny = 0.f, sp = 0.f, den = 0.f;
-            int nz = 0;
-            for (int d = 0; d < CL; ++d) {
-              const float4 v = AG4[d * G + gg];
-              nx += v.x; ny += v.y; sp += v.z; nz |= NZP[d * G + gg];
-              den += DY[d * G + gg];
-            }
-            den = fmaf(regf, sp, den);
-            const int n = SCH == KZ_AHK ? K : nN;
-            if (SCH == KZ_VR_OAHK) flv[gg] += 2LL * nN;  // aggregation_weights charge
-            const long long ycost = SCH == KZ_AHK ? 6LL * Nt * K + 2LL * Nt * max(K - 1, 0) : costN;
-            const int span = SCH == KZ_AHK ? Nt : unionN;
-            bool step = false;
-            if (nz && n > 0) {
-              long long f = 6LL * n + 2LL * max(n - 1, 0) + ycost + 4LL * span + 3LL * n + 2;
-              if (den != 0.f) {
-                step = true;
-                f += 2 + 8LL * span + 8LL * n;
-                GAMv[gg] = make_float2(nx / den, ny / den);
-              }
-              flv[gg] += f;
-            }
-            if (step) {
-              stepv[gg] = 1;
-              if (SCH == KZ_AHK) itv[gg] += 1;
-            } else {
-              noopv[gg] += 1;
-              if (SCH == KZ_AHK) {  // ahk_step returned False: InstanceRun.done (solvers.py:407-413)
-                donev[gg] = 1;
-                sdone[gg] = 1;
-                if (residual) {
-                  nchk[gg] += 1;
-                  convv[gg] = 1;
-                }
-              }
-            }
-          }
-        }
-        __syncthreads();
-        if (stepv[g]) {
-          const T gm = GAMv[g];
-#pragma unroll
-          for (int k = 0; k < E; ++k) m0[k] = cfma(gm, y0[k], m0[k]);
-        }
-        if (stepv[g + LPA]) {
-          const T gm = GAMv[g + LPA];
-#pragma unroll
-          for (int k = 0; k < E; ++k) m1[k] = cfma(gm, y1[k], m1[k]);
-        }
-        // owner: q += gamma phi over its aggregated rows
-        for (int e = tid; e < nown * G; e += nthr) {
-          const int il = e / G, gg = e % G;
-          if (!stepv[gg] || (SCH == KZ_VR_OAHK && inset[o_lo + il] != 2)) continue;
-          Qo[xo(il, gg)] = cfma(GAMv[gg], Fo[xo(il, gg)], Qo[xo(il, gg)]);
-        }
-      }
+    if constexpr (AGG && SCH != KZ_VR_OAHK_G) {
+      if (SCH == KZ_AHK)
+        agg_step(lptr[w], lptr[w + 1], lst, K, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0), Nt, 0);
+      else if (nN > 0)
+        agg_step(nptr[w], nptr[w + 1], nlst, nN, costN, unionN, 2);
     }
     __syncthreads();
     KZ_PHASE();
@@ -1341,11 +1463,14 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
                               int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
   static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr || getenv("KZ_DISABLE_CLUSTER") != nullptr;
   if (disabled || resume || P.dtype != KZ_C64) return 0;
-  if (!(scheme == KZ_GK || scheme == KZ_GRK || scheme == KZ_VR_OGRK || scheme == KZ_AHK || scheme == KZ_VR_OAHK))
+  if (!(scheme == KZ_GK || scheme == KZ_GRK || scheme == KZ_VR_OGRK || scheme == KZ_AHK || scheme == KZ_VR_OAHK ||
+        scheme == KZ_VR_OAHK_G))
     return 0;
   const bool lockstep = S.mode == KZ_STOP_LOCKSTEP && S.epsilon == 0.0;
   const bool resid = S.mode == KZ_STOP_RESIDUAL && S.epsilon > 0.0;
   if (!(lockstep || resid) || S.max_iters < 1 || S.check_every < 1) return 0;
+  // grouped vr-oahk: fixed T only (the cfg3 workload), set ids fit uint8; residual / NMSE runs take the generic kernel
+  if (scheme == KZ_VR_OAHK_G && (!lockstep || P.n_users > 254 || !P.ogrp_sys || !P.ogrp_ptr)) return 0;
   if (O.nmse_trace || O.resid_trace || O.flops_trace || S.rhs_mask) return 0;
   if (!(P.flags & KZ_PROBLEM_CONTIGUOUS) || P.max_support < 1 || P.n_antennas % clu::CH != 0) return 0;
   const bool stochastic = scheme == KZ_GRK || scheme == KZ_VR_OGRK;
@@ -1365,7 +1490,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   // streamed (ST) candidates first when enabled: H_eff read through L1 / L2, two CTAs per SM; they need the padded
   // copy in the workspace (kz_solve_workspace_bytes_for reports it), 20-bit piece offsets and, for the aggregation
   // schemes, 16 rhs (m and y of 32 rhs do not fit the 128 registers of two CTAs per SM)
-  const bool agg_scheme = scheme == KZ_AHK || scheme == KZ_VR_OAHK;
+  const bool agg_scheme = scheme == KZ_AHK || scheme == KZ_VR_OAHK || scheme == KZ_VR_OAHK_G;
   Cand cands[7] = {{32, 8, 0, 0, 0, 0, 0, true, true}, {16, 8, 0, 0, 0, 0, 0, true, true},
                    {32, 8}, {16, 8}, {16, 4}, {16, 4}, {32, 4}};
   const size_t two = (size_t)(smsm / 2 - 1024);
@@ -1446,6 +1571,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
       case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 32, false>(a, W, CL, smem, s); break;
       case KZ_AHK: rc = cluster_launch<KZ_AHK, 32, false>(a, W, CL, smem, s); break;
       case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 32, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK_G: rc = cluster_launch<KZ_VR_OAHK_G, 32, false>(a, W, CL, smem, s); break;
     }
   } else {
     switch (scheme) {
@@ -1454,6 +1580,7 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
       case KZ_VR_OGRK: rc = cluster_launch<KZ_VR_OGRK, 16, false>(a, W, CL, smem, s); break;
       case KZ_AHK: rc = cluster_launch<KZ_AHK, 16, false>(a, W, CL, smem, s); break;
       case KZ_VR_OAHK: rc = cluster_launch<KZ_VR_OAHK, 16, false>(a, W, CL, smem, s); break;
+      case KZ_VR_OAHK_G: rc = cluster_launch<KZ_VR_OAHK_G, 16, false>(a, W, CL, smem, s); break;
     }
   }
   if (rc == 1) *launches = (lockstep ? 2 : 1) + (ST ? 1 : 0);
