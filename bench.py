@@ -64,26 +64,56 @@ def parse():
 
 # --------------------------------------------------------------------------- CPU reference leg
 
+REF_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+
+
+def reference_kind() -> str:
+    """"reference" when the unmodified kaczprec package is installed in baseline/_ref (python -m pip install
+    --no-index --no-build-isolation --no-deps --target baseline/_ref <copy of /root/reference/pkg>; git-ignored, it
+    travels to the GPU box with the snapshot), else "port" (oracle/, pinned bitwise to the reference)."""
+    return "reference" if os.path.isdir(os.path.join(REF_DIR, "kaczprec")) else "port"
+
+
 def _cpu_task(args):
-    """One (scheme, realization) precoder with the oracle port: RZF + solve + assembly + metrics."""
-    cfg_name, seed, scheme, iters = args
+    """One (scheme, realization) precoder on the CPU: RZF + solve + assembly + metrics, with the reference's own
+    kaczprec (kind "reference") or the oracle port (kind "port"), through the same public calls."""
+    cfg_name, seed, scheme, iters, kind = args
     from threadpoolctl import threadpool_limits
     with threadpool_limits(1):
-        import oracle as O
+        if kind == "reference":
+            if REF_DIR not in sys.path:
+                sys.path.insert(0, REF_DIR)
+            import kaczprec.assembly as KA
+            import kaczprec.channel as KC
+            import kaczprec.metrics as KM
+            import kaczprec.rzf as KR
+            import kaczprec.solvers as KS
+
+            def region(s, ln, nt):
+                return KC.VisibilityRegion(frozenset(range(s, s + ln)), nt, 1)
+            ArrayConfig, ChannelMatrix, AugmentedSystem = KC.ArrayConfig, KC.ChannelMatrix, KS.AugmentedSystem
+            rzf_precoder, run_precoding, nmse, rate = KR.rzf_precoder, KS.run_precoding, KM.nmse, \
+                KM.spectral_efficiency
+            del KA
+        else:
+            import oracle as O
+            region, ArrayConfig, ChannelMatrix, AugmentedSystem = (O.contiguous_region, O.ArrayConfig,
+                                                                    O.ChannelMatrix, O.AugmentedSystem)
+            rzf_precoder, run_precoding, nmse, rate = O.rzf_precoder, O.run_precoding, O.nmse, O.spectral_efficiency
         from paper_2501_10689_b200.channel import CONFIGS, generate, solver_seed_sequence
         cfg = CONFIGS[cfg_name]
         ch = generate(cfg, [seed])
         nt, k = ch.n_antennas, ch.n_users
-        vrs = tuple(O.contiguous_region(int(ch.start[0, i]), int(ch.length[0, i]), nt) for i in range(k))
-        chan = O.ChannelMatrix(h=ch.dense(0), vrs=vrs, cfg=O.ArrayConfig(nt, cfg.carrier_freq, nt))
+        vrs = tuple(region(int(ch.start[0, i]), int(ch.length[0, i]), nt) for i in range(k))
+        chan = ChannelMatrix(h=ch.dense(0), vrs=vrs, cfg=ArrayConfig(nt, cfg.carrier_freq, nt))
         reg = float(ch.reg[0])
-        sys_ = O.AugmentedSystem.from_channel(chan, reg)  # preprocessing, untimed (as the GPU batch build)
+        sys_ = AugmentedSystem.from_channel(chan, reg)  # preprocessing, untimed (as the GPU batch build)
         t0 = time.perf_counter()
-        ref = O.rzf_precoder(chan, reg)
-        run = O.run_precoding(scheme, sys_, ref, epsilon=0.0, max_iters=iters,
-                              rng=np.random.default_rng(solver_seed_sequence(seed)))
-        O.nmse(run.precoder.f, ref.f)
-        O.spectral_efficiency(chan.h, run.precoder.f, float(ch.snr_linear[0]))
+        ref = rzf_precoder(chan, reg)
+        run = run_precoding(scheme, sys_, ref, epsilon=0.0, max_iters=iters,
+                            rng=np.random.default_rng(solver_seed_sequence(seed)))
+        nmse(run.precoder.f, ref.f)
+        rate(chan.h, run.precoder.f, float(ch.snr_linear[0]))
         return time.perf_counter() - t0
 
 
@@ -92,11 +122,12 @@ def cpu_reference_steps(cfg_name, schemes, iters, steps, warmup, cores):
     on `cores` worker processes.  Returns (per-step wall times, precoders per step)."""
     import multiprocessing as mp
     r = max(1, cores // len(schemes))
+    kind = reference_kind()
     ctx = mp.get_context("fork")
     walls = []
     with ctx.Pool(processes=min(cores, r * len(schemes))) as pool:
         for s in range(warmup + steps):
-            tasks = [(cfg_name, 10_000 + s * r + j, sc, iters) for j in range(r) for sc in schemes]
+            tasks = [(cfg_name, 10_000 + s * r + j, sc, iters, kind) for j in range(r) for sc in schemes]
             t0 = time.perf_counter()
             pool.map(_cpu_task, tasks, chunksize=1)
             if s >= warmup:
@@ -531,10 +562,12 @@ def main():
                 "scaling": a.scaling, "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
                 "config": {"workload": workload, "sample_per_step": f"{r} realizations x {len(schemes)} schemes",
                            "parallelism": f"process pool x{min(cores, per_step)}"},
-                "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, per_step), "kind": "port",
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, per_step), "kind": reference_kind(),
                                  "sample": f"{r} realizations x {len(schemes)} schemes per step, T={iters}, "
-                                           "oracle/ numpy port of kaczprec (the reference is pure Python and is "
-                                           "not on the GPU box; the port is pinned bitwise to it)"},
+                                           + ("the unmodified kaczprec package from baseline/_ref"
+                                              if reference_kind() == "reference" else
+                                              "oracle/ numpy port of kaczprec (pinned bitwise to the reference; "
+                                              "baseline/_ref not installed)")},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -544,9 +577,11 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not tol:
         cores = host_cores()
         walls, per_step, r = cpu_reference_steps(a.config, schemes, iters, 1, 0, cores)
-        cpu_baseline = {"value": per_step / walls[0], "unit": UNIT, "cores": min(cores, per_step), "kind": "port",
+        kind = reference_kind()
+        cpu_baseline = {"value": per_step / walls[0], "unit": UNIT, "cores": min(cores, per_step), "kind": kind,
                         "sample": f"{r} realization(s) x {len(schemes)} schemes (T={iters}, RZF+solve+assembly+"
-                                  "metrics) with the oracle/ numpy port, one process per precoder"}
+                                  "metrics) with " + ("the unmodified kaczprec from baseline/_ref" if kind == "reference"
+                                                      else "the oracle/ numpy port") + ", one process per precoder"}
 
     import torch
     import torch.distributed as dist
