@@ -160,6 +160,7 @@ template <class T> __device__ __forceinline__ T warp_csum(T v) {
   return v;
 }
 
+__device__ inline double np_pairwise_sum(const double* a, int n);
 // numpy pairwise summation (umath loops, PW_BLOCKSIZE 128, 8-way unroll),
 // evaluated by one thread.  Blocks above 128 split at n/2 rounded down to a
 // multiple of 8, exactly as numpy does.
@@ -176,6 +177,29 @@ __device__ inline double np_pairwise_block(const double* a, int m) {
     for (int j = 0; j < 8; ++j) r[j] += a[i + j];
   double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
   for (int i = full; i < m; ++i) res += a[i];
+  return res;
+}
+// the same sum with the warp: lanes 0..7 run the eight accumulator chains of a block (independent loads, the same
+// additions in the same order), lane 0 combines them and adds the tail -- bitwise np_pairwise_block for n <= 128;
+// result in every lane
+__device__ inline double np_pairwise_sum_warp(const double* a, int n, int lane) {
+  if (n > 128 || n < 8) {
+    double t = 0.0;
+    if (lane == 0) t = np_pairwise_sum(a, n);
+    return __shfl_sync(FULL, t, 0);
+  }
+  const int full = n - (n % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    r = a[lane];
+#pragma unroll 4
+    for (int i = 8 + lane; i < full; i += 8) r += a[i];
+  }
+  double rr[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) rr[j] = __shfl_sync(FULL, r, j);
+  double res = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+  for (int i = full; i < n; ++i) res += a[i];
   return res;
 }
 __device__ inline double np_pairwise_sum(const double* a, int n) {

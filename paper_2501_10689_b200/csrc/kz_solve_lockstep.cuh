@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   auto pick_weighted = [&](int gg, bool& drew) -> int {
     drew = false;
     if constexpr (EXACT) {
+      const double u = draw_u(gg);  // independent of the weights: issued first (read only; drawn iff tot > 0)
       double* wb = scr + (size_t)w * 2 * K;
       double* cb = wb + K;
       for (int i = lane; i < K; i += 32) {
@@ -451,22 +452,30 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         wb[i] = np_abs2((double)r.x, (double)r.y);
       }
       __syncwarp();
-      double tot = 0.0;
-      if (lane == 0) tot = np_pairwise_sum(wb, K);
-      tot = __shfl_sync(FULL, tot, 0);
+      const double tot = np_pairwise_sum_warp(wb, K, lane);
       if (tot == 0.0) return -1;
       for (int i = lane; i < K; i += 32) wb[i] = wb[i] / tot;
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {  // numpy's sequential cumsum; loads batched ahead of the dependent additions
         double acc = 0.0;
-        for (int i = 0; i < K; ++i) {
+        int i = 0;
+        for (; i + 8 <= K; i += 8) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = wb[i + j];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc += v[j];
+            cb[i + j] = acc;
+          }
+        }
+        for (; i < K; ++i) {
           acc += wb[i];
           cb[i] = acc;
         }
       }
       __syncwarp();
       double last = cb[K - 1];
-      double u = draw_u(gg);
       drew = true;
       for (int base = 0; base < K; base += 32) {
         int i = base + lane;
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   // weights, y = sum phi h (ascending rows), den, gamma, update.  (solvers.py:248-309)
   T y[NPT];
   auto aggregate = [&](const int* rows, int n, bool all_rows, const int* cp, const int* cl, int span,
-                       bool dense, bool mark_done) {
+                       bool dense, bool mark_done, long long ysum) {
     // weights phi_i = r_i/e_i, num = vdot(phi, r), ||phi||^2 (warp per rhs)
     for (int gg = w; gg < G; gg += W) {
       if (g0 + gg >= K || donev[gg]) continue;
@@ -611,8 +620,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       }
       long long f = 6LL * n + 2LL * max(n - 1, 0);
       if (dense) f += 6LL * Nt * n + 2LL * Nt * max(n - 1, 0);
-      else
-        for (int k = 0; k < n; ++k) f += 8LL * rowL[all_rows ? k : rows[k]];
+      else f += ysum;  // sum of 8 |Gamma_i| over the rows (formed once per launch)
       f += 4LL * span + 3LL * n + 2;
       double den = 0.0;
       for (int ww = 0; ww < W; ++ww) den += Dp[ww * G + gg];
@@ -645,6 +653,11 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   };
 
   // ---------------------------------------------------------------- iterations
+  // flop charges that depend only on the partition, formed once per launch (not per iteration): ahk_step's y
+  // charge over the non-orthogonal rows (sum of 8 |Gamma_i|) and the orthogonal group's refresh + block step
+  long long ysumN = 0, ysumO2 = 0;
+  for (int k = 0; k < nN; ++k) ysumN += 8LL * rowL[nlist[k]];
+  for (int k = 0; k < nO; ++k) ysumO2 += 2 * (8LL * rowL[olist[k]] + 4);
   int t = 0;
   const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
   const long long dense_rk = 2 + 8LL * Nt + 2;
@@ -772,7 +785,7 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K && !donev[gg]) flv[gg] += dense_refresh;
       __syncthreads(); KZ_PHASE();
-      aggregate(nullptr, K, true, clist_ptr, clist, Nt, true, true);
+      aggregate(nullptr, K, true, clist_ptr, clist, Nt, true, true, 0);
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K && nzv[gg]) itv[gg] += 1;
     } else {  // KZ_VR_OAHK
@@ -789,12 +802,8 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         Rs[xs(i, gg)] = czero<T>();
         Phi[xs(i, gg)] = gm;  // gamma of the block step (P is free here)
       }
-      for (int gg = tid; gg < G; gg += nthr) {
-        if (g0 + gg >= K) continue;
-        long long f = 0;
-        for (int k = 0; k < nO; ++k) f += 2 * (8LL * rowL[olist[k]] + 4);
-        flv[gg] += f;
-      }
+      for (int gg = tid; gg < G; gg += nthr)
+        if (g0 + gg < K) flv[gg] += ysumO2;
       __syncthreads(); KZ_PHASE();
       for (int q = ocl_ptr[w]; q < ocl_ptr[w + 1]; ++q) {
         int i = ocl[q];
@@ -805,14 +814,10 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         refresh_partials(ncl_ptr, ncl);
         __syncthreads(); KZ_PHASE();
         finalize(nlist, nN, false);
-        for (int gg = tid; gg < G; gg += nthr) {
-          if (g0 + gg >= K) continue;
-          long long f = 0;
-          for (int k = 0; k < nN; ++k) f += 8LL * rowL[nlist[k]] + 4;
-          flv[gg] += f;
-        }
+        for (int gg = tid; gg < G; gg += nthr)
+          if (g0 + gg < K) flv[gg] += ysumN + 4LL * nN;  // refresh charge of the N rows
         __syncthreads(); KZ_PHASE();
-        aggregate(nlist, nN, false, ncl_ptr, ncl, p.P.non_union_size[b], false, false);
+        aggregate(nlist, nN, false, ncl_ptr, ncl, p.P.non_union_size[b], false, false, ysumN);
       }
       for (int gg = tid; gg < G; gg += nthr)
         if (g0 + gg < K) itv[gg] += 1;
