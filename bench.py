@@ -436,6 +436,43 @@ def e2e_run(wl, n_steps, seed0, stream, dev_id, warm_compute=True):
             "clocks": clk.summary()}
 
 
+def e2e_drops_run(wl, n_steps, seed0, stream, dev_id):
+    """End to end from the user drops, input preparation included: every step draws the realizations' drops on the
+    host (channel.generate_drops: positions, angles, VR starts; the seeded streams of the reference model), builds
+    the batch on the device (DeviceBatch.from_drops: drop parameters over PCIe, channel synthesis + VR partition
+    by kz_channel_synth / kz_partition_*), runs the step and reads V / NMSE / sum-rate back to pinned host memory.
+    The host work sits inside the CUDA-event interval (the stream waits for it)."""
+    import torch
+    kz = wl.kz
+    copy_stream = torch.cuda.Stream(device=dev_id)
+    outs = wl.out_buffers()
+    d2h = sum(sum(t.numel() * t.element_size() for t in o) for o in outs.values())
+    seeds = range(wl.lo, wl.hi)
+
+    def one(s):
+        drops = kz.generate_drops(wl.cfg, seeds)
+        d = kz.DeviceBatch.from_drops(drops, dtype=wl.dtype, device=dev_id)
+        wl.step(d, seed0 + s, out_host=outs, copy_stream=copy_stream, stream=stream)
+        return drops
+
+    drops = one(0)  # untimed warm-up
+    h2d = sum(v.nbytes for v in vars(drops).values() if isinstance(v, np.ndarray))  # the drop parameters
+    stream.wait_stream(copy_stream)
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    with ClockSampler(dev_id.index or 0) as clk:
+        e0.record(stream)
+        for s in range(1, n_steps + 1):
+            one(s)
+        stream.wait_stream(copy_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    return {"ms_per_step": e0.elapsed_time(e1) / n_steps, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": n_steps, "clocks": clk.summary(),
+            "path": "channel.generate_drops (host) -> DeviceBatch.from_drops (kz_channel_synth + kz_partition) -> "
+                    "rzf_batched -> solve_batch + epilogue per scheme -> V/NMSE/sum-rate to pinned host"}
+
+
 def roofline(wl, per_scheme, iters_by_scheme=None):
     """Dominant launch (largest mean solve time) against the FP32 FMA peak: achieved = algorithmic flops
     (8 x H elements the algorithm streams) / mean launch time (CUDA events on the launch stream)."""
@@ -645,6 +682,10 @@ def main():
         e2e = {"value": len(schemes) * n_total / (e["ms_per_step"] / 1e3), "unit": UNIT, **e,
                "path": "kz.DeviceBatch(pinned, upload stream, one step ahead) -> rzf_batched -> solve_batch + "
                        "epilogue per scheme -> V/NMSE/sum-rate to pinned host (copy stream)"}
+        if world == 1 and a.config == "cfg2":
+            ed = e2e_drops_run(wl, max(1, min(a.steps, 3)), 5500, stream, dev_id)
+            e2e["with_input_preparation"] = {"value": len(schemes) * n_total / (ed["ms_per_step"] / 1e3),
+                                             "unit": UNIT, **ed}
 
     # N=1 sub-records (rank 0, one GPU): the complex128 oracle mode of the same step, and cfg3 / cfg4
     c128 = configs = None
@@ -673,10 +714,10 @@ def main():
                 configs[name] = config_record(name, dev_id, stream, flush, a.config_steps, 1,
                                               do_e2e=not a.no_e2e)
             # BASELINE cfg3's own variant (orthogonal row groups + at most 8 hyperplanes per aggregated step;
-            # no reference counterpart, CPU restatement oracle/grouped.py) on the global-memory kernel, at a
-            # reduced batch (its many sequential sub-steps per iteration run there, ~12x the cluster kernel)
+            # no reference counterpart, CPU restatement oracle/grouped.py) on the cluster kernel's grouped path,
+            # at the config's stated 4096 realizations
             configs["cfg3_grouped"] = config_record("cfg3", dev_id, stream, flush, a.config_steps, 1,
-                                                    do_e2e=not a.no_e2e, n_systems=256, schemes=["vr-oahk-g"],
+                                                    do_e2e=not a.no_e2e, n_systems=4096, schemes=["vr-oahk-g"],
                                                     orth_groups=4, agg_cap=8)
 
     if rank == 0:
