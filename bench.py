@@ -662,7 +662,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(f"{a.config}/{dom}")
+            tj = json.load(fh)  # DRAM bytes per launch (tools/ncu_capture.sh: the cfg2 solve launches)
+            traffic = tj.get(f"{a.config}/{dom}", tj.get(dom) if a.config == "cfg2" else None)
     except (OSError, ValueError):
         pass
     roof["traffic"] = traffic

@@ -14,7 +14,7 @@ $cmd > gpurun_out/ncu/plain_full.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:wide_kernel -c 1 -o gpurun_out/ncu/full_vroahk $cmd \
     > gpurun_out/ncu/full.log 2>&1
 # launch list of the benchmark step
-bcmd="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-c128"
+bcmd="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-c128 --no-configs"
 $bcmd > gpurun_out/ncu/bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches.csv $bcmd \
     > gpurun_out/ncu/launch_run.log 2>&1
