@@ -367,56 +367,58 @@ class DeviceBatch:
         dev = torch.device(device if device is not None else "cuda")
         if dev.type != "cuda":
             raise ValueError("the Kaczmarz path runs on CUDA devices only (no CPU fallback)")
-        lb = _lib.lib()
-        b, k, nt = drops.n_systems, drops.n_users, drops.n_antennas
-        rows = b * k
-        lens = drops.length.reshape(-1).astype(np.int64)
-        val_ptr = np.zeros(rows + 1, dtype=np.int64)
-        np.cumsum(lens, out=val_ptr[1:])
-        # the small host-side arrays (layout hints and CSR of the supports)
-        host = HostBatch(b, k, nt, np.arange(rows + 1, dtype=np.int32), drops.start.reshape(-1).astype(np.int32),
-                         drops.length.reshape(-1).astype(np.int32), val_ptr, np.zeros(0, dtype=np.complex128),
-                         np.zeros(0), np.asarray(drops.reg, dtype=np.float64), np.zeros(0, np.int32),
-                         np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
-                         np.zeros(0, np.int32), np.zeros(0, np.int32), True,
-                         np.asarray(drops.snr_linear, dtype=np.float64))
-        up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a if dt is None else a.astype(dt))).to(dev)  # noqa: E731
-        t = {"row_seg_ptr": up(host.row_seg_ptr), "seg_start": up(host.seg_start), "seg_len": up(host.seg_len),
-             "row_val_ptr": up(val_ptr), "reg": up(host.reg), "snr_linear": up(host.snr_linear)}
-        wl, r0, th = up(drops.wavelength, np.float64), up(drops.r0, np.float64), up(drops.theta, np.float64)
-        kd = _lib.KzDrop()
-        kd.n_systems, kd.n_users, kd.n_antennas = b, k, nt
-        kd.dtype = _lib.KZ_C128 if dtype == "c128" else _lib.KZ_C64
-        kd.element_spacing = float(drops.element_spacing)
-        kd.wavelength, kd.r0, kd.theta = wl.data_ptr(), r0.data_ptr(), th.data_ptr()
-        kd.vr_start, kd.vr_len, kd.reg = t["seg_start"].data_ptr(), t["seg_len"].data_ptr(), t["reg"].data_ptr()
-        cdt = torch.complex128 if dtype == "c128" else torch.complex64
-        t["heff"] = torch.empty(int(val_ptr[-1]), dtype=cdt, device=dev)
-        t["row_energy"] = torch.empty(rows, dtype=torch.float64, device=dev)
+        # everything (uploads, kernels, the one size read-back) on `stream`: a caller can build the next batch on
+        # an upload stream while the compute stream works
         s = stream if stream is not None else torch.cuda.current_stream()
         sp = C.c_void_p(s.cuda_stream)
-        _lib.check(lb.kz_channel_synth(C.byref(kd), t["row_val_ptr"].data_ptr(), t["heff"].data_ptr(),
-                                       t["row_energy"].data_ptr(), sp))
-        ccnt = torch.empty(rows, dtype=torch.int32, device=dev)
-        ocnt = torch.empty(b, dtype=torch.int32, device=dev)
-        t["non_union_size"] = torch.empty(b, dtype=torch.int32, device=dev)
-        inset = torch.empty(rows, dtype=torch.uint8, device=dev)
-        _lib.check(lb.kz_partition_counts(C.byref(kd), ccnt.data_ptr(), ocnt.data_ptr(),
-                                          t["non_union_size"].data_ptr(), inset.data_ptr(), sp))
-        z = torch.zeros(1, dtype=torch.int32, device=dev)
         with torch.cuda.stream(s):
+            lb = _lib.lib()
+            b, k, nt = drops.n_systems, drops.n_users, drops.n_antennas
+            rows = b * k
+            lens = drops.length.reshape(-1).astype(np.int64)
+            val_ptr = np.zeros(rows + 1, dtype=np.int64)
+            np.cumsum(lens, out=val_ptr[1:])
+            # the small host-side arrays (layout hints and CSR of the supports)
+            host = HostBatch(b, k, nt, np.arange(rows + 1, dtype=np.int32), drops.start.reshape(-1).astype(np.int32),
+                             drops.length.reshape(-1).astype(np.int32), val_ptr, np.zeros(0, dtype=np.complex128),
+                             np.zeros(0), np.asarray(drops.reg, dtype=np.float64), np.zeros(0, np.int32),
+                             np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                             np.zeros(0, np.int32), np.zeros(0, np.int32), True,
+                             np.asarray(drops.snr_linear, dtype=np.float64))
+            up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a if dt is None else a.astype(dt))).to(dev)  # noqa: E731
+            t = {"row_seg_ptr": up(host.row_seg_ptr), "seg_start": up(host.seg_start), "seg_len": up(host.seg_len),
+                 "row_val_ptr": up(val_ptr), "reg": up(host.reg), "snr_linear": up(host.snr_linear)}
+            wl, r0, th = up(drops.wavelength, np.float64), up(drops.r0, np.float64), up(drops.theta, np.float64)
+            kd = _lib.KzDrop()
+            kd.n_systems, kd.n_users, kd.n_antennas = b, k, nt
+            kd.dtype = _lib.KZ_C128 if dtype == "c128" else _lib.KZ_C64
+            kd.element_spacing = float(drops.element_spacing)
+            kd.wavelength, kd.r0, kd.theta = wl.data_ptr(), r0.data_ptr(), th.data_ptr()
+            kd.vr_start, kd.vr_len, kd.reg = t["seg_start"].data_ptr(), t["seg_len"].data_ptr(), t["reg"].data_ptr()
+            cdt = torch.complex128 if dtype == "c128" else torch.complex64
+            t["heff"] = torch.empty(int(val_ptr[-1]), dtype=cdt, device=dev)
+            t["row_energy"] = torch.empty(rows, dtype=torch.float64, device=dev)
+            _lib.check(lb.kz_channel_synth(C.byref(kd), t["row_val_ptr"].data_ptr(), t["heff"].data_ptr(),
+                                           t["row_energy"].data_ptr(), sp))
+            ccnt = torch.empty(rows, dtype=torch.int32, device=dev)
+            ocnt = torch.empty(b, dtype=torch.int32, device=dev)
+            t["non_union_size"] = torch.empty(b, dtype=torch.int32, device=dev)
+            inset = torch.empty(rows, dtype=torch.uint8, device=dev)
+            _lib.check(lb.kz_partition_counts(C.byref(kd), ccnt.data_ptr(), ocnt.data_ptr(),
+                                              t["non_union_size"].data_ptr(), inset.data_ptr(), sp))
+            z = torch.zeros(1, dtype=torch.int32, device=dev)
             t["coupled_ptr"] = torch.cat([z, torch.cumsum(ccnt, 0, dtype=torch.int32)])
             t["orth_ptr"] = torch.cat([z, torch.cumsum(ocnt, 0, dtype=torch.int32)])
             t["ogrp_sys"] = torch.arange(b + 1, dtype=torch.int32, device=dev)  # one orthogonal group per system
             t["ogrp_ptr"] = t["orth_ptr"]
             t["non_ptr"] = torch.cat([z, torch.cumsum(k - ocnt, 0, dtype=torch.int32)])
             n_c, n_o = int(t["coupled_ptr"][-1]), int(t["orth_ptr"][-1])  # sizes: one small device->host read
-        t["coupled_idx"] = torch.empty(max(n_c, 1), dtype=torch.int32, device=dev)
-        t["orth_idx"] = torch.empty(max(n_o, 1), dtype=torch.int32, device=dev)
-        t["non_idx"] = torch.empty(max(rows - n_o, 1), dtype=torch.int32, device=dev)
-        _lib.check(lb.kz_partition_fill(C.byref(kd), t["coupled_ptr"].data_ptr(), t["orth_ptr"].data_ptr(),
-                                        t["non_ptr"].data_ptr(), t["coupled_idx"].data_ptr(),
-                                        t["orth_idx"].data_ptr(), t["non_idx"].data_ptr(), sp))
+            t["coupled_idx"] = torch.empty(max(n_c, 1), dtype=torch.int32, device=dev)
+            t["orth_idx"] = torch.empty(max(n_o, 1), dtype=torch.int32, device=dev)
+            t["non_idx"] = torch.empty(max(rows - n_o, 1), dtype=torch.int32, device=dev)
+            _lib.check(lb.kz_partition_fill(C.byref(kd), t["coupled_ptr"].data_ptr(), t["orth_ptr"].data_ptr(),
+                                            t["non_ptr"].data_ptr(), t["coupled_idx"].data_ptr(),
+                                            t["orth_idx"].data_ptr(), t["non_idx"].data_ptr(), sp))
         obj = cls.__new__(cls)
         obj.host, obj.dtype, obj.device, obj.t = host, dtype, dev, t
         obj._drop_keep = (wl, r0, th, ccnt, ocnt, inset)
