@@ -269,7 +269,8 @@ class Workload:
         self.dev_id = dev_id
         self.tol = cfg.extra.get("residual_tol")
         self.iters = cfg.n_iters
-        seeds = range(lo, hi)
+        # one drop per realization; a wideband config (cfg5) is one drop whose subcarriers are the systems
+        seeds = [0, range(lo, hi)] if cfg.n_subcarriers > 1 else range(lo, hi)
         if device_inputs:  # drops -> channel entries + VR partition on the device
             self.host = None
             self.dev = kz.DeviceBatch.from_drops(kz.generate_drops(cfg, seeds), dtype=dtype, device=dev_id)
@@ -512,11 +513,14 @@ def roofline(wl, per_scheme, iters_by_scheme=None):
 
 
 def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2e=True, chunk=4096, n_systems=0,
-                  schemes=None, orth_groups=1, agg_cap=0):
-    """A BASELINE config other than the headline at its stated size on this GPU (N=1 sub-record)."""
+                  schemes=None, orth_groups=1, agg_cap=0, iters=0):
+    """A BASELINE config other than the headline at its stated size on this GPU (N=1 sub-record); iters > 0
+    overrides the config's T (cfg5's iteration-count sweep)."""
     import torch
     import paper_2501_10689_b200 as kz
     cfg = kz.CONFIGS[name]
+    if iters:
+        cfg = type(cfg)(**{**cfg.__dict__, "n_iters": iters})
     schemes = list(schemes or cfg.schemes)
     B = n_systems or cfg.n_systems
     t0 = time.perf_counter()
@@ -737,6 +741,10 @@ def main():
             configs["cfg3_grouped"] = config_record("cfg3", dev_id, stream, flush, a.config_steps, 1,
                                                     do_e2e=not a.no_e2e, n_systems=4096, schemes=["vr-oahk-g"],
                                                     orth_groups=4, agg_cap=8)
+            # cfg5: wideband OFDM, 1024 subcarriers of one drop, AHK and VR-OAHK at each T of its sweep
+            for T in CONFIGS["cfg5"].extra["iter_sweep"]:
+                configs[f"cfg5_T{T}"] = config_record("cfg5", dev_id, stream, flush, a.config_steps, 1,
+                                                      do_e2e=not a.no_e2e, iters=T)
 
     if rank == 0:
         line = {
