@@ -97,7 +97,7 @@ struct Plan {
   int K, W, CL, KO, NS, pcap, nlcap;
   size_t rowS, rowL, rvo, c0, c1, en, ien, inset, loc, cost, cmask, lrow, lh, lcc, lptr, lst, optr, olst, nptr, nlst, H, Qo,
       Ro, Fo, IN, Phl, dloc, dlst, dcnt, blk, AG4, GAMv, stepv, BS, BI, SPP, NZP, DY, Dp, SEL, GAM, done, sdone, live, iters, prev, noop, conv, nchk, flops,
-      misc, mbar, sptr, setn, setc, setspan, total;
+      misc, mbar, sptr, setn, setc, setspan, rhsv, nck, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
@@ -175,6 +175,8 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.setn = o; o = al(o + (gog ? 4 * (size_t)K : 0));
   p.setc = o; o = al(o + (gog ? 8 * (size_t)K : 0));
   p.setspan = o; o = al(o + (gog ? 4 * (size_t)K : 0));
+  p.rhsv = o; o = al(o + 4 * (size_t)G);  // rhs of each slot (residual-mode greedy runs: grouped by |X_c|)
+  p.nck = o; o = al(o + (greedy ? 4 * (size_t)K : 0));
   p.total = o;
   return p;
 }
@@ -196,6 +198,7 @@ struct CluArgs {
   int rcap;     // local rows reserved per CTA (0: min(K, pcap))
   int32_t* tstop;
   const float2* hpad;  // streamed variant: H_eff padded to whole chunks, row r of system b at (b K + r) NS CH
+  int order;  // residual-mode greedy runs: slots take the rhs in ascending order of their coupled-set size
 };
 
 // prepares CluArgs::hpad for the streamed variant: row r's chunk pieces c0_r .. c0_r + NS - 1, zero outside the
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   int* nchk = (int*)(sm + pl.nchk);
   long long* flv = (long long*)(sm + pl.flops);
   int* misc = (int*)(sm + pl.misc);
+  int* rhsv = (int*)(sm + pl.rhsv);  // the rhs (column of V) each slot gg serves; >= K: none
 
   const float regf = (float)p.P.reg[b];
   const T* heff = (const T*)p.P.heff;
@@ -327,6 +331,28 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     en[i] = (float)p.P.row_energy[r];
     ien[i] = (float)(1.0 / p.P.row_energy[r]);
     inset[i] = 0;
+  }
+  // slot -> rhs.  Residual-mode greedy runs: the cluster's G slots take consecutive ranks of a stable ascending sort
+  // of the rhs by coupled-set size |X_c|, which tracks the iteration count to the tolerance (correlation 0.95 at
+  // cfg4, tools/rhs_grouping_probe.py), so a cluster's rhs finish close together (less lockstep waste); every rhs's
+  // arithmetic is unchanged (results bitwise equal to the index order)
+  if (GREEDY && p.order && residual && p.P.coupled_ptr) {
+    int* nck = (int*)(sm + pl.nck);
+    for (int c = tid; c < K; c += nthr)
+      nck[c] = p.P.coupled_ptr[(size_t)b * K + c + 1] - p.P.coupled_ptr[(size_t)b * K + c];
+    for (int gg = tid; gg < G; gg += nthr) rhsv[gg] = K;
+    __syncthreads();
+    for (int c = tid; c < K; c += nthr) {
+      const int nc = nck[c];
+      int rank = 0;
+      for (int j = 0; j < K; ++j) {
+        const int nj = nck[j];
+        rank += (nj < nc || (nj == nc && j < c)) ? 1 : 0;
+      }
+      if (rank >= g0 && rank < g0 + G) rhsv[rank - g0] = c;
+    }
+  } else {
+    for (int gg = tid; gg < G; gg += nthr) rhsv[gg] = g0 + gg < K ? g0 + gg : K;
   }
   if (AGG && p.P.orth_ptr && tid == 0) {  // partition ranges read alongside the rows (one latency round)
     if (GRP) {
@@ -647,11 +673,11 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   for (int e = tid; e < KO * G; e += nthr) {
     const int il = e / G, gg = e % G;
     Qo[xo(il, gg)] = make_float2(0.f, 0.f);
-    Ro[xo(il, gg)] = make_float2(o_lo + il == g0 + gg ? 1.f : 0.f, 0.f);
+    Ro[xo(il, gg)] = make_float2(o_lo + il == rhsv[gg] ? 1.f : 0.f, 0.f);
     Fo[xo(il, gg)] = make_float2(0.f, 0.f);
   }
   for (int gg = tid; gg < G; gg += nthr) {
-    donev[gg] = g0 + gg < K ? 0 : 1;
+    donev[gg] = rhsv[gg] < K ? 0 : 1;
     sdone[gg] = 0;
     livev[gg] = 0;
     itv[gg] = 0;
@@ -785,10 +811,10 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     const T q = Qo[xo(il, gg)];
     if (dense) {  // solvers.py:149-153
       T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
-      if (i == g0 + gg) r.x += 1.f;
+      if (i == rhsv[gg]) r.x += 1.f;
       return r;
     }
-    const float tg = i == g0 + gg ? 1.f : 0.f;  // solvers.py:166
+    const float tg = i == rhsv[gg] ? 1.f : 0.f;  // solvers.py:166
     return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
   };
   auto push_phi = [&](int il, int gg, T v) {
@@ -858,7 +884,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     }
   };
   auto draw_u = [&](int gg) -> double {
-    const int cc = g0 + gg, d = itv[gg];
+    const int cc = rhsv[gg], d = itv[gg];
     if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)cc, (uint64_t)d);
     return p.R.uniforms[((size_t)b * K + cc) * p.R.stream_len + d];
   };
@@ -1197,7 +1223,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
           Qo[xo(il, gg)] = make_float2(q.x + gm.x, q.y + gm.y);
           Ro[xo(il, gg)] = make_float2(0.f, 0.f);
           const int it = itv[gg];
-          if (p.O.rows && it < p.O.rows_cap) p.O.rows[((size_t)b * K + g0 + gg) * p.O.rows_cap + it] = isel;
+          if (p.O.rows && it < p.O.rows_cap) p.O.rows[((size_t)b * K + rhsv[gg]) * p.O.rows_cap + it] = isel;
         }
         if (step && hl < CL) {
           if (hl == c) {
@@ -1368,7 +1394,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   if (p.O.iterates) {
     auto store_m = [&](const T (&mr)[E], int r) {
-      const int cc = g0 + g + LPA * r, chunk = chunk_of(w);
+      const int cc = rhsv[g + LPA * r], chunk = chunk_of(w);
       if (cc >= K || chunk >= Nt / CH) return;
       T* M = (T*)p.O.iterates + ((size_t)b * K + cc) * Nt + chunk * CH;
 #pragma unroll
@@ -1380,11 +1406,11 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   T* vout = (T*)p.O.v;
   for (int e = tid; e < nown * G; e += nthr) {
     const int il = e / G, gg = e % G;
-    if (g0 + gg < K) vout[((size_t)b * K + o_lo + il) * K + g0 + gg] = Qo[xo(il, gg)];
+    if (rhsv[gg] < K) vout[((size_t)b * K + o_lo + il) * K + rhsv[gg]] = Qo[xo(il, gg)];
   }
   if (c == 0)
     for (int gg = tid; gg < G; gg += nthr) {
-      const int cc = g0 + gg;
+      const int cc = rhsv[gg];
       if (cc >= K) continue;
       const size_t r = (size_t)b * K + cc;
       if (p.O.iters) p.O.iters[r] = itv[gg];
@@ -1547,6 +1573,8 @@ inline int cluster_try_launch(const kz_problem& P, int scheme, const kz_stop& S,
   a.rcap = cands[pick].rcap;
   a.tstop = (int32_t*)ws;
   a.hpad = ST && ws ? (const float2*)(ws + cluster_hpad_offset(P)) : nullptr;
+  static const int env_order = getenv("KZ_CLUSTER_RHS_ORDER") ? atoi(getenv("KZ_CLUSTER_RHS_ORDER")) : 1;
+  a.order = env_order;
   int rc = 0;
   if (ST) {
     if (GG == 32) {

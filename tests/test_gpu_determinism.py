@@ -83,3 +83,24 @@ def test_bounds_checked_build_runs_every_kernel():
     assert "[kz checked]" not in r.stdout + r.stderr
     for phase in ("wide / rkwarp / lockstep ok", "cluster ok", "rzf / epilogue ok", "drops ok", "generic ok"):
         assert phase in r.stdout
+
+
+def test_cluster_rhs_grouping_is_bitwise_neutral():
+    """Residual-mode greedy runs group a cluster's rhs by coupled-set size (KZ_CLUSTER_RHS_ORDER=1, the default);
+    every rhs's arithmetic is unchanged, so V / iterations / flops equal the index-order run (=0) bit for bit."""
+    code = (
+        "import numpy as np, paper_2501_10689_b200 as kz, torch\n"
+        "dev = kz.HostBatch.from_contiguous(kz.generate('cfg4', range(1))).to_device('c64')\n"
+        "r = kz.solve_batch(dev, 'grk', mode='residual', epsilon=1e-4, max_iters=256 * 10000, rng=('philox', 9))\n"
+        "np.savez(OUT, v=r.v.cpu().numpy(), it=r.iters.cpu().numpy(), fl=r.flops.cpu().numpy())\n")
+    outs = []
+    for order in ("0", "1"):
+        path = f"/tmp/kz_rhs_order_{order}.npz"
+        env = dict(os.environ, KZ_CLUSTER_RHS_ORDER=order)
+        r = subprocess.run([sys.executable, "-c", code.replace("OUT", repr(path))], cwd=ROOT, env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        import numpy as np
+        outs.append(np.load(path))
+    for key in ("v", "it", "fl"):
+        assert (outs[0][key] == outs[1][key]).all(), key
