@@ -100,3 +100,22 @@ def c64_nmse_ok(n64, n128):
     the NMSE by ~1e-8) the two agree to 1e-6 absolute (for a c128 NMSE at 1e-15 this is NMSE_64 <= 1e-6)."""
     n64, n128 = np.asarray(n64, dtype=np.float64), np.asarray(n128, dtype=np.float64)
     return np.where(n128 >= 1e-5, np.abs(n64 - n128) <= C64_REL * n128, np.abs(n64 - n128) <= C64_FLOOR)
+
+
+def oracle_precoding_task(args):
+    """run_precoding (fixed T, deterministic scheme) of one system of a named config through the oracle port
+    (spawn-pool worker: regenerates its channel from the seeds spec given to channel.generate).  Returns the
+    complex128 NMSE vs RZF and the Eq. (7) sum-rate."""
+    cfg_name, seeds, scheme, iters = args
+    from threadpoolctl import threadpool_limits
+    from paper_2501_10689_b200.channel import generate
+    with threadpool_limits(1):
+        ch = generate(cfg_name, seeds)
+        chan = oracle_channel_contiguous(ch, 0)
+        reg = float(ch.reg[0])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        run = O.run_precoding(scheme, sys_, ref, epsilon=0.0, max_iters=iters, traces=False)
+        f = O.assemble_dense(chan, run.v).f
+        _, sr = O.spectral_efficiency(chan.h, f, float(ch.snr_linear[0]))
+        return O.nmse(f, ref.f), sr
