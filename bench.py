@@ -715,7 +715,7 @@ def main():
                "path": "kz.DeviceBatch(pinned, upload stream, one step ahead) -> rzf_batched -> solve_batch + "
                        "epilogue per scheme -> V/NMSE/sum-rate to pinned host (copy stream)"}
         if world == 1 and a.config == "cfg2":
-            ed = e2e_drops_run(wl, max(1, min(a.steps, 3)), 5500, stream, dev_id)
+            ed = e2e_drops_run(wl, max(1, min(a.steps, 5)), 5500, stream, dev_id)
             e2e["with_input_preparation"] = {"value": len(schemes) * n_total / (ed["ms_per_step"] / 1e3),
                                              "unit": UNIT, **ed}
 
