@@ -104,3 +104,30 @@ def test_cluster_rhs_grouping_is_bitwise_neutral():
         outs.append(np.load(path))
     for key in ("v", "it", "fl"):
         assert (outs[0][key] == outs[1][key]).all(), key
+
+
+def test_cluster_rhs_grouping_ragged_rhs_count():
+    """The grouped slot assignment with K not a multiple of the rhs per cluster (K = 40: a partly empty second
+    cluster per system) and both greedy schemes that take it (gk, grk): bitwise equal to the index order."""
+    code = (
+        "import numpy as np, paper_2501_10689_b200 as kz, torch\n"
+        "ch = kz.generate(kz.NearFieldConfig('rag', 1024, 40, (96, 400)), range(3))\n"
+        "dev = kz.HostBatch.from_contiguous(ch).to_device('c64')\n"
+        "out = {}\n"
+        "for sc in ('gk', 'grk'):\n"
+        "    rng = ('philox', 4) if sc == 'grk' else None\n"
+        "    r = kz.solve_batch(dev, sc, mode='residual', epsilon=1e-4, max_iters=40 * 10000, rng=rng)\n"
+        "    assert bool(r.converged.all())\n"
+        "    out[sc + '_v'] = r.v.cpu().numpy(); out[sc + '_it'] = r.iters.cpu().numpy()\n"
+        "np.savez(OUT, **out)\n")
+    import numpy as np
+    res = []
+    for order in ("0", "1"):
+        path = f"/tmp/kz_rhs_rag_{order}.npz"
+        r = subprocess.run([sys.executable, "-c", code.replace("OUT", repr(path))], cwd=ROOT,
+                           env=dict(os.environ, KZ_CLUSTER_RHS_ORDER=order), capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res.append(np.load(path))
+    for key in res[0].files:
+        assert (res[0][key] == res[1][key]).all(), key

@@ -118,3 +118,22 @@ def test_grouped_cluster_kernel_c64_vs_restatement(groups, cap):
         assert int(res.flops[b].sum()) + 4 * nt * k + asm == pytest.approx(run.flops_measured, rel=5e-3)
         steps = T * k * (groups + -(-k // (cap if cap > 0 else k)))
         assert abs(int(res.noop_steps[b].sum()) - run.noop_steps) <= 0.01 * steps
+
+
+def test_grouped_cluster_extreme_caps():
+    """Grouped cluster path at the extremes: one hyperplane per aggregated step (agg_cap = 1: every N row its own
+    set) and a single group with all of N in one block; complex64 V within 1e-4 of the restatement."""
+    from oracle.grouped import run_precoding_grouped
+    kz = _kz()
+    T = 3
+    ch = kz.generate("cfg3", [9])
+    k = ch.n_users
+    for groups, cap in ((3, 1), (1, 200)):
+        host = kz.HostBatch.from_contiguous(ch, orth_groups=groups, agg_cap=cap)
+        res = kz.solve_batch(host.to_device("c64"), "vr-oahk-g", mode="lockstep", max_iters=T)
+        assert res.launches == 2
+        chan = oracle_channel_contiguous(ch, 0)
+        reg = float(ch.reg[0])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        run = run_precoding_grouped(sys_, O.rzf_precoder(chan, reg), groups, min(cap, k), T)
+        assert rel(res.v[0].cpu().numpy(), run.v) <= 1e-4, (groups, cap)
