@@ -1439,7 +1439,7 @@ inline size_t cluster_hpad_offset(const kz_problem& P) { return kz_align(ls_extr
 inline size_t cluster_hpad_bytes(const kz_problem& P, int NS) {
   return (size_t)P.n_systems * P.n_users * NS * clu::CH * sizeof(float2);
 }
-inline size_t g_cluster_dry_ws = 0;  // workspace the dispatched cluster variant needs (dry launches)
+inline thread_local size_t g_cluster_dry_ws = 0;  // workspace the dispatched cluster variant needs (dry launches)
 
 template <int SCH, int GG, bool ST>
 inline int cluster_launch(const CluArgs& a, int W, int CL, size_t smem, cudaStream_t s) {
