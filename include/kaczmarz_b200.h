@@ -185,8 +185,10 @@ size_t kz_solve_workspace_bytes(const kz_problem* prob, const kz_stop* stop);
 /* Bytes the kz_solve(prob, scheme, stop, rng, out, resume = 0) call would need for the kernel it dispatches to:
    the on-chip kernels (contiguous supports, fixed T or per-rhs residual tolerance) keep every iterate in
    registers / shared memory / TMEM and need only B*K int32 of stop bookkeeping, so a batch as large as
-   BASELINE cfg4 (B = 16384, K = 256, Nt = 4096) runs in one call; the global-memory kernel needs
-   kz_solve_workspace_bytes.  Decides without launching (device attributes of the current device). */
+   BASELINE cfg4 (B = 16384, K = 256, Nt = 4096) runs in one call; the cluster kernel's streamed variant (residual-
+   mode aggregation schemes) adds a chunk-padded copy of H_eff (B*K*ceil(max_support/32 + 1)*32 complex64; with a
+   smaller workspace the staged variant runs instead); the global-memory kernel needs kz_solve_workspace_bytes.
+   Decides without launching (device attributes of the current device). */
 size_t kz_solve_workspace_bytes_for(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const kz_rng* rng,
                                     const kz_out* out);
 
