@@ -46,6 +46,19 @@ def waste(order):
 print(f"{a.config} {a.scheme} B={a.batch}: mean iters {its.mean():.2f}, max {its.max():.0f}")
 print(f"  useful lane fraction, rhs in index order (the kernel's):  {waste(lambda b: np.arange(k)):.3f}")
 print(f"  sorted by the iteration count itself (upper bound):     {waste(lambda b: np.argsort(its[b])):.3f}")
-for name, feat in (("coupled-set size", ncoup), ("row energy", energy), ("VR start", start)):
+# overlap mass: sum over the coupled rows of the shared support length (contiguous VRs)
+L = ch.length.astype(float)
+ov = np.zeros((a.batch, k))
+for b in range(a.batch):
+    s_, e_ = start[b], start[b] + L[b]
+    ov[b] = np.clip(np.minimum(e_[:, None], e_[None, :]) - np.maximum(s_[:, None], s_[None, :]), 0, None).sum(axis=1)
+# |<h_c, h_j>|^2 summed over j (the Gram row energy)
+gram = np.zeros((a.batch, k))
+for b in range(a.batch):
+    h = ch.dense(b)
+    g = np.abs(h.conj().T @ h) ** 2
+    gram[b] = g.sum(axis=1) - np.diag(g)
+for name, feat in (("coupled-set size", ncoup), ("row energy", energy), ("VR start", start),
+                   ("overlap mass", ov), ("Gram row energy", gram), ("|X| + overlap/L", ncoup + ov / L)):
     r = np.corrcoef(feat.ravel(), its.ravel())[0, 1]
     print(f"  sorted by {name:17s} (corr {r:+.2f}):                {waste(lambda b: np.argsort(feat[b])):.3f}")
