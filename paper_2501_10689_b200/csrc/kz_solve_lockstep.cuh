@@ -55,8 +55,11 @@ struct LsArgs {
   int hcap;    // H elements reserved in shared memory
   char* ws;    // solve workspace (M block written at exit)
   GenLayout L;
-  int32_t* tstop;  // [B * groups] outer iteration at which the CTA finished
+  int32_t* tstop;  // [B * groups] outer iteration at which the CTA finished (| KZ_TSTOP_CONV: NMSE stop reached)
+  const double* f_ref;  // NMSE-stopped wide kernel: direct-solver precoder [B][Nt][K] complex128, else null
+  double eps;           // NMSE tolerance (0: run to T or all-done, NMSE only traced)
 };
+constexpr int32_t KZ_TSTOP_CONV = 1 << 30;
 
 // ------------------------------------------------------------------ smem plan
 struct LsPlan {
@@ -868,10 +871,14 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
 __global__ void kz_lockstep_finalize(const int32_t* tstop, int groups, int B, int32_t* n_outer, uint8_t* sys_conv) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  int t = 0;
-  for (int q = 0; q < groups; ++q) t = max(t, tstop[b * groups + q]);
+  int t = 0, conv = 0;
+  for (int q = 0; q < groups; ++q) {
+    const int32_t v = tstop[b * groups + q];
+    t = max(t, v & ~KZ_TSTOP_CONV);
+    conv |= (v & KZ_TSTOP_CONV) != 0;
+  }
   if (n_outer) n_outer[b] = t;
-  if (sys_conv) sys_conv[b] = 0;
+  if (sys_conv) sys_conv[b] = conv ? 1 : 0;
 }
 
 template <class T>
@@ -888,6 +895,8 @@ template <class T, int SCH>
 inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
                      size_t smem, int S, int hcap, cudaStream_t s) {
   LsArgs a;
+  a.f_ref = nullptr;
+  a.eps = 0.0;
   a.bulk = 0;
   a.P = P;
   a.R = R;
@@ -944,8 +953,13 @@ namespace kz {
 inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S, const kz_rng& R, const kz_out& O,
                                int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
   static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr;  // A/B switch for tests
-  if (disabled || resume || S.mode != KZ_STOP_LOCKSTEP || S.epsilon != 0.0) return 0;
-  if (O.nmse_trace || O.resid_trace || O.flops_trace || S.rhs_mask) return 0;
+  if (disabled || resume || S.mode != KZ_STOP_LOCKSTEP) return 0;
+  // NMSE-stopped (or NMSE / flop traced) lockstep runs: the wide complex64 kernel in its cluster form; the
+  // residual trace, rhs masks and the complex128 path stay on the generic kernel
+  static const bool no_nm = getenv("KZ_DISABLE_WIDE_NMSE") != nullptr;  // A/B switch
+  const bool nm = S.epsilon != 0.0 || O.nmse_trace || O.flops_trace;
+  if (nm && (no_nm || P.dtype != KZ_C64)) return 0;
+  if (O.resid_trace || S.rhs_mask) return 0;
   if (!(P.flags & KZ_PROBLEM_CONTIGUOUS) || P.max_support < 1) return 0;
   if (P.n_antennas % 32 != 0 || P.n_antennas > 512 || P.n_antennas < 32) return 0;
   const bool stochastic = scheme == KZ_URK || scheme == KZ_SWOR_ERK || scheme == KZ_GRK || scheme == KZ_VR_OGRK;
@@ -961,9 +975,15 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   int rc;
   static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: 16-rhs chunked kernel only
+  if (nm) {
+    rc = wide_dispatch(P, scheme, R, O, S.max_iters, true, S.f_ref, S.epsilon, ws, tstop, maxsm, s);
+    if (rc == 1) *launches = 2;
+    return rc;
+  }
   if (P.dtype == KZ_C64) {
     rc = chunked ? 0 : rkwarp_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
-    if (rc == 0 && !chunked) rc = wide_dispatch(P, scheme, R, O, S.max_iters, ws, tstop, maxsm, s);
+    if (rc == 0 && !chunked)
+      rc = wide_dispatch(P, scheme, R, O, S.max_iters, false, nullptr, 0.0, ws, tstop, maxsm, s);
     if (rc == 0) {
       size_t smem = ls_smem_bytes<float2>(P, &Sl, &hcap);
       if ((int)smem > maxsm) return 0;

@@ -249,6 +249,8 @@ inline int rkwarp_dispatch(const kz_problem& P, int scheme, const kz_rng& R, con
   }
   if (nw < 1) return 0;
   LsArgs a;
+  a.f_ref = nullptr;
+  a.eps = 0.0;
   a.bulk = 0;
   a.P = P;
   a.R = R;

@@ -47,10 +47,40 @@ __device__ __forceinline__ int xs(int i, int rhs) { return i * G + (rhs ^ (i & 1
 struct Plan {
   int K, W, SL, hcap;
   size_t rowS, rowL, c0, c1, hoff, en, inv_en, cost, cmask, inset, lptr, lst, optr, olst, nptr, nlst, H, P, Q, R, Phi, Dp, sel,
-      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, WP, lspl, ospl, nspl, total;
+      gam, num, sp, nz, noop, done, iters, flops, prev, pool, poolcnt, misc, mbar, WP, lspl, ospl, nspl, nmx, red, total;
 };
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+
+// distributed shared memory of the NMSE-stopped variant (one cluster = the ceil(K / 32) CTAs of a system)
+__device__ __forceinline__ uint32_t dsm_addr(const void* p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsm_st(double* p, int rank, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsm_st(long long* p, int rank, long long v) {
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void dsm_st(int* p, int rank, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// fixed-order CTA sum of a double (warp tree, then the warp partials in warp order): identical in every thread
+__device__ __forceinline__ double cta_sum_d(double v, double* red, int w, int lane, int nw) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < nw; ++q) s += red[q];
+  __syncthreads();  // red is rewritten by the next sum
+  return s;
+}
 
 __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   Plan p;
@@ -99,6 +129,12 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.lspl = o; o = al(o + 8 * (size_t)p.W);
   p.ospl = o; o = al(o + 8 * (size_t)p.W);
   p.nspl = o; o = al(o + 8 * (size_t)p.W);
+  // NMSE-stopped runs: per-CTA partials pushed to every CTA of the system's cluster ([2][4] ||M||^2, [4] ||F_ref -
+  // F_now||^2, [2][4] flop sums, [2][4] done counts; the first exchange of an iteration alternates between two
+  // buffers so a fast CTA's next push cannot overwrite slots a slow CTA still reads) and the CTA reduction
+  // scratch (one double per warp)
+  p.nmx = o; o = al(o + 8 * 8 + 8 * 4 + 8 * 8 + 4 * 8);
+  p.red = o; o = al(o + 8 * (size_t)p.W);
   // per-warp weight partials of the aggregation schemes ([warp][rhs]: num float2, ||phi||^2, nonzero flag); they
   // live in R (unused by AHK / VR-OAHK) when it is large enough
   if ((size_t)K * G * 8 >= (size_t)p.W * G * 16) {
@@ -112,7 +148,11 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
 
 }  // namespace wide
 
-template <int SCH>
+// NM: run_precoding's NMSE stop (solvers.py:583-603) -- the system's ceil(K / 32) CTAs form one thread-block
+// cluster, evaluate err = ||F_ref - M / ||M|| || / ||F_ref|| after every outer iteration from the register-resident
+// iterate (two fixed-order fp64 reductions exchanged over DSMEM) and leave together at the first err < eps, at
+// all-done or at the cap T
+template <int SCH, bool NM>
 __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__ LsArgs p) {
   using namespace wide;
   using T = float2;
@@ -359,6 +399,29 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     if (inset[i] == 2) { costN += 8LL * rowL[i]; ++nN; }
   }
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
+
+  // NMSE-stopped runs: ||F_ref|| of the whole system (every CTA of the cluster forms the same fixed-order sum)
+  double* xC0 = (double*)(sm + pl.nmx);  // [2][4]
+  double* xS = xC0 + 8;                  // [4]
+  long long* xF0 = (long long*)(xC0 + 12);  // [2][4]
+  int* xD0 = (int*)(xC0 + 20);              // [2][4]
+  double* red = (double*)(sm + pl.red);
+  const bool need_err = NM && (p.eps > 0.0 || p.O.nmse_trace);
+  const double* fref = need_err ? p.f_ref + (size_t)b * Nt * K * 2 : nullptr;
+  double fref_norm = 0.0;
+  if constexpr (NM) {
+    if (need_err) {
+      double s2 = 0.0;
+      const double2* f2 = reinterpret_cast<const double2*>(fref);
+      for (int e = tid; e < Nt * K; e += nthr) {
+        const double2 f = __ldg(f2 + e);
+        s2 = fma(f.x, f.x, fma(f.y, f.y, s2));
+      }
+      fref_norm = sqrt(cta_sum_d(s2, red, w, lane, W));
+    }
+    cluster_barrier();  // every CTA of the system is resident before the first DSMEM store
+  }
+  bool conv = false;
 
   constexpr int E = 16;  // antennas per thread per chunk
   const int a = lane >> 4, g = lane & 15;
@@ -996,10 +1059,78 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       __syncthreads();  // bookkeeping visible before the all-done test
       KZ_PHASE();
     }
-    bool all_done = true;
-    for (int gg = 0; gg < G; ++gg)
-      if (!donev[gg]) all_done = false;
-    if (all_done) break;
+    if constexpr (NM) {
+      // run_precoding's check (solvers.py:593-603): f_now = cols / ||cols||, err = ||f_ref - f_now|| / ||f_ref||,
+      // the loop leaves at err < eps, then at the cap or when every rhs is done.  Both norms are fp64 sums of the
+      // fp32 iterate (products exact in fp64), reduced per CTA in a fixed order and summed over the cluster in
+      // rank order, so every CTA takes the same decision
+      __syncthreads();  // this iteration's done flags and flop counts are visible
+      double c2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        c2 = fma((double)m0[k].x, (double)m0[k].x, fma((double)m0[k].y, (double)m0[k].y, c2));
+        c2 = fma((double)m1[k].x, (double)m1[k].x, fma((double)m1[k].y, (double)m1[k].y, c2));
+      }
+      const double cs = cta_sum_d(c2, red, w, lane, W);
+      double* xC = xC0 + 4 * (t & 1);
+      long long* xF = xF0 + 4 * (t & 1);
+      int* xD = xD0 + 4 * (t & 1);
+      if (tid < ngroups) {
+        int nd = 0;
+        long long fs = 0;
+        for (int gg = 0; gg < G; ++gg)
+          if (g0 + gg < K) {
+            nd += donev[gg];
+            fs += flv[gg];
+          }
+        dsm_st(xC + grp, tid, cs);
+        dsm_st(xD + grp, tid, nd);
+        dsm_st(xF + grp, tid, fs);
+      }
+      cluster_barrier();
+      double C = 0.0;
+      int nd = 0;
+      long long fs = 0;
+      for (int r = 0; r < ngroups; ++r) {
+        C += xC[r];
+        nd += xD[r];
+        fs += xF[r];
+      }
+      double err = 0.0;
+      if (need_err) {
+        const double mn = sqrt(C), inv = mn > 0.0 ? 1.0 / mn : 1.0;
+        double d2 = 0.0;
+        const double2* fr = reinterpret_cast<const double2*>(fref) + (size_t)(w * CH + 2 * a) * K + g0 + g;
+        const bool v0 = g0 + g < K, v1 = g0 + g + 16 < K;  // rhs slots past K (ragged last group) hold m = 0
+#pragma unroll 4
+        for (int k = 0; k < E; ++k) {
+          const size_t o = (size_t)(4 * (k >> 1) + (k & 1)) * K;
+          const double2 f0 = v0 ? __ldg(fr + o) : make_double2(0.0, 0.0);
+          const double2 f1 = v1 ? __ldg(fr + o + 16) : make_double2(0.0, 0.0);
+          const double dx0 = fma(-(double)m0[k].x, inv, f0.x), dy0 = fma(-(double)m0[k].y, inv, f0.y);
+          const double dx1 = fma(-(double)m1[k].x, inv, f1.x), dy1 = fma(-(double)m1[k].y, inv, f1.y);
+          d2 = fma(dx0, dx0, fma(dy0, dy0, d2));
+          d2 = fma(dx1, dx1, fma(dy1, dy1, d2));
+        }
+        const double ds = cta_sum_d(d2, red, w, lane, W);
+        if (tid < ngroups) dsm_st(xS + grp, tid, ds);
+        cluster_barrier();
+        double S2 = 0.0;
+        for (int r = 0; r < ngroups; ++r) S2 += xS[r];
+        err = sqrt(S2) / fref_norm;
+      }
+      if (grp == 0 && tid == 0 && t - 1 < p.O.trace_cap) {
+        if (p.O.nmse_trace) p.O.nmse_trace[(size_t)b * p.O.trace_cap + t - 1] = err;
+        if (p.O.flops_trace) p.O.flops_trace[(size_t)b * p.O.trace_cap + t - 1] = fs;
+      }
+      conv = p.eps > 0.0 && err < p.eps;
+      if (conv || nd == K) break;
+    } else {
+      bool all_done = true;
+      for (int gg = 0; gg < G; ++gg)
+        if (!donev[gg]) all_done = false;
+      if (all_done) break;
+    }
     // next iteration's writers of sel/gam run after the refresh barrier: no extra barrier needed
   }
   const int t_end = t > p.T ? p.T : t;
@@ -1011,7 +1142,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   }
 
   // ------------------------------------------------------------------ outputs
-  if (tid == 0) p.tstop[blockIdx.x] = t_end;
+  if (tid == 0) p.tstop[blockIdx.x] = t_end | (conv ? KZ_TSTOP_CONV : 0);
   KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   auto store_m = [&](const T (&mr)[E], int r) {
     const int c = g0 + g + 16 * r;
@@ -1048,9 +1179,9 @@ inline size_t wide_smem_bytes(const kz_problem& P, int* S_out, int* hcap_out) {
   return wide::plan(K, P.n_antennas, S, hcap).total;
 }
 
-template <int SCH>
-inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
-                       size_t smem, int S, int hcap, cudaStream_t s) {
+template <int SCH, bool NM>
+inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, const double* f_ref,
+                       double eps, char* ws, int32_t* tstop, size_t smem, int S, int hcap, cudaStream_t s) {
   LsArgs a;
   a.P = P;
   a.R = R;
@@ -1061,35 +1192,61 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
   a.ws = ws;
   a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
   a.tstop = tstop;
+  a.f_ref = f_ref;
+  a.eps = eps;
   a.bulk = bulk_staging_ok(P);
   const int groups = (P.n_users + wide::G - 1) / wide::G;
-  if (cudaFuncSetAttribute(kz_wide_kernel<SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return -1;
+  auto kern = kz_wide_kernel<SCH, NM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.n_systems * groups));
+  cfg.blockDim = dim3((unsigned)P.n_antennas);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (NM) {  // the system's CTAs form one cluster (NMSE partials over DSMEM)
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)groups;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+  }
   if (g_dry_launch) return 1;
   note_tma(a.bulk);
-  kz_wide_kernel<SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);
   return 1;
 }
 
-// 1 launched, 0 not eligible / not a single-row scheme, -1 failure
-inline int wide_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
-                         int32_t* tstop, int maxsm, cudaStream_t s) {
+// 1 launched, 0 not eligible / not a single-row scheme, -1 failure.  nm: NMSE-stopped / traced lockstep run
+// (f_ref, eps; T = the cap)
+inline int wide_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, bool nm,
+                         const double* f_ref, double eps, char* ws, int32_t* tstop, int maxsm, cudaStream_t s) {
   if (P.dtype != KZ_C64 || P.n_antennas % wide::CH != 0 || P.n_users < 17 || P.n_users > 128) return 0;
   int S, hcap;
   size_t smem = wide_smem_bytes(P, &S, &hcap);
   if ((int)smem > maxsm) return 0;
+#define KZ_WIDE_CASE(SC)                                                                                    \
+  case SC:                                                                                                  \
+    return nm ? wide_launch<SC, true>(P, R, O, T_iters, f_ref, eps, ws, tstop, smem, S, hcap, s)           \
+              : wide_launch<SC, false>(P, R, O, T_iters, f_ref, eps, ws, tstop, smem, S, hcap, s);
   switch (scheme) {
-    case KZ_URK: return wide_launch<KZ_URK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_SWOR_ERK: return wide_launch<KZ_SWOR_ERK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_GK: return wide_launch<KZ_GK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_GRK: return wide_launch<KZ_GRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_VR_OGRK: return wide_launch<KZ_VR_OGRK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_AHK: return wide_launch<KZ_AHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
-    case KZ_VR_OAHK: return wide_launch<KZ_VR_OAHK>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s);
+    KZ_WIDE_CASE(KZ_URK)
+    KZ_WIDE_CASE(KZ_SWOR_ERK)
+    KZ_WIDE_CASE(KZ_GK)
+    KZ_WIDE_CASE(KZ_GRK)
+    KZ_WIDE_CASE(KZ_VR_OGRK)
+    KZ_WIDE_CASE(KZ_AHK)
+    KZ_WIDE_CASE(KZ_VR_OAHK)
   }
+#undef KZ_WIDE_CASE
   return 0;
 }
 

@@ -281,13 +281,16 @@ def _stream_ptr(stream):
 def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_iters: int, epsilon: float = 0.0,
                 check_every: int = 1, f_ref=None, v_ref=None, rng=None, rows_cap: int = 0, trace_cap: int = 0,
                 rhs_mask=None, chunk: int | None = None, stream=None, workspace=None,
-                want_iterates: bool = False, system_base: int = 0) -> BatchResult:
+                want_iterates: bool = False, system_base: int = 0,
+                traces=("nmse", "resid", "flops")) -> BatchResult:
     """Run `scheme` on every (system, rhs) of `dev` with one kz_solve launch.
 
     mode: "lockstep" (run_precoding), "residual" / "oracle" (solve / solve_all).
     rng : None, ("philox", seed), or a HostStreams.
     system_base: global index of system 0 of `dev` (Philox draws are keyed by the global system index, so a
     realization's rows do not depend on how the batch is chunked or sharded).
+    traces: which per-outer-iteration traces trace_cap > 0 records (subset of nmse / resid / flops).  A lockstep
+    complex64 run without the residual trace (NMSE-stopped or not) stays on the register-resident wide kernel.
     """
     import torch
     scheme = canonical_scheme(scheme, extended=True)
@@ -314,9 +317,15 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
         res.rows = torch.full((b, k, rows_cap), -1, dtype=torch.int32, device=d)
     if trace_cap:
         n = b if mode == "lockstep" else b * k
-        res.nmse_trace = z(n, trace_cap, dt=torch.float64)
-        res.resid_trace = z(n, trace_cap, dt=torch.float64)
-        res.flops_trace = z(n, trace_cap, dt=torch.int64)
+        bad = set(traces) - {"nmse", "resid", "flops"}
+        if bad:
+            raise ValueError(f"unknown traces {sorted(bad)!r}")
+        if "nmse" in traces:
+            res.nmse_trace = z(n, trace_cap, dt=torch.float64)
+        if "resid" in traces:
+            res.resid_trace = z(n, trace_cap, dt=torch.float64)
+        if "flops" in traces:
+            res.flops_trace = z(n, trace_cap, dt=torch.int64)
         res.n_checks = z(b, k, dt=torch.int32)
 
     stop = _lib.KzStop()
@@ -355,9 +364,10 @@ def solve_batch(dev: DeviceBatch, scheme: str, *, mode: str = "lockstep", max_it
         out.rows_cap = rows_cap
     if trace_cap:
         out.trace_cap = trace_cap
-        out.nmse_trace = res.nmse_trace.data_ptr()
-        out.resid_trace = res.resid_trace.data_ptr()
-        out.flops_trace = res.flops_trace.data_ptr()
+        ptr = lambda t: 0 if t is None else t.data_ptr()  # noqa: E731
+        out.nmse_trace = ptr(res.nmse_trace)
+        out.resid_trace = ptr(res.resid_trace)
+        out.flops_trace = ptr(res.flops_trace)
         out.n_checks = res.n_checks.data_ptr()
 
     rg = _lib.KzRng()

@@ -119,3 +119,22 @@ def oracle_precoding_task(args):
         f = O.assemble_dense(chan, run.v).f
         _, sr = O.spectral_efficiency(chan.h, f, float(ch.snr_linear[0]))
         return O.nmse(f, ref.f), sr
+
+
+def oracle_cfg2_nmse_stop_task(args):
+    """run_precoding with the NMSE stop (solvers.py:556-603) on cfg2 realization `system`, the greedy schemes fed
+    the device's Philox draws (spawn-pool worker).  Returns the stop iteration, converged flag and NMSE trace."""
+    system, scheme, seed, eps = args
+    from threadpoolctl import threadpool_limits
+    from oracle.philox import PhiloxGenerator
+    from paper_2501_10689_b200.channel import generate
+    with threadpool_limits(1):
+        ch = generate("cfg2", [system])
+        chan = oracle_channel_contiguous(ch, 0)
+        reg = float(ch.reg[0])
+        sys_ = O.AugmentedSystem.from_channel(chan, reg)
+        ref = O.rzf_precoder(chan, reg)
+        rng = PhiloxGenerator(seed, system) if scheme in ("urk", "swor-erk", "grk", "vr-ogrk") else None
+        run = O.run_precoding(scheme, sys_, ref, epsilon=eps, max_iters=2000, rng=rng)
+        return {"system": system, "scheme": scheme, "n": run.n_iters, "conv": run.converged,
+                "trace": np.asarray(run.nmse_trace)}
