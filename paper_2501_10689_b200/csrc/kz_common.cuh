@@ -231,4 +231,84 @@ __device__ __forceinline__ double philox_uniform(uint64_t seed, uint32_t b, uint
   return (double)bits * (1.0 / 9007199254740992.0);
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// NMSE-stopped lockstep runs (run_precoding, solvers.py:583-603) on the on-chip kernels: the CTAs of one system form
+// a thread-block cluster (at most NMX_MAX), reduce fixed-order fp64 partials per CTA and push them to every CTA of
+// the cluster over DSMEM; every CTA sums the slots in rank order, so all of them take the same stop decision.
+// Slots: [2][NMX_MAX] ||M||^2, [NMX_MAX] ||F_ref - F_now||^2, [2][NMX_MAX] flop sums, [2][NMX_MAX] done counts (the
+// first exchange of an iteration alternates between two buffers by iteration parity, so a fast CTA's next push
+// cannot overwrite slots a slow CTA still reads; the second exchange is ordered by the first of the next iteration)
+constexpr int NMX_MAX = 8;
+__host__ __device__ inline size_t nmx_bytes() { return (size_t)NMX_MAX * (16 + 8 + 16 + 8); }
+struct NmxSlots {
+  double* C;
+  double* S;
+  long long* F;
+  int* D;
+};
+__device__ __forceinline__ NmxSlots nmx_slots(unsigned char* base) {
+  NmxSlots x;
+  x.C = (double*)base;
+  x.S = x.C + 2 * NMX_MAX;
+  x.F = (long long*)(x.S + NMX_MAX);
+  x.D = (int*)(x.F + 2 * NMX_MAX);
+  return x;
+}
+__device__ __forceinline__ uint32_t dsm_addr(const void* p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsm_st(double* p, int rank, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsm_st(long long* p, int rank, long long v) {
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void dsm_st(int* p, int rank, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// fixed-order CTA sum of a double (warp tree, then the warp partials in warp order): identical in every thread
+__device__ __forceinline__ double cta_sum_d(double v, double* red, int w, int lane, int nw) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < nw; ++q) s += red[q];
+  __syncthreads();  // red is rewritten by the next sum
+  return s;
+}
+// first exchange of iteration t: the CTA's ||M||^2 (cs, every thread), done count and flop sum (nd, fs: threads
+// tid < nct) -> the system's totals in every thread
+__device__ __forceinline__ void nmx_round1(const NmxSlots& x, int t, int rank, int nct, int tid, double cs, int nd,
+                                           long long fs, double& C, int& ndt, long long& fst) {
+  const int o = NMX_MAX * (t & 1);
+  if (tid < nct) {
+    dsm_st(x.C + o + rank, tid, cs);
+    dsm_st(x.D + o + rank, tid, nd);
+    dsm_st(x.F + o + rank, tid, fs);
+  }
+  cluster_barrier();
+  C = 0.0;
+  ndt = 0;
+  fst = 0;
+  for (int r = 0; r < nct; ++r) {
+    C += x.C[o + r];
+    ndt += x.D[o + r];
+    fst += x.F[o + r];
+  }
+}
+// second exchange: the CTA's ||F_ref - F_now||^2 -> the system's total
+__device__ __forceinline__ double nmx_round2(const NmxSlots& x, int rank, int nct, int tid, double ds) {
+  if (tid < nct) dsm_st(x.S + rank, tid, ds);
+  cluster_barrier();
+  double S2 = 0.0;
+  for (int r = 0; r < nct; ++r) S2 += x.S[r];
+  return S2;
+}
+
 }  // namespace kz

@@ -65,7 +65,7 @@ constexpr int32_t KZ_TSTOP_CONV = 1 << 30;
 struct LsPlan {
   int K, W, G, S, hcap, cs, KW;
   size_t rowS, rowL, rowB, rvo, c0, c1, en, cost, cmask, clist_ptr, clist, olist, nlist, ocl_ptr, ocl, ncl_ptr, ncl,
-      H, P, Q, R, Dp, scr, sel, gam, num, sp, nz, done, iters, noop, flops, prev, pool, poolcnt, misc, total;
+      H, P, Q, R, Dp, scr, sel, gam, num, sp, nz, done, iters, noop, flops, prev, pool, poolcnt, misc, nmx, red, total;
 };
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -112,11 +112,15 @@ __host__ __device__ inline LsPlan ls_plan(int K, int W, int G, int S, int hcap, 
   p.pool = o; o = a16(o + 4 * (size_t)G * p.KW);
   p.poolcnt = o; o = a16(o + 4 * G);
   p.misc = o; o = a16(o + 64);
+  p.nmx = o; o = a16(o + nmx_bytes());  // NMSE-stopped runs: cluster exchange slots (kz_common.cuh)
+  p.red = o; o = a16(o + 8 * (size_t)W);
   p.total = o;
   return p;
 }
 
-template <class T, int SCH>
+// NM: run_precoding's NMSE stop (solvers.py:583-603) over the system's ceil(K / G) CTAs as one thread-block cluster
+// (the complex128 oracle mode; complex64 takes the wide kernel), as in kz_solve_wide.cuh
+template <class T, int SCH, bool NM = false>
 __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   using Tr = Ls<T>;
   using Rl = typename Cx<T>::real;
@@ -668,6 +672,25 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
   int t = 0;
   const long long dense_refresh = 6LL * K * Nt + 2LL * K * (Nt + 1) + 2LL * K;
   const long long dense_rk = 2 + 8LL * Nt + 2;
+  // NMSE-stopped runs: ||F_ref|| of the whole system (the same fixed-order sum in every CTA of the cluster)
+  const NmxSlots nms = nmx_slots(sm + pl.nmx);
+  double* red = (double*)(sm + pl.red);
+  const bool need_err = NM && (p.eps > 0.0 || p.O.nmse_trace);
+  const double* fref = need_err ? p.f_ref + (size_t)b * Nt * K * 2 : nullptr;
+  double fref_norm = 0.0;
+  bool conv = false;
+  if constexpr (NM) {
+    if (need_err) {
+      double s2 = 0.0;
+      const double2* f2 = reinterpret_cast<const double2*>(fref);
+      for (int e = tid; e < Nt * K; e += nthr) {
+        const double2 f = __ldg(f2 + e);
+        s2 = fma(f.x, f.x, fma(f.y, f.y, s2));
+      }
+      fref_norm = sqrt(cta_sum_d(s2, red, w, lane, W));
+    }
+    cluster_barrier();  // every CTA of the system is resident before the first DSMEM store
+  }
   for (t = 1; t <= p.T; ++t) {
     KZ_ITER();
     if constexpr (SCH == KZ_GRK || SCH == KZ_GK || SCH == KZ_VR_OGRK) {
@@ -830,17 +853,58 @@ __global__ void __launch_bounds__(512, 1) kz_lockstep_kernel(LsArgs p) {
         if (g0 + gg < K) itv[gg] += 1;
     }
     __syncthreads(); KZ_PHASE();
-    // every rhs of this group done (greedy None / aggregated no-op) -> stop early
-    bool all_done = true;
-    for (int gg = 0; gg < G; ++gg)
-      if (!donev[gg]) all_done = false;
-    if (all_done) break;
+    if constexpr (NM) {
+      // run_precoding's check (solvers.py:593-603): err = ||f_ref - cols / ||cols|| || / ||f_ref||; leave at
+      // err < eps, then at the cap or when every rhs of the system is done
+      double c2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) c2 = fma((double)m[k].x, (double)m[k].x, fma((double)m[k].y, (double)m[k].y, c2));
+      const double cs = cta_sum_d(c2, red, w, lane, W);
+      int nd = 0;
+      long long fs = 0;
+      if (tid < ngroups)
+        for (int gg = 0; gg < G; ++gg)
+          if (g0 + gg < K) {
+            nd += donev[gg];
+            fs += flv[gg];
+          }
+      double C;
+      nmx_round1(nms, t, grp, ngroups, tid, cs, nd, fs, C, nd, fs);
+      double err = 0.0;
+      if (need_err) {
+        const double mn = sqrt(C), inv = mn > 0.0 ? 1.0 / mn : 1.0;
+        const int c = g0 + g;
+        double d2 = 0.0;
+        if (c < K) {
+          const double2* fr = reinterpret_cast<const double2*>(fref) + c;
+#pragma unroll
+          for (int k = 0; k < NPT; ++k) {
+            const double2 f = __ldg(fr + (size_t)ant(k) * K);
+            const double dx = fma(-(double)m[k].x, inv, f.x), dy = fma(-(double)m[k].y, inv, f.y);
+            d2 = fma(dx, dx, fma(dy, dy, d2));
+          }
+        }
+        err = sqrt(nmx_round2(nms, grp, ngroups, tid, cta_sum_d(d2, red, w, lane, W))) / fref_norm;
+      }
+      if (grp == 0 && tid == 0 && t - 1 < p.O.trace_cap) {
+        if (p.O.nmse_trace) p.O.nmse_trace[(size_t)b * p.O.trace_cap + t - 1] = err;
+        if (p.O.flops_trace) p.O.flops_trace[(size_t)b * p.O.trace_cap + t - 1] = fs;
+      }
+      conv = p.eps > 0.0 && err < p.eps;
+      if (conv || nd == K) break;
+    } else {
+      // every rhs of this group done (greedy None / aggregated no-op) -> stop early
+      bool all_done = true;
+      for (int gg = 0; gg < G; ++gg)
+        if (!donev[gg]) all_done = false;
+      if (all_done) break;
+    }
   }
   const int t_end = t > p.T ? p.T : t;
 
   // ---------------------------------------------------------------- outputs
   __syncthreads(); KZ_PHASE();
-  if (tid == 0) p.tstop[blockIdx.x] = t_end;
+  if (tid == 0) p.tstop[blockIdx.x] = t_end | (conv ? KZ_TSTOP_CONV : 0);
   KZ_TDUMP((long long*)((char*)p.tstop + ((size_t)p.P.n_systems * p.P.n_users * 4 + 7) / 8 * 8));
   {
     const int c = g0 + g;
@@ -891,12 +955,12 @@ inline size_t ls_smem_bytes(const kz_problem& P, int* S_out, int* hcap_out) {
   return ls_plan(K, W, Ls<T>::G, S, hcap, (int)sizeof(T), Ls<T>::EXACT).total;
 }
 
-template <class T, int SCH>
+template <class T, int SCH, bool NM = false>
 inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int T_iters, char* ws, int32_t* tstop,
-                     size_t smem, int S, int hcap, cudaStream_t s) {
+                     size_t smem, int S, int hcap, cudaStream_t s, const double* f_ref = nullptr, double eps = 0.0) {
   LsArgs a;
-  a.f_ref = nullptr;
-  a.eps = 0.0;
+  a.f_ref = f_ref;
+  a.eps = eps;
   a.bulk = 0;
   a.P = P;
   a.R = R;
@@ -908,11 +972,32 @@ inline int ls_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, int 
   a.L = gen_layout(P.n_systems, P.n_users, P.n_antennas, P.dtype);
   a.tstop = tstop;
   const int groups = (P.n_users + Ls<T>::G - 1) / Ls<T>::G;
-  if (cudaFuncSetAttribute(kz_lockstep_kernel<T, SCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return -1;
+  auto kern = kz_lockstep_kernel<T, SCH, NM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.n_systems * groups));
+  cfg.blockDim = dim3((unsigned)P.n_antennas);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (NM) {  // the system's CTAs form one cluster (NMSE partials over DSMEM)
+    if (groups > NMX_MAX) return 0;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)groups;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+    if (getenv("KZ_VERBOSE"))
+      fprintf(stderr, "[kz lockstep nmse] cluster %d smem %zu: max active clusters %d\n", groups, smem, nclusters);
+  }
   if (g_dry_launch) return 1;
-  kz_lockstep_kernel<T, SCH><<<P.n_systems * groups, P.n_antennas, smem, s>>>(a);
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return -1;
   kz_lockstep_finalize<<<(P.n_systems + 127) / 128, 128, 0, s>>>(tstop, groups, P.n_systems, O.n_outer,
                                                                   O.sys_converged);
   return 1;
@@ -943,6 +1028,26 @@ inline int ls_dispatch(const kz_problem& P, int scheme, const kz_rng& R, const k
   return 0;
 }
 
+// NMSE-stopped / traced complex128 lockstep runs (oracle mode): the chunked kernel as a cluster per system
+inline int ls_dispatch_nm(const kz_problem& P, int scheme, const kz_rng& R, const kz_out& O, int T_iters, char* ws,
+                          int32_t* tstop, size_t smem, int S, int hcap, const double* f_ref, double eps,
+                          cudaStream_t s) {
+  using T = double2;
+#define KZ_LS_NM(SC) \
+  case SC: return ls_launch<T, SC, true>(P, R, O, T_iters, ws, tstop, smem, S, hcap, s, f_ref, eps);
+  switch (scheme) {
+    KZ_LS_NM(KZ_URK)
+    KZ_LS_NM(KZ_SWOR_ERK)
+    KZ_LS_NM(KZ_GK)
+    KZ_LS_NM(KZ_GRK)
+    KZ_LS_NM(KZ_VR_OGRK)
+    KZ_LS_NM(KZ_AHK)
+    KZ_LS_NM(KZ_VR_OAHK)
+  }
+#undef KZ_LS_NM
+  return 0;
+}
+
 }  // namespace kz
 
 #include "kz_solve_wide.cuh"
@@ -954,11 +1059,11 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
                                int resume, char* ws, size_t ws_bytes, cudaStream_t s, int32_t* launches) {
   static const bool disabled = getenv("KZ_DISABLE_FAST") != nullptr;  // A/B switch for tests
   if (disabled || resume || S.mode != KZ_STOP_LOCKSTEP) return 0;
-  // NMSE-stopped (or NMSE / flop traced) lockstep runs: the wide complex64 kernel in its cluster form; the
-  // residual trace, rhs masks and the complex128 path stay on the generic kernel
-  static const bool no_nm = getenv("KZ_DISABLE_WIDE_NMSE") != nullptr;  // A/B switch
+  // NMSE-stopped (or NMSE / flop traced) lockstep runs: the wide complex64 kernel or the chunked complex128 kernel in
+  // their cluster forms; the residual trace and rhs masks stay on the generic kernel
+  static const bool no_nm = getenv("KZ_DISABLE_ONCHIP_NMSE") != nullptr;  // A/B switch
   const bool nm = S.epsilon != 0.0 || O.nmse_trace || O.flops_trace;
-  if (nm && (no_nm || P.dtype != KZ_C64)) return 0;
+  if (nm && no_nm) return 0;
   if (O.resid_trace || S.rhs_mask) return 0;
   if (!(P.flags & KZ_PROBLEM_CONTIGUOUS) || P.max_support < 1) return 0;
   if (P.n_antennas % 32 != 0 || P.n_antennas > 512 || P.n_antennas < 32) return 0;
@@ -976,7 +1081,13 @@ inline int lockstep_try_launch(const kz_problem& P, int scheme, const kz_stop& S
   int rc;
   static const bool chunked = getenv("KZ_CHUNKED_C64") != nullptr;  // A/B: 16-rhs chunked kernel only
   if (nm) {
-    rc = wide_dispatch(P, scheme, R, O, S.max_iters, true, S.f_ref, S.epsilon, ws, tstop, maxsm, s);
+    if (P.dtype == KZ_C64) {
+      rc = wide_dispatch(P, scheme, R, O, S.max_iters, true, S.f_ref, S.epsilon, ws, tstop, maxsm, s);
+    } else {
+      size_t smem = ls_smem_bytes<double2>(P, &Sl, &hcap);
+      if ((int)smem > maxsm) return 0;
+      rc = ls_dispatch_nm(P, scheme, R, O, S.max_iters, ws, tstop, smem, Sl, hcap, S.f_ref, S.epsilon, s);
+    }
     if (rc == 1) *launches = 2;
     return rc;
   }

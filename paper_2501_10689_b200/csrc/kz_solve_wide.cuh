@@ -52,36 +52,6 @@ struct Plan {
 
 __host__ __device__ inline size_t al(size_t x) { return (x + 15) & ~size_t(15); }
 
-// distributed shared memory of the NMSE-stopped variant (one cluster = the ceil(K / 32) CTAs of a system)
-__device__ __forceinline__ uint32_t dsm_addr(const void* p, int rank) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void dsm_st(double* p, int rank, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "d"(v) : "memory");
-}
-__device__ __forceinline__ void dsm_st(long long* p, int rank, long long v) {
-  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "l"(v) : "memory");
-}
-__device__ __forceinline__ void dsm_st(int* p, int rank, int v) {
-  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, rank)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// fixed-order CTA sum of a double (warp tree, then the warp partials in warp order): identical in every thread
-__device__ __forceinline__ double cta_sum_d(double v, double* red, int w, int lane, int nw) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int q = 0; q < nw; ++q) s += red[q];
-  __syncthreads();  // red is rewritten by the next sum
-  return s;
-}
-
 __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   Plan p;
   p.K = K;
@@ -129,11 +99,8 @@ __host__ __device__ inline Plan plan(int K, int Nt, int SL, int hcap) {
   p.lspl = o; o = al(o + 8 * (size_t)p.W);
   p.ospl = o; o = al(o + 8 * (size_t)p.W);
   p.nspl = o; o = al(o + 8 * (size_t)p.W);
-  // NMSE-stopped runs: per-CTA partials pushed to every CTA of the system's cluster ([2][4] ||M||^2, [4] ||F_ref -
-  // F_now||^2, [2][4] flop sums, [2][4] done counts; the first exchange of an iteration alternates between two
-  // buffers so a fast CTA's next push cannot overwrite slots a slow CTA still reads) and the CTA reduction
-  // scratch (one double per warp)
-  p.nmx = o; o = al(o + 8 * 8 + 8 * 4 + 8 * 8 + 4 * 8);
+  // NMSE-stopped runs: the cluster exchange slots (kz_common.cuh nmx_*) and the CTA reduction scratch
+  p.nmx = o; o = al(o + nmx_bytes());
   p.red = o; o = al(o + 8 * (size_t)p.W);
   // per-warp weight partials of the aggregation schemes ([warp][rhs]: num float2, ||phi||^2, nonzero flag); they
   // live in R (unused by AHK / VR-OAHK) when it is large enough
@@ -401,10 +368,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   const int unionN = (AGG && p.P.non_union_size) ? p.P.non_union_size[b] : 0;
 
   // NMSE-stopped runs: ||F_ref|| of the whole system (every CTA of the cluster forms the same fixed-order sum)
-  double* xC0 = (double*)(sm + pl.nmx);  // [2][4]
-  double* xS = xC0 + 8;                  // [4]
-  long long* xF0 = (long long*)(xC0 + 12);  // [2][4]
-  int* xD0 = (int*)(xC0 + 20);              // [2][4]
+  const NmxSlots nms = nmx_slots(sm + pl.nmx);
   double* red = (double*)(sm + pl.red);
   const bool need_err = NM && (p.eps > 0.0 || p.O.nmse_trace);
   const double* fref = need_err ? p.f_ref + (size_t)b * Nt * K * 2 : nullptr;
@@ -1072,30 +1036,16 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         c2 = fma((double)m1[k].x, (double)m1[k].x, fma((double)m1[k].y, (double)m1[k].y, c2));
       }
       const double cs = cta_sum_d(c2, red, w, lane, W);
-      double* xC = xC0 + 4 * (t & 1);
-      long long* xF = xF0 + 4 * (t & 1);
-      int* xD = xD0 + 4 * (t & 1);
-      if (tid < ngroups) {
-        int nd = 0;
-        long long fs = 0;
+      int nd = 0;
+      long long fs = 0;
+      if (tid < ngroups)
         for (int gg = 0; gg < G; ++gg)
           if (g0 + gg < K) {
             nd += donev[gg];
             fs += flv[gg];
           }
-        dsm_st(xC + grp, tid, cs);
-        dsm_st(xD + grp, tid, nd);
-        dsm_st(xF + grp, tid, fs);
-      }
-      cluster_barrier();
-      double C = 0.0;
-      int nd = 0;
-      long long fs = 0;
-      for (int r = 0; r < ngroups; ++r) {
-        C += xC[r];
-        nd += xD[r];
-        fs += xF[r];
-      }
+      double C;
+      nmx_round1(nms, t, grp, ngroups, tid, cs, nd, fs, C, nd, fs);
       double err = 0.0;
       if (need_err) {
         const double mn = sqrt(C), inv = mn > 0.0 ? 1.0 / mn : 1.0;
@@ -1112,12 +1062,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           d2 = fma(dx0, dx0, fma(dy0, dy0, d2));
           d2 = fma(dx1, dx1, fma(dy1, dy1, d2));
         }
-        const double ds = cta_sum_d(d2, red, w, lane, W);
-        if (tid < ngroups) dsm_st(xS + grp, tid, ds);
-        cluster_barrier();
-        double S2 = 0.0;
-        for (int r = 0; r < ngroups; ++r) S2 += xS[r];
-        err = sqrt(S2) / fref_norm;
+        err = sqrt(nmx_round2(nms, grp, ngroups, tid, cta_sum_d(d2, red, w, lane, W))) / fref_norm;
       }
       if (grp == 0 && tid == 0 && t - 1 < p.O.trace_cap) {
         if (p.O.nmse_trace) p.O.nmse_trace[(size_t)b * p.O.trace_cap + t - 1] = err;
@@ -1216,6 +1161,8 @@ inline int wide_launch(const kz_problem& P, const kz_rng& R, const kz_out& O, in
       cudaGetLastError();
       return 0;
     }
+    if (getenv("KZ_VERBOSE"))
+      fprintf(stderr, "[kz wide nmse] cluster %d smem %zu: max active clusters %d\n", groups, smem, nclusters);
   }
   if (g_dry_launch) return 1;
   note_tma(a.bulk);

@@ -124,7 +124,8 @@ def oracle_precoding_task(args):
 def oracle_cfg2_nmse_stop_task(args):
     """run_precoding with the NMSE stop (solvers.py:556-603) on cfg2 realization `system`, the greedy schemes fed
     the device's Philox draws (spawn-pool worker).  Returns the stop iteration, converged flag and NMSE trace."""
-    system, scheme, seed, eps = args
+    system, scheme, seed, eps = args[:4]
+    cap = args[4] if len(args) > 4 else 2000
     from threadpoolctl import threadpool_limits
     from oracle.philox import PhiloxGenerator
     from paper_2501_10689_b200.channel import generate
@@ -135,6 +136,7 @@ def oracle_cfg2_nmse_stop_task(args):
         sys_ = O.AugmentedSystem.from_channel(chan, reg)
         ref = O.rzf_precoder(chan, reg)
         rng = PhiloxGenerator(seed, system) if scheme in ("urk", "swor-erk", "grk", "vr-ogrk") else None
-        run = O.run_precoding(scheme, sys_, ref, epsilon=eps, max_iters=2000, rng=rng)
+        run = O.run_precoding(scheme, sys_, ref, epsilon=eps, max_iters=cap, rng=rng)
         return {"system": system, "scheme": scheme, "n": run.n_iters, "conv": run.converged,
-                "trace": np.asarray(run.nmse_trace)}
+                "trace": np.asarray(run.nmse_trace), "flops": np.asarray(run.flops_trace), "v": run.v,
+                "rows": [np.asarray(r, dtype=np.int32) for r in run.rows]}

@@ -153,3 +153,39 @@ def test_wide_nmse_stop_vs_oracle_c128(scheme):
         sel = g > 1e-5
         tol = 5e-2 if scheme in ("grk", "vr-ogrk") else 1e-3  # see _compare_with_generic
         assert np.all(np.abs(a[sel] - g[sel]) <= tol * g[sel]), (s, np.max(np.abs(a[sel] - g[sel]) / g[sel]))
+
+
+@pytest.mark.parametrize("scheme", ["urk", "swor-erk", "gk", "grk", "vr-ogrk", "ahk", "vr-oahk"])
+def test_c128_nmse_stop_matches_oracle(scheme):
+    """complex128 oracle mode, epsilon = 1e-6 (the reference default): the chunked lockstep kernel as a cluster of
+    ceil(K / 8) CTAs per system against the oracle fed the device's Philox draws -- stop iteration identical,
+    every selected row identical, V within 1e-10, NMSE trace within 1e-9 and the flop trace exact."""
+    from helpers import oracle_cfg2_nmse_stop_task, spawn_pool_map
+    kz = _kz()
+    eps, cap = 1e-6, 3000
+    systems = range(3)
+    orc = {r["system"]: r for r in spawn_pool_map(oracle_cfg2_nmse_stop_task,
+                                                   [(s, scheme, SEED, eps, cap) for s in systems])}
+    ch = kz.generate("cfg2", systems)
+    d128 = kz.HostBatch.from_contiguous(ch).to_device("c128")
+    rz = kz.rzf_batched(d128, want_f=True)
+    rng = ("philox", SEED) if scheme in kz.STOCHASTIC_SCHEMES else None
+    res = kz.solve_batch(d128, scheme, mode="lockstep", max_iters=cap, epsilon=eps, f_ref=rz["f"], rng=rng,
+                         trace_cap=cap, traces=("nmse", "flops"), rows_cap=cap)
+    assert res.launches == 2  # on-chip kernel + finalize (the generic kernel is one launch)
+    n = res.n_outer.cpu().numpy()
+    tr, fl = res.nmse_trace.cpu().numpy(), res.flops_trace.cpu().numpy()
+    rows, v = res.rows.cpu().numpy(), res.v.cpu().numpy()
+    setup = 4 * ch.n_antennas * ch.n_users
+    for s in systems:
+        o = orc[s]
+        assert bool(res.sys_converged[s]) == o["conv"]
+        assert int(n[s]) == o["n"], (s, int(n[s]), o["n"])
+        m = o["n"]
+        assert np.max(np.abs(tr[s, :m] - o["trace"]) / o["trace"]) <= 1e-9
+        assert np.array_equal(fl[s, :m] + setup, o["flops"])
+        if scheme not in ("ahk", "vr-oahk"):
+            for c in range(ch.n_users):
+                got = rows[s, c][rows[s, c] >= 0]
+                assert np.array_equal(got, o["rows"][c]), (s, c)
+        assert np.linalg.norm(v[s] - o["v"]) <= 1e-10 * np.linalg.norm(o["v"])
