@@ -172,6 +172,18 @@ int kz_solve(const kz_problem* prob, int32_t scheme, const kz_stop* stop, const 
   return cuda_check("kz_solve(generic)");
 }
 
+// batched Gram on the FP64 tensor cores (kz_gram_tc_kernel): contiguous supports, K <= 256
+static bool gram_tc_ok(const kz_problem* prob) {
+  static const bool off = getenv("KZ_GRAM_TC") && atoi(getenv("KZ_GRAM_TC")) == 0;
+  return !off && (prob->flags & KZ_PROBLEM_CONTIGUOUS) && prob->n_users <= GRAM_TC_KMAX;
+}
+static void launch_gram_tc(const kz_problem* prob, double2* out, size_t sys_stride, int add_reg, cudaStream_t s) {
+  if (prob->dtype == KZ_C128)
+    kz_gram_tc_kernel<double2><<<prob->n_systems, GRAM_TC_THREADS, 0, s>>>(*prob, out, sys_stride, add_reg);
+  else
+    kz_gram_tc_kernel<float2><<<prob->n_systems, GRAM_TC_THREADS, 0, s>>>(*prob, out, sys_stride, add_reg);
+}
+
 // the blocked Gauss-Jordan kernel inverts in place in v_out; only the legacy kernel needs a workspace
 static bool rzf_uses_gj(const kz_problem* prob) {
   int dev = 0, maxsm = 0;
@@ -201,13 +213,18 @@ int kz_rzf(const kz_problem* prob, double* v_out, double* f_out, double* beta_ou
   if (rzf_uses_gj(prob)) {  // KZ_RZF_LEGACY=1: A/B switch to the unblocked Cholesky kernel
     const int nb = rzf_nb(prob->n_users);
     const int nthr = prob->n_users <= 96 ? 256 : RZF_THREADS;  // small Grams: fewer threads, cheaper barriers
+    // the Gram on the FP64 tensor cores (contiguous supports; KZ_GRAM_TC=0: the CUDA-core pair sums)
+    const int tc = gram_tc_ok(prob) ? 1 : 0;
+    if (tc) launch_gram_tc(prob, (double2*)v_out, (size_t)prob->n_users * prob->n_users, 1, s);
     if (prob->dtype == KZ_C128) {
       cudaFuncSetAttribute(kz_rzf_gj_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kz_rzf_gj_kernel<double2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb);
+      kz_rzf_gj_kernel<double2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb, tc);
     } else {
       cudaFuncSetAttribute(kz_rzf_gj_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kz_rzf_gj_kernel<float2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb);
+      kz_rzf_gj_kernel<float2><<<prob->n_systems, nthr, smem, s>>>(*prob, v_out, f_out, beta_out, pd_ok, nb, tc);
     }
+    g_launches = 1 + tc;
+    return cuda_check("kz_rzf");
   } else if (prob->dtype == KZ_C128) {
     kz_rzf_kernel<double2><<<prob->n_systems, DENSE_THREADS, 0, s>>>(*prob, v_out, f_out, beta_out, pd_ok, (double2*)workspace);
   } else {
@@ -251,6 +268,14 @@ int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double
   cudaStream_t s = (cudaStream_t)stream;
   if (gram_path) {
     const size_t smem = epilogue_gram_smem();
+    kz_problem pr = *prob;  // G0 on the tensor cores unless the caller's workspace already holds it
+    int tc = 0;
+    if (!(pr.flags & KZ_PROBLEM_GRAM_CACHED) && gram_tc_ok(prob)) {
+      launch_gram_tc(prob, (double2*)workspace, 2 * (size_t)prob->n_users * prob->n_users, 0, s);
+      pr.flags |= KZ_PROBLEM_GRAM_CACHED;
+      tc = 1;
+    }
+    prob = &pr;
     if (prob->dtype == KZ_C128) {
       cudaFuncSetAttribute(kz_epilogue_gram_kernel<double2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
@@ -264,7 +289,7 @@ int kz_epilogue(const kz_problem* prob, const void* v, void* f_out, const double
           *prob, (const float2*)v, v_ref, beta_ref, snr_linear, beta_out, nmse_out, rates_out, sum_rate_out,
           (double2*)workspace);
     }
-    g_launches = 1;
+    g_launches = 1 + tc;
     return cuda_check("kz_epilogue(gram)");
   }
   if (prob->flags & KZ_PROBLEM_CONTIGUOUS) {

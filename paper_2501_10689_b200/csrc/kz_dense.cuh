@@ -220,6 +220,100 @@ __global__ void __launch_bounds__(DENSE_THREADS) kz_rzf_kernel(kz_problem P, dou
   if (beta_out && threadIdx.x == 0) beta_out[b] = beta;
 }
 
+// ---------------------------------------------------------------- K2a: batched Gram on the FP64 tensor cores
+// G = H^H H (+ xi I) per system (rzf.py:38-40; also the epilogue's G0) for contiguous supports, on the DMMA pipe
+// (mma.sync m8n8k4 f64: the only dense contraction of the path, north_star).  The rows are ranked by VR start, so
+// a block of 8 consecutive ranks covers a short antenna interval [bs, be); one warp forms one 8 x 8 block pair
+// (I <= J) of G over the intersection of the two blocks' intervals, 4 antennas per step:
+//   Re G += Hr_I^T Hr_J + Hi_I^T Hi_J,   Im G += Hr_I^T Hi_J - Hi_I^T Hr_J      (conj(h_i) h_j, 4 DMMA per step)
+// with H read straight from the packed rows (zero outside each row's VR).  Blocks whose intervals do not meet are
+// structural zeros (written, never multiplied).  fp64 throughout, so G agrees with the CUDA-core pair sums to
+// rounding (1e-16 relative).
+constexpr int GRAM_TC_THREADS = 256;
+constexpr int GRAM_TC_KMAX = 256;
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <class TH>
+__global__ void __launch_bounds__(GRAM_TC_THREADS) kz_gram_tc_kernel(kz_problem P, double2* g_out,
+                                                                     size_t sys_stride, int add_reg) {
+  __shared__ int ord[GRAM_TC_KMAX];       // rank -> row
+  __shared__ int rs[GRAM_TC_KMAX], rl[GRAM_TC_KMAX];
+  __shared__ long long rv[GRAM_TC_KMAX];
+  __shared__ int bs[GRAM_TC_KMAX / 8], be[GRAM_TC_KMAX / 8];
+  const int b = blockIdx.x, K = P.n_users;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const TH* hv = (const TH*)P.heff;
+  double2* G = g_out + (size_t)b * sys_stride;
+  const double reg = add_reg ? P.reg[b] : 0.0;
+  for (int i = tid; i < K; i += blockDim.x) {
+    const size_t r = (size_t)b * K + i;
+    rs[i] = P.seg_start[P.row_seg_ptr[r]];
+    rl[i] = P.seg_len[P.row_seg_ptr[r]];
+    rv[i] = P.row_val_ptr[r];
+  }
+  __syncthreads();
+  for (int i = tid; i < K; i += blockDim.x) {  // rank by (start, index)
+    int rk = 0;
+    for (int j = 0; j < K; ++j) rk += (rs[j] < rs[i] || (rs[j] == rs[i] && j < i)) ? 1 : 0;
+    ord[rk] = i;
+  }
+  __syncthreads();
+  const int NB = (K + 7) / 8;
+  for (int q = tid; q < NB; q += blockDim.x) {
+    int lo = 1 << 30, hi = 0;
+    for (int k = 8 * q; k < min(K, 8 * q + 8); ++k) {
+      lo = min(lo, rs[ord[k]]);
+      hi = max(hi, rs[ord[k]] + rl[ord[k]]);
+    }
+    bs[q] = lo;
+    be[q] = hi;
+  }
+  __syncthreads();
+  const int gid = lane >> 2, tig = lane & 3;
+  const int npair = NB * (NB + 1) / 2;
+  for (int e = warp; e < npair; e += nw) {
+    int J = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (J * (J + 1) / 2 > e) --J;
+    while ((J + 1) * (J + 2) / 2 <= e) ++J;
+    const int I = e - J * (J + 1) / 2;  // I <= J
+    const int ra = 8 * I + gid, rb = 8 * J + gid;
+    const int ia = ra < K ? ord[ra] : -1, jb = rb < K ? ord[rb] : -1;
+    const int sa = ia >= 0 ? rs[ia] : 0, la = ia >= 0 ? rl[ia] : 0;
+    const int sb = jb >= 0 ? rs[jb] : 0, lb = jb >= 0 ? rl[jb] : 0;
+    const TH* pa = hv + (ia >= 0 ? rv[ia] : 0) - sa;
+    const TH* pb = hv + (jb >= 0 ? rv[jb] : 0) - sb;
+    double cre[2] = {0.0, 0.0}, cim[2] = {0.0, 0.0};
+    const int lo = max(bs[I], bs[J]), hi = min(be[I], be[J]);
+    for (int n0 = lo & ~3; n0 < hi; n0 += 4) {
+      const int n = n0 + tig;
+      const double2 x = (n >= sa && n < sa + la) ? to_d2(pa[n]) : make_double2(0.0, 0.0);  // A[gid][tig] = h_ia(n)
+      const double2 y = (n >= sb && n < sb + lb) ? to_d2(pb[n]) : make_double2(0.0, 0.0);  // B[tig][gid] = h_jb(n)
+      dmma884(cre, x.x, y.x);
+      dmma884(cre, x.y, y.y);
+      dmma884(cim, x.x, y.y);
+      dmma884(cim, -x.y, y.x);
+    }
+    // C[gid][2 tig + c]: row = rank 8I + gid, column = rank 8J + 2 tig + c
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int rc = 8 * J + 2 * tig + c;
+      if (ia < 0 || rc >= K) continue;
+      const int jc = ord[rc];
+      if (ia == jc) {
+        G[(size_t)ia * K + ia] = make_double2(cre[c] + reg, 0.0);
+      } else {
+        G[(size_t)ia * K + jc] = make_double2(cre[c], cim[c]);
+        if (I != J) G[(size_t)jc * K + ia] = make_double2(cre[c], -cim[c]);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K2: RZF, blocked Gauss-Jordan
 // V = (H^H H + xi I)^{-1} in place in v_out: the Gram (full Hermitian) is built from the pairwise support
 // intersections, then inverted by blocked Gauss-Jordan (block NB: the NB x NB pivot block is inverted in shared
@@ -247,7 +341,8 @@ __device__ __forceinline__ double2 zfma(double2 a, double2 b, double2 acc) {  //
 
 template <class TH>
 __global__ void __launch_bounds__(RZF_THREADS, 1) kz_rzf_gj_kernel(kz_problem P, double* v_out, double* f_out,
-                                                                double* beta_out, uint8_t* pd_ok, int NB) {
+                                                                double* beta_out, uint8_t* pd_ok, int NB,
+                                                                int gram_ready) {
   extern __shared__ __align__(16) unsigned char rzf_sm[];
   const int b = blockIdx.x;
   const int K = P.n_users, Nt = P.n_antennas;
@@ -279,7 +374,9 @@ __global__ void __launch_bounds__(RZF_THREADS, 1) kz_rzf_gj_kernel(kz_problem P,
       A[(size_t)j * K + i] = make_double2(g.x, -g.y);
     }
   };
-  if (P.flags & KZ_PROBLEM_CONTIGUOUS) {
+  if (gram_ready) {
+    // G + xi I already in v_out (kz_gram_tc_kernel)
+  } else if (P.flags & KZ_PROBLEM_CONTIGUOUS) {
     const int lane = tid & 31, nw = nthr >> 5;
     const TH* hv = (const TH*)P.heff;
     for (int e = tid >> 5; e < npair; e += nw) {
