@@ -13,6 +13,12 @@ and end-to-end figure:
   configs.cfg3            BASELINE configs[2]: Nt=1024, K=128, VR ~ U[128,512], VR-OAHK T=200, B=4096, c64
   configs.cfg4            BASELINE configs[3]: Nt=4096, K=256, VR=512, GRK + VR-OAHK to residual 1e-4
                           (solve_all semantics), B=16384 (the largest single-GPU config), c64
+  configs.cfg3_grouped    cfg3's own variant: 4 orthogonal row groups, <= 8 hyperplanes per aggregated step
+  configs.cfg2_nmse_stop  the reference's default run_precoding(epsilon=1e-6) on the cfg2 workload (NMSE stop
+                          against RZF on the on-chip kernels, cap 10^4 K)
+  configs.cfg5_T{10,20,50,100}  BASELINE configs[4]: wideband, 1024 subcarriers, AHK + VR-OAHK per T of the sweep
+Every config record carries per_scheme_views: each scheme's solve time against the FP32-FMA roofline (algorithmic
+flops) and the HBM roofline (compulsory bytes: H_eff once + V).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   python bench.py --config cfg4 --scaling strong     (torchrun: 16384 realizations split over the ranks)
@@ -267,9 +273,11 @@ class Workload:
     """One config's step on this rank's systems: inputs resident in HBM, per step RZF + per scheme (solve +
     epilogue), chunked over `chunk` systems (bounded per-call outputs / workspaces)."""
 
-    def __init__(self, cfg, schemes, dtype, lo, hi, dev_id, chunk=0, device_inputs=False, orth_groups=1, agg_cap=0):
+    def __init__(self, cfg, schemes, dtype, lo, hi, dev_id, chunk=0, device_inputs=False, orth_groups=1, agg_cap=0,
+                 nmse_eps=0.0):
         import paper_2501_10689_b200 as kz
         self.kz, self.cfg, self.schemes, self.dtype = kz, cfg, schemes, dtype
+        self.nmse_eps = nmse_eps  # > 0: run_precoding's NMSE stop against the RZF precoder (cap = the config's T)
         self.lo, self.hi, self.B = lo, hi, hi - lo
         self.dev_id = dev_id
         self.tol = cfg.extra.get("residual_tol")
@@ -306,7 +314,7 @@ class Workload:
         for lo in range(0, self.B, self.chunk):
             hi = min(self.B, lo + self.chunk)
             sub = dev.view(lo, hi) if (lo, hi) != (0, self.B) else dev
-            rz = kz.rzf_batched(sub)
+            rz = kz.rzf_batched(sub, want_f=self.nmse_eps > 0)
             launches += rz["launches"]
             ews, gram = None, False  # the epilogues of a chunk share H, so the Gram G0 is formed once
             for sc in self.schemes:
@@ -315,6 +323,10 @@ class Workload:
                 if self.tol:
                     res = kz.solve_batch(sub, sc, mode="residual", epsilon=self.tol, max_iters=10_000 * k,
                                          rng=self.rng(sc, seed), workspace=self.ws.get(sc),
+                                         system_base=self.lo + lo)
+                elif self.nmse_eps > 0:
+                    res = kz.solve_batch(sub, sc, mode="lockstep", max_iters=self.iters, epsilon=self.nmse_eps,
+                                         f_ref=rz["f"], rng=self.rng(sc, seed), workspace=self.ws.get(sc),
                                          system_base=self.lo + lo)
                 else:
                     res = kz.solve_batch(sub, sc, mode="lockstep", max_iters=self.iters, rng=self.rng(sc, seed),
@@ -522,8 +534,27 @@ def roofline(wl, per_scheme, iters_by_scheme=None):
                                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
 
 
+def scheme_views(wl, per_scheme, iters_by_scheme, steps):
+    """Every scheme's solve launches per step against both rooflines: FP32 FMA (algorithmic flops) and HBM
+    (compulsory bytes: H_eff read once per launch + V written), so a launch that is staging-bound (few
+    iterations per rhs, e.g. cfg4 VR-OAHK at ~2.4) is read against the bound that applies to it."""
+    peak, _ = fp32_peak()
+    hbm = float(peaks_json().get("hbm_gbs", 6550.7))
+    csize = 16 if wl.dtype == "c128" else 8
+    h_bytes = float(wl.sup.sum()) * csize
+    v_bytes = float(wl.B) * wl.cfg.n_users ** 2 * csize
+    out = {}
+    for sc, ev in per_scheme.items():
+        t = float(np.sum([a.elapsed_time(b) for a, b in ev])) / steps / 1e3
+        fl = 8.0 * wl.elems(sc, iters_by_scheme.get(sc))
+        out[sc] = {"solve_s_per_step": t, "fma_TFLOPs": fl / t / 1e12, "fma_frac": fl / t / 1e12 / peak,
+                   "hbm_compulsory_GBps": (h_bytes + v_bytes) / t / 1e9,
+                   "hbm_frac": (h_bytes + v_bytes) / t / 1e9 / hbm}
+    return out
+
+
 def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2e=True, chunk=4096, n_systems=0,
-                  schemes=None, orth_groups=1, agg_cap=0, iters=0):
+                  schemes=None, orth_groups=1, agg_cap=0, iters=0, nmse_eps=0.0):
     """A BASELINE config other than the headline at its stated size on this GPU (N=1 sub-record); iters > 0
     overrides the config's T (cfg5's iteration-count sweep)."""
     import torch
@@ -536,7 +567,7 @@ def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2
     t0 = time.perf_counter()
     grouped = orth_groups > 1 or agg_cap > 0
     wl = Workload(cfg, schemes, dtype, 0, B, dev_id, chunk=chunk, device_inputs=not grouped,
-                  orth_groups=orth_groups, agg_cap=agg_cap)
+                  orth_groups=orth_groups, agg_cap=agg_cap, nmse_eps=nmse_eps)
     torch.cuda.synchronize()
     prep_s = time.perf_counter() - t0
     # warm-up on one chunk (kernel / allocator init), then full device-timed steps
@@ -567,7 +598,9 @@ def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2
                         f"{','.join(schemes)} x {wl.B} realizations, "
                         + (f"{orth_groups} orthogonal groups, <= {agg_cap} hyperplanes per aggregated step, "
                            if grouped else "")
-                        + (f"residual tolerance {wl.tol} (solve_all semantics)" if wl.tol else f"T={cfg.n_iters}")
+                        + (f"residual tolerance {wl.tol} (solve_all semantics)" if wl.tol else
+                           f"run_precoding NMSE stop at {nmse_eps:g} vs RZF (cap {cfg.n_iters})" if nmse_eps else
+                           f"T={cfg.n_iters}")
                         + ", RZF + solve + F/NMSE/sum-rate epilogue"),
            "value": len(schemes) * wl.B / (ms / 1e3), "unit": UNIT, "dtype": "complex64" if dtype == "c64"
            else "complex128", "steps": steps, "warmup": f"{max(1, warmup)} step(s) on the first {warm.B} systems",
@@ -576,7 +609,8 @@ def config_record(name, dev_id, stream, flush, steps, warmup, dtype="c64", do_e2
            "median_nmse": {sc: float(torch.cat(c["nmse"]).median()) for sc, c in collect.items()},
            "mean_sum_rate": {sc: float(torch.cat(c["sum_rate"]).mean()) for sc, c in collect.items()},
            "rhs_iterations_per_s": float(sum(float(t.double().sum()) for t in iters.values()) / (ms / 1e3)),
-           "roofline": roof, "clocks": clk.summary(),
+           "roofline": roof, "per_scheme_views": scheme_views(wl, per_scheme, iters, steps),
+           "clocks": clk.summary(),
            "inputs": ("host packing (HostBatch.from_contiguous with the orthogonal groups)" if grouped else
                       "seeded drops -> kz_channel_synth / kz_partition on the device")
            + f" ({prep_s:.1f} s); L2 flushed between steps (256 MiB write)",
@@ -751,6 +785,12 @@ def main():
             configs["cfg3_grouped"] = config_record("cfg3", dev_id, stream, flush, a.config_steps, 1,
                                                     do_e2e=not a.no_e2e, n_systems=4096, schemes=["vr-oahk-g"],
                                                     orth_groups=4, agg_cap=8)
+            # the reference's default precoder run (run_precoding(epsilon=1e-6), solvers.py:556-603) on the cfg2
+            # workload: every scheme NMSE-stopped against the RZF precoder on the on-chip kernels (the reference's
+            # own cap, 10^4 K outer iterations)
+            configs["cfg2_nmse_stop"] = config_record("cfg2", dev_id, stream, flush, a.config_steps, 1,
+                                                      do_e2e=not a.no_e2e, iters=10_000 * CONFIGS["cfg2"].n_users,
+                                                      nmse_eps=1e-6)
             # cfg5: wideband OFDM, 1024 subcarriers of one drop, AHK and VR-OAHK at each T of its sweep
             for T in CONFIGS["cfg5"].extra["iter_sweep"]:
                 configs[f"cfg5_T{T}"] = config_record("cfg5", dev_id, stream, flush, a.config_steps, 1,
