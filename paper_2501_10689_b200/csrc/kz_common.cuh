@@ -30,6 +30,11 @@
 // most 24 warps, whose per-warp slots stop below 36)
 #define KZ_SETUP_MARK(k) do { if (threadIdx.x == 0) kz_sm[(k) & 7] = clock64() - kz_s0; } while (0)
 #define KZ_WSTAMP() (kz_wacc += clock64() - kz_w0)
+// per-warp arrival time at one chosen point of the iteration (-DKZ_WSTAMP_AT=k picks the point k)
+#ifndef KZ_WSTAMP_AT
+#define KZ_WSTAMP_AT 0
+#endif
+#define KZ_WSTAMP_IF(k) do { if (KZ_WSTAMP_AT == (k)) KZ_WSTAMP(); } while (0)
 #define KZ_TDUMP(ptr) do { if ((ptr)) { long long* o_ = (ptr) + (size_t)blockIdx.x * 44; \
   if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 24) o_[12 + (threadIdx.x >> 5)] = kz_wacc; \
   if (threadIdx.x == 0 && blockDim.x <= 768) for (int q_ = 0; q_ < 8; ++q_) o_[36 + q_] = kz_sm[q_]; \
@@ -42,6 +47,7 @@
 #define KZ_ITER() ((void)0)
 #define KZ_SETUP_MARK(k) do {} while (0)
 #define KZ_WSTAMP() ((void)0)
+#define KZ_WSTAMP_IF(k) do {} while (0)
 #define KZ_TDUMP(ptr) do {} while (0)
 #endif
 

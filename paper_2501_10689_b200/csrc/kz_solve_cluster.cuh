@@ -137,7 +137,10 @@ __host__ __device__ inline Plan plan(int scheme, int K, int W, int CL, int NS, i
   p.nptr = o; o = al(o + (oahk ? 4 * (W + 1) : 0));
   p.olst = o; o = al(o + (oahk ? 8 * (size_t)pcap : 0));  // O entries then N entries (disjoint rows)
   p.nlst = p.olst;
-  p.H = o; o = al(o + (streamed ? 0 : 8 * (size_t)pcap * CH));  // streamed: H from the padded global copy
+  // one spare 16-byte unit per local row: row n starts at bank group n mod 8, so the rows a quarter-warp's
+  // LDS.128 gathers in the greedy projection (one row per rhs lane) spread over the eight groups instead of
+  // sharing one (chunk-padded rows alone are multiples of 256 bytes).  streamed: H from the padded global copy
+  p.H = o; o = al(o + (streamed ? 0 : 8 * ((size_t)pcap * CH + 2 * (size_t)p.nlcap)));
   p.Qo = o; o = al(o + 8 * (size_t)p.KO * G);
   p.Ro = o; o = al(o + (greedy ? 8 * (size_t)p.KO * G : 0));
   p.Fo = o; o = al(o + (agg ? 8 * (size_t)p.KO * G : 0));
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
     if (i < K) loc[i] = ov ? idx : -1;
     if (ov && idx < pl.nlcap) {
       lrow[idx] = i;
-      lh[idx] = (hcar + sc - np) * CH;
+      lh[idx] = (hcar + sc - np) * CH + 2 * idx;
       lcc[idx] = l0 | (l1 << 8);
     }
   }
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(256, ST ? 2 : 1) kz_cluster_kernel(const __gri
   };
 
   // conj(h) . m over this warp's chunk for both rhs, reduced over the a-lanes; lane < G ends with rhs lane
-  const int hcap_el = ST ? K * NS * CH : pl.pcap * CH;  // elements of H_eff the kernel may read
+  const int hcap_el = ST ? K * NS * CH : pl.pcap * CH + 2 * pl.nlcap;  // elements of H_eff the kernel may read
   auto dot16 = [&](int h0) -> T {
     KZ_CHECK(h0 >= 0 && (h0 & 1) == 0 && h0 + CH <= hcap_el, "cluster: refresh piece inside H");
     const float4* hp = H4 + (h0 >> 1) + a;

@@ -38,7 +38,7 @@ namespace wide {
 constexpr int G = 32;
 constexpr int CH = 32;  // chunk = antennas per warp
 template <int A, int B> struct JRange { static constexpr int lo = A, hi = B; };
-constexpr int HSKEW = 6;  // spare H elements per row for the bank skew of the row bases
+constexpr int HSKEW = 2;  // spare H elements (one 16-byte unit) per row: consecutive rows start one bank group apart
 // [row][rhs] arrays (P slots, Q, R) are XOR-swizzled on the rhs index so that
 // both access directions (lanes over rhs: refresh / projection; lanes over
 // rows: finalise / selection) are bank-conflict free.
@@ -197,8 +197,9 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     int carry = 0;
     for (int base = 0; base < K; base += 32) {
       int i = base + lane;
-      // each row gets HSKEW spare elements and starts 2 (i & 3) elements into its allocation: the rows a warp
-      // projects (one per lane, chunk-aligned otherwise) then fall on four different 16-byte bank groups
+      // each row is followed by one spare 16-byte unit, so row i starts at bank group i mod 8 (16-byte units mod 128
+      // bytes; the chunk-padded rows alone are multiples of 256 bytes): the eight rows a quarter-warp's LDS.128
+      // gathers in the projection (one row per rhs lane) then spread over all eight groups instead of sharing one
       int v = i < K ? (c1[i] - c0[i] + 1) * CH + HSKEW : 0;
       int sc = v;
 #pragma unroll
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         int t2 = __shfl_up_sync(FULL, sc, o);
         if (lane >= o) sc += t2;
       }
-      if (i < K) hoff[i] = carry + sc - v + 2 * (i & 3);
+      if (i < K) hoff[i] = carry + sc - v;
       carry += __shfl_sync(FULL, sc, 31);
     }
   }
@@ -469,13 +470,14 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       refresh_seg(JRange<4, 8>{}, std::integral_constant<int, 2>{}, L, spl[2 * w + 1], ptr[w + 1]);
     }
   };
-  auto resid = [&](int i, int gg) -> T {  // from the slot partials, fixed order
+  // bt: every slot load issued at once (predicated), then the sums in slot order -- for callers with registers to
+  // spare (the greedy selection; the aggregation weights, formed while the iterate is parked in TMEM)
+  auto resid_b = [&](auto bt, int i, int gg) -> T {  // from the slot partials, fixed order
     KZ_CHECK(i >= 0 && i < K && gg >= 0 && gg < G && c1[i] - c0[i] < SL, "wide: residual row / slots");
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
     const int ns = c1[i] - c0[i];
-    if (SCH != KZ_VR_OAHK && SL <= 8) {  // every slot load issued at once (predicated), then the sums in slot
-                                          // order (vr-oahk: register pressure, measured slower)
+    if (decltype(bt)::value && SL <= 8) {
       T v[8];
 #pragma unroll
       for (int s = 0; s < 8; ++s) v[s] = s <= ns ? pp[(size_t)s * G] : make_float2(0.f, 0.f);
@@ -502,6 +504,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     float tg = i == c ? 1.f : 0.f;  // VR form (solvers.py:166)
     return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
   };
+  auto resid = [&](int i, int gg) -> T { return resid_b(std::bool_constant<SCH != KZ_VR_OAHK>{}, i, gg); };
   auto draw_u = [&](int gg) -> double {
     int c = g0 + gg, d = itv[gg];
     if (p.R.kind == KZ_RNG_PHILOX) return philox_uniform(p.R.seed, (uint32_t)(b + p.R.system_base), (uint32_t)c, (uint64_t)d);
@@ -559,13 +562,20 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           if (act)
 #pragma unroll 4
             for (int i = hl; i < K; i += 16) {
-              bool upd = true;
+              T r;
               if constexpr (SCH == KZ_VR_OGRK) {
-                int pr = prevv[gg];
-                upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
+                // only the rows coupled to the previous pick take their new residual (solvers.py:398-406); the
+                // slot sums of all four rows of the lane are formed without branches (loads in flight together)
+                // and the uncoupled rows keep the stored value
+                const int pr = prevv[gg];
+                const bool upd = pr >= 0 && ((cmask[pr * KW + (i >> 5)] >> (i & 31)) & 1u);
+                const T rn = resid(i, gg), ro = Rs[xs(i, gg)];
+                r = upd ? rn : ro;
+                if (upd) Rs[xs(i, gg)] = r;
+              } else {
+                r = resid(i, gg);
+                Rs[xs(i, gg)] = r;
               }
-              T r = upd ? resid(i, gg) : Rs[xs(i, gg)];
-              if (upd) Rs[xs(i, gg)] = r;
               wsum += r.x * r.x + r.y * r.y;
             }
           __syncwarp();
@@ -751,10 +761,10 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         float nx = 0.f, ny = 0.f, sp = 0.f;
         bool nz = false;
         if (g0 + gg < K && !donev[gg])
-#pragma unroll(SCH == KZ_VR_OAHK ? 1 : 4)
+#pragma unroll 4
           for (int i = w; i < K; i += W) {
             if (which && inset[i] != which) continue;
-            const T r = resid(i, gg);
+            const T r = resid_b(std::true_type{}, i, gg);
             const float ie = inv_en[i];
             const T ph = make_float2(r.x * ie, r.y * ie);
             Phi[xs(i, gg)] = ph;
@@ -798,10 +808,10 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           float nx = 0.f, ny = 0.f, sp = 0.f;
           bool nz = false;
           if (act)
-#pragma unroll(SCH == KZ_VR_OAHK ? 1 : 4)
+#pragma unroll 4
             for (int i = hl; i < K; i += 16) {
               if (which && inset[i] != which) continue;
-              const T r = resid(i, gg);
+              const T r = resid_b(std::true_type{}, i, gg);
               const float ie = inv_en[i];
               const T ph = make_float2(r.x * ie, r.y * ie);
               Phi[xs(i, gg)] = ph;
@@ -829,28 +839,31 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           }
         }
       };
+      // the iterate goes to TMEM (asynchronous stores, drained after the aggregation barrier) as soon as this
+      // warp's refresh is done: the weights are then formed with the registers free (every slot load of four
+      // rows in flight), and the stores drain under the weights phase
+      auto park = [&]() {
+        float f0[16], f1[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          f0[2 * k] = m0[k].x; f0[2 * k + 1] = m0[k].y;
+          f1[2 * k] = m0[k + 8].x; f1[2 * k + 1] = m0[k + 8].y;
+        }
+        tmem::st16(my_tmem, f0);
+        tmem::st16(my_tmem + 16, f1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          f0[2 * k] = m1[k].x; f0[2 * k + 1] = m1[k].y;
+          f1[2 * k] = m1[k + 8].x; f1[2 * k + 1] = m1[k + 8].y;
+        }
+        tmem::st16(my_tmem + 32, f0);
+        tmem::st16(my_tmem + 48, f1);
+      };
       // aggregated projection (solvers.py:257-309): m parked in TMEM while y = sum phi h
       // (ascending rows) occupies the registers
       auto aggregate = [&](const int* ptr, const int* spl, const int2* L, int nrows, int span, bool dense, bool mark_done,
                            long long ycost) {
         if constexpr (PAR_W) reduce_weights(nrows);
-        {
-          float f0[16], f1[16];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            f0[2 * k] = m0[k].x; f0[2 * k + 1] = m0[k].y;
-            f1[2 * k] = m0[k + 8].x; f1[2 * k + 1] = m0[k + 8].y;
-          }
-          tmem::st16(my_tmem, f0);
-          tmem::st16(my_tmem + 16, f1);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            f0[2 * k] = m1[k].x; f0[2 * k + 1] = m1[k].y;
-            f1[2 * k] = m1[k + 8].x; f1[2 * k + 1] = m1[k + 8].y;
-          }
-          tmem::st16(my_tmem + 32, f0);
-          tmem::st16(my_tmem + 48, f1);
-        }
 #pragma unroll
         for (int k = 0; k < E; ++k) m0[k] = m1[k] = make_float2(0.f, 0.f);  // registers now hold y
         auto agg_entry = [&](auto jr, int2 e) {  // y += phi_i h_i on the entry's j range
@@ -888,11 +901,14 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           s0 = fmaf(m0[k].x, m0[k].x, fmaf(m0[k].y, m0[k].y, s0));
           s1 = fmaf(m1[k].x, m1[k].x, fmaf(m1[k].y, m1[k].y, s1));
         }
-        {  // ||y||^2 partial of this warp, stored [rhs][warp] so a rhs' partials are one contiguous run
+        {  // ||y||^2 partial of this warp, stored [warp][rhs]: the warp's store and every lane-over-rhs read of
+           // the step lengths below are bank-conflict free ([rhs][warp] with 16 warps put the 16 rhs of an LDS.128
+           // on two 16-byte bank groups: 8-way conflicts in every thread's 8 loads)
           const float sd = a ? s0 : s1;
           const float rv = __shfl_xor_sync(FULL, sd, 16);
-          Dp[(g + 16 * a) * W + w] = (a ? s1 : s0) + rv;
+          Dp[w * G + g + 16 * a] = (a ? s1 : s0) + rv;
         }
+        KZ_WSTAMP_IF(5);
         __syncthreads();
         KZ_PHASE();
         tmem::wait_st();
@@ -901,20 +917,22 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         tmem::ld16(my_tmem, f0);  // the parked iterate streams in while the step lengths are formed
         tmem::ld16(my_tmem + 16, f1);
         KZ_PHASE();  // [timing] TMEM load issue
-        // step lengths of this thread's two rhs (fixed-order pairwise sums => identical in every thread)
+        // step length of this lane's own rhs g + 16 a (fixed-order pairwise sum of the warps' ||y||^2 partials: the
+        // same value in every warp), the partner lane's by one exchange
         auto gamma_of = [&](int rr, bool& step) -> T {
           step = false;
           if (!nzv[rr]) return make_float2(0.f, 0.f);
-          const float* dp = Dp + rr * W;
+          const float* dp = Dp + rr;
           float den;
           if (W == 16) {
-            const float4* d4 = reinterpret_cast<const float4*>(dp);
-            const float4 u0 = d4[0], u1 = d4[1], u2 = d4[2], u3 = d4[3];
-            den = ((u0.x + u0.y) + (u0.z + u0.w) + ((u1.x + u1.y) + (u1.z + u1.w))) +
-                  ((u2.x + u2.y) + (u2.z + u2.w) + ((u3.x + u3.y) + (u3.z + u3.w)));
+            float u[16];
+#pragma unroll
+            for (int ww = 0; ww < 16; ++ww) u[ww] = dp[ww * G];
+            den = ((u[0] + u[1]) + (u[2] + u[3]) + ((u[4] + u[5]) + (u[6] + u[7]))) +
+                  ((u[8] + u[9]) + (u[10] + u[11]) + ((u[12] + u[13]) + (u[14] + u[15])));
           } else {
             den = 0.f;
-            for (int ww = 0; ww < W; ++ww) den += dp[ww];
+            for (int ww = 0; ww < W; ++ww) den += dp[ww * G];
           }
           den = fmaf(regf, spv[rr], den);
           if (den == 0.f) return make_float2(0.f, 0.f);
@@ -922,8 +940,13 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           T nm = numv[rr];
           return make_float2(nm.x / den, nm.y / den);
         };
-        bool st0, st1;
-        const T gm0 = gamma_of(g, st0), gm1 = gamma_of(g + 16, st1);
+        bool st_own;
+        const T gm_own = gamma_of(g + 16 * a, st_own);
+        const T gm_oth = make_float2(__shfl_xor_sync(FULL, gm_own.x, 16), __shfl_xor_sync(FULL, gm_own.y, 16));
+        const bool st_oth = __shfl_xor_sync(FULL, (int)st_own, 16) != 0;
+        const bool st0 = a ? st_oth : st_own, st1 = a ? st_own : st_oth;
+        const T gm0 = a ? gm_oth : gm_own, gm1 = a ? gm_own : gm_oth;
+        KZ_WSTAMP_IF(6);
         KZ_PHASE();  // [timing] step lengths
         {
           tmem::wait_ld();
@@ -943,6 +966,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
             m1[k + 8] = st1 ? cfma(gm1, m1[k + 8], o1) : o1;
           }
         }
+        KZ_WSTAMP_IF(7);
         KZ_PHASE();  // [timing] iterate reload + update
         // q += gamma phi over the aggregated rows (threads over (row, rhs))
         {  // rhs of entry e is e % G == lane = g + 16 a (nthr is a multiple of 32): this thread's own step
@@ -975,11 +999,13 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
             flv[lane] += f;
           }
         }
+        KZ_WSTAMP_IF(8);
         (void)dense;
       };
 
       if constexpr (SCH == KZ_AHK) {
         refresh_list(lptr, lspl, lst);
+        park();
         if (tid < G && g0 + tid < K && !donev[tid]) flv[tid] += dense_refresh;
         __syncthreads();
         KZ_PHASE();
@@ -990,6 +1016,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       } else {
         // exact block projection on the orthogonal group O (solvers.py:312-332)
         refresh_list(optr, ospl, olst);
+        KZ_WSTAMP_IF(1);
         __syncthreads();
         KZ_PHASE();
         for (int e = tid; e < K * G; e += nthr) {
@@ -1002,6 +1029,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           Phi[xs(i, rr)] = gm;
         }
         if (tid < G && g0 + tid < K) flv[tid] += 2 * costO + (nN ? costN + 4LL * nN : 0);
+        KZ_WSTAMP_IF(2);
         __syncthreads();
         KZ_PHASE();
         for (int q = optr[w]; q < optr[w + 1]; ++q) {
@@ -1011,9 +1039,12 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         }
         if (nN > 0) {
           refresh_list(nptr, nspl, nlst);
+          park();
+          KZ_WSTAMP_IF(3);
           __syncthreads();
           KZ_PHASE();
           if constexpr (PAR_W) weights(2); else weights_rhs(2, nN);
+          KZ_WSTAMP_IF(4);
           __syncthreads();
           KZ_PHASE();
           aggregate(nptr, nspl, nlst, nN, unionN, false, false, costN);

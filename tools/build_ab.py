@@ -2,7 +2,8 @@
 
     python tools/build_ab.py csrc/kz_solve_wide.cuh=/tmp/old_wide.cuh [...]
 then run the same command with KZ_LIB_VARIANT=ab (A) and without (B) in one gpurun call
-(--name=X as the first argument builds libkaczmarz_b200_X.so for a third arm, KZ_LIB_VARIANT=X).
+(--name=X as the first argument builds libkaczmarz_b200_X.so for a third arm, KZ_LIB_VARIANT=X;
+-DNAME=VALUE arguments are passed to nvcc for that arm).
 """
 import os
 import shutil
@@ -22,11 +23,13 @@ name = "ab"
 args = sys.argv[1:]
 if args and args[0].startswith("--name="):
     name = args.pop(0).split("=", 1)[1]
+defs = [x for x in args if x.startswith("-D")]  # extra preprocessor definitions for this arm
+args = [x for x in args if not x.startswith("-D")]
 for arg in args:
     rel, path = arg.split("=", 1)
     shutil.copy(path, os.path.join(tmp, "pkg", rel))
 out = B.lib_path(name)
-cmd = [B._nvcc(), *B.NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *[os.path.join(src, s) for s in B.SOURCES],
+cmd = [B._nvcc(), *B.NVCC_FLAGS, *defs, "-I", os.path.join(ROOT, "include"), *[os.path.join(src, s) for s in B.SOURCES],
        "-o", out]
 res = subprocess.run(cmd, capture_output=True, text=True)
 open(out + ".log", "w").write(res.stderr)

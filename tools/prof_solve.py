@@ -23,6 +23,7 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--residual", type=float, default=0.0, help="residual tolerance (solve_all semantics); 0: fixed T")
 ap.add_argument("--groups", type=int, default=1, help="orthogonal groups per system (vr-oahk-g)")
 ap.add_argument("--cap", type=int, default=0, help="hyperplanes per aggregated step (vr-oahk-g; 0: all)")
+ap.add_argument("--dump", default="", help="save V, iters, flops of the last run to this .npz (bitwise A/B of builds)")
 a = ap.parse_args()
 cfg = kz.CONFIGS[a.config]
 ch = kz.generate(cfg, [0, range(a.batch)] if cfg.n_subcarriers > 1 else range(a.batch))
@@ -44,3 +45,7 @@ for r in range(a.reps):
 times.sort()
 print(f"{a.scheme} {a.dtype} B={a.batch} T={a.iters}: min {times[0]:.3f} ms, median {times[len(times) // 2]:.3f} ms "
       f"over {len(times)} (launches {res.launches})")
+if a.dump:
+    import numpy as np
+    np.savez(a.dump, v=res.v.cpu().numpy(), iters=res.iters.cpu().numpy(),
+             flops=res.flops.cpu().numpy() if res.flops is not None else np.zeros(0))
