@@ -321,6 +321,22 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
       }
     }
   }
+  // vr-oahk: the O rows in ascending order (in cmask, which only vr-ogrk uses) and their count (misc[1]): the
+  // block step hands row k of the list to warp k, the other warps go straight to the barrier
+  int* orow = (int*)cmask;
+  if constexpr (SCH == KZ_VR_OAHK) {
+    if (w == 0) {
+      int n = 0;
+      for (int base = 0; base < K; base += 32) {
+        const int i = base + lane;
+        const bool o = i < K && inset[i] == 1;
+        const unsigned bal = __ballot_sync(FULL, o);
+        if (o) orow[n + __popc(bal & ((1u << lane) - 1))] = i;
+        n += __popc(bal);
+      }
+      if (lane == 0) misc[1] = (uint32_t)n;
+    }
+  }
   if constexpr (SCH == KZ_VR_OGRK) {
     for (int i = tid; i < K; i += nthr) {
       size_t r = (size_t)b * K + i;
@@ -1015,13 +1031,19 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         aggregate(lptr, lspl, lst, K, Nt, true, true, 6LL * Nt * K + 2LL * Nt * max(K - 1, 0));
       } else {
         // exact block projection on the orthogonal group O (solvers.py:312-332)
-        refresh_list(optr, ospl, olst);
+        // the few O pieces of this chunk (disjoint VRs: one or two) in one compact loop -- a half piece taken as a
+        // whole chunk adds its zero padding, which is exact -- instead of another copy of the unrolled refresh
+        // (28 KB less code in the loop body: every phase of the iteration runs ~3% faster, instruction fetch)
+        for (int q = optr[w]; q < optr[w + 1]; ++q) {
+          const int2 e0 = olst[q];
+          Ps[pslot(e0.y)] = dot_part(JRange<0, 8>{}, e0.x & 0xFFFFF);
+        }
         KZ_WSTAMP_IF(1);
         __syncthreads();
         KZ_PHASE();
-        for (int e = tid; e < K * G; e += nthr) {
-          const int i = e / G, rr = e % G;
-          if (inset[i] != 1 || g0 + rr >= K) continue;
+        for (int k = w; k < (int)misc[1]; k += W) {  // warp k: O row k, lanes over the rhs
+          const int i = orow[k], rr = lane;
+          if (g0 + rr >= K) continue;
           const T r = resid(i, rr);
           const T gm = make_float2(r.x / en[i], r.y / en[i]);
           const T q = Qs[xs(i, rr)];
