@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   };
   // bt: every slot load issued at once (predicated), then the sums in slot order -- for callers with registers to
   // spare (the greedy selection; the aggregation weights, formed while the iterate is parked in TMEM)
-  auto resid_b = [&](auto bt, int i, int gg) -> T {  // from the slot partials, fixed order
+  auto resid_q = [&](auto bt, int i, int gg, const T q) -> T {  // from the slot partials, fixed order; q = q_i
     KZ_CHECK(i >= 0 && i < K && gg >= 0 && gg < G && c1[i] - c0[i] < SL, "wide: residual row / slots");
     const T* pp = Ps + (size_t)i * SL * G + (gg ^ (i & 15));
     float dx = 0.f, dy = 0.f;
@@ -510,7 +510,6 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         dy += v.y;
       }
     }
-    T q = Qs[xs(i, gg)];
     const int c = g0 + gg;
     if (SCH == KZ_GK || SCH == KZ_GRK || SCH == KZ_AHK) {  // dense form (solvers.py:149-153)
       T r = make_float2(-dx - q.x * regf, -dy - q.y * regf);
@@ -520,6 +519,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
     float tg = i == c ? 1.f : 0.f;  // VR form (solvers.py:166)
     return make_float2((tg - dx) - q.x * regf, (0.f - dy) - q.y * regf);
   };
+  auto resid_b = [&](auto bt, int i, int gg) -> T { return resid_q(bt, i, gg, Qs[xs(i, gg)]); };
   auto resid = [&](int i, int gg) -> T { return resid_b(std::bool_constant<SCH != KZ_VR_OAHK>{}, i, gg); };
   auto draw_u = [&](int gg) -> double {
     int c = g0 + gg, d = itv[gg];
@@ -776,11 +776,20 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         const int gg = lane;
         float nx = 0.f, ny = 0.f, sp = 0.f;
         bool nz = false;
+        // the previous aggregated step's q += gamma phi on these rows is applied here, where q_i is loaded
+        // anyway (sel / gam: that step's flag and length per rhs; the old phi is still in Phi)
+        const bool pend = sel[gg] > 0;
+        const T pg = gam[gg];
         if (g0 + gg < K && !donev[gg])
 #pragma unroll 4
           for (int i = w; i < K; i += W) {
             if (which && inset[i] != which) continue;
-            const T r = resid_b(std::true_type{}, i, gg);
+            T q = Qs[xs(i, gg)];
+            if (pend) {
+              q = cfma(pg, Phi[xs(i, gg)], q);
+              Qs[xs(i, gg)] = q;
+            }
+            const T r = resid_q(std::true_type{}, i, gg, q);
             const float ie = inv_en[i];
             const T ph = make_float2(r.x * ie, r.y * ie);
             Phi[xs(i, gg)] = ph;
@@ -823,11 +832,18 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
           const bool act = g0 + gg < K && !donev[gg];
           float nx = 0.f, ny = 0.f, sp = 0.f;
           bool nz = false;
+          const bool pend = sel[gg] > 0;  // the previous step's q += gamma phi, applied where q_i is loaded
+          const T pg = gam[gg];
           if (act)
 #pragma unroll 4
             for (int i = hl; i < K; i += 16) {
               if (which && inset[i] != which) continue;
-              const T r = resid_b(std::true_type{}, i, gg);
+              T q = Qs[xs(i, gg)];
+              if (pend) {
+                q = cfma(pg, Phi[xs(i, gg)], q);
+                Qs[xs(i, gg)] = q;
+              }
+              const T r = resid_q(std::true_type{}, i, gg, q);
               const float ie = inv_en[i];
               const T ph = make_float2(r.x * ie, r.y * ie);
               Phi[xs(i, gg)] = ph;
@@ -984,16 +1000,11 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
         }
         KZ_WSTAMP_IF(7);
         KZ_PHASE();  // [timing] iterate reload + update
-        // q += gamma phi over the aggregated rows (threads over (row, rhs))
-        {  // rhs of entry e is e % G == lane = g + 16 a (nthr is a multiple of 32): this thread's own step
-          const bool stq = a ? st1 : st0;
-          const T gq = a ? gm1 : gm0;
-          if (stq && g0 + lane < K)
-            for (int e = tid; e < K * G; e += nthr) {
-              const int i = e / G;
-              if (SCH == KZ_VR_OAHK && inset[i] != 2) continue;
-              Qs[xs(i, lane)] = cfma(gq, Phi[xs(i, lane)], Qs[xs(i, lane)]);
-            }
+        // q += gamma phi over the aggregated rows is left pending (flag in sel, length in gam): the next weights
+        // pass applies it row by row where it loads q_i anyway, flush_q below after the last iteration
+        if (w == 0) {
+          sel[lane] = (a ? st1 : st0) && g0 + lane < K ? 1 : 0;
+          gam[lane] = a ? gm1 : gm0;
         }
         KZ_PHASE();  // [timing] coefficient update
         // bookkeeping once per rhs (warp 0: lane = rhs slot)
@@ -1134,6 +1145,17 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   const int t_end = t > p.T ? p.T : t;
   __syncthreads();
   KZ_PHASE();
+  if constexpr (AGG) {  // the last aggregated step's pending q += gamma phi
+    if (sel[lane] > 0 && g0 + lane < K) {
+      const T gq = gam[lane];
+      for (int e = tid; e < K * G; e += nthr) {
+        const int i = e / G;
+        if (SCH == KZ_VR_OAHK && inset[i] != 2) continue;
+        Qs[xs(i, lane)] = cfma(gq, Phi[xs(i, lane)], Qs[xs(i, lane)]);
+      }
+    }
+    __syncthreads();
+  }
   if constexpr (AGG) {
     tmem::fence_after();
     if (w == 0) tmem::dealloc(misc[0], 256);
