@@ -27,6 +27,9 @@
 #ifndef KZ_WIDE_HALF_MASK
 #define KZ_WIDE_HALF_MASK ((1 << KZ_GK) | (1 << KZ_GRK) | (1 << KZ_VR_OGRK) | (1 << KZ_VR_OAHK))
 #endif
+#ifndef KZ_WIDE_NF
+#define KZ_WIDE_NF 4  // whole-chunk refresh pieces in flight per warp (vr-oahk: 2)
+#endif
 #ifndef KZ_WIDE_PARW_MASK
 #define KZ_WIDE_PARW_MASK (1 << KZ_VR_OAHK)
 #endif
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) kz_wide_kernel(const __grid_constant__
   // refresh partials of warp w's pieces of a list: whole-chunk pieces (four in flight; vr-oahk two: its larger
   // live state would spill), then the first-half and second-half pieces (two in flight)
   auto refresh_list = [&](const int* ptr, const int* spl, const int2* L) {
-    using NF = std::integral_constant<int, SCH == KZ_VR_OAHK ? 2 : 4>;
+    using NF = std::integral_constant<int, SCH == KZ_VR_OAHK ? 2 : KZ_WIDE_NF>;
     refresh_seg(JRange<0, 8>{}, NF{}, L, ptr[w], spl[2 * w]);
     if constexpr (HALF) {
       refresh_seg(JRange<0, 4>{}, std::integral_constant<int, 2>{}, L, spl[2 * w], spl[2 * w + 1]);
