@@ -614,3 +614,53 @@ def test_cfg3_cfg5_c64_vs_oracle_at_stated_iterations():
                 n64, s64 = float(out["nmse"][b]), float(out["sum_rate"][b])
                 assert c64_nmse_ok(n64, n128), (name, sc, b, n64, n128)
                 assert s64 == pytest.approx(s128, rel=1e-3), (name, sc, b, s64, s128)
+
+
+def _custom_contiguous(nt, starts, lengths, seed, snr_db=10.0):
+    """One system with the given contiguous VRs (unit-norm random rows), as a ContiguousChannels batch."""
+    from paper_2501_10689_b200.channel import ContiguousChannels
+    rng = np.random.default_rng(seed)
+    k = len(starts)
+    vals, ptr = [], [0]
+    for ln in lengths:
+        v = rng.standard_normal(ln) + 1j * rng.standard_normal(ln)
+        vals.append(v / np.linalg.norm(v))
+        ptr.append(ptr[-1] + ln)
+    snr = 10.0 ** (snr_db / 10.0)
+    return ContiguousChannels(nt, k, np.asarray([starts], dtype=np.int32), np.asarray([lengths], dtype=np.int32),
+                              np.concatenate(vals), np.asarray(ptr, dtype=np.int64), np.asarray([k / snr]),
+                              np.asarray([snr]))
+
+
+@pytest.mark.parametrize("case", ["all_orthogonal", "many_orthogonal_plus_overlap"])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_wide_vr_oahk_many_orthogonal_rows(case, dtype):
+    """VR-OAHK on the register-resident kernels with more orthogonal rows than warps (the block step hands one O row
+    to each warp in turn) and, in the first case, no non-orthogonal rows at all (no aggregated step, nothing
+    pending for the coefficient update); the second case has short VRs inside single chunks, half pieces and an
+    aggregated step whose q += gamma phi is applied by the next weights pass / flushed at the end.  Against the
+    complex128 oracle (solvers.py:312-332, 407-421)."""
+    kz = _kz()
+    nt = 512
+    if case == "all_orthogonal":
+        starts, lengths = [16 * i for i in range(32)], [16] * 32          # 32 disjoint VRs: N is empty
+    else:
+        starts = [12 * i for i in range(24)] + [300 + 5 * i for i in range(16)]  # 24 disjoint + 16 overlapping
+        lengths = [12] * 24 + [128] * 16
+    ch = _custom_contiguous(nt, starts, lengths, seed=11)
+    dev = kz.HostBatch.from_contiguous(ch).to_device(dtype)
+    T = 6
+    res = kz.solve_batch(dev, "vr-oahk", mode="lockstep", max_iters=T)
+    chan = oracle_channel_contiguous(ch, 0)
+    sys_ = O.AugmentedSystem.from_channel(chan, float(ch.reg[0]))
+    if case == "all_orthogonal":
+        assert len(sys_.partition.non_orthogonal) == 0
+    else:
+        assert len(sys_.partition.orthogonal) > 16 and len(sys_.partition.non_orthogonal) > 0
+    run = O.run_precoding("vr-oahk", sys_, O.rzf_precoder(chan, float(ch.reg[0])), epsilon=0.0, max_iters=T,
+                          traces=False)
+    v = res.v[0].cpu().numpy()
+    assert rel(v, run.v) <= (REL_C128 if dtype == "c128" else 1e-4)
+    assert int(res.noop_steps[0].sum()) == run.noop_steps
+    if dtype == "c128":
+        np.testing.assert_array_equal(res.iters[0].cpu().numpy(), run.iters)

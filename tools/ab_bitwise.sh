@@ -6,7 +6,7 @@ set -- $ARMS
 for sc in ${SCHEMES:-grk vr-ogrk ahk vr-oahk}; do
   for arm in $ARMS; do
     v=$arm; [ "$arm" = cur ] && v=""
-    KZ_LIB_VARIANT=$v python tools/prof_solve.py --scheme $sc --batch ${BATCH:-64} --iters ${ITERS:-200} --reps 1 --dump /tmp/abv_$arm.npz > /dev/null
+    KZ_LIB_VARIANT=$v python tools/prof_solve.py --config ${CONFIG:-cfg2} --scheme $sc --batch ${BATCH:-64} --iters ${ITERS:-200} --reps 1 --dump /tmp/abv_$arm.npz > /dev/null
   done
   python - "$sc" /tmp/abv_$1.npz /tmp/abv_$2.npz <<'PY'
 import sys, numpy as np
