@@ -254,6 +254,25 @@ def measured_views():
     return out or None
 
 
+def reg_ffma_stream_view(achieved_tflops):
+    """The dominant launch against the rate the refresh inner loop reaches in isolation (tools/refresh_forms.cu,
+    profiles/r02_refresh_forms.json, form A = the kernel's 2 rhs x 16 antennas blocking; the FFMAs alone, form E,
+    run at the same rate: register-operand FFMA streams stop at ~0.65 warp-instructions/clk per SM sub-partition
+    on this B200, whatever the shared-memory traffic)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_refresh_forms.json")) as fh:
+            for line in fh:
+                d = json.loads(line)
+                if d.get("form", "").startswith("A:"):
+                    rate = float(d["ffma_per_clk_per_smsp"])
+                    peak = NOMINAL_FP32_TFLOPS * rate
+                    return {"ffma_per_clk_per_smsp": rate, "peak_TFLOPs": peak, "frac": achieved_tflops / peak,
+                            "peak_source": "profiles/r02_refresh_forms.json form A x the nominal FP32 peak"}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 def peaks_json():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -733,6 +752,7 @@ def main():
         pass
     roof["traffic"] = traffic
     roof["measured_views"] = measured_views()
+    roof["reg_ffma_stream_view"] = reg_ffma_stream_view(roof["achieved"])
     roof["note"] = ("H_eff is on-chip (shared memory, or a thread-block cluster's shared memory for Nt > 512) and "
                     "each streamed h element feeds 2 rhs in registers (8 FFMA per complex element), so the launch "
                     "is CUDA-core FP32-FMA bound (SURVEY 8(d): report the FMA roofline); flops = 8 x the H_eff "

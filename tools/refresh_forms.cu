@@ -14,7 +14,7 @@
 constexpr int THREADS = 512, NPIECE = 64, ROWS = 64, ROW_EL = 160 + 2, ITERS = 200;
 
 template <int FORM>
-__global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long long* cyc, const int* order) {
+__global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long long* cyc, const int* order, float seed) {
   extern __shared__ __align__(16) unsigned char sm[];
   float2* Hs = (float2*)sm;                          // ROWS rows of ROW_EL elements
   float2* Ps = Hs + ROWS * ROW_EL;                   // [NPIECE][32] per warp slot array (shared by the warps: timing only)
@@ -26,13 +26,39 @@ __global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long l
   const float4* H4 = reinterpret_cast<const float4*>(Hs);
   float2 m[32];  // the thread's iterate: FORM A m[r * 16 + k] (2 rhs x 16), FORM B m[r * 8 + k] (4 rhs x 8)
 #pragma unroll
-  for (int k = 0; k < 32; ++k) m[k] = make_float2(1.f + 0.01f * k + 1e-3f * tid, 0.5f - 0.01f * k);
+  for (int k = 0; k < 32; ++k) m[k] = make_float2(seed + 0.01f * k + 1e-3f * tid, 0.5f * seed - 0.01f * k * seed + 2e-3f * tid);  // run-time values: no immediates
   long long t0 = clock64();
+  float4 hreg[8];
+  float2 accs = make_float2(0.f, 0.f);
   for (int it = 0; it < ITERS; ++it) {
+#pragma unroll 8
     for (int q = 0; q < NPIECE; ++q) {
+      if (FORM == 4 && (q & 7) == 0) {  // eight row elements per eight pieces: 1/8 of the loop's LDS traffic
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hreg[j] = H4[(ord[q] * (ROW_EL / 2) + it + 2 * j + 16 * (threadIdx.x >> 9)) & 4095];
+      }
       const int row = ord[q];
       const int h0 = row * ROW_EL + 32 * ((w + q) & 3);  // a chunk of the row (element offset, even)
-      if (FORM == 0) {
+      if (FORM == 4) {
+        // form A's FFMAs alone: h stays in registers (loaded once per outer iteration), no exchange, no store
+        const int a = lane >> 4;
+        float x0 = 0, y0 = 0, x1 = 0, y1 = 0, u0 = 0, v0 = 0, u1 = 0, v1 = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 h = hreg[(j + q) & 7];  // a different row element per piece: nothing is loop invariant
+          const int k = 2 * j;
+          x0 = fmaf(h.x, m[k].x, x0); x0 = fmaf(h.y, m[k].y, x0);
+          y0 = fmaf(h.x, m[k].y, y0); y0 = fmaf(-h.y, m[k].x, y0);
+          x1 = fmaf(h.z, m[k + 1].x, x1); x1 = fmaf(h.w, m[k + 1].y, x1);
+          y1 = fmaf(h.z, m[k + 1].y, y1); y1 = fmaf(-h.w, m[k + 1].x, y1);
+          u0 = fmaf(h.x, m[16 + k].x, u0); u0 = fmaf(h.y, m[16 + k].y, u0);
+          v0 = fmaf(h.x, m[16 + k].y, v0); v0 = fmaf(-h.y, m[16 + k].x, v0);
+          u1 = fmaf(h.z, m[17 + k].x, u1); u1 = fmaf(h.w, m[17 + k].y, u1);
+          v1 = fmaf(h.z, m[17 + k].y, v1); v1 = fmaf(-h.w, m[17 + k].x, v1);
+        }
+        accs.x += (x0 + x1) + (u0 + u1) + (float)a;
+        accs.y += (y0 + y1) + (v0 + v1);
+      } else if (FORM == 0) {
         const int a = lane >> 4;
         const float4* hp = H4 + ((h0 + 2 * a) >> 1);
         float x0 = 0, y0 = 0, x1 = 0, y1 = 0, u0 = 0, v0 = 0, u1 = 0, v1 = 0;
@@ -50,6 +76,29 @@ __global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long l
           v1 = fmaf(h.z, m[17 + k].y, v1); v1 = fmaf(-h.w, m[17 + k].x, v1);
         }
         const float px = x0 + x1, py = y0 + y1, qx = u0 + u1, qy = v0 + v1;
+        const float sx = a ? px : qx, sy = a ? py : qy;
+        const float rx = __shfl_xor_sync(0xffffffffu, sx, 16), ry = __shfl_xor_sync(0xffffffffu, sy, 16);
+        Ps[q * 32 + lane] = a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
+      } else if (FORM == 2 || FORM == 3) {
+        // form A's blocking with the FFMAs of one h element ordered so that each shares one multiplicand with its
+        // predecessor (m.x h.x, m.x h.y, m.y h.y, m.y h.x, ...): one new register operand per FFMA
+        const int a = lane >> 4;
+        const float4* hp = H4 + ((h0 + 2 * a) >> 1);
+        float x0 = 0, y0 = 0, x1 = 0, y1 = 0, u0 = 0, v0 = 0, u1 = 0, v1 = 0;
+        float xa = 0, ya = 0, xb = 0, yb = 0, ua = 0, va = 0, ub = 0, vb = 0;
+#define KZ_F(acc, p, q) do { if (FORM == 3) asm volatile("fma.rn.f32 %0, %1, %2, %0;" : "+f"(acc) : "f"(p), "f"(q)); else acc = fmaf(p, q, acc); } while (0)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 h = hp[2 * j];
+          const int k = 2 * j;
+          const float nhy = -h.y, nhw = -h.w;
+          KZ_F(x0, m[k].x, h.x); KZ_F(y0, m[k].x, nhy); KZ_F(xa, m[k].y, h.y); KZ_F(ya, m[k].y, h.x);
+          KZ_F(va, m[16 + k].y, h.x); KZ_F(ua, m[16 + k].y, h.y); KZ_F(v0, m[16 + k].x, nhy); KZ_F(u0, m[16 + k].x, h.x);
+          KZ_F(x1, m[k + 1].x, h.z); KZ_F(y1, m[k + 1].x, nhw); KZ_F(xb, m[k + 1].y, h.w); KZ_F(yb, m[k + 1].y, h.z);
+          KZ_F(vb, m[17 + k].y, h.z); KZ_F(ub, m[17 + k].y, h.w); KZ_F(v1, m[17 + k].x, nhw); KZ_F(u1, m[17 + k].x, h.z);
+        }
+#undef KZ_F
+        const float px = (x0 + xa) + (x1 + xb), py = (y0 + ya) + (y1 + yb), qx = (u0 + ua) + (u1 + ub), qy = (v0 + va) + (v1 + vb);
         const float sx = a ? px : qx, sy = a ? py : qy;
         const float rx = __shfl_xor_sync(0xffffffffu, sx, 16), ry = __shfl_xor_sync(0xffffffffu, sy, 16);
         Ps[q * 32 + lane] = a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
@@ -94,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long l
   float2 s = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 32; ++k) { s.x += m[k].x; s.y += m[k].y; }
-  s.x += Ps[lane].x;
+  s.x += Ps[lane].x + accs.x + accs.y;
   out[blockIdx.x * THREADS + tid] = s;
 }
 
@@ -104,7 +153,7 @@ void run(const char* name, int sms, float2* out, long long* cyc, const int* orde
   cudaFuncSetAttribute(refresh_kernel<FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   long long h[1024];
   for (int rep = 0; rep < 2; ++rep) {
-    refresh_kernel<FORM><<<sms, THREADS, smem>>>(out, cyc, order);
+    refresh_kernel<FORM><<<sms, THREADS, smem>>>(out, cyc, order, 1.0f + 1e-3f * rep);
     cudaDeviceSynchronize();
     cudaMemcpy(h, cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
     double mc = 0;
@@ -130,5 +179,8 @@ int main() {
   cudaMemcpy(order, ho, sizeof(ho), cudaMemcpyHostToDevice);
   run<0>("A: 2 rhs x 16 antennas per thread (wide kernel)", sms, out, cyc, order);
   run<1>("B: 4 rhs x 8 antennas per thread", sms, out, cyc, order);
+  run<4>("E: form A, the 128 FFMAs alone (h in registers, no exchange / store)", sms, out, cyc, order);
+  run<2>("C: form A, FFMAs ordered to share one multiplicand with the predecessor (16 accumulators)", sms, out, cyc, order);
+  run<3>("D: form C with the FFMA order pinned (asm volatile)", sms, out, cyc, order);
   return 0;
 }
