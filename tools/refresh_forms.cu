@@ -39,7 +39,37 @@ __global__ void __launch_bounds__(THREADS, 1) refresh_kernel(float2* out, long l
       }
       const int row = ord[q];
       const int h0 = row * ROW_EL + 32 * ((w + q) & 3);  // a chunk of the row (element offset, even)
-      if (FORM == 4) {
+      if (FORM == 5) {
+        // form A's blocking with packed FFMA2 (fma.rn.f32x2): the iterate of the two rhs planar, MX[k] = (m0[k].x, m1[k].x),
+        // MY[k] = (m0[k].y, m1[k].y) (here: m[k] and m[16 + k] reinterpreted), h components broadcast to pairs;
+        // RE += (hx,hx) MX + (hy,hy) MY, IM += (hx,hx) MY, IN += (hy,hy) MX (IM - IN at the end); two accumulator sets
+        const int a = lane >> 4;
+        const float4* hp = H4 + ((h0 + 2 * a) >> 1);
+        unsigned long long re0 = 0, im0 = 0, in0 = 0, re1 = 0, im1 = 0, in1 = 0;
+        const unsigned long long* MX = reinterpret_cast<const unsigned long long*>(m);       // 16 pairs
+        const unsigned long long* MY = reinterpret_cast<const unsigned long long*>(m + 16);  // 16 pairs
+#define KZ_F2(acc, hh, mm) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(hh), "l"(mm))
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 h = hp[2 * j];
+          const int k = 2 * j;
+          unsigned long long hxx, hyy, hzz, hww;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hxx) : "f"(h.x));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hyy) : "f"(h.y));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hzz) : "f"(h.z));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hww) : "f"(h.w));
+          KZ_F2(re0, hxx, MX[k]); KZ_F2(im0, hxx, MY[k]); KZ_F2(in0, hyy, MX[k]); KZ_F2(re0, hyy, MY[k]);
+          KZ_F2(re1, hzz, MX[k + 1]); KZ_F2(im1, hzz, MY[k + 1]); KZ_F2(in1, hww, MX[k + 1]); KZ_F2(re1, hww, MY[k + 1]);
+        }
+#undef KZ_F2
+        float2 r0 = *reinterpret_cast<float2*>(&re0), r1 = *reinterpret_cast<float2*>(&re1);
+        float2 i0 = *reinterpret_cast<float2*>(&im0), i1 = *reinterpret_cast<float2*>(&im1);
+        float2 n0 = *reinterpret_cast<float2*>(&in0), n1 = *reinterpret_cast<float2*>(&in1);
+        const float px = r0.x + r1.x, py = (i0.x + i1.x) - (n0.x + n1.x), qx = r0.y + r1.y, qy = (i0.y + i1.y) - (n0.y + n1.y);
+        const float sx = a ? px : qx, sy = a ? py : qy;
+        const float rx = __shfl_xor_sync(0xffffffffu, sx, 16), ry = __shfl_xor_sync(0xffffffffu, sy, 16);
+        Ps[q * 32 + lane] = a ? make_float2(qx + rx, qy + ry) : make_float2(px + rx, py + ry);
+      } else if (FORM == 4) {
         // form A's FFMAs alone: h stays in registers (loaded once per outer iteration), no exchange, no store
         const int a = lane >> 4;
         float x0 = 0, y0 = 0, x1 = 0, y1 = 0, u0 = 0, v0 = 0, u1 = 0, v1 = 0;
@@ -180,6 +210,7 @@ int main() {
   run<0>("A: 2 rhs x 16 antennas per thread (wide kernel)", sms, out, cyc, order);
   run<1>("B: 4 rhs x 8 antennas per thread", sms, out, cyc, order);
   run<4>("E: form A, the 128 FFMAs alone (h in registers, no exchange / store)", sms, out, cyc, order);
+  run<5>("F: form A with packed FFMA2 (planar iterate over the two rhs, 6 accumulator pairs)", sms, out, cyc, order);
   run<2>("C: form A, FFMAs ordered to share one multiplicand with the predecessor (16 accumulators)", sms, out, cyc, order);
   run<3>("D: form C with the FFMA order pinned (asm volatile)", sms, out, cyc, order);
   return 0;
